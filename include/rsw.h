@@ -1,0 +1,151 @@
+/*
+ * rsw.h — C-ABI of librsw.so: the B200-native (sm_100a) hot path of the asymptotic parareal
+ * method for the 1-D rotating shallow water (RSW) equations, arxiv 1303.6615.
+ *
+ *   u_t + ε^{-1} L u = N(u) + D u,   u = (v1, v2, h) on the periodic domain [0, 2π)
+ *                                                    (Eq. full eqn; RSW P:1045-1095)
+ *
+ * Citations "P:n" are lines of /root/reference/PAPER.md; "R#" are the readings listed in
+ * DESIGN.md §3 (where the paper is silent, ambiguous or garbled).
+ *
+ * ----------------------------------------------------------------------------------------------
+ * STATE LAYOUT (every state argument):
+ *   double[batch][3][n/2+1][2]  — field-major (v1, v2, h), wavenumber k = 0..n/2, (re, im).
+ *   û_k = (1/n) Σ_j u_j e^{-ikx_j}, x_j = 2πj/n (so k = 0 is the mean).  Real fields (R16):
+ *   Im(û_0) must be 0.  Dealiasing (R10): modes k > n/3 must be 0 on input and are 0 on output.
+ *   Violations return RSW_ERR_CONFIG only where checking is free; otherwise they are undefined.
+ *
+ * MEMORY: all state pointers are DEVICE pointers (caller-owned, e.g. torch CUDA tensors),
+ *   8-byte aligned, on the current device, unless a parameter says "host".
+ *   The library never retains a caller pointer after a call returns.  It caches per-configuration
+ *   coefficient tables and workspace (keyed by every parameter that affects them) until
+ *   rsw_shutdown().
+ * STREAMS: `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All work
+ *   is enqueued on it; only parareal_iterate synchronises (once per iteration, to read r_k).
+ * ERRORS: every argument is validated before any launch; no exceptions cross the ABI;
+ *   rsw_last_error() returns a thread-local message describing the last non-OK status.
+ * There is NO CPU fallback: a call that cannot run on the GPU returns RSW_ERR_CUDA.
+ * ----------------------------------------------------------------------------------------------
+ */
+#ifndef RSW_H_
+#define RSW_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Physical parameters: ε Rossby number, F (Froude = F^{1/2} ε), μ hyperviscosity
+   (D̂(k) = -μk^4, sign R2), n = grid points = FFT length (power of two, 16..1024). */
+typedef struct {
+  double eps, F, mu;
+  int32_t n;
+} rsw_params;
+
+typedef enum {
+  RSW_OK = 0,
+  RSW_ERR_CONFIG = 1,     /* invalid argument (nothing was launched) */
+  RSW_NOT_CONVERGED = 2,  /* parareal: tol > 0 and no r_k < tol within max_iters (U valid) */
+  RSW_ERR_DIVERGED = 3,   /* parareal: r_k non-finite or > 1e6 (SPEC S:399 guard) */
+  RSW_ERR_CUDA = 4,
+  RSW_ERR_NCCL = 5
+} rsw_status;
+
+enum { RSW_FINE_ETDRK4 = 0, RSW_FINE_STRANG = 1 };
+enum { RSW_COARSE_RK4 = 0, RSW_COARSE_MIDPOINT = 1 };
+enum { RSW_FLAG_LINEAR_ONLY = 1u }; /* N ≡ 0: exact-linear test mode only */
+
+/* N(u) = -(v1 ∂x v1, v1 ∂x v2, ∂x(h v1)) for n_states independent states, evaluated
+   pseudo-spectrally (inverse FFT -> pointwise products -> FFT, 2/3 rule).
+   Operator table, sign R1.  u_in and out must not alias.
+   (The inner kernel of every other entry point, exposed for parity tests.) */
+rsw_status rsw_nonlinear(const rsw_params* p, int32_t n_states, const double* u_in, double* out,
+                         void* stream);
+
+/* Fine propagator φ_ΔT (the parfor of Alg.4): each of n_slices independent states is
+   advanced by dT with m = ceil(dT/dt - 1e-9) steps of dt_eff = dT/m (R9) of
+     scheme RSW_FINE_ETDRK4: ETDRK4 (Cox & Matthews 2002; cited P:1168-1169), or
+     scheme RSW_FINE_STRANG: Strang splitting, Alg.3 P:518-548 with the explicit midpoint (R7),
+   the linear part e^{hA}, A = -L̂/ε + D̂ (R3), applied exactly per wavenumber in the eigenbasis of
+   L̂.  flags: RSW_FLAG_LINEAR_ONLY.  u_in == u_out is allowed (in-place). */
+rsw_status rsw_fine_propagate(const rsw_params* p, int32_t scheme, uint32_t flags, double dT,
+                              double dt, int32_t n_slices, const double* u_in, double* u_out,
+                              void* stream);
+
+/* HMM averaged nonlinearity (Eq. numerical average, discretized P:289-293; ε-scaled form P:313;
+   Alg.1; kernel ρ P:383-390), for n_states independent states:
+     N̄(v) = Σ_{m=1}^{M-1} w_m e^{τ_m L̂} N(e^{-τ_m L̂} v),  τ_m = s_m/ε, s_m = T0 m/M  (R4),
+     w_m = ρ(m/M) / Σ_j ρ(j/M),  ρ(s) = exp(-1/(s(1-s)))  (R5).
+   The sum over samples is evaluated in ascending m (deterministic).  rhs_out must not alias. */
+rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n_states,
+                            const double* u_in, double* rhs_out, void* stream);
+
+/* Coarse propagator φ̄_ΔT (Alg.2, φ̄ P:415-417) for n_states independent states:
+     v = e^{ΔT D̂/2} u;  one RK4 (R6; or midpoint, RSW_COARSE_MIDPOINT) step of size dT on v' = N̄(v);
+     v = e^{ΔT D̂/2} v;  G(u) = e^{-(ΔT/ε) L̂} v   (back-transform sign R3).
+   u_in == u_out is allowed. */
+rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, double dT, double T0,
+                                int32_t M, int32_t n_states, const double* u_in, double* u_out,
+                                void* stream);
+
+typedef struct {
+  double dT, dt, T0, tol;
+  int32_t M, n_slices, max_iters, fine_scheme, coarse_scheme;
+} parareal_config;
+
+typedef struct rsw_comm rsw_comm; /* opaque; NULL = single GPU */
+
+/* Optional per-call statistics (may be NULL).  Times are device-measured (CUDA events) ms. */
+typedef struct {
+  double fine_ms, comm_ms, coarse_ms, total_ms;
+  int64_t fine_slice_steps; /* slice-steps advanced by THIS rank's fine sweeps */
+  int64_t kernel_launches;  /* kernels this library launched during the call */
+} rsw_parareal_stats;
+
+/* The asymptotic parareal iteration (Eq. HMM parareal iteration P:428-430; Alg.4):
+     k = 0:  U_0 = u0, U_{n+1} = G(U_n), n = 0..S-1;
+     k >= 1: F_n = F(U^{k-1}_n) in parallel (this rank's shard, then an all-gather over `comm`);
+             serial sweep U^k_{n+1} = G(U^k_n) + (F_n - G_n), G_n <- G(U^k_n)   (R13, R14);
+             r_k = max_{n=1..S} ||U^k_n - U^{k-1}_n|| / ||U^k_n||  (relative L2, R12).
+   u0: device [3][n/2+1][2].  U: device [S+1][3][n/2+1][2] (replicated, bitwise identical on every
+   rank).  resid_hist: HOST double[max_iters].  iters_done: HOST.  tol <= 0: run exactly
+   max_iters iterations; tol > 0: stop at the first r_k < tol (RSW_NOT_CONVERGED if none).
+   Requires 0 <= max_iters <= n_slices and n_slices divisible by the comm world size. */
+rsw_status parareal_iterate(const rsw_params* p, const parareal_config* cfg, const double* u0,
+                            double* U, double* resid_hist, int32_t* iters_done, rsw_comm* comm,
+                            void* stream);
+
+/* As parareal_iterate, additionally returning the last iteration's fine endpoints F_n and coarse
+   values G_n (device [S][3][n/2+1][2] each; either may be NULL) and statistics (host; may be
+   NULL). */
+rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, const double* u0,
+                               double* U, double* resid_hist, int32_t* iters_done, rsw_comm* comm,
+                               void* stream, double* F_out, double* G_out,
+                               rsw_parareal_stats* stats);
+
+/* Slices owned by `rank` of `world` in the fine sweep: [*lo, *hi) (contiguous blocks, §8(e)). */
+rsw_status rsw_shard_range(int32_t n_slices, int32_t rank, int32_t world, int32_t* lo,
+                           int32_t* hi);
+
+/* NCCL communicator owned by the library (NCCL is loaded at run time).  out128/id128: 128 host
+   bytes (ncclUniqueId), created on rank 0 and broadcast by the caller (e.g. torch.distributed). */
+rsw_status rsw_nccl_unique_id(void* out128);
+rsw_status rsw_comm_init(const void* id128, int32_t rank, int32_t world, rsw_comm** out);
+rsw_status rsw_comm_destroy(rsw_comm* comm);
+
+/* Measured FP64 peak of the current device (DFMA chains on every SM, M0 microbenchmark):
+   *tflops (host) = 2 * DFMA lanes * iterations / kernel time.  Used as the roofline denominator. */
+rsw_status rsw_fp64_peak(double* tflops, void* stream);
+
+/* Analytic flop counts per unit of work, for throughput reporting:
+   which = 0: F_N (one N(u)), 1: ETDRK4 step, 2: Strang step, 3: one N̄ sample. */
+double rsw_flops_per_unit(int32_t n, int32_t which);
+
+const char* rsw_last_error(void); /* thread-local; never NULL */
+void rsw_shutdown(void);          /* frees cached tables and workspace */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSW_H_ */

@@ -1,0 +1,720 @@
+// rsw_capi.cu — host side of librsw.so: argument validation, the per-configuration coefficient
+// tables (K6, closed forms), workspace, the parareal driver (Alg.4) and the NCCL
+// communicator.  Implements include/rsw.h.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/rsw.h"
+#include "rsw_internal.h"
+
+using cd = std::complex<double>;
+
+namespace {
+
+thread_local std::string g_err;
+rsw_status fail(rsw_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(RSW_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+
+bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
+
+rsw_status check_params(const rsw_params* p) {
+  if (!p) return fail(RSW_ERR_CONFIG, "params is NULL");
+  if (!finite_pos(p->eps)) return fail(RSW_ERR_CONFIG, "eps must be finite and > 0");
+  if (!finite_pos(p->F)) return fail(RSW_ERR_CONFIG, "F must be finite and > 0");
+  if (!(std::isfinite(p->mu) && p->mu >= 0.0)) return fail(RSW_ERR_CONFIG, "mu must be finite and >= 0");
+  const int n = p->n;
+  if (n < 16 || n > 1024 || (n & (n - 1)))
+    return fail(RSW_ERR_CONFIG, "n must be a power of two in 16..1024");
+  return RSW_OK;
+}
+
+int n_fine_steps(double dT, double dt) { return (int)std::ceil(dT / dt - 1e-9); }  // R9
+
+// ---------------------------------------------------------------------------------------------
+// φ-functions on the host (R11): Taylor series (30 terms) for |z| < 1, direct formula otherwise.
+// ---------------------------------------------------------------------------------------------
+cd phi_host(int j, cd z) {
+  if (j == 0) return std::exp(z);
+  if (std::abs(z) < 1.0) {
+    // φ_j(z) = Σ_{m>=0} z^m / (m+j)!
+    double fact = 1.0;
+    for (int i = 2; i <= j; ++i) fact *= i;
+    cd term = 1.0 / fact, sum = 0.0;
+    for (int m = 0; m < 30; ++m) {
+      sum += term;
+      term *= z / double(m + j + 1);
+    }
+    return sum;
+  }
+  const cd ez = std::exp(z);
+  if (j == 1) return (ez - 1.0) / z;
+  if (j == 2) return (ez - 1.0 - z) / (z * z);
+  return (ez - 1.0 - z - 0.5 * z * z) / (z * z * z);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Device-resident tables, cached per (device, parameters)
+// ---------------------------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+template <typename T>
+cudaError_t upload(DevBuf& b, const std::vector<T>& v) {
+  b.bytes = v.size() * sizeof(T);
+  cudaError_t e = cudaMalloc(&b.p, b.bytes);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(b.p, v.data(), b.bytes, cudaMemcpyHostToDevice);
+}
+
+struct GeomTables {
+  DevBuf a, p, q, tw;
+};
+
+struct FineTables {
+  DevBuf cp, c0;
+};
+
+struct AvgTables {
+  DevBuf w, phase;
+};
+
+struct CoarseTables {
+  DevBuf dhalf, back;
+};
+
+std::mutex g_mu;
+std::map<std::tuple<int, int, double>, std::unique_ptr<GeomTables>> g_geom;  // (dev, n, F)
+std::map<std::tuple<int, int, double, double, double, double>, std::unique_ptr<FineTables>> g_fine;
+std::map<std::tuple<int, int, double, double, double, int>, std::unique_ptr<AvgTables>> g_avg;
+std::map<std::tuple<int, int, double, double, double, double>, std::unique_ptr<CoarseTables>> g_coarse;
+
+int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+cudaError_t get_geom(const rsw_params* p, GeomTables** out) {
+  auto key = std::make_tuple(cur_dev(), p->n, p->F);
+  auto it = g_geom.find(key);
+  if (it != g_geom.end()) {
+    *out = it->second.get();
+    return cudaSuccess;
+  }
+  const int n = p->n, K = n / 3;
+  std::vector<double> a(K + 1), pp(K + 1), q(K + 1);
+  for (int k = 0; k <= K; ++k) {
+    a[k] = double(k) / std::sqrt(p->F);
+    const double w = std::sqrt(1.0 + a[k] * a[k]);  // ω_k = √(1 + k²/F)
+    pp[k] = 1.0 / (std::sqrt(2.0) * w);
+    q[k] = 1.0 / w;
+  }
+  std::vector<double2> tw(n);
+  const double pi = 3.14159265358979323846264338327950288;
+  for (int m = 0; m < n; ++m) {
+    const double ang = 2.0 * pi * double(m) / double(n);
+    tw[m] = make_double2(std::cos(ang), -std::sin(ang));
+  }
+  auto g = std::make_unique<GeomTables>();
+  cudaError_t e;
+  if ((e = upload(g->a, a)) || (e = upload(g->p, pp)) || (e = upload(g->q, q)) || (e = upload(g->tw, tw)))
+    return e;
+  *out = g.get();
+  g_geom[key] = std::move(g);
+  return cudaSuccess;
+}
+
+rsw::ModeGeom geom_of(const GeomTables* g) {
+  return rsw::ModeGeom{(const double*)g->a.p, (const double*)g->p.p, (const double*)g->q.p};
+}
+
+cudaError_t get_fine(const rsw_params* p, double h, FineTables** out) {
+  auto key = std::make_tuple(cur_dev(), p->n, p->eps, p->F, p->mu, h);
+  auto it = g_fine.find(key);
+  if (it != g_fine.end()) {
+    *out = it->second.get();
+    return cudaSuccess;
+  }
+  const int K = p->n / 3;
+  std::vector<double2> cp(6 * (K + 1));
+  std::vector<double> c0(6 * (K + 1));
+  for (int k = 0; k <= K; ++k) {
+    const double a = double(k) / std::sqrt(p->F), w = std::sqrt(1.0 + a * a);
+    const double k4 = double(k) * k * k * k;
+    // eigenvalues of A = -L̂/ε + D̂ (R2, R3): λ_α = -iαω/ε - μk^4
+    const cd lam_p(-p->mu * k4, -w / p->eps);
+    const cd lam_0(-p->mu * k4, 0.0);
+    for (int al = 0; al < 2; ++al) {
+      const cd z = h * (al == 0 ? lam_p : lam_0);
+      cd v[6];
+      v[0] = std::exp(z);
+      v[1] = std::exp(0.5 * z);
+      v[2] = 0.5 * h * phi_host(1, 0.5 * z);
+      const cd p1 = phi_host(1, z), p2 = phi_host(2, z), p3 = phi_host(3, z);
+      v[3] = h * (p1 - 3.0 * p2 + 4.0 * p3);
+      v[4] = h * (2.0 * p2 - 4.0 * p3);
+      v[5] = h * (4.0 * p3 - p2);
+      for (int i = 0; i < 6; ++i) {
+        if (al == 0) cp[i * (K + 1) + k] = make_double2(v[i].real(), v[i].imag());
+        else c0[i * (K + 1) + k] = v[i].real();
+      }
+    }
+  }
+  auto t = std::make_unique<FineTables>();
+  cudaError_t e;
+  if ((e = upload(t->cp, cp)) || (e = upload(t->c0, c0))) return e;
+  *out = t.get();
+  g_fine[key] = std::move(t);
+  return cudaSuccess;
+}
+
+cudaError_t get_avg(const rsw_params* p, double T0, int M, AvgTables** out) {
+  auto key = std::make_tuple(cur_dev(), p->n, p->eps, p->F, T0, M);
+  auto it = g_avg.find(key);
+  if (it != g_avg.end()) {
+    *out = it->second.get();
+    return cudaSuccess;
+  }
+  const int K = p->n / 3;
+  // weights (R5): w_m = ρ(m/M) / Σ_{j=1}^{M-1} ρ(j/M), ρ(s) = exp(-1/(s(1-s)))
+  std::vector<double> w(M, 0.0);
+  double tot = 0.0;
+  for (int m = 1; m <= M - 1; ++m) {
+    const double s = double(m) / M;
+    w[m] = std::exp(-1.0 / (s * (1.0 - s)));
+    tot += w[m];
+  }
+  for (int m = 1; m <= M - 1; ++m) w[m] /= tot;
+  // phase[m][k] = e^{i ω_k τ_m}, τ_m = s_m/ε, s_m = T0 m/M  (R4)
+  std::vector<double2> ph((size_t)(M + 1) * (K + 1));
+  for (int m = 0; m <= M; ++m) {
+    const double tau = (T0 * double(m) / double(M)) / p->eps;
+    for (int k = 0; k <= K; ++k) {
+      const double a = double(k) / std::sqrt(p->F), om = std::sqrt(1.0 + a * a);
+      const double ang = om * tau;
+      ph[(size_t)m * (K + 1) + k] = make_double2(std::cos(ang), std::sin(ang));
+    }
+  }
+  auto t = std::make_unique<AvgTables>();
+  cudaError_t e;
+  if ((e = upload(t->w, w)) || (e = upload(t->phase, ph))) return e;
+  *out = t.get();
+  g_avg[key] = std::move(t);
+  return cudaSuccess;
+}
+
+cudaError_t get_coarse(const rsw_params* p, double dT, CoarseTables** out) {
+  auto key = std::make_tuple(cur_dev(), p->n, p->eps, p->F, p->mu, dT);
+  auto it = g_coarse.find(key);
+  if (it != g_coarse.end()) {
+    *out = it->second.get();
+    return cudaSuccess;
+  }
+  const int K = p->n / 3;
+  std::vector<double> dh(K + 1);
+  std::vector<double2> bt(K + 1);
+  for (int k = 0; k <= K; ++k) {
+    const double k4 = double(k) * k * k * k;
+    dh[k] = std::exp(-p->mu * k4 * 0.5 * dT);  // e^{(ΔT/2) D̂}
+    const double a = double(k) / std::sqrt(p->F), om = std::sqrt(1.0 + a * a);
+    const double ang = om * dT / p->eps;       // e^{-(ΔT/ε) L̂}: α=+1 entry e^{-iωΔT/ε} (R3)
+    bt[k] = make_double2(std::cos(ang), -std::sin(ang));
+  }
+  auto t = std::make_unique<CoarseTables>();
+  cudaError_t e;
+  if ((e = upload(t->dhalf, dh)) || (e = upload(t->back, bt))) return e;
+  *out = t.get();
+  g_coarse[key] = std::move(t);
+  return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Workspace (per device), grown on demand
+// ---------------------------------------------------------------------------------------------
+struct Workspace {
+  DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf;
+  double* rhost = nullptr;
+  std::vector<cudaEvent_t> ev;
+  ~Workspace() {
+    if (rhost) cudaFreeHost(rhost);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+std::map<int, std::unique_ptr<Workspace>> g_ws;
+
+cudaError_t ensure(DevBuf& b, size_t bytes) {
+  if (b.bytes >= bytes) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e == cudaSuccess) b.bytes = bytes;
+  return e;
+}
+
+Workspace* workspace() {
+  auto& w = g_ws[cur_dev()];
+  if (!w) {
+    w = std::make_unique<Workspace>();
+    cudaMallocHost(&w->rhost, sizeof(double) * 8);
+    w->ev.resize(8);
+    for (auto& e : w->ev) cudaEventCreate(&e);
+  }
+  return w.get();
+}
+
+size_t state_doubles(int n) { return (size_t)3 * (n / 2 + 1) * 2; }
+
+int coarse_parts(int M) {
+  const int pairs = M / 2;  // sample pairs (2p+1, 2p+2), p < M/2
+  return pairs < 1 ? 1 : pairs;
+}
+
+// One coarse chain: states U[0..nsteps] (U[0] given), G[0..nsteps-1]; F may be null.
+struct Chain {
+  const rsw_params* p;
+  int scheme, M;
+  double dT;
+  rsw::AvgTab at;
+  rsw::CoarseArgs ca;
+};
+
+rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, double T0, int M, Workspace* ws,
+                       double* U, double* G, const double* F, double* rparts, int nsteps) {
+  GeomTables* g;
+  AvgTables* at;
+  CoarseTables* ct;
+  CUDA_TRY(get_geom(p, &g));
+  CUDA_TRY(get_avg(p, T0, M, &at));
+  CUDA_TRY(get_coarse(p, dT, &ct));
+  const int K = p->n / 3, Kc = 2 * K + 1, np = coarse_parts(M);
+  CUDA_TRY(ensure(ws->part, sizeof(double2) * (size_t)np * 3 * Kc));
+  CUDA_TRY(ensure(ws->vky, sizeof(double2) * 3 * 3 * (size_t)Kc));
+  ch.p = p;
+  ch.scheme = scheme;
+  ch.M = M;
+  ch.dT = dT;
+  ch.at = rsw::AvgTab{geom_of(g), (const double*)at->w.p, (const double2*)at->phase.p, (const double2*)g->tw.p};
+  rsw::CoarseArgs& ca = ch.ca;
+  ca.g = geom_of(g);
+  ca.part = (const double2*)ws->part.p;
+  ca.nparts = np;
+  ca.scheme = scheme;
+  ca.dT = dT;
+  ca.dhalf = (const double*)ct->dhalf.p;
+  ca.back = (const double2*)ct->back.p;
+  ca.v = (double2*)ws->vky.p;
+  ca.ks = ca.v + 3 * Kc;
+  ca.y = ca.v + 6 * Kc;
+  ca.U = U;
+  ca.G = G;
+  ca.F = F;
+  ca.rparts = rparts;
+  ca.n_end = nsteps;
+  return RSW_OK;
+}
+
+// Serial coarse sweep over the chain (Alg.4's serial loop): launches per slice n:
+// for each RK stage s: samples (sample-parallel N̄ partials) -> combine (stage update).
+rsw_status run_chain(const Chain& ch, cudaStream_t st, int64_t* launches) {
+  const int n = ch.p->n, nst = ch.scheme == 0 ? 4 : 2;
+  CUDA_TRY(rsw::launch_coarse_combine(n, ch.ca, 0, 0, st));
+  int64_t L = 1;
+  for (int s = 0; s < ch.ca.n_end; ++s) {
+    for (int stg = 1; stg <= nst; ++stg) {
+      CUDA_TRY(rsw::launch_coarse_samples(n, ch.ca.y, const_cast<double2*>(ch.ca.part), ch.ca.nparts, ch.M,
+                                          ch.at, st));
+      CUDA_TRY(rsw::launch_coarse_combine(n, ch.ca, stg, s, st));
+      L += 2;
+    }
+  }
+  if (launches) *launches += L;
+  return RSW_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// NCCL communicator (loaded at run time: torch's libnccl when torch is imported first)
+// ---------------------------------------------------------------------------------------------
+struct rsw_comm {
+  void* comm = nullptr;  // ncclComm_t
+  int rank = 0, world = 1;
+};
+
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+rsw_status load_nccl() {
+  if (g_nccl.h) return RSW_OK;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(RSW_ERR_NCCL, std::string("cannot load libnccl: ") + dlerror());
+  g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
+  g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.commDestroy || !g_nccl.allGather)
+    return fail(RSW_ERR_NCCL, "libnccl is missing symbols");
+  g_nccl.h = h;
+  return RSW_OK;
+}
+
+rsw_status nccl_fail(ncclResult_t r, const char* what) {
+  return fail(RSW_ERR_NCCL, std::string(what) + ": " + (g_nccl.errStr ? g_nccl.errStr(r) : "nccl error"));
+}
+}  // namespace
+
+extern "C" {
+
+const char* rsw_last_error(void) { return g_err.c_str(); }
+
+rsw_status rsw_shard_range(int32_t S, int32_t rank, int32_t world, int32_t* lo, int32_t* hi) {
+  if (!lo || !hi || S < 1 || world < 1 || rank < 0 || rank >= world || S % world != 0)
+    return fail(RSW_ERR_CONFIG, "invalid shard request (n_slices must be divisible by world)");
+  const int per = S / world;
+  *lo = rank * per;
+  *hi = *lo + per;
+  return RSW_OK;
+}
+
+double rsw_flops_per_unit(int32_t n, int32_t which) {
+  // F_N = 15 N log2 N + 3N + 46 K_r;  ETDRK4 = 4 F_N + 180 K_r;
+  // Strang = 2 F_N + 52 K_r;  one N̄ sample = F_N + 40 K_r   (K_r = floor(N/3) + 1)
+  const double N = n, Kr = n / 3 + 1, lg = std::log2(N);
+  const double FN = 15.0 * N * lg + 3.0 * N + 46.0 * Kr;
+  switch (which) {
+    case 0: return FN;
+    case 1: return 4.0 * FN + 180.0 * Kr;
+    case 2: return 2.0 * FN + 52.0 * Kr;
+    case 3: return FN + 40.0 * Kr;
+    default: return 0.0;
+  }
+}
+
+rsw_status rsw_nonlinear(const rsw_params* p, int32_t n_states, const double* u_in, double* out, void* stream) {
+  rsw_status s = check_params(p);
+  if (s != RSW_OK) return s;
+  if (n_states < 0) return fail(RSW_ERR_CONFIG, "n_states < 0");
+  if (n_states == 0) return RSW_OK;
+  if (!u_in || !out) return fail(RSW_ERR_CONFIG, "NULL state pointer");
+  if (u_in == out) return fail(RSW_ERR_CONFIG, "u_in and out must not alias");
+  std::lock_guard<std::mutex> lk(g_mu);
+  GeomTables* g;
+  CUDA_TRY(get_geom(p, &g));
+  rsw::FineTab tab{geom_of(g), nullptr, nullptr, (const double2*)g->tw.p};
+  CUDA_TRY(rsw::launch_nonlinear(p->n, u_in, out, n_states, tab, (cudaStream_t)stream));
+  return RSW_OK;
+}
+
+rsw_status rsw_fine_propagate(const rsw_params* p, int32_t scheme, uint32_t flags, double dT, double dt,
+                              int32_t n_slices, const double* u_in, double* u_out, void* stream) {
+  rsw_status s = check_params(p);
+  if (s != RSW_OK) return s;
+  if (scheme != RSW_FINE_ETDRK4 && scheme != RSW_FINE_STRANG) return fail(RSW_ERR_CONFIG, "unknown fine scheme");
+  if (flags & ~(uint32_t)RSW_FLAG_LINEAR_ONLY) return fail(RSW_ERR_CONFIG, "unknown flags");
+  if (!finite_pos(dT) || !finite_pos(dt) || dt > dT) return fail(RSW_ERR_CONFIG, "need 0 < dt <= dT");
+  if (n_slices < 0) return fail(RSW_ERR_CONFIG, "n_slices < 0");
+  if (n_slices == 0) return RSW_OK;
+  if (!u_in || !u_out) return fail(RSW_ERR_CONFIG, "NULL state pointer");
+  const int m = n_fine_steps(dT, dt);
+  const double h = dT / m;
+  std::lock_guard<std::mutex> lk(g_mu);
+  GeomTables* g;
+  FineTables* ft;
+  CUDA_TRY(get_geom(p, &g));
+  CUDA_TRY(get_fine(p, h, &ft));
+  rsw::FineTab tab{geom_of(g), (const double2*)ft->cp.p, (const double*)ft->c0.p, (const double2*)g->tw.p};
+  CUDA_TRY(rsw::launch_fine(p->n, scheme, (flags & RSW_FLAG_LINEAR_ONLY) != 0, u_in, u_out, n_slices, m, h, tab,
+                            (cudaStream_t)stream));
+  return RSW_OK;
+}
+
+rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n_states, const double* u_in,
+                            double* rhs_out, void* stream) {
+  rsw_status s = check_params(p);
+  if (s != RSW_OK) return s;
+  if (!finite_pos(T0)) return fail(RSW_ERR_CONFIG, "T0 must be finite and > 0");
+  if (M < 2) return fail(RSW_ERR_CONFIG, "M must be >= 2");
+  if (n_states < 0) return fail(RSW_ERR_CONFIG, "n_states < 0");
+  if (n_states == 0) return RSW_OK;
+  if (!u_in || !rhs_out) return fail(RSW_ERR_CONFIG, "NULL state pointer");
+  if (u_in == rhs_out) return fail(RSW_ERR_CONFIG, "u_in and rhs_out must not alias");
+  std::lock_guard<std::mutex> lk(g_mu);
+  GeomTables* g;
+  AvgTables* at;
+  CUDA_TRY(get_geom(p, &g));
+  CUDA_TRY(get_avg(p, T0, M, &at));
+  rsw::AvgTab tab{geom_of(g), (const double*)at->w.p, (const double2*)at->phase.p, (const double2*)g->tw.p};
+  CUDA_TRY(rsw::launch_avg_states(p->n, u_in, rhs_out, n_states, M, tab, (cudaStream_t)stream));
+  return RSW_OK;
+}
+
+rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, double dT, double T0, int32_t M,
+                                int32_t n_states, const double* u_in, double* u_out, void* stream) {
+  rsw_status s = check_params(p);
+  if (s != RSW_OK) return s;
+  if (coarse_scheme != RSW_COARSE_RK4 && coarse_scheme != RSW_COARSE_MIDPOINT)
+    return fail(RSW_ERR_CONFIG, "unknown coarse scheme");
+  if (!finite_pos(dT) || !finite_pos(T0)) return fail(RSW_ERR_CONFIG, "dT and T0 must be finite and > 0");
+  if (M < 2) return fail(RSW_ERR_CONFIG, "M must be >= 2");
+  if (n_states < 0) return fail(RSW_ERR_CONFIG, "n_states < 0");
+  if (n_states == 0) return RSW_OK;
+  if (!u_in || !u_out) return fail(RSW_ERR_CONFIG, "NULL state pointer");
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace* ws = workspace();
+  const size_t L = state_doubles(p->n);
+  CUDA_TRY(ensure(ws->Ubuf, sizeof(double) * 2 * L));
+  CUDA_TRY(ensure(ws->Gbuf, sizeof(double) * L));
+  double* Ut = (double*)ws->Ubuf.p;
+  Chain ch;
+  s = setup_chain(ch, p, coarse_scheme, dT, T0, M, ws, Ut, (double*)ws->Gbuf.p, nullptr, nullptr, 1);
+  if (s != RSW_OK) return s;
+  for (int i = 0; i < n_states; ++i) {
+    CUDA_TRY(cudaMemcpyAsync(Ut, u_in + i * L, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
+    s = run_chain(ch, st, nullptr);
+    if (s != RSW_OK) return s;
+    CUDA_TRY(cudaMemcpyAsync(u_out + i * L, Ut + L, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
+  }
+  return RSW_OK;
+}
+
+rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
+                               double* resid_hist, int32_t* iters_done, rsw_comm* comm, void* stream,
+                               double* F_out, double* G_out, rsw_parareal_stats* stats) {
+  rsw_status s = check_params(p);
+  if (s != RSW_OK) return s;
+  if (!cfg) return fail(RSW_ERR_CONFIG, "cfg is NULL");
+  if (!finite_pos(cfg->dT) || !finite_pos(cfg->dt) || cfg->dt > cfg->dT)
+    return fail(RSW_ERR_CONFIG, "need 0 < dt <= dT");
+  if (!finite_pos(cfg->T0)) return fail(RSW_ERR_CONFIG, "T0 must be finite and > 0");
+  if (cfg->M < 2) return fail(RSW_ERR_CONFIG, "M must be >= 2");
+  const int S = cfg->n_slices;
+  if (S < 1) return fail(RSW_ERR_CONFIG, "n_slices must be >= 1");
+  if (cfg->max_iters < 0 || cfg->max_iters > S) return fail(RSW_ERR_CONFIG, "need 0 <= max_iters <= n_slices");
+  if (cfg->fine_scheme != RSW_FINE_ETDRK4 && cfg->fine_scheme != RSW_FINE_STRANG)
+    return fail(RSW_ERR_CONFIG, "unknown fine scheme");
+  if (cfg->coarse_scheme != RSW_COARSE_RK4 && cfg->coarse_scheme != RSW_COARSE_MIDPOINT)
+    return fail(RSW_ERR_CONFIG, "unknown coarse scheme");
+  if (!u0 || !U || !iters_done || (cfg->max_iters > 0 && !resid_hist))
+    return fail(RSW_ERR_CONFIG, "NULL pointer argument");
+  const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
+  int32_t lo, hi;
+  if ((s = rsw_shard_range(S, rank, world, &lo, &hi)) != RSW_OK) return s;
+
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace* ws = workspace();
+  const int n = p->n, K = n / 3;
+  const size_t L = state_doubles(n);
+  const int m = n_fine_steps(cfg->dT, cfg->dt);
+  const double h = cfg->dT / m;
+  GeomTables* g;
+  FineTables* ft;
+  CUDA_TRY(get_geom(p, &g));
+  CUDA_TRY(get_fine(p, h, &ft));
+  rsw::FineTab ftab{geom_of(g), (const double2*)ft->cp.p, (const double*)ft->c0.p, (const double2*)g->tw.p};
+  CUDA_TRY(ensure(ws->F, sizeof(double) * L * S));
+  CUDA_TRY(ensure(ws->G, sizeof(double) * L * S));
+  CUDA_TRY(ensure(ws->rparts, sizeof(double) * 2 * (size_t)S * (K + 1)));
+  CUDA_TRY(ensure(ws->rdev, sizeof(double) * 2));
+  double* F = (double*)ws->F.p;
+  double* G = (double*)ws->G.p;
+  int64_t launches = 0;
+  double fine_ms = 0, comm_ms = 0, coarse_ms = 0;
+  cudaEvent_t* ev = ws->ev.data();
+  CUDA_TRY(cudaEventRecord(ev[6], st));
+
+  // k = 0: U_0 = u0, U_{n+1} = G(U_n)   (Alg.4)
+  if (U != u0) CUDA_TRY(cudaMemcpyAsync(U, u0, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
+  Chain ch0;
+  if ((s = setup_chain(ch0, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, nullptr, nullptr, S)))
+    return s;
+  CUDA_TRY(cudaEventRecord(ev[0], st));
+  if ((s = run_chain(ch0, st, &launches))) return s;
+  CUDA_TRY(cudaEventRecord(ev[1], st));
+  {
+    float ms;
+    CUDA_TRY(cudaEventSynchronize(ev[1]));
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    coarse_ms += ms;
+  }
+  Chain ch;
+  if ((s = setup_chain(ch, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, F, (double*)ws->rparts.p,
+                       S)))
+    return s;
+  rsw_status status = (cfg->tol > 0 && cfg->max_iters > 0) ? RSW_NOT_CONVERGED : RSW_OK;
+  int done = 0;
+  int64_t fine_steps = 0;
+  for (int k = 1; k <= cfg->max_iters; ++k) {
+    // parfor n: F_n = φ(U^{k-1}_n) on this rank's shard
+    CUDA_TRY(cudaEventRecord(ev[0], st));
+    CUDA_TRY(rsw::launch_fine(n, cfg->fine_scheme, false, U + (size_t)lo * L, F + (size_t)lo * L, hi - lo, m, h,
+                              ftab, st));
+    ++launches;
+    fine_steps += (int64_t)(hi - lo) * m;
+    CUDA_TRY(cudaEventRecord(ev[1], st));
+    if (comm && world > 1) {
+      ncclResult_t r = g_nccl.allGather(F + (size_t)lo * L, F, (size_t)(hi - lo) * L, ncclDouble,
+                                        (ncclComm_t)comm->comm, st);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+    }
+    CUDA_TRY(cudaEventRecord(ev[2], st));
+    // serial sweep: U^k_{n+1} = G(U^k_n) + (F_n - G_n)
+    if ((s = run_chain(ch, st, &launches))) return s;
+    CUDA_TRY(rsw::launch_resid_max((const double*)ws->rparts.p, S, K + 1, (double*)ws->rdev.p, nullptr, st));
+    ++launches;
+    CUDA_TRY(cudaEventRecord(ev[3], st));
+    CUDA_TRY(cudaMemcpyAsync(ws->rhost, ws->rdev.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    float a, b, c;
+    CUDA_TRY(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    CUDA_TRY(cudaEventElapsedTime(&b, ev[1], ev[2]));
+    CUDA_TRY(cudaEventElapsedTime(&c, ev[2], ev[3]));
+    fine_ms += a;
+    comm_ms += b;
+    coarse_ms += c;
+    const double r = ws->rhost[0];
+    resid_hist[k - 1] = r;
+    done = k;
+    if (!std::isfinite(r) || r > 1e6) {
+      status = fail(RSW_ERR_DIVERGED, "parareal residual non-finite or > 1e6");
+      break;
+    }
+    if (cfg->tol > 0 && r < cfg->tol) {
+      status = RSW_OK;
+      break;
+    }
+  }
+  *iters_done = done;
+  if (F_out) CUDA_TRY(cudaMemcpyAsync(F_out, F, sizeof(double) * L * S, cudaMemcpyDeviceToDevice, st));
+  if (G_out) CUDA_TRY(cudaMemcpyAsync(G_out, G, sizeof(double) * L * S, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaEventRecord(ev[7], st));
+  if (stats) {
+    float tot;
+    CUDA_TRY(cudaEventSynchronize(ev[7]));
+    CUDA_TRY(cudaEventElapsedTime(&tot, ev[6], ev[7]));
+    stats->fine_ms = fine_ms;
+    stats->comm_ms = comm_ms;
+    stats->coarse_ms = coarse_ms;
+    stats->total_ms = tot;
+    stats->fine_slice_steps = fine_steps;
+    stats->kernel_launches = launches;
+  }
+  if (status == RSW_NOT_CONVERGED) g_err = "parareal: tolerance not reached within max_iters";
+  return status;
+}
+
+rsw_status parareal_iterate(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
+                            double* resid_hist, int32_t* iters_done, rsw_comm* comm, void* stream) {
+  return parareal_iterate_ex(p, cfg, u0, U, resid_hist, iters_done, comm, stream, nullptr, nullptr, nullptr);
+}
+
+rsw_status rsw_nccl_unique_id(void* out128) {
+  if (!out128) return fail(RSW_ERR_CONFIG, "NULL id buffer");
+  rsw_status s = load_nccl();
+  if (s != RSW_OK) return s;
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.getUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(out128, &id, sizeof(id));
+  return RSW_OK;
+}
+
+rsw_status rsw_comm_init(const void* id128, int32_t rank, int32_t world, rsw_comm** out) {
+  if (!id128 || !out || world < 1 || rank < 0 || rank >= world) return fail(RSW_ERR_CONFIG, "invalid comm args");
+  rsw_status s = load_nccl();
+  if (s != RSW_OK) return s;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ncclComm_t c;
+  ncclResult_t r = g_nccl.commInitRank(&c, world, id, rank);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+  rsw_comm* cm = new rsw_comm;
+  cm->comm = c;
+  cm->rank = rank;
+  cm->world = world;
+  *out = cm;
+  return RSW_OK;
+}
+
+rsw_status rsw_comm_destroy(rsw_comm* comm) {
+  if (!comm) return RSW_OK;
+  if (comm->comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)comm->comm);
+  delete comm;
+  return RSW_OK;
+}
+
+rsw_status rsw_fp64_peak(double* tflops, void* stream) {
+  if (!tflops) return fail(RSW_ERR_CONFIG, "NULL output");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev, sms;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* d;
+  CUDA_TRY(cudaMalloc(&d, sizeof(double)));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, iters = 4096;
+  rsw::launch_dfma_peak(d, blocks, 64, st);  // warm-up
+  cudaEventRecord(e0, st);
+  rsw::launch_dfma_peak(d, blocks, iters, st);
+  cudaEventRecord(e1, st);
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(RSW_ERR_CUDA, cudaGetErrorString(e));
+  const double flops = 2.0 * blocks * 256.0 * iters * 16.0 * 8.0;
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  return RSW_OK;
+}
+
+void rsw_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_geom.clear();
+  g_fine.clear();
+  g_avg.clear();
+  g_coarse.clear();
+  g_ws.clear();
+}
+
+}  // extern "C"

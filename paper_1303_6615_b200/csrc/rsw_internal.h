@@ -1,0 +1,61 @@
+// rsw_internal.h — internal structs shared by the kernels (rsw_kernels.cu) and the host library
+// (rsw_capi.cu).  Not part of the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rsw_device.cuh"
+
+namespace rsw {
+
+// ETDRK4 / Strang per-mode diagonal coefficients in the eigenbasis (K6 host tables):
+//   cp[i][|κ|] : α=+1 value (complex), α=-1 is its conjugate;  c0[i][|κ|] : α=0 value (real)
+//   i = 0 E=e^{z}, 1 E2=e^{z/2}, 2 Q=(h/2)φ1(z/2), 3 f1=h(φ1-3φ2+4φ3)(z), 4 f2=h(2φ2-4φ3)(z),
+//   5 f3=h(4φ3-φ2)(z);  z = h λ_α,  λ_α = -iαω/ε - μκ^4.
+struct FineTab {
+  ModeGeom g;
+  const double2* cp;
+  const double* c0;
+  const double2* tw;  // e^{-2πi m/N}, m = 0..N-1
+};
+
+// Averaging tables: w[m] (m = 0..M-1, w[0] = 0), phase[m][|κ|] = e^{iω_κ τ_m} (m = 0..M)
+struct AvgTab {
+  ModeGeom g;
+  const double* w;
+  const double2* phase;
+  const double2* tw;
+};
+
+// Arguments of the coarse combine kernel (one state chain)
+struct CoarseArgs {
+  ModeGeom g;
+  const double2* part;  // [nparts][3][Kc]
+  int nparts;
+  int scheme;           // 0 RK4, 1 midpoint
+  double dT;
+  const double* dhalf;  // e^{-μκ^4 ΔT/2}
+  const double2* back;  // e^{-iω ΔT/ε}
+  double2* v;           // [3][Kc]
+  double2* ks;          // [3][Kc]
+  double2* y;           // [3][Kc]
+  double* U;            // [S+1][3][N/2+1][2] (chain states)
+  double* G;            // [S][3][N/2+1][2]
+  const double* F;      // [S][...] or null (k = 0 sweep / plain coarse step)
+  double* rparts;       // [S][K+1][2] residual partials or null
+  int n_end;            // number of chain steps (S)
+};
+
+cudaError_t launch_fine(int n, int scheme, bool lin, const double* in, double* out, int S, int m, double h,
+                        const FineTab& tab, cudaStream_t st);
+cudaError_t launch_nonlinear(int n, const double* in, double* out, int S, const FineTab& tab, cudaStream_t st);
+cudaError_t launch_avg_states(int n, const double* in, double* out, int S, int M, const AvgTab& tab,
+                              cudaStream_t st);
+cudaError_t launch_coarse_samples(int n, const double2* y, double2* part, int nparts, int M, const AvgTab& tab,
+                                  cudaStream_t st);
+cudaError_t launch_coarse_combine(int n, const CoarseArgs& ca, int stage, int slice, cudaStream_t st);
+cudaError_t launch_resid_max(const double* rparts, int S, int Kp1, double* r_out, double* per_slice,
+                             cudaStream_t st);
+cudaError_t launch_dfma_peak(double* out, int blocks, int iters, cudaStream_t st);
+
+}  // namespace rsw

@@ -1,0 +1,131 @@
+"""GPU (librsw.so, sm_100a) vs CPU oracle parity on identical seeded inputs:
+relative weighted L2 (R12) <= 1e-10 per state / slice endpoint / iterate, identical iteration
+counts.  Every call goes through the C-ABI (paper_1303_6615_b200 is a ctypes binding)."""
+import numpy as np
+import pytest
+
+from paper_1303_6615_b200 import inputs
+from tests.helpers import rel_l2, to_np
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def P(rsw, eps, F, mu, n):
+    return rsw.Params(eps, F, mu, n)
+
+
+@pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512, 1024])
+def test_nonlinear(rsw_gpu, orc, n):
+    u = inputs.random_states(n, 3, seed=n, decay=1.0)  # odd batch: exercises the dummy pair slot
+    got = to_np(rsw_gpu.nonlinear(P(rsw_gpu, 1e-2, 1.0, 1e-4, n), dev(u)))
+    ref = orc.nonlinear(u, 1e-2, 1.0, 1e-4, n)
+    err = rel_l2(got, ref, n)
+    assert err.max() < 1e-12, err
+    assert np.all(got[:, :, n // 3 + 1:, :] == 0.0)
+    assert np.all(got[:, :, 0, 1] == 0.0)
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_fine_c1(rsw_gpu, orc, scheme):
+    w = inputs.C1
+    u = np.stack([inputs.initial_state(w, seed=s) for s in range(5)])
+    got = to_np(rsw_gpu.fine_propagate(P(rsw_gpu, w.eps, w.F, w.mu, w.n), dev(u), w.dT, w.dt, scheme))
+    ref = orc.fine_propagate(u, w.eps, w.F, w.mu, w.n, w.dT, w.dt, scheme)
+    err = rel_l2(got, ref, w.n)
+    assert err.max() < TOL, err
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("n,eps,mu,dt,steps", [(128, 1e-2, 1e-4, 5e-4, 40), (256, 1e-3, 1e-5, 1e-4, 25),
+                                               (512, 1e-3, 1e-5, 1e-4, 6), (1024, 1e-4, 1e-6, 2e-5, 4)])
+def test_fine_sizes(rsw_gpu, orc, scheme, n, eps, mu, dt, steps):
+    u = inputs.random_states(n, 3, seed=7, kmax=min(64, n // 3))
+    dT = steps * dt * 0.99  # non-integer dT/dt: ceil rule R9
+    got = to_np(rsw_gpu.fine_propagate(P(rsw_gpu, eps, 1.0, mu, n), dev(u), dT, dt, scheme))
+    ref = orc.fine_propagate(u, eps, 1.0, mu, n, dT, dt, scheme)
+    err = rel_l2(got, ref, n)
+    assert err.max() < TOL, err
+
+
+def test_fine_linear_only(rsw_gpu, orc):
+    n = 128
+    u = inputs.random_states(n, 4, seed=3)
+    got = to_np(rsw_gpu.fine_propagate(P(rsw_gpu, 1e-2, 1.0, 1e-4, n), dev(u), 0.1, 1e-3, 0,
+                                       flags=rsw_gpu.FLAG_LINEAR_ONLY))
+    ref = orc.fine_propagate(u, 1e-2, 1.0, 1e-4, n, 0.1, 1e-3, 0, flags=1)
+    assert rel_l2(got, ref, n).max() < 1e-12
+
+
+def test_fine_in_place(rsw_gpu, orc):
+    w = inputs.C1
+    u = np.stack([inputs.initial_state(w, seed=s) for s in range(3)])
+    t = dev(u)
+    rsw_gpu.fine_propagate(P(rsw_gpu, w.eps, w.F, w.mu, w.n), t, w.dT, w.dt, 0, out=t)
+    ref = orc.fine_propagate(u, w.eps, w.F, w.mu, w.n, w.dT, w.dt, 0)
+    assert rel_l2(to_np(t), ref, w.n).max() < TOL
+
+
+@pytest.mark.parametrize("n,eps,T0,M", [(64, 1e-2, 0.05, 32), (128, 1e-2, 0.05, 64), (256, 1e-3, 0.01, 128),
+                                        (512, 1e-3, 0.01, 256)])
+def test_averaged_rhs(rsw_gpu, orc, n, eps, T0, M):
+    nb = 3 if n < 512 else 2
+    u = inputs.random_states(n, nb, seed=11)
+    got = to_np(rsw_gpu.averaged_rhs(P(rsw_gpu, eps, 1.0, 1e-5, n), dev(u), T0, M))
+    ref = orc.averaged_rhs(u, eps, 1.0, 1e-5, n, T0, M)
+    assert rel_l2(got, ref, n).max() < TOL
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("wname", ["C1", "C3"])
+def test_coarse(rsw_gpu, orc, scheme, wname):
+    w = inputs.WORKLOADS[wname]
+    u = np.stack([inputs.initial_state(w, seed=s) for s in range(2)])
+    got = to_np(rsw_gpu.coarse_propagate(P(rsw_gpu, w.eps, w.F, w.mu, w.n), dev(u), w.dT, w.T0, w.M, scheme))
+    ref = orc.coarse_propagate(u, w.eps, w.F, w.mu, w.n, w.dT, w.T0, w.M, scheme)
+    assert rel_l2(got, ref, w.n).max() < TOL
+
+
+def _parareal_both(rsw, orc, w, seed=0, max_iters=None, tol=None):
+    u0 = inputs.initial_state(w, seed=seed)
+    mi = w.max_iters if max_iters is None else max_iters
+    tl = w.tol if tol is None else tol
+    g = rsw.parareal_iterate(P(rsw, w.eps, w.F, w.mu, w.n), dev(u0), dT=w.dT, dt=w.dt, T0=w.T0, M=w.M,
+                             n_slices=w.n_slices, max_iters=mi, tol=tl, want_FG=True)
+    r = orc.parareal(u0, w.eps, w.F, w.mu, w.n, dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices,
+                     max_iters=mi, tol=tl, want_FG=True)
+    return g, r
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 4])
+def test_parareal_c1_every_iterate(rsw_gpu, orc, k):
+    w = inputs.C1
+    g, r = _parareal_both(rsw_gpu, orc, w, max_iters=k)
+    assert g["iters"] == r["iters"] == k
+    err = rel_l2(to_np(g["U"]), r["U"], w.n)
+    assert err[1:].max() < TOL, err
+    assert np.array_equal(to_np(g["U"])[0], inputs.initial_state(w))
+    if k:
+        assert np.allclose(g["resid"], r["resid"], rtol=1e-8, atol=0)
+        assert rel_l2(to_np(g["F"]), r["F"], w.n).max() < TOL
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_parareal_c1_seeds(rsw_gpu, orc, seed):
+    g, r = _parareal_both(rsw_gpu, orc, inputs.C1, seed=seed)
+    assert rel_l2(to_np(g["U"]), r["U"], 64)[1:].max() < TOL
+    assert np.allclose(g["resid"], r["resid"], rtol=1e-8, atol=0)
+
+
+def test_parareal_c1_strang_midpoint(rsw_gpu, orc):
+    w = inputs.C1
+    u0 = inputs.initial_state(w)
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=3, fine_scheme=1, coarse_scheme=1)
+    g = rsw_gpu.parareal_iterate(P(rsw_gpu, w.eps, w.F, w.mu, w.n), dev(u0), **kw)
+    r = orc.parareal(u0, w.eps, w.F, w.mu, w.n, **kw)
+    assert rel_l2(to_np(g["U"]), r["U"], w.n)[1:].max() < TOL
