@@ -1,0 +1,266 @@
+#!/usr/bin/env python
+"""bench.py — fp64 RSW fine slice-steps/s and parareal time-to-solution on B200 (BASELINE.json).
+
+One bench "step" = one complete asymptotic-parareal solve of the workload (the k = 0 coarse sweep,
+then `max_iters` iterations of: fine sweep on this rank's slices -> NCCL all-gather of the slice
+endpoints -> serial coarse sweep with the fused parareal update -> residual), i.e. one pass of every
+SURVEY.md §8(a) row, with u0 resident in HBM.  value = fine slice-steps of the whole job / time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl rsw|reference]
+  (N > 1: launched by torch.distributed.run, one rank per GPU, NCCL)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1303_6615_b200 import inputs  # noqa: E402
+
+METRIC = "fp64 RSW fine slice-steps/s and parareal time-to-solution"
+UNIT = "slice-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--impl", default="rsw", choices=["rsw", "reference"])
+    ap.add_argument("--fine-scheme", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=0, help="oracle sample: steps per slice")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()),
+                                   default=None)}
+
+
+# ---------------------------------------------------------------------------------------------
+def cpu_baseline(w, steps_per_slice: int = 0):
+    """The CPU oracle, as it stands, timed on this host's cores on a bounded sample of the workload:
+    its fine sweep (ETDRK4, OpenMP over slices) on `cores` slices x `steps` fine steps."""
+    import numpy as np
+    import oracle
+    oracle.build()
+    cores = oracle.num_threads()
+    steps = steps_per_slice or {64: 125, 128: 125, 256: 60, 1024: 12}.get(w.n, 20)
+    u0 = inputs.initial_state(w)
+    u = np.repeat(u0[None], cores, axis=0)
+    dT = steps * w.dt_eff
+    t0 = time.perf_counter()
+    oracle.fine_propagate(u, w.eps, w.F, w.mu, w.n, dT, w.dt_eff * (1 + 1e-12), 0)
+    dt = time.perf_counter() - t0
+    return {"value": cores * steps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"oracle ETDRK4 fine sweep, {cores} slices x {steps} steps of {w.name} "
+                      f"(n={w.n}), {dt:.1f} s wall"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = inputs.WORKLOADS[args.config]
+    vals = []
+    for i in range(args.warmup + args.steps):
+        b = cpu_baseline(w, args.cpu_sample_steps or {1024: 4}.get(w.n, 0))
+        if i >= args.warmup:
+            vals.append(b["value"])
+    v = statistics.median(vals)
+    b["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "n": w.n, "slices": w.n_slices, "note": "oracle fine sweep sample"},
+            "cpu_baseline": b, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                                       "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1303_6615_b200 as rsw
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = rsw.Comm.from_torch_distributed()
+    rsw.load()
+    w = inputs.WORKLOADS[args.config]
+    p = rsw.Params(w.eps, w.F, w.mu, w.n)
+    u0_host = torch.from_numpy(inputs.initial_state(w)).pin_memory()
+    u0 = u0_host.cuda()
+    U = torch.empty((w.n_slices + 1,) + w.state_shape, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")  # > 126 MB L2
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=w.max_iters, tol=w.tol,
+              fine_scheme=args.fine_scheme, comm=comm, U=U)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        res = rsw.parareal_iterate(p, u0, **kw)
+    barrier()
+
+    # ---- timed region: K whole solves, device events on the launching (current) stream
+    stream = torch.cuda.current_stream()
+    per = []
+    stats = []
+    launches = 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = rsw.parareal_iterate(p, u0, **kw)
+            e1.record(stream)
+            e1.synchronize()
+            per.append(e0.elapsed_time(e1))
+            stats.append(res["stats"])
+            launches += res["stats"]["kernel_launches"]
+        barrier()
+    ms = statistics.median(per)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    iters = res["iters"]
+    total_slice_steps = iters * w.n_slices * w.m_fine  # all ranks together
+    value = total_slice_steps / (ms_max * 1e-3)
+
+    # fine kernel roofline (dominant-by-FLOP kernel; its share of the step is reported beside it)
+    fine_ms = statistics.median(s["fine_ms"] for s in stats) / max(iters, 1)   # per launch
+    coarse_ms = statistics.median(s["coarse_ms"] for s in stats)
+    comm_ms = statistics.median(s["comm_ms"] for s in stats)
+    f_step = rsw.flops_per_unit(w.n, "etdrk4" if args.fine_scheme == 0 else "strang")
+    local_slices = w.n_slices // world
+    fine_flops = local_slices * w.m_fine * f_step
+    achieved_tf = fine_flops / (fine_ms * 1e-3) / 1e12
+    nominal_peak = 148 * 64 * 2 * 1965e6 / 1e12  # FP64 FMA units x clock
+    measured_peak = rsw.fp64_peak_tflops()
+
+    # ---- e2e: same solve through the C-ABI from pinned host buffers, H2D + D2H inside the region
+    U_host = torch.empty(U.shape, dtype=torch.float64).pin_memory()
+    e2e = []
+    for _ in range(max(1, args.steps)):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        u0d = u0_host.to("cuda", non_blocking=True)
+        rsw.parareal_iterate(p, u0d, **kw)
+        U_host.copy_(U, non_blocking=True)
+        e1.record(stream)
+        e1.synchronize()
+        e2e.append(e0.elapsed_time(e1))
+    t = torch.tensor([statistics.median(e2e)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "n": w.n, "slices": w.n_slices, "fine_steps_per_slice": w.m_fine,
+                       "dt_eff": w.dt_eff, "iterations": iters, "M": w.M, "T0": w.T0, "eps": w.eps,
+                       "fine_scheme": "ETDRK4" if args.fine_scheme == 0 else "Strang",
+                       "parallelism": f"slices sharded over {world} GPU(s), NCCL all-gather, replicated coarse",
+                       "l2": "flushed (256 MB write) before every timed step"},
+            "time_to_solution_ms": ms_max,
+            "phases_ms": {"fine": statistics.median(s["fine_ms"] for s in stats), "allgather": comm_ms,
+                          "coarse": coarse_ms, "total_library": statistics.median(s["total_ms"] for s in stats)},
+            "fine_kernel_slice_steps_per_s": local_slices * w.m_fine / (fine_ms * 1e-3) * world,
+            "roofline": {"bound": "alu", "kernel": "k_fine (ETDRK4 fine sweep)", "achieved": achieved_tf,
+                         "peak": nominal_peak, "unit": "TFLOP/s", "frac": achieved_tf / nominal_peak,
+                         "traffic": None, "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz",
+                         "peak_measured_dfma": measured_peak, "frac_of_measured": achieved_tf / measured_peak,
+                         "flops_per_launch": fine_flops,
+                         "share_of_step": statistics.median(s["fine_ms"] for s in stats) / ms_max},
+            "clocks": clk.summary(),
+            "e2e": {"value": total_slice_steps / (e2e_ms * 1e-3), "unit": UNIT, "ms": e2e_ms,
+                    "h2d_bytes_per_step": u0_host.numel() * 8, "d2h_bytes_per_step": U_host.numel() * 8},
+            "gpu_launches": launches,
+            "resid": res["resid"],
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(w, args.cpu_sample_steps)
+        print(json.dumps(line), flush=True)
+    if comm:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
