@@ -34,7 +34,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C5"])
     ap.add_argument("--impl", default="rsw", choices=["rsw", "reference"])
     ap.add_argument("--fine-scheme", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

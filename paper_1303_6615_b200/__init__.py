@@ -202,7 +202,7 @@ def shard_range(n_slices: int, rank: int, world: int):
 
 def parareal_iterate(p: Params, u0, *, dT, dt, T0, M, n_slices, max_iters, tol=0.0,
                      fine_scheme=FINE_ETDRK4, coarse_scheme=COARSE_RK4, comm: Comm | None = None,
-                     U=None, want_FG=False):
+                     U=None, want_FG=False, allow_diverged=False):
     """Asymptotic parareal (Eq. HMM parareal iteration P:428-430, Alg.4).
     Returns dict(U, resid, iters, status, stats[, F, G])."""
     import torch
@@ -219,7 +219,7 @@ def parareal_iterate(p: Params, u0, *, dT, dt, T0, M, n_slices, max_iters, tol=0
                                     resid, ctypes.byref(it), comm.handle if comm else None, _stream(),
                                     ctypes.c_void_p(F.data_ptr()) if want_FG else None,
                                     ctypes.c_void_p(G.data_ptr()) if want_FG else None, ctypes.byref(st))
-    _check(rc, ok=(RSW_OK, RSW_NOT_CONVERGED))
+    _check(rc, ok=(RSW_OK, RSW_NOT_CONVERGED) + ((RSW_ERR_DIVERGED,) if allow_diverged else ()))
     out = dict(U=U, resid=[resid[i] for i in range(it.value)], iters=it.value, status=rc,
                stats=dict(fine_ms=st.fine_ms, comm_ms=st.comm_ms, coarse_ms=st.coarse_ms,
                           total_ms=st.total_ms, fine_slice_steps=st.fine_slice_steps,
