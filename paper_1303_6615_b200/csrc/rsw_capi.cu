@@ -257,7 +257,7 @@ cudaError_t get_coarse(const rsw_params* p, double dT, CoarseTables** out) {
 // Workspace (per device), grown on demand
 // ---------------------------------------------------------------------------------------------
 struct Workspace {
-  DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf;
+  DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof;
   double* rhost = nullptr;
   std::vector<cudaEvent_t> ev;
   ~Workspace() {
@@ -290,9 +290,13 @@ Workspace* workspace() {
 
 size_t state_doubles(int n) { return (size_t)3 * (n / 2 + 1) * 2; }
 
-int coarse_parts(int M) {
-  const int pairs = M / 2;  // sample pairs (2p+1, 2p+2), p < M/2
-  return pairs < 1 ? 1 : pairs;
+int coarse_parts(int M, int n) {
+  // partial sums: one per CTA of the coarse sweep (>= the sample pairs (2p+1, 2p+2), p < M/2,
+  // and >= (K+1)/16 so that each CTA owns at most 16 modes); bounded by the SM count
+  int parts = M / 2;
+  const int need = (n / 3 + 1 + 15) / 16;
+  if (parts < need) parts = need;
+  return parts < 1 ? 1 : parts;
 }
 
 // One coarse chain: states U[0..nsteps] (U[0] given), G[0..nsteps-1]; F may be null.
@@ -312,7 +316,7 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   CUDA_TRY(get_geom(p, &g));
   CUDA_TRY(get_avg(p, T0, M, &at));
   CUDA_TRY(get_coarse(p, dT, &ct));
-  const int K = p->n / 3, Kc = 2 * K + 1, np = coarse_parts(M);
+  const int K = p->n / 3, Kc = 2 * K + 1, np = coarse_parts(M, p->n);
   CUDA_TRY(ensure(ws->part, sizeof(double2) * (size_t)np * 3 * Kc));
   CUDA_TRY(ensure(ws->vky, sizeof(double2) * 3 * 3 * (size_t)Kc));
   ch.p = p;
@@ -336,24 +340,43 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   ca.F = F;
   ca.rparts = rparts;
   ca.n_end = nsteps;
+  ca.prof = nullptr;
   return RSW_OK;
 }
 
-// Serial coarse sweep over the chain (Alg.4's serial loop): launches per slice n:
-// for each RK stage s: samples (sample-parallel N̄ partials) -> combine (stage update).
-rsw_status run_chain(const Chain& ch, cudaStream_t st, int64_t* launches) {
-  const int n = ch.p->n, nst = ch.scheme == 0 ? 4 : 2;
-  CUDA_TRY(rsw::launch_coarse_combine(n, ch.ca, 0, 0, st));
-  int64_t L = 1;
-  for (int s = 0; s < ch.ca.n_end; ++s) {
-    for (int stg = 1; stg <= nst; ++stg) {
-      CUDA_TRY(rsw::launch_coarse_samples(n, ch.ca.y, const_cast<double2*>(ch.ca.part), ch.ca.nparts, ch.M,
-                                          ch.at, st));
-      CUDA_TRY(rsw::launch_coarse_combine(n, ch.ca, stg, s, st));
-      L += 2;
-    }
+// Serial coarse sweep over the chain (Alg.4's serial loop): one persistent cooperative
+// launch runs every slice's coarse step (sample-parallel N̄, grid barriers between stages).
+rsw_status run_chain(const Chain& ch, Workspace* ws, double* r_out, cudaStream_t st, int64_t* launches) {
+  CUDA_TRY(ensure(ws->bar, 2 * sizeof(unsigned)));
+  int grid = 0;
+  static const bool prof = getenv("RSW_PROFILE_COARSE") != nullptr;
+  rsw::CoarseArgs ca = ch.ca;
+  ca.prof = nullptr;
+  if (prof) {
+    CUDA_TRY(ensure(ws->prof, 64 * 4 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(ws->prof.p, 0, 64 * 4 * sizeof(unsigned long long), st));
+    ca.prof = (unsigned long long*)ws->prof.p;
   }
-  if (launches) *launches += L;
+  CUDA_TRY(rsw::launch_coarse_sweep(ch.p->n, ca, ch.at, ch.M, (unsigned*)ws->bar.p, r_out, &grid, st));
+  if (launches) *launches += 1;
+  if (prof) {  // debug: mean phase durations over the first 64 stages (CTA 0), to stderr
+    unsigned long long h[256];
+    CUDA_TRY(cudaMemcpyAsync(h, ws->prof.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    double a = 0, b = 0, c = 0, d = 0;
+    int cnt = 0;
+    for (int i = 0; i + 1 < 64; ++i) {
+      if (!h[(i + 1) * 4]) break;
+      a += h[i * 4 + 1] - h[i * 4];
+      b += h[i * 4 + 2] - h[i * 4 + 1];
+      c += h[i * 4 + 3] - h[i * 4 + 2];
+      d += h[(i + 1) * 4] - h[i * 4 + 3];
+      ++cnt;
+    }
+    if (cnt)
+      fprintf(stderr, "[rsw coarse n=%d grid=%d] per stage (ns): samples %.0f  barrier1 %.0f  update %.0f  barrier2 %.0f\n",
+              ch.p->n, grid, a / cnt, b / cnt, c / cnt, d / cnt);
+  }
   return RSW_OK;
 }
 
@@ -507,7 +530,7 @@ rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, doub
   if (s != RSW_OK) return s;
   for (int i = 0; i < n_states; ++i) {
     CUDA_TRY(cudaMemcpyAsync(Ut, u_in + i * L, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
-    s = run_chain(ch, st, nullptr);
+    s = run_chain(ch, ws, nullptr, st, nullptr);
     if (s != RSW_OK) return s;
     CUDA_TRY(cudaMemcpyAsync(u_out + i * L, Ut + L, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
   }
@@ -566,7 +589,7 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   if ((s = setup_chain(ch0, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, nullptr, nullptr, S)))
     return s;
   CUDA_TRY(cudaEventRecord(ev[0], st));
-  if ((s = run_chain(ch0, st, &launches))) return s;
+  if ((s = run_chain(ch0, ws, nullptr, st, &launches))) return s;
   CUDA_TRY(cudaEventRecord(ev[1], st));
   {
     float ms;
@@ -596,9 +619,7 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     }
     CUDA_TRY(cudaEventRecord(ev[2], st));
     // serial sweep: U^k_{n+1} = G(U^k_n) + (F_n - G_n)
-    if ((s = run_chain(ch, st, &launches))) return s;
-    CUDA_TRY(rsw::launch_resid_max((const double*)ws->rparts.p, S, K + 1, (double*)ws->rdev.p, nullptr, st));
-    ++launches;
+    if ((s = run_chain(ch, ws, (double*)ws->rdev.p, st, &launches))) return s;
     CUDA_TRY(cudaEventRecord(ev[3], st));
     CUDA_TRY(cudaMemcpyAsync(ws->rhost, ws->rdev.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));

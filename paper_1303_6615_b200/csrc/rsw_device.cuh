@@ -96,6 +96,17 @@ __device__ __forceinline__ void dftR(double2* v) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Padded work-buffer layout: element i of a field lives at i + i/8, field stride NP = N + N/8.
+// Every access pattern of the path (Stockham loads, the stride-R stores of the first pass,
+// grid-point and mode loops) is then free of shared-memory bank conflicts for 16-byte elements.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
+template <int N>
+struct WL {
+  static constexpr int NP = N + N / 8;
+};
+
+// ---------------------------------------------------------------------------------------------
 // Stockham autosort FFT over the 3 fields of W (in place: load all, barrier, compute, store).
 // Pass with radix R after NS = product of previous radices (natural order in and out):
 //   for j in [0, N/R): k = j mod NS; v_r = W[j + r N/R] * w^{r k N/(NS R)}; DFT_R;
@@ -112,9 +123,9 @@ __device__ __forceinline__ void stockham_pass(double2* W, const double2* __restr
     const int b = threadIdx.x + i * T;
     if (NB % T == 0 || b < NB) {
       const int f = b / (N / R), j = b % (N / R);
-      const double2* in = W + f * N + j;
+      const double2* in = W + f * WL<N>::NP;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[i][r] = in[r * (N / R)];
+      for (int r = 0; r < R; ++r) v[i][r] = in[pad(j + r * (N / R))];
     }
   }
   __syncthreads();
@@ -132,9 +143,10 @@ __device__ __forceinline__ void stockham_pass(double2* W, const double2* __restr
         }
       }
       dftR<R, SIGN>(v[i]);
-      double2* out = W + f * N + (j / NS) * NS * R + k;
+      double2* out = W + f * WL<N>::NP;
+      const int base = (j / NS) * NS * R + k;
 #pragma unroll
-      for (int r = 0; r < R; ++r) out[r * NS] = v[i][r];
+      for (int r = 0; r < R; ++r) out[pad(base + r * NS)] = v[i][r];
     }
   }
   __syncthreads();
@@ -193,28 +205,34 @@ __device__ __forceinline__ void to_prim(double as, double p, double q, const dou
 template <int N, int T>
 __device__ __forceinline__ void nl_physical(double2* W, const double2* __restrict__ tw) {
   fft3<N, T, +1>(W, tw);  // synthesis: u(x_n) = Σ_κ Z_κ e^{iκ x_n}
+  constexpr int NP = WL<N>::NP;
   for (int n = threadIdx.x; n < N; n += T) {
-    const double2 v1 = W[n], v2x = W[N + n], h = W[2 * N + n];
-    W[n] = make_double2(0.5 * v1.x * v1.x, 0.5 * v1.y * v1.y);
-    W[N + n] = make_double2(v1.x * v2x.x, v1.y * v2x.y);
-    W[2 * N + n] = make_double2(h.x * v1.x, h.y * v1.y);
+    const int i = pad(n);
+    const double2 v1 = W[i], v2x = W[NP + i], h = W[2 * NP + i];
+    W[i] = make_double2(0.5 * v1.x * v1.x, 0.5 * v1.y * v1.y);
+    W[NP + i] = make_double2(v1.x * v2x.x, v1.y * v2x.y);
+    W[2 * NP + i] = make_double2(h.x * v1.x, h.y * v1.y);
   }
   __syncthreads();
   fft3<N, T, -1>(W, tw);  // analysis (unnormalised)
 }
 
 // prologue helper: write prim(x) of entry j into W as the N-eval input (v1, iκ v2, h)
-__device__ __forceinline__ void put_input(double2* W, int N, int k_full, double kap, const double2* u) {
-  W[k_full] = u[0];
-  W[N + k_full] = cmuli(cscale(u[1], kap));
-  W[2 * N + k_full] = u[2];
+template <int N>
+__device__ __forceinline__ void put_input(double2* W, int k_full, double kap, const double2* u) {
+  constexpr int NP = WL<N>::NP;
+  const int i = pad(k_full);
+  W[i] = u[0];
+  W[NP + i] = cmuli(cscale(u[1], kap));
+  W[2 * NP + i] = u[2];
 }
 
 // epilogue helper: read the N-eval output of entry k_full, return N̂ (primitive)
-__device__ __forceinline__ void get_output(const double2* W, int N, int k_full, double kap, double invN,
-                                           double2* nh) {
-  const double2 Q0 = cscale(W[k_full], invN), Q1 = cscale(W[N + k_full], invN),
-                Q2 = cscale(W[2 * N + k_full], invN);
+template <int N>
+__device__ __forceinline__ void get_output(const double2* W, int k_full, double kap, double invN, double2* nh) {
+  constexpr int NP = WL<N>::NP;
+  const int i = pad(k_full);
+  const double2 Q0 = cscale(W[i], invN), Q1 = cscale(W[NP + i], invN), Q2 = cscale(W[2 * NP + i], invN);
   nh[0] = cmulmi(cscale(Q0, kap));  // -iκ Q0
   nh[1] = make_double2(-Q1.x, -Q1.y);
   nh[2] = cmulmi(cscale(Q2, kap));  // -iκ Q2
@@ -226,7 +244,7 @@ __device__ __forceinline__ void zero_tail(double2* W) {
   constexpr int K = N / 3, NZ = N - (2 * K + 1);
   for (int i = threadIdx.x; i < 3 * NZ; i += T) {
     const int f = i / NZ, k = K + 1 + i % NZ;
-    W[f * N + k] = make_double2(0.0, 0.0);
+    W[f * WL<N>::NP + pad(k)] = make_double2(0.0, 0.0);
   }
 }
 

@@ -44,6 +44,7 @@ struct CoarseArgs {
   const double* F;      // [S][...] or null (k = 0 sweep / plain coarse step)
   double* rparts;       // [S][K+1][2] residual partials or null
   int n_end;            // number of chain steps (S)
+  unsigned long long* prof;  // optional phase timestamps (CTA 0; RSW_PROFILE_COARSE=1), else null
 };
 
 cudaError_t launch_fine(int n, int scheme, bool lin, const double* in, double* out, int S, int m, double h,
@@ -51,11 +52,8 @@ cudaError_t launch_fine(int n, int scheme, bool lin, const double* in, double* o
 cudaError_t launch_nonlinear(int n, const double* in, double* out, int S, const FineTab& tab, cudaStream_t st);
 cudaError_t launch_avg_states(int n, const double* in, double* out, int S, int M, const AvgTab& tab,
                               cudaStream_t st);
-cudaError_t launch_coarse_samples(int n, const double2* y, double2* part, int nparts, int M, const AvgTab& tab,
-                                  cudaStream_t st);
-cudaError_t launch_coarse_combine(int n, const CoarseArgs& ca, int stage, int slice, cudaStream_t st);
-cudaError_t launch_resid_max(const double* rparts, int S, int Kp1, double* r_out, double* per_slice,
-                             cudaStream_t st);
+cudaError_t launch_coarse_sweep(int n, const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar, double* r_out,
+                                int* grid_used, cudaStream_t st);
 cudaError_t launch_dfma_peak(double* out, int blocks, int iters, cudaStream_t st);
 
 }  // namespace rsw

@@ -92,7 +92,7 @@ __device__ __forceinline__ void prologue_from(double2* W, const double2* X, cons
 #pragma unroll
     for (int al = 0; al < 3; ++al) c[al] = X[al * Kc + j];
     to_prim(as, __ldg(g.p + ak), __ldg(g.q + ak), c, u);
-    put_input(W, N, full_index(kap, N), (double)kap, u);
+    put_input<N>(W, full_index(kap, N), (double)kap, u);
   }
   zero_tail<N, T>(W);
 }
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(T) k_fine(const double* u_in, double* u_out, i
   constexpr double invN = 1.0 / N;
   extern __shared__ double2 smem[];
   double2* W = smem;
-  double2* S0 = W + 3 * N;
+  double2* S0 = W + 3 * WL<N>::NP;
   double2* S1 = S0 + 3 * Kc;
   double2* S2 = S1 + 3 * Kc;
   const int sA = 2 * blockIdx.x, sB = sA + 1;
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(T) k_fine(const double* u_in, double* u_out, i
         double2 nn[3];
         if (!LIN) {
           double2 nh[3];
-          get_output(W, N, kf, (double)kap, invN, nh);
+          get_output<N>(W, kf, (double)kap, invN, nh);
           to_eigen(as, p, q, nh, nn);
         } else {
 #pragma unroll
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(T) k_fine(const double* u_in, double* u_out, i
         if (!LIN) {
           double2 u[3];
           to_prim(as, p, q, x, u);
-          put_input(W, N, kf, (double)kap, u);
+          put_input<N>(W, kf, (double)kap, u);
         }
       }
       if (!LIN) zero_tail<N, T>(W);
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(T) k_nonlinear(const double* u_in, double* out
   constexpr double invN = 1.0 / N;
   extern __shared__ double2 smem[];
   double2* W = smem;
-  double2* C = W + 3 * N;
+  double2* C = W + 3 * WL<N>::NP;
   const int sA = 2 * blockIdx.x, sB = sA + 1;
   const size_t L = (size_t)3 * NH * 2;
   load_pair_eigen<N, T>(u_in + sA * L, (sB < n_states) ? u_in + sB * L : nullptr, tab.g, C);
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(T) k_nonlinear(const double* u_in, double* out
     const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
     const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
     double2 nh[3], nn[3];
-    get_output(W, N, full_index(kap, N), (double)kap, invN, nh);
+    get_output<N>(W, full_index(kap, N), (double)kap, invN, nh);
     to_eigen(as, __ldg(tab.g.p + ak), __ldg(tab.g.q + ak), nh, nn);
 #pragma unroll
     for (int al = 0; al < 3; ++al) C[al * Kc + j] = nn[al];
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
   constexpr double invN = 1.0 / N;
   extern __shared__ double2 smem[];
   double2* W = smem;
-  double2* C = W + 3 * N;
+  double2* C = W + 3 * WL<N>::NP;
   double2* A = C + 3 * Kc;
   const int sA = 2 * blockIdx.x, sB = sA + 1;
   const size_t L = (size_t)3 * NH * 2;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
         c[1] = C[Kc + j];                 // α=0
         c[2] = cmulc(C[2 * Kc + j], ph);  // α=+1: e^{-iωτ}
         to_prim(as, __ldg(tab.g.p + ak), __ldg(tab.g.q + ak), c, u);
-        put_input(W, N, full_index(kap, N), (double)kap, u);
+        put_input<N>(W, full_index(kap, N), (double)kap, u);
       }
       zero_tail<N, T>(W);
       __syncthreads();
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
       const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
       const double p = __ldg(tab.g.p + ak), q = __ldg(tab.g.q + ak);
       double2 nh[3], nn[3];
-      get_output(W, N, kf, (double)kap, invN, nh);
+      get_output<N>(W, kf, (double)kap, invN, nh);
       to_eigen(as, p, q, nh, nn);
       const double2 ph = __ldg(tab.phase + (size_t)m * (K + 1) + ak);
       A[j] = caxpy(wm, cmulc(nn[0], ph), A[j]);               // α=-1: e^{-iωτ}
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
         c[1] = C[Kc + j];
         c[2] = cmulc(C[2 * Kc + j], ph2);
         to_prim(as, p, q, c, u);
-        put_input(W, N, kf, (double)kap, u);
+        put_input<N>(W, kf, (double)kap, u);
       }
     }
     zero_tail<N, T>(W);
@@ -311,21 +311,56 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
 }
 
 // ---------------------------------------------------------------------------------------------
-// K4 (coarse step, one state): samples kernel.  CTA b evaluates the sample pairs
-// (m_A, m_B) = (2p+1, 2p+2), p = b, b + gridDim.x, ..., packing the two rotated copies of the
-// same state y into one complex field, and writes its partial sum (eigen, signed κ) to part[b].
+// K4: the serial coarse sweep (Alg.4's serial loop P:583-587 over Alg.2 coarse steps) as ONE
+// persistent cooperative kernel.  Per RK stage of slice n:
+//   phase 1 (all CTAs, sample-parallel as Alg.1): CTA b evaluates its sample pairs
+//     (m_A, m_B) = (2p+1, 2p+2), p = b, b+P, ..., packing the two rotated copies P-_m y of the
+//     stage input into one complex field, and writes its partial Σ w_m P+_m N(P-_m y) to part[b];
+//   grid barrier;
+//   phase 2 (distributed over |κ|): CTA b owns |κ| ≡ b (mod P) and reduces part[0..P-1] for its 6
+//     eigen entries (α, ±κ) in a fixed order, then applies the RK4 / midpoint stage update; at the
+//     last stage also the D half step, the back-transform e^{-(ΔT/ε)L̂}, the parareal update
+//     U_{n+1} = G + (F_n - G_n) with the residual partials (R12), and slice n+1's first input;
+//   grid barrier.
+// Cross-CTA data (y, part) is read with ld.global.cg (L2), never through the incoherent L1.
 // ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// grid barrier: monotone arrival counter, arrive with a gpu-scope release RMW, spin with
+// gpu-scope acquire loads (1.2 us at 128-148 CTAs on B200, vs 2.2 us for a volatile-flag barrier;
+// tools/micro/barrier_bench.cu).  `epoch` counts this CTA's barriers; the counter is zeroed by the
+// host before the launch.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    (void)old;
+    const unsigned target = epoch * nblocks;
+    while (ld_acquire_gpu(bar) < target) {
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int N, int T>
-__global__ void __launch_bounds__(T) k_coarse_samples(const double2* __restrict__ y, double2* __restrict__ part,
-                                                      int M, const AvgTab tab) {
+__device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* part, int M, const AvgTab& tab,
+                                                     double2* W, double2* C, double2* A) {
   constexpr int K = N / 3, Kc = 2 * K + 1;
   constexpr double invN = 1.0 / N;
-  extern __shared__ double2 smem[];
-  double2* W = smem;
-  double2* C = W + 3 * N;
-  double2* A = C + 3 * Kc;
   for (int i = threadIdx.x; i < 3 * Kc; i += T) {
-    C[i] = y[i];
+    C[i] = __ldcg(y + i);
     A[i] = make_double2(0.0, 0.0);
   }
   __syncthreads();
@@ -339,16 +374,16 @@ __global__ void __launch_bounds__(T) k_coarse_samples(const double2* __restrict_
       const double2 pA = __ldg(tab.phase + (size_t)mA * (K + 1) + ak);
       const double2 pB = hasB ? __ldg(tab.phase + (size_t)mB * (K + 1) + ak) : make_double2(1.0, 0.0);
       double2 c[3], u[3];
-      // packed eigen input: P-_{mA} y + i P-_{mB} y
+      // packed eigen input: P-_{mA} y + i P-_{mB} y   (P-: α=-1 -> e^{+iωτ}, α=+1 -> e^{-iωτ})
       const double2 ym = C[j], y0 = C[Kc + j], yp = C[2 * Kc + j];
-      double2 bm = hasB ? cmul(ym, pB) : make_double2(0.0, 0.0);
-      double2 b0 = hasB ? y0 : make_double2(0.0, 0.0);
-      double2 bp = hasB ? cmulc(yp, pB) : make_double2(0.0, 0.0);
+      const double2 bm = hasB ? cmul(ym, pB) : make_double2(0.0, 0.0);
+      const double2 b0 = hasB ? y0 : make_double2(0.0, 0.0);
+      const double2 bp = hasB ? cmulc(yp, pB) : make_double2(0.0, 0.0);
       c[0] = cadd(cmul(ym, pA), cmuli(bm));
       c[1] = cadd(y0, cmuli(b0));
       c[2] = cadd(cmulc(yp, pA), cmuli(bp));
       to_prim(as, __ldg(tab.g.p + ak), __ldg(tab.g.q + ak), c, u);
-      put_input(W, N, full_index(kap, N), (double)kap, u);
+      put_input<N>(W, full_index(kap, N), (double)kap, u);
     }
     zero_tail<N, T>(W);
     __syncthreads();
@@ -359,8 +394,8 @@ __global__ void __launch_bounds__(T) k_coarse_samples(const double2* __restrict_
       const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
       const double p = __ldg(tab.g.p + ak), q = __ldg(tab.g.q + ak);
       double2 zp[3], zm[3], na[3], nb[3], ea[3], eb[3];
-      get_output(W, N, full_index(kap, N), (double)kap, invN, zp);
-      get_output(W, N, full_index(-kap, N), (double)(-kap), invN, zm);
+      get_output<N>(W, full_index(kap, N), (double)kap, invN, zp);
+      get_output<N>(W, full_index(-kap, N), (double)(-kap), invN, zm);
 #pragma unroll
       for (int f = 0; f < 3; ++f) {  // unpack: N_A(κ) = (Z(κ) + conj Z(-κ))/2, N_B = (Z - conj Z(-κ))/(2i)
         const double2 zc = cconj(zm[f]);
@@ -370,7 +405,7 @@ __global__ void __launch_bounds__(T) k_coarse_samples(const double2* __restrict_
       to_eigen(as, p, q, na, ea);
       to_eigen(as, p, q, nb, eb);
       const double2 pA = __ldg(tab.phase + (size_t)mA * (K + 1) + ak);
-      A[j] = caxpy(wA, cmulc(ea[0], pA), A[j]);
+      A[j] = caxpy(wA, cmulc(ea[0], pA), A[j]);  // P+: α=-1 -> e^{-iωτ}, α=+1 -> e^{+iωτ}
       A[Kc + j] = caxpy(wA, ea[1], A[Kc + j]);
       A[2 * Kc + j] = caxpy(wA, cmul(ea[2], pA), A[2 * Kc + j]);
       if (hasB) {
@@ -386,183 +421,203 @@ __global__ void __launch_bounds__(T) k_coarse_samples(const double2* __restrict_
   for (int i = threadIdx.x; i < 3 * Kc; i += T) P[i] = A[i];
 }
 
-// ---------------------------------------------------------------------------------------------
-// K4 (coarse step, one state): combine kernel.  One CTA per |κ| (handles κ and -κ, 6 eigen
-// entries): deterministic sum of the partials, the RK4 / midpoint stage logic of Alg.2, and at
-// the last stage the D half step, the back-transform e^{-(ΔT/ε)L̂}, the parareal update
-// U_{n+1} = G + (F_n - G_n) (Eq. HMM parareal iteration), the residual partials (R12), and the
-// first stage input of slice n+1.
-//   mode: 0 = init from U[n] (no partials), 1..4 = RK stage s done, with `final` set on the last.
-// ---------------------------------------------------------------------------------------------
-template <int N>
-__global__ void __launch_bounds__(128) k_coarse_combine(CoarseArgs ca, int stage, int n) {
-  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
-  const int ak = blockIdx.x;  // |κ|
-  const int jp = ak, jm = (ak == 0) ? 0 : Kc - ak;
-  const int ne = (ak == 0) ? 3 : 6;  // entries handled: (α, +κ) and (α, -κ)
-  __shared__ double2 red[6][128];
-  double2 ksum[6];
-#pragma unroll
-  for (int e = 0; e < 6; ++e) ksum[e] = make_double2(0.0, 0.0);
-  if (stage > 0) {
-    for (int b = threadIdx.x; b < ca.nparts; b += 128) {
-      const double2* P = ca.part + (size_t)b * 3 * Kc;
-#pragma unroll
-      for (int e = 0; e < 6; ++e) {
-        if (e < ne) {
-          const int al = e % 3, j = (e < 3) ? jp : jm;
-          ksum[e] = cadd(ksum[e], P[al * Kc + j]);
-        }
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < 6; ++e) red[e][threadIdx.x] = ksum[e];
-    __syncthreads();
-    for (int s = 64; s > 0; s >>= 1) {
-      if (threadIdx.x < s) {
-#pragma unroll
-        for (int e = 0; e < 6; ++e) red[e][threadIdx.x] = cadd(red[e][threadIdx.x], red[e][threadIdx.x + s]);
-      }
-      __syncthreads();
-    }
-  }
-  if (threadIdx.x != 0) return;
-  const double a = ca.g.a[ak], p = ca.g.p[ak], q = ca.g.q[ak];
+// phase 2 of one RK stage, thread-parallel over the CTA's owned modes |κ| = b + o P (o < NOWN):
+// items i = o*6 + e, entries e = (α, +κ) for e < 3, (α, -κ) for e >= 3.  The stage base v and the RK
+// accumulator ks of owned modes live in this CTA's shared memory for the whole sweep; the stage
+// input y is published to global memory for the samples phase of every CTA.
+template <int N, int T, int NOWN>
+__device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int stage, int n, double2* Vs,
+                                                    double2* KSs, double2* kk, double2* un_s, double* nd_s) {
+  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1, NW = T / 32;
+  const int P = gridDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t Ls = (size_t)3 * NH;
   const double dT = ca.dT;
-  double2* V = ca.v;   // [3][Kc] stage base v (after the first D half step)
-  double2* KS = ca.ks; // [3][Kc] RK accumulator
-  double2* Y = ca.y;   // [3][Kc] next stage input
-  const size_t Ls = (size_t)3 * NH;  // complex entries per half-spectrum state
-  bool finalize = false;
-  for (int e = 0; e < ne; ++e) {
-    const int al = e % 3, j = (e < 3) ? jp : jm, idx = al * Kc + j;
-    const double2 kk = red[e][0];
-    if (stage == 0) break;
-    if (ca.scheme == 0) {  // RK4
-      if (stage == 1) {
-        KS[idx] = kk;
-        Y[idx] = caxpy(0.5 * dT, kk, V[idx]);
-      } else if (stage == 2) {
-        KS[idx] = caxpy(2.0, kk, KS[idx]);
-        Y[idx] = caxpy(0.5 * dT, kk, V[idx]);
-      } else if (stage == 3) {
-        KS[idx] = caxpy(2.0, kk, KS[idx]);
-        Y[idx] = caxpy(dT, kk, V[idx]);
-      } else {
-        KS[idx] = cadd(KS[idx], kk);
-        V[idx] = caxpy(dT / 6.0, KS[idx], V[idx]);
-        finalize = true;
+  auto entry = [&](int o, int e, int& ak, int& al, int& j) {
+    ak = blockIdx.x + o * P;
+    al = e % 3;
+    j = (e < 3) ? ak : ((ak == 0) ? 0 : Kc - ak);
+  };
+  const bool last = (ca.scheme == 0) ? (stage == 4) : (stage == 2);
+  if (stage > 0) {
+    // deterministic reduction of the partials: one warp per item, lanes stride over parts, xor tree
+    for (int it = warp; it < NOWN * 6; it += NW) {
+      int ak, al, j;
+      entry(it / 6, it % 6, ak, al, j);
+      double2 s = make_double2(0.0, 0.0);
+      if (ak <= K)
+        for (int b = lane; b < ca.nparts; b += 32) s = cadd(s, __ldcg(ca.part + (size_t)b * 3 * Kc + al * Kc + j));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
       }
-    } else {  // midpoint: v + ΔT N̄(v + ΔT/2 N̄(v))
-      if (stage == 1) {
-        Y[idx] = caxpy(0.5 * dT, kk, V[idx]);
-      } else {
-        V[idx] = caxpy(dT, kk, V[idx]);
-        finalize = true;
+      if (lane == 0) kk[it] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < NOWN * 6) {
+      int ak, al, j;
+      const int it = threadIdx.x;
+      entry(it / 6, it % 6, ak, al, j);
+      if (ak <= K && !(ak == 0 && it % 6 >= 3)) {
+        const double2 k = kk[it];
+        double2& V = Vs[it];
+        double2& KS = KSs[it];
+        double2* Y = ca.y + al * Kc + j;
+        if (ca.scheme == 0) {  // classical RK4 (R6): (k1 + 2k2 + 2k3 + k4) accumulated in this order
+          if (stage == 1) {
+            KS = k;
+            *Y = caxpy(0.5 * dT, k, V);
+          } else if (stage == 2) {
+            KS = caxpy(2.0, k, KS);
+            *Y = caxpy(0.5 * dT, k, V);
+          } else if (stage == 3) {
+            KS = caxpy(2.0, k, KS);
+            *Y = caxpy(dT, k, V);
+          } else {
+            KS = cadd(KS, k);
+            V = caxpy(dT / 6.0, KS, V);
+          }
+        } else {  // midpoint (Alg.2, R7): v + ΔT N̄(v + ΔT/2 N̄(v))
+          if (stage == 1) *Y = caxpy(0.5 * dT, k, V);
+          else V = caxpy(dT, k, V);
+        }
       }
     }
-  }
-  if (stage == 0 || finalize) {
-    const double dh = ca.dhalf[ak];
-    const double2 bt = ca.back[ak];  // e^{-iω ΔT/ε}  (α=+1 entry of e^{-(ΔT/ε)L̂})
-    const double2* Uin = reinterpret_cast<const double2*>(ca.U) + (size_t)n * Ls;
-    double2* Uout = reinterpret_cast<double2*>(ca.U) + (size_t)(n + 1) * Ls;
-    double2 unew[3];
-    if (finalize) {
-      // D half step, back-transform, primitive G at +κ
-      double2 cg[3], G[3];
+    __syncthreads();
+    if (!last) return;
+    // finalize: D half step, back-transform, primitive G, parareal update (thread per (o, f))
+    if (threadIdx.x < NOWN * 3) {
+      const int o = threadIdx.x / 3, f = threadIdx.x % 3, ak = blockIdx.x + o * P;
+      if (ak <= K) {
+        const double a = __ldg(ca.g.a + ak), p = __ldg(ca.g.p + ak), q = __ldg(ca.g.q + ak);
+        const double dh = __ldg(ca.dhalf + ak);
+        const double2 bt = __ldg(ca.back + ak);  // e^{-iωΔT/ε}: α=+1 entry of e^{-(ΔT/ε)L̂} (R3)
+        double2 cg[3], G[3];
 #pragma unroll
-      for (int al = 0; al < 3; ++al) {
-        double2 c = cscale(V[al * Kc + jp], dh);
-        cg[al] = (al == 1) ? c : (al == 2 ? cmul(c, bt) : cmulc(c, bt));
-      }
-      to_prim(a, p, q, cg, G);
-      if (ak == 0) {
-#pragma unroll
-        for (int f = 0; f < 3; ++f) G[f].y = 0.0;
-      }
-      double2* Gst = reinterpret_cast<double2*>(ca.G) + (size_t)n * Ls;
-      double num = 0.0, den = 0.0;
-      const double wk = (ak == 0 || 2 * ak == N) ? 1.0 : 2.0;
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        double2 un;
-        if (ca.F) {
-          const double2 Fv = reinterpret_cast<const double2*>(ca.F)[(size_t)n * Ls + f * NH + ak];
-          un = cadd(G[f], csub(Fv, Gst[f * NH + ak]));
-        } else {
-          un = G[f];
+        for (int al = 0; al < 3; ++al) {
+          const double2 c = cscale(Vs[o * 6 + al], dh);  // e^{(ΔT/2) D̂} (Alg.2)
+          cg[al] = (al == 1) ? c : (al == 2 ? cmul(c, bt) : cmulc(c, bt));
         }
-        const double2 uo = Uout[f * NH + ak];
-        const double2 d = csub(un, uo);
-        num += wk * (d.x * d.x + d.y * d.y);
-        den += wk * (un.x * un.x + un.y * un.y);
-        Gst[f * NH + ak] = G[f];
-        Uout[f * NH + ak] = un;
-        unew[f] = un;
-      }
-      if (ca.rparts) {
-        ca.rparts[((size_t)n * (K + 1) + ak) * 2 + 0] = num;
-        ca.rparts[((size_t)n * (K + 1) + ak) * 2 + 1] = den;
-      }
-      if (ak == K) {  // modes K < k <= N/2 stay zero
-        for (int k = K + 1; k < NH; ++k)
-          for (int f = 0; f < 3; ++f) {
-            Uout[f * NH + k] = make_double2(0.0, 0.0);
-            Gst[f * NH + k] = make_double2(0.0, 0.0);
+        to_prim(a, p, q, cg, G);
+        double2 g = G[f];
+        if (ak == 0) g.y = 0.0;
+        double2* Gst = reinterpret_cast<double2*>(ca.G) + (size_t)n * Ls + f * NH + ak;
+        double2* Uo = reinterpret_cast<double2*>(ca.U) + (size_t)(n + 1) * Ls + f * NH + ak;
+        double2 un = g;
+        if (ca.F) {  // U^k_{n+1} = G(U^k_n) + (F_n - G_n)   (Eq. HMM parareal iteration P:428-430)
+          const double2 Fv = __ldcg(reinterpret_cast<const double2*>(ca.F) + (size_t)n * Ls + f * NH + ak);
+          un = cadd(g, csub(Fv, *Gst));
+        }
+        const double2 d = csub(un, *Uo);
+        const double wk = (ak == 0 || 2 * ak == N) ? 1.0 : 2.0;
+        nd_s[threadIdx.x * 2] = wk * (d.x * d.x + d.y * d.y);
+        nd_s[threadIdx.x * 2 + 1] = wk * (un.x * un.x + un.y * un.y);
+        *Gst = g;
+        *Uo = un;
+        un_s[threadIdx.x] = un;
+        if (ak == K)  // modes K < k <= N/2 stay zero
+          for (int k = K + 1; k < NH; ++k) {
+            Uo[k - K] = make_double2(0.0, 0.0);
+            Gst[k - K] = make_double2(0.0, 0.0);
           }
       }
-      if (n + 1 >= ca.n_end) return;  // no next slice
-    } else {
-#pragma unroll
-      for (int f = 0; f < 3; ++f) unew[f] = Uin[f * NH + ak];
     }
-    // first stage input of the next slice: v = e^{ΔT D̂/2} u (eigen, both signs of κ)
-    double2 cpos[3], cneg[3], uneg[3];
-#pragma unroll
-    for (int f = 0; f < 3; ++f) uneg[f] = cconj(unew[f]);
-    to_eigen(a, p, q, unew, cpos);
-    to_eigen(-a, p, q, uneg, cneg);
-#pragma unroll
-    for (int al = 0; al < 3; ++al) {
-      const double2 vp = cscale(cpos[al], dh), vn = cscale(cneg[al], dh);
-      V[al * Kc + jp] = vp;
-      Y[al * Kc + jp] = vp;
-      if (ak > 0) {
-        V[al * Kc + jm] = vn;
-        Y[al * Kc + jm] = vn;
+    __syncthreads();
+    if (ca.rparts && threadIdx.x < NOWN) {
+      const int ak = blockIdx.x + threadIdx.x * P;
+      if (ak <= K) {
+        const double* t = nd_s + threadIdx.x * 6;
+        ca.rparts[((size_t)n * (K + 1) + ak) * 2 + 0] = t[0] + t[2] + t[4];
+        ca.rparts[((size_t)n * (K + 1) + ak) * 2 + 1] = t[1] + t[3] + t[5];
       }
     }
-  }
-}
-
-// residual r_k = max_n sqrt(Σ_κ num / Σ_κ den)  (fixed order; one CTA)
-__global__ void __launch_bounds__(256) k_resid_max(const double* rparts, int S, int Kp1, double* r_out,
-                                                   double* per_slice) {
-  __shared__ double red[256];
-  double mx = 0.0;
-  bool bad = false;
-  for (int n = threadIdx.x; n < S; n += 256) {
-    double num = 0.0, den = 0.0;
-    for (int k = 0; k < Kp1; ++k) {
-      num += rparts[((size_t)n * Kp1 + k) * 2];
-      den += rparts[((size_t)n * Kp1 + k) * 2 + 1];
-    }
-    const double r = sqrt(num / den);
-    if (per_slice) per_slice[n] = r;
-    if (!(r == r) || isinf(r)) bad = true;
-    mx = fmax(mx, r);
-  }
-  red[threadIdx.x] = bad ? __longlong_as_double(0x7ff8000000000000LL) : mx;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      const double a = red[threadIdx.x], b = red[threadIdx.x + s];
-      red[threadIdx.x] = (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(a, b);
+    if (n + 1 >= ca.n_end) return;  // no next slice
+  } else {
+    // stage 0: load U_0 of owned modes
+    if (threadIdx.x < NOWN * 3) {
+      const int o = threadIdx.x / 3, f = threadIdx.x % 3, ak = blockIdx.x + o * P;
+      if (ak <= K) un_s[threadIdx.x] = reinterpret_cast<const double2*>(ca.U)[(size_t)n * Ls + f * NH + ak];
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *r_out = red[0];
+  // first stage input of the next slice: v = e^{ΔT D̂/2} u (Alg.2), eigen, both signs of κ
+  if (threadIdx.x < NOWN * 6) {
+    int ak, al, j;
+    const int it = threadIdx.x, o = it / 6, e = it % 6;
+    entry(o, e, ak, al, j);
+    if (ak <= K && !(ak == 0 && e >= 3)) {
+      const double a = __ldg(ca.g.a + ak), p = __ldg(ca.g.p + ak), q = __ldg(ca.g.q + ak);
+      double2 u[3], c[3];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) u[f] = (e < 3) ? un_s[o * 3 + f] : cconj(un_s[o * 3 + f]);
+      to_eigen(e < 3 ? a : -a, p, q, u, c);
+      const double2 v = cscale(c[al], __ldg(ca.dhalf + ak));
+      Vs[it] = v;
+      ca.y[al * Kc + j] = v;
+    }
+  }
+  __syncthreads();
+}
+
+template <int N, int T, int NOWN>
+__global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const AvgTab tab, int M, unsigned* bar,
+                                                    double* r_out) {
+  constexpr int K = N / 3, Kc = 2 * K + 1;
+  extern __shared__ double2 smem[];
+  double2* W = smem;
+  double2* C = W + 3 * WL<N>::NP;
+  double2* A = C + 3 * Kc;
+  double2* Vs = A + 3 * Kc;      // [NOWN*6]
+  double2* KSs = Vs + NOWN * 6;  // [NOWN*6]
+  double2* kk = KSs + NOWN * 6;  // [NOWN*6]
+  double2* un_s = kk + NOWN * 6; // [NOWN*3]
+  double* red = reinterpret_cast<double*>(un_s + NOWN * 3);  // [max(T, NOWN*6)]
+  const unsigned P = gridDim.x;
+  const int nst = ca.scheme == 0 ? 4 : 2;
+  unsigned epoch = 0;
+  const bool prof = ca.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  int ps = 0;
+  coarse_update_phase<N, T, NOWN>(ca, 0, 0, Vs, KSs, kk, un_s, red);  // slice 0: v = e^{ΔT D̂/2} U_0
+  grid_barrier(bar, P, epoch);
+  for (int n = 0; n < ca.n_end; ++n) {
+    for (int st = 1; st <= nst; ++st) {
+      if (prof && ps < 64) ca.prof[ps * 4 + 0] = gtimer();
+      coarse_samples_phase<N, T>(ca.y, const_cast<double2*>(ca.part), M, tab, W, C, A);
+      if (prof && ps < 64) ca.prof[ps * 4 + 1] = gtimer();
+      grid_barrier(bar, P, epoch);
+      if (prof && ps < 64) ca.prof[ps * 4 + 2] = gtimer();
+      coarse_update_phase<N, T, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red);
+      if (prof && ps < 64) ca.prof[ps * 4 + 3] = gtimer();
+      grid_barrier(bar, P, epoch);
+      ++ps;
+    }
+  }
+  if (r_out && blockIdx.x == 0) {  // r_k = max_n sqrt(Σ num / Σ den) over slices (fixed order)
+    double mx = 0.0;
+    bool bad = false;
+    for (int s = threadIdx.x; s < ca.n_end; s += T) {
+      double num = 0.0, den = 0.0;
+      for (int k = 0; k <= K; ++k) {
+        num += __ldcg(ca.rparts + ((size_t)s * (K + 1) + k) * 2);
+        den += __ldcg(ca.rparts + ((size_t)s * (K + 1) + k) * 2 + 1);
+      }
+      const double r = sqrt(num / den);
+      if (!(r == r) || isinf(r)) bad = true;
+      mx = fmax(mx, r);
+    }
+    double* rr = red;
+    rr[threadIdx.x] = bad ? __longlong_as_double(0x7ff8000000000000LL) : mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      bool nan = false;
+      for (int t = 0; t < T; ++t) {
+        if (rr[t] != rr[t]) nan = true;
+        m = fmax(m, rr[t]);
+      }
+      *r_out = nan ? __longlong_as_double(0x7ff8000000000000LL) : m;
+    }
+  }
 }
 
 // M0: DFMA peak probe — independent FMA chains, every SM
@@ -588,11 +643,11 @@ template <int N>
 constexpr int threads_for() { return (3 * N / 8) > 96 ? (3 * N / 8) : 96; }
 
 template <int N>
-constexpr size_t fine_smem() { return sizeof(double2) * (3 * N + 3 * 3 * (2 * (N / 3) + 1)); }
+constexpr size_t fine_smem() { return sizeof(double2) * (3 * WL<N>::NP + 3 * 3 * (2 * (N / 3) + 1)); }
 template <int N>
-constexpr size_t nl_smem() { return sizeof(double2) * (3 * N + 3 * (2 * (N / 3) + 1)); }
+constexpr size_t nl_smem() { return sizeof(double2) * (3 * WL<N>::NP + 3 * (2 * (N / 3) + 1)); }
 template <int N>
-constexpr size_t avg_smem() { return sizeof(double2) * (3 * N + 2 * 3 * (2 * (N / 3) + 1)); }
+constexpr size_t avg_smem() { return sizeof(double2) * (3 * WL<N>::NP + 2 * 3 * (2 * (N / 3) + 1)); }
 
 template <typename KernelT>
 static cudaError_t set_smem(KernelT k, size_t bytes) {
@@ -641,21 +696,55 @@ static cudaError_t launch_avg_n(const double* in, double* out, int S, int M, con
   return cudaGetLastError();
 }
 
-template <int N>
-static cudaError_t launch_coarse_samples_n(const double2* y, double2* part, int nparts, int M, const AvgTab& tab,
-                                           cudaStream_t st) {
+template <int N, int NOWN>
+constexpr size_t coarse_smem() {
+  return sizeof(double2) * (3 * WL<N>::NP + 2 * 3 * (2 * (N / 3) + 1) + NOWN * 21) +
+         sizeof(double) * (threads_for<N>() > NOWN * 6 ? threads_for<N>() : NOWN * 6);
+}
+
+template <int N, int NOWN>
+static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar,
+                                            double* r_out, int grid, cudaStream_t st) {
   constexpr int T = threads_for<N>();
-  auto kfn = k_coarse_samples<N, T>;
-  cudaError_t e = set_smem(kfn, avg_smem<N>());
+  auto kfn = k_coarse_sweep<N, T, NOWN>;
+  const size_t sm = coarse_smem<N, NOWN>();
+  cudaError_t e = set_smem(kfn, sm);
   if (e != cudaSuccess) return e;
-  kfn<<<nparts, T, avg_smem<N>(), st>>>(y, part, M, tab);
-  return cudaGetLastError();
+  int dev, sms, per_sm;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, T, sm)) != cudaSuccess) return e;
+  if (grid > per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
+  CoarseArgs c2 = ca;
+  c2.nparts = grid;
+  if ((e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st)) != cudaSuccess) return e;
+  void* args[] = {(void*)&c2, (void*)&tab, (void*)&M, (void*)&bar, (void*)&r_out};
+  return cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(T), args, sm, st);
 }
 
 template <int N>
-static cudaError_t launch_coarse_combine_n(const CoarseArgs& ca, int stage, int n, cudaStream_t st) {
-  k_coarse_combine<N><<<N / 3 + 1, 128, 0, st>>>(ca, stage, n);
-  return cudaGetLastError();
+static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar,
+                                         double* r_out, int* grid_used, cudaStream_t st) {
+  int dev, sms;
+  cudaError_t e;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  constexpr int K = N / 3;
+  // one sample pair per CTA, but enough CTAs that each owns <= 16 modes in the update phase;
+  // at most one CTA per SM (co-residency of the cooperative launch)
+  int grid = M / 2;
+  if (grid < (K + 1 + 15) / 16) grid = (K + 1 + 15) / 16;
+  if (grid > sms) grid = sms;
+  if (grid > ca.nparts) grid = ca.nparts;
+  if (grid < 1) grid = 1;
+  const int nown = (K + 1 + grid - 1) / grid;  // owned modes per CTA in the update phase
+  if (grid_used) *grid_used = grid;
+  if (nown <= 1) return launch_coarse_sweep_nown<N, 1>(ca, tab, M, bar, r_out, grid, st);
+  if (nown <= 2) return launch_coarse_sweep_nown<N, 2>(ca, tab, M, bar, r_out, grid, st);
+  if (nown <= 4) return launch_coarse_sweep_nown<N, 4>(ca, tab, M, bar, r_out, grid, st);
+  if (nown <= 8) return launch_coarse_sweep_nown<N, 8>(ca, tab, M, bar, r_out, grid, st);
+  if (nown <= 16) return launch_coarse_sweep_nown<N, 16>(ca, tab, M, bar, r_out, grid, st);
+  return cudaErrorInvalidConfiguration;
 }
 
 #define RSW_DISPATCH(n, CALL)                  \
@@ -687,21 +776,11 @@ cudaError_t launch_avg_states(int n, const double* in, double* out, int S, int M
   RSW_DISPATCH(n, C)
 #undef C
 }
-cudaError_t launch_coarse_samples(int n, const double2* y, double2* part, int nparts, int M, const AvgTab& tab,
-                                  cudaStream_t st) {
-#define C(NN) launch_coarse_samples_n<NN>(y, part, nparts, M, tab, st)
+cudaError_t launch_coarse_sweep(int n, const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar, double* r_out,
+                                int* grid_used, cudaStream_t st) {
+#define C(NN) launch_coarse_sweep_n<NN>(ca, tab, M, bar, r_out, grid_used, st)
   RSW_DISPATCH(n, C)
 #undef C
-}
-cudaError_t launch_coarse_combine(int n, const CoarseArgs& ca, int stage, int slice, cudaStream_t st) {
-#define C(NN) launch_coarse_combine_n<NN>(ca, stage, slice, st)
-  RSW_DISPATCH(n, C)
-#undef C
-}
-cudaError_t launch_resid_max(const double* rparts, int S, int Kp1, double* r_out, double* per_slice,
-                             cudaStream_t st) {
-  k_resid_max<<<1, 256, 0, st>>>(rparts, S, Kp1, r_out, per_slice);
-  return cudaGetLastError();
 }
 cudaError_t launch_dfma_peak(double* out, int blocks, int iters, cudaStream_t st) {
   k_dfma_peak<<<blocks, 256, 0, st>>>(out, iters);
