@@ -93,16 +93,21 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------------
-def cpu_baseline(w, steps_per_slice: int = 0):
+def cpu_baseline(w, steps_per_slice: int = 0, target_s: float = 15.0):
     """The CPU oracle, as it stands, timed on this host's cores on a bounded sample of the workload:
-    its fine sweep (ETDRK4, OpenMP over slices) on `cores` slices x `steps` fine steps."""
+    its ETDRK4 fine sweep (OpenMP over slices) on `cores` slices x `steps` fine steps, the step count
+    calibrated so the sample takes about `target_s` seconds."""
     import numpy as np
     import oracle
     oracle.build()
     cores = oracle.num_threads()
-    steps = steps_per_slice or {64: 125, 128: 125, 256: 60, 1024: 12}.get(w.n, 20)
     u0 = inputs.initial_state(w)
     u = np.repeat(u0[None], cores, axis=0)
+    if not steps_per_slice:
+        t0 = time.perf_counter()
+        oracle.fine_propagate(u, w.eps, w.F, w.mu, w.n, w.dt_eff, w.dt_eff * (1 + 1e-12), 0)
+        steps_per_slice = max(1, int(target_s / max(time.perf_counter() - t0, 1e-6)))
+    steps = steps_per_slice
     dT = steps * w.dt_eff
     t0 = time.perf_counter()
     oracle.fine_propagate(u, w.eps, w.F, w.mu, w.n, dT, w.dt_eff * (1 + 1e-12), 0)
@@ -120,7 +125,7 @@ def run_reference(args):
     w = inputs.WORKLOADS[args.config]
     vals = []
     for i in range(args.warmup + args.steps):
-        b = cpu_baseline(w, args.cpu_sample_steps or {1024: 4}.get(w.n, 0))
+        b = cpu_baseline(w, args.cpu_sample_steps, target_s=20.0)
         if i >= args.warmup:
             vals.append(b["value"])
     v = statistics.median(vals)

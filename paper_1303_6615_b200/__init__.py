@@ -16,7 +16,7 @@ import os
 from . import inputs  # noqa: F401  (seeded generators; no method arithmetic)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librsw.so")
+LIB_PATH = os.environ.get("RSW_LIB") or os.path.join(_HERE, "librsw.so")
 
 RSW_OK, RSW_ERR_CONFIG, RSW_NOT_CONVERGED, RSW_ERR_DIVERGED, RSW_ERR_CUDA, RSW_ERR_NCCL = range(6)
 FINE_ETDRK4, FINE_STRANG = 0, 1

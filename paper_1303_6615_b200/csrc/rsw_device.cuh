@@ -152,13 +152,15 @@ __device__ __forceinline__ void stockham_pass(double2* W, const double2* __restr
   __syncthreads();
 }
 
-template <int N, int T, int SIGN, int NS = 1>
+// RMAX: largest radix (8: fewer shared-memory passes, best for throughput; 4: twice the threads,
+// best for latency-bound launches such as the serial coarse sweep)
+template <int N, int T, int SIGN, int RMAX, int NS = 1>
 __device__ __forceinline__ void fft3(double2* W, const double2* __restrict__ tw) {
   if constexpr (NS < N) {
     constexpr int rem = N / NS;
-    constexpr int R = (rem % 8 == 0) ? 8 : rem;
+    constexpr int R = (rem % RMAX == 0) ? RMAX : rem;
     stockham_pass<N, T, R, NS, SIGN>(W, tw);
-    fft3<N, T, SIGN, NS * R>(W, tw);
+    fft3<N, T, SIGN, RMAX, NS * R>(W, tw);
   }
 }
 
@@ -202,9 +204,9 @@ __device__ __forceinline__ void to_prim(double as, double p, double q, const dou
 // The caller's epilogue applies 1/N, the derivative factors (-iκ, -1, -iκ) and the 2/3 mask:
 //   N(u) = -(∂x(v1²/2), v1 ∂x v2, ∂x(h v1))   (P:1090-1094 with R1; v1 v1x = ∂x(v1²/2))
 // ---------------------------------------------------------------------------------------------
-template <int N, int T>
+template <int N, int T, int RMAX>
 __device__ __forceinline__ void nl_physical(double2* W, const double2* __restrict__ tw) {
-  fft3<N, T, +1>(W, tw);  // synthesis: u(x_n) = Σ_κ Z_κ e^{iκ x_n}
+  fft3<N, T, +1, RMAX>(W, tw);  // synthesis: u(x_n) = Σ_κ Z_κ e^{iκ x_n}
   constexpr int NP = WL<N>::NP;
   for (int n = threadIdx.x; n < N; n += T) {
     const int i = pad(n);
@@ -214,7 +216,7 @@ __device__ __forceinline__ void nl_physical(double2* W, const double2* __restric
     W[2 * NP + i] = make_double2(h.x * v1.x, h.y * v1.y);
   }
   __syncthreads();
-  fft3<N, T, -1>(W, tw);  // analysis (unnormalised)
+  fft3<N, T, -1, RMAX>(W, tw);  // analysis (unnormalised)
 }
 
 // prologue helper: write prim(x) of entry j into W as the N-eval input (v1, iκ v2, h)

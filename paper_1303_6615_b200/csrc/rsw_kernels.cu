@@ -6,6 +6,18 @@
 
 namespace rsw {
 
+// FFT radix and CTA size per kernel class: radix 8 (fewer shared-memory passes) for the
+// throughput kernels (fine sweep, N̄ batch, N); radix 4 with twice the threads for the
+// latency-bound serial coarse sweep.  T = 3N/R: one radix-R butterfly of each field per thread.
+template <int N>
+__host__ __device__ constexpr int radix_for() { return N >= 512 ? 8 : 4; }
+template <int N>
+__host__ __device__ constexpr int threads_for() { return (3 * N / radix_for<N>()) > 96 ? (3 * N / radix_for<N>()) : 96; }
+template <int N>
+__host__ __device__ constexpr int coarse_radix() { return N >= 1024 ? 8 : 4; }
+template <int N>
+__host__ __device__ constexpr int coarse_threads() { return (3 * N / coarse_radix<N>()) > 96 ? (3 * N / coarse_radix<N>()) : 96; }
+
 // ---------------------------------------------------------------------------------------------
 // shared helpers: load a pair of half-spectrum states into packed eigen coordinates, and store
 // ---------------------------------------------------------------------------------------------
@@ -143,7 +155,7 @@ __global__ void __launch_bounds__(T) k_fine(const double* u_in, double* u_out, i
   for (int step = 0; step < m_steps; ++step) {
     const bool last_step = (step == m_steps - 1);
     for (int st = 0; st < nst; ++st) {
-      if (!LIN) nl_physical<N, T>(W, tab.tw);
+      if (!LIN) nl_physical<N, T, radix_for<N>()>(W, tab.tw);
       // epilogue (this stage's update) fused with the prologue of the next N-eval
       for (int j = threadIdx.x; j < Kc; j += T) {
         const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
@@ -231,7 +243,7 @@ __global__ void __launch_bounds__(T) k_nonlinear(const double* u_in, double* out
   __syncthreads();
   prologue_from<N, T>(W, C, tab.g);
   __syncthreads();
-  nl_physical<N, T>(W, tab.tw);
+  nl_physical<N, T, radix_for<N>()>(W, tab.tw);
   for (int j = threadIdx.x; j < Kc; j += T) {
     const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
     const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
@@ -280,7 +292,7 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
       zero_tail<N, T>(W);
       __syncthreads();
     }
-    nl_physical<N, T>(W, tab.tw);
+    nl_physical<N, T, radix_for<N>()>(W, tab.tw);
     const double wm = __ldg(tab.w + m);
     for (int j = threadIdx.x; j < Kc; j += T) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
@@ -338,9 +350,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks, un
   __syncthreads();
   if (threadIdx.x == 0) {
     ++epoch;
-    unsigned old;
-    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
-    (void)old;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     const unsigned target = epoch * nblocks;
     while (ld_acquire_gpu(bar) < target) {
     }
@@ -387,7 +397,7 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
     }
     zero_tail<N, T>(W);
     __syncthreads();
-    nl_physical<N, T>(W, tab.tw);
+    nl_physical<N, T, coarse_radix<N>()>(W, tab.tw);
     const double wA = __ldg(tab.w + mA), wB = hasB ? __ldg(tab.w + mB) : 0.0;
     for (int j = threadIdx.x; j < Kc; j += T) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
@@ -639,8 +649,7 @@ __global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters) {
 // ---------------------------------------------------------------------------------------------
 // launch wrappers (host side of this translation unit)
 // ---------------------------------------------------------------------------------------------
-template <int N>
-constexpr int threads_for() { return (3 * N / 8) > 96 ? (3 * N / 8) : 96; }
+
 
 template <int N>
 constexpr size_t fine_smem() { return sizeof(double2) * (3 * WL<N>::NP + 3 * 3 * (2 * (N / 3) + 1)); }
@@ -699,13 +708,13 @@ static cudaError_t launch_avg_n(const double* in, double* out, int S, int M, con
 template <int N, int NOWN>
 constexpr size_t coarse_smem() {
   return sizeof(double2) * (3 * WL<N>::NP + 2 * 3 * (2 * (N / 3) + 1) + NOWN * 21) +
-         sizeof(double) * (threads_for<N>() > NOWN * 6 ? threads_for<N>() : NOWN * 6);
+         sizeof(double) * (coarse_threads<N>() > NOWN * 6 ? coarse_threads<N>() : NOWN * 6);
 }
 
 template <int N, int NOWN>
 static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar,
                                             double* r_out, int grid, cudaStream_t st) {
-  constexpr int T = threads_for<N>();
+  constexpr int T = coarse_threads<N>();
   auto kfn = k_coarse_sweep<N, T, NOWN>;
   const size_t sm = coarse_smem<N, NOWN>();
   cudaError_t e = set_smem(kfn, sm);
