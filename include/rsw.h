@@ -111,7 +111,9 @@ typedef struct {
    u0: device [3][n/2+1][2].  U: device [S+1][3][n/2+1][2] (replicated, bitwise identical on every
    rank).  resid_hist: HOST double[max_iters].  iters_done: HOST.  tol <= 0: run exactly
    max_iters iterations; tol > 0: stop at the first r_k < tol (RSW_NOT_CONVERGED if none).
-   Requires 0 <= max_iters <= n_slices and n_slices divisible by the comm world size. */
+   Requires 0 <= max_iters <= n_slices and n_slices divisible by the comm world size.
+   Testing: with comm == NULL and the environment variable RSW_VIRTUAL_WORLD=P, the fine sweep runs
+   as P separate shard launches (the blocks P ranks would compute); results must be bitwise equal. */
 rsw_status parareal_iterate(const rsw_params* p, const parareal_config* cfg, const double* u0,
                             double* U, double* resid_hist, int32_t* iters_done, rsw_comm* comm,
                             void* stream);

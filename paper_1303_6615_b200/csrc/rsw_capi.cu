@@ -353,14 +353,14 @@ rsw_status run_chain(const Chain& ch, Workspace* ws, double* r_out, cudaStream_t
   rsw::CoarseArgs ca = ch.ca;
   ca.prof = nullptr;
   if (prof) {
-    CUDA_TRY(ensure(ws->prof, 64 * 4 * sizeof(unsigned long long)));
-    CUDA_TRY(cudaMemsetAsync(ws->prof.p, 0, 64 * 4 * sizeof(unsigned long long), st));
+    CUDA_TRY(ensure(ws->prof, 512 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(ws->prof.p, 0, 512 * sizeof(unsigned long long), st));
     ca.prof = (unsigned long long*)ws->prof.p;
   }
   CUDA_TRY(rsw::launch_coarse_sweep(ch.p->n, ca, ch.at, ch.M, (unsigned*)ws->bar.p, r_out, &grid, st));
   if (launches) *launches += 1;
   if (prof) {  // debug: mean phase durations over the first 64 stages (CTA 0), to stderr
-    unsigned long long h[256];
+    unsigned long long h[512];
     CUDA_TRY(cudaMemcpyAsync(h, ws->prof.p, sizeof(h), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     double a = 0, b = 0, c = 0, d = 0;
@@ -373,6 +373,10 @@ rsw_status run_chain(const Chain& ch, Workspace* ws, double* r_out, cudaStream_t
       d += h[(i + 1) * 4] - h[i * 4 + 3];
       ++cnt;
     }
+    if (h[256])
+      fprintf(stderr, "[rsw coarse n=%d] samples phase cycles: load y %llu, prologue %llu, N-eval %llu, epilogue %llu, store %llu\n",
+              ch.p->n, h[257] - h[256] - (h[258] - h[257]) * 0, h[257] - h[256], h[258] - h[257], h[259] - h[258],
+              h[260] - h[259]);
     if (cnt)
       fprintf(stderr, "[rsw coarse n=%d grid=%d] per stage (ns): samples %.0f  barrier1 %.0f  update %.0f  barrier2 %.0f\n",
               ch.p->n, grid, a / cnt, b / cnt, c / cnt, d / cnt);
@@ -603,13 +607,28 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     return s;
   rsw_status status = (cfg->tol > 0 && cfg->max_iters > 0) ? RSW_NOT_CONVERGED : RSW_OK;
   int done = 0;
+  const char* vw = getenv("RSW_VIRTUAL_WORLD");
+  const int vworld = vw ? atoi(vw) : 1;
+  if (!comm && vworld > 1 && S % vworld != 0) return fail(RSW_ERR_CONFIG, "RSW_VIRTUAL_WORLD must divide n_slices");
   int64_t fine_steps = 0;
   for (int k = 1; k <= cfg->max_iters; ++k) {
     // parfor n: F_n = φ(U^{k-1}_n) on this rank's shard
     CUDA_TRY(cudaEventRecord(ev[0], st));
-    CUDA_TRY(rsw::launch_fine(n, cfg->fine_scheme, false, U + (size_t)lo * L, F + (size_t)lo * L, hi - lo, m, h,
-                              ftab, st));
-    ++launches;
+    if (!comm && vworld > 1) {
+      // test knob RSW_VIRTUAL_WORLD=P: run the P shards' fine sweeps as separate launches into their
+      // blocks of F (what P ranks would compute before the all-gather) on this one GPU
+      for (int r = 0; r < vworld; ++r) {
+        int32_t vlo, vhi;
+        if ((s = rsw_shard_range(S, r, vworld, &vlo, &vhi)) != RSW_OK) return s;
+        CUDA_TRY(rsw::launch_fine(n, cfg->fine_scheme, false, U + (size_t)vlo * L, F + (size_t)vlo * L, vhi - vlo,
+                                  m, h, ftab, st));
+        ++launches;
+      }
+    } else {
+      CUDA_TRY(rsw::launch_fine(n, cfg->fine_scheme, false, U + (size_t)lo * L, F + (size_t)lo * L, hi - lo, m, h,
+                                ftab, st));
+      ++launches;
+    }
     fine_steps += (int64_t)(hi - lo) * m;
     CUDA_TRY(cudaEventRecord(ev[1], st));
     if (comm && world > 1) {

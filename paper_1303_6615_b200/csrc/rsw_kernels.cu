@@ -366,7 +366,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 template <int N, int T>
 __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* part, int M, const AvgTab& tab,
-                                                     double2* W, double2* C, double2* A) {
+                                                     double2* W, double2* C, double2* A, const double2* PH,
+                                                     const double* GA, const double* GP, const double* GQ,
+                                                     unsigned long long* cyc = nullptr) {
+#define STAMP(i) \
+  if (cyc && threadIdx.x == 0) cyc[i] = clock64();
+  STAMP(0)
+  // PH: this CTA's phases e^{iωτ_m} for its first pair, [2][Kc] (null: load from the table);
+  // GA/GP/GQ: geometry a, p, q per |κ| staged in shared memory
   constexpr int K = N / 3, Kc = 2 * K + 1;
   constexpr double invN = 1.0 / N;
   for (int i = threadIdx.x; i < 3 * Kc; i += T) {
@@ -378,11 +385,13 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
   for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
     const int mA = 2 * pr + 1, mB = 2 * pr + 2;
     const bool hasB = mB <= M - 1;
+    const bool cached = PH && pr == (int)blockIdx.x;
     for (int j = threadIdx.x; j < Kc; j += T) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
-      const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
-      const double2 pA = __ldg(tab.phase + (size_t)mA * (K + 1) + ak);
-      const double2 pB = hasB ? __ldg(tab.phase + (size_t)mB * (K + 1) + ak) : make_double2(1.0, 0.0);
+      const double as = kap < 0 ? -GA[ak] : GA[ak];
+      const double2 pA = cached ? PH[j] : __ldg(tab.phase + (size_t)mA * (K + 1) + ak);
+      const double2 pB = !hasB ? make_double2(1.0, 0.0)
+                               : (cached ? PH[Kc + j] : __ldg(tab.phase + (size_t)mB * (K + 1) + ak));
       double2 c[3], u[3];
       // packed eigen input: P-_{mA} y + i P-_{mB} y   (P-: α=-1 -> e^{+iωτ}, α=+1 -> e^{-iωτ})
       const double2 ym = C[j], y0 = C[Kc + j], yp = C[2 * Kc + j];
@@ -392,17 +401,19 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       c[0] = cadd(cmul(ym, pA), cmuli(bm));
       c[1] = cadd(y0, cmuli(b0));
       c[2] = cadd(cmulc(yp, pA), cmuli(bp));
-      to_prim(as, __ldg(tab.g.p + ak), __ldg(tab.g.q + ak), c, u);
+      to_prim(as, GP[ak], GQ[ak], c, u);
       put_input<N>(W, full_index(kap, N), (double)kap, u);
     }
     zero_tail<N, T>(W);
     __syncthreads();
+    STAMP(1)
     nl_physical<N, T, coarse_radix<N>()>(W, tab.tw);
+    STAMP(2)
     const double wA = __ldg(tab.w + mA), wB = hasB ? __ldg(tab.w + mB) : 0.0;
     for (int j = threadIdx.x; j < Kc; j += T) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
-      const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
-      const double p = __ldg(tab.g.p + ak), q = __ldg(tab.g.q + ak);
+      const double as = kap < 0 ? -GA[ak] : GA[ak];
+      const double p = GP[ak], q = GQ[ak];
       double2 zp[3], zm[3], na[3], nb[3], ea[3], eb[3];
       get_output<N>(W, full_index(kap, N), (double)kap, invN, zp);
       get_output<N>(W, full_index(-kap, N), (double)(-kap), invN, zm);
@@ -414,21 +425,24 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       }
       to_eigen(as, p, q, na, ea);
       to_eigen(as, p, q, nb, eb);
-      const double2 pA = __ldg(tab.phase + (size_t)mA * (K + 1) + ak);
+      const double2 pA = cached ? PH[j] : __ldg(tab.phase + (size_t)mA * (K + 1) + ak);
       A[j] = caxpy(wA, cmulc(ea[0], pA), A[j]);  // P+: α=-1 -> e^{-iωτ}, α=+1 -> e^{+iωτ}
       A[Kc + j] = caxpy(wA, ea[1], A[Kc + j]);
       A[2 * Kc + j] = caxpy(wA, cmul(ea[2], pA), A[2 * Kc + j]);
       if (hasB) {
-        const double2 pB = __ldg(tab.phase + (size_t)mB * (K + 1) + ak);
+        const double2 pB = cached ? PH[Kc + j] : __ldg(tab.phase + (size_t)mB * (K + 1) + ak);
         A[j] = caxpy(wB, cmulc(eb[0], pB), A[j]);
         A[Kc + j] = caxpy(wB, eb[1], A[Kc + j]);
         A[2 * Kc + j] = caxpy(wB, cmul(eb[2], pB), A[2 * Kc + j]);
       }
     }
     __syncthreads();  // all mirror reads of W done before the next prologue overwrites it
+    STAMP(3)
   }
   double2* P = part + (size_t)blockIdx.x * 3 * Kc;
   for (int i = threadIdx.x; i < 3 * Kc; i += T) P[i] = A[i];
+  STAMP(4)
+#undef STAMP
 }
 
 // phase 2 of one RK stage, thread-parallel over the CTA's owned modes |κ| = b + o P (o < NOWN):
@@ -437,7 +451,8 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
 // input y is published to global memory for the samples phase of every CTA.
 template <int N, int T, int NOWN>
 __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int stage, int n, double2* Vs,
-                                                    double2* KSs, double2* kk, double2* un_s, double* nd_s) {
+                                                    double2* KSs, double2* kk, double2* un_s, double* nd_s,
+                                                    double2* red_buf) {
   constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1, NW = T / 32;
   const int P = gridDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t Ls = (size_t)3 * NH;
@@ -448,21 +463,39 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
     j = (e < 3) ? ak : ((ak == 0) ? 0 : Kc - ak);
   };
   const bool last = (ca.scheme == 0) ? (stage == 4) : (stage == 2);
+  // prefetch the finalize operands (F_n, old G_n, old U_{n+1}) before the reduction's L2 round trip
+  double2 pf_F = make_double2(0.0, 0.0), pf_G = make_double2(0.0, 0.0), pf_U = make_double2(0.0, 0.0);
+  if (stage > 0 && last && threadIdx.x < NOWN * 3) {
+    const int o = threadIdx.x / 3, f = threadIdx.x % 3, ak = blockIdx.x + o * P;
+    if (ak <= K) {
+      if (ca.F) pf_F = __ldcg(reinterpret_cast<const double2*>(ca.F) + (size_t)n * Ls + f * NH + ak);
+      pf_G = reinterpret_cast<const double2*>(ca.G)[(size_t)n * Ls + f * NH + ak];
+      pf_U = reinterpret_cast<const double2*>(ca.U)[(size_t)(n + 1) * Ls + f * NH + ak];
+    }
+  }
   if (stage > 0) {
-    // deterministic reduction of the partials: one warp per item, lanes stride over parts, xor tree
-    for (int it = warp; it < NOWN * 6; it += NW) {
+    // deterministic reduction of the partials: TQ threads per item issue all their loads at once,
+    // then a fixed-order tree in shared memory
+    constexpr int ITEMS = NOWN * 6;
+    constexpr int TQ0 = T / ITEMS;
+    constexpr int TQ = TQ0 >= 32 ? 32 : TQ0 >= 16 ? 16 : TQ0 >= 8 ? 8 : TQ0 >= 4 ? 4 : TQ0 >= 2 ? 2 : 1;
+    double2* rd = reinterpret_cast<double2*>(red_buf);
+    const int it = threadIdx.x / TQ, qd = threadIdx.x % TQ;
+    if (it < ITEMS) {
       int ak, al, j;
       entry(it / 6, it % 6, ak, al, j);
-      double2 s = make_double2(0.0, 0.0);
+      double2 sacc = make_double2(0.0, 0.0);
       if (ak <= K)
-        for (int b = lane; b < ca.nparts; b += 32) s = cadd(s, __ldcg(ca.part + (size_t)b * 3 * Kc + al * Kc + j));
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
-        s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
-      }
-      if (lane == 0) kk[it] = s;
+        for (int b = qd; b < ca.nparts; b += TQ) sacc = cadd(sacc, __ldcg(ca.part + (size_t)b * 3 * Kc + al * Kc + j));
+      rd[threadIdx.x] = sacc;
     }
+    __syncthreads();
+#pragma unroll
+    for (int w = TQ / 2; w > 0; w >>= 1) {
+      if (it < ITEMS && qd < w) rd[threadIdx.x] = cadd(rd[threadIdx.x], rd[threadIdx.x + w]);
+      __syncthreads();
+    }
+    if (it < ITEMS && qd == 0) kk[it] = rd[threadIdx.x];
     __syncthreads();
     if (threadIdx.x < NOWN * 6) {
       int ak, al, j;
@@ -514,11 +547,8 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
         double2* Gst = reinterpret_cast<double2*>(ca.G) + (size_t)n * Ls + f * NH + ak;
         double2* Uo = reinterpret_cast<double2*>(ca.U) + (size_t)(n + 1) * Ls + f * NH + ak;
         double2 un = g;
-        if (ca.F) {  // U^k_{n+1} = G(U^k_n) + (F_n - G_n)   (Eq. HMM parareal iteration P:428-430)
-          const double2 Fv = __ldcg(reinterpret_cast<const double2*>(ca.F) + (size_t)n * Ls + f * NH + ak);
-          un = cadd(g, csub(Fv, *Gst));
-        }
-        const double2 d = csub(un, *Uo);
+        if (ca.F) un = cadd(g, csub(pf_F, pf_G));  // U^k_{n+1} = G(U^k_n) + (F_n - G_n)
+        const double2 d = csub(un, pf_U);
         const double wk = (ak == 0 || 2 * ak == N) ? 1.0 : 2.0;
         nd_s[threadIdx.x * 2] = wk * (d.x * d.x + d.y * d.y);
         nd_s[threadIdx.x * 2 + 1] = wk * (un.x * un.x + un.y * un.y);
@@ -577,27 +607,50 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   double2* W = smem;
   double2* C = W + 3 * WL<N>::NP;
   double2* A = C + 3 * Kc;
-  double2* Vs = A + 3 * Kc;      // [NOWN*6]
-  double2* KSs = Vs + NOWN * 6;  // [NOWN*6]
-  double2* kk = KSs + NOWN * 6;  // [NOWN*6]
-  double2* un_s = kk + NOWN * 6; // [NOWN*3]
-  double* red = reinterpret_cast<double*>(un_s + NOWN * 3);  // [max(T, NOWN*6)]
+  double2* Vs = A + 3 * Kc;       // [NOWN*6]
+  double2* KSs = Vs + NOWN * 6;   // [NOWN*6]
+  double2* kk = KSs + NOWN * 6;   // [NOWN*6]
+  double2* un_s = kk + NOWN * 6;  // [NOWN*3]
+  double2* rdb = un_s + NOWN * 3; // [T]
+  double2* PH = rdb + T;          // [2][Kc]
+  double* red = reinterpret_cast<double*>(PH + 2 * Kc);  // [max(T, NOWN*6)]
+  double* GA = red + (T > NOWN * 6 ? T : NOWN * 6);      // [K+1] each
+  double* GP = GA + (K + 1);
+  double* GQ = GP + (K + 1);
+  // per-CTA constants for the whole sweep: geometry, and the phases of this CTA's sample pair
+  for (int k = threadIdx.x; k <= K; k += T) {
+    GA[k] = __ldg(tab.g.a + k);
+    GP[k] = __ldg(tab.g.p + k);
+    GQ[k] = __ldg(tab.g.q + k);
+  }
+  const bool one_pair = (int)gridDim.x >= M / 2;
+  if (one_pair && (int)blockIdx.x < M / 2) {
+    const int mA = 2 * blockIdx.x + 1, mB = 2 * blockIdx.x + 2;
+    for (int j = threadIdx.x; j < Kc; j += T) {
+      const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+      PH[j] = __ldg(tab.phase + (size_t)mA * (K + 1) + ak);
+      PH[Kc + j] = __ldg(tab.phase + (size_t)mB * (K + 1) + ak);
+    }
+  }
+  __syncthreads();
+  const double2* PHc = one_pair ? PH : nullptr;
   const unsigned P = gridDim.x;
   const int nst = ca.scheme == 0 ? 4 : 2;
   unsigned epoch = 0;
-  const bool prof = ca.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool prof = ca.prof && blockIdx.x == 0;
   int ps = 0;
-  coarse_update_phase<N, T, NOWN>(ca, 0, 0, Vs, KSs, kk, un_s, red);  // slice 0: v = e^{ΔT D̂/2} U_0
+  coarse_update_phase<N, T, NOWN>(ca, 0, 0, Vs, KSs, kk, un_s, red, rdb);  // slice 0: v = e^{ΔT D̂/2} U_0
   grid_barrier(bar, P, epoch);
   for (int n = 0; n < ca.n_end; ++n) {
     for (int st = 1; st <= nst; ++st) {
-      if (prof && ps < 64) ca.prof[ps * 4 + 0] = gtimer();
-      coarse_samples_phase<N, T>(ca.y, const_cast<double2*>(ca.part), M, tab, W, C, A);
-      if (prof && ps < 64) ca.prof[ps * 4 + 1] = gtimer();
+      if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 0] = gtimer();
+      coarse_samples_phase<N, T>(ca.y, const_cast<double2*>(ca.part), M, tab, W, C, A, PHc, GA, GP, GQ,
+                                 (prof && ps == 8) ? ca.prof + 256 : nullptr);
+      if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 1] = gtimer();
       grid_barrier(bar, P, epoch);
-      if (prof && ps < 64) ca.prof[ps * 4 + 2] = gtimer();
-      coarse_update_phase<N, T, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red);
-      if (prof && ps < 64) ca.prof[ps * 4 + 3] = gtimer();
+      if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 2] = gtimer();
+      coarse_update_phase<N, T, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red, rdb);
+      if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 3] = gtimer();
       grid_barrier(bar, P, epoch);
       ++ps;
     }
@@ -707,8 +760,9 @@ static cudaError_t launch_avg_n(const double* in, double* out, int S, int M, con
 
 template <int N, int NOWN>
 constexpr size_t coarse_smem() {
-  return sizeof(double2) * (3 * WL<N>::NP + 2 * 3 * (2 * (N / 3) + 1) + NOWN * 21) +
-         sizeof(double) * (coarse_threads<N>() > NOWN * 6 ? coarse_threads<N>() : NOWN * 6);
+  constexpr int T = coarse_threads<N>(), K = N / 3, Kc = 2 * K + 1;
+  return sizeof(double2) * (3 * WL<N>::NP + 2 * 3 * Kc + NOWN * 21 + T + 2 * Kc) +
+         sizeof(double) * ((T > NOWN * 6 ? T : NOWN * 6) + 3 * (K + 1));
 }
 
 template <int N, int NOWN>
