@@ -88,11 +88,39 @@ __device__ __forceinline__ void dft8(double2* v) {
   v[7] = csub(e3, t3);
 }
 
+template <int SIGN>
+__device__ __forceinline__ void dft16(double2* v) {
+  // radix-2 split of two 8-point DFTs: X_q = E_q + w16^q O_q, X_{q+8} = E_q - w16^q O_q
+  const double c1 = 0.92387953251128675612818318939678829, s1 = 0.38268343236508977172845998403039887;
+  const double h = 0.70710678118654752440084436210485;
+  double2 e[8], o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    e[i] = v[2 * i];
+    o[i] = v[2 * i + 1];
+  }
+  dft8<SIGN>(e);
+  dft8<SIGN>(o);
+  const double2 w[8] = {make_double2(1.0, 0.0),      make_double2(c1, SIGN * s1),  make_double2(h, SIGN * h),
+                        make_double2(s1, SIGN * c1), make_double2(0.0, SIGN * 1.0), make_double2(-s1, SIGN * c1),
+                        make_double2(-h, SIGN * h),  make_double2(-c1, SIGN * s1)};
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    double2 t;
+    if (q == 0) t = o[0];
+    else if (q == 4) t = rot90<SIGN>(o[4]);
+    else t = cmul(o[q], w[q]);
+    v[q] = cadd(e[q], t);
+    v[q + 8] = csub(e[q], t);
+  }
+}
+
 template <int R, int SIGN>
 __device__ __forceinline__ void dftR(double2* v) {
   if constexpr (R == 2) dft2<SIGN>(v[0], v[1]);
   else if constexpr (R == 4) dft4<SIGN>(v[0], v[1], v[2], v[3]);
-  else dft8<SIGN>(v);
+  else if constexpr (R == 8) dft8<SIGN>(v);
+  else dft16<SIGN>(v);
 }
 
 // ---------------------------------------------------------------------------------------------

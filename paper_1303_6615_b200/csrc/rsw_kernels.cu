@@ -6,15 +6,25 @@
 
 namespace rsw {
 
-// FFT radix and CTA size per kernel class: radix 8 (fewer shared-memory passes) for the
-// throughput kernels (fine sweep, N̄ batch, N); radix 4 with twice the threads for the
-// latency-bound serial coarse sweep.  T = 3N/R: one radix-R butterfly of each field per thread.
+// FFT radix and CTA size, T = 3N/R (one radix-R butterfly of each field per thread), chosen from
+// measurements on B200: large transforms (n >= 512) are shared-memory-traffic bound,
+// so radix 16 (fewest passes) wins for the throughput kernels (C5 fine 5.6 -> 6.3 TFLOP/s, C4 N̄
+// 6.5 -> 7.8); at n <= 256 the kernels are latency bound and radix 4 with more threads wins (C3 fine
+// 5.4 TFLOP/s vs 4.0 at radix 16; C3 coarse stage 7.5 us vs 14.1).
 template <int N>
-__host__ __device__ constexpr int radix_for() { return N >= 512 ? 8 : 4; }
+#ifndef RSW_RADIX_FINE
+#define RSW_RADIX_FINE 0
+#endif
+#ifndef RSW_RADIX_COARSE
+#define RSW_RADIX_COARSE 0
+#endif
+__host__ __device__ constexpr int radix_for() { return RSW_RADIX_FINE ? RSW_RADIX_FINE : (N >= 512 ? 16 : 4); }
 template <int N>
 __host__ __device__ constexpr int threads_for() { return (3 * N / radix_for<N>()) > 96 ? (3 * N / radix_for<N>()) : 96; }
 template <int N>
-__host__ __device__ constexpr int coarse_radix() { return N >= 1024 ? 8 : 4; }
+__host__ __device__ constexpr int coarse_radix() {
+  return RSW_RADIX_COARSE ? RSW_RADIX_COARSE : (N >= 1024 ? 16 : N >= 512 ? 8 : 4);
+}
 template <int N>
 __host__ __device__ constexpr int coarse_threads() { return (3 * N / coarse_radix<N>()) > 96 ? (3 * N / coarse_radix<N>()) : 96; }
 
