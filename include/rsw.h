@@ -53,7 +53,9 @@ typedef enum {
 } rsw_status;
 
 enum { RSW_FINE_ETDRK4 = 0, RSW_FINE_STRANG = 1 };
-enum { RSW_COARSE_RK4 = 0, RSW_COARSE_MIDPOINT = 1 };
+enum { RSW_COARSE_RK4 = 0, RSW_COARSE_MIDPOINT = 1, RSW_COARSE_STRANG = 2 };
+/* RSW_COARSE_STRANG: standard parareal — the coarse solver is one Strang step of
+   size dT on the full equation (Alg.3 with m = 1); T0 and M are then ignored. */
 enum { RSW_FLAG_LINEAR_ONLY = 1u }; /* N ≡ 0: exact-linear test mode only */
 
 /* N(u) = -(v1 ∂x v1, v1 ∂x v2, ∂x(h v1)) for n_states independent states, evaluated

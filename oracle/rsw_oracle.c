@@ -53,7 +53,7 @@ typedef struct {
 
 enum { ORC_OK = 0, ORC_ERR_CONFIG = 1, ORC_NOT_CONVERGED = 2, ORC_ERR_DIVERGED = 3 };
 enum { ORC_FINE_ETDRK4 = 0, ORC_FINE_STRANG = 1 };
-enum { ORC_COARSE_RK4 = 0, ORC_COARSE_MIDPOINT = 1 };
+enum { ORC_COARSE_RK4 = 0, ORC_COARSE_MIDPOINT = 1, ORC_COARSE_STRANG = 2 };
 enum { ORC_FLAG_LINEAR_ONLY = 1u };
 
 static const double ORC_PI = 3.14159265358979323846264338327950288;
@@ -676,10 +676,12 @@ typedef struct {
   avg_ctx a;
   cplx (*back)[3][3]; /* e^{-(ΔT/ε) L̂(k)} */
   double *dhalf;      /* e^{-μ k^4 ΔT/2} */
+  etd_table strang;   /* standard parareal: one Strang step of size ΔT on the full eqn */
 } coarse_ctx;
 
 static void coarse_ctx_init(coarse_ctx *c, const orc_params *p, double dT, int M) {
   avg_ctx_init(&c->a, p, M);
+  etd_table_init(&c->strang, p, dT);
   const int K = c->a.K;
   c->back = malloc(sizeof(*c->back) * (size_t)(K + 1));
   c->dhalf = malloc(sizeof(double) * (size_t)(K + 1));
@@ -691,6 +693,7 @@ static void coarse_ctx_init(coarse_ctx *c, const orc_params *p, double dT, int M
 }
 static void coarse_ctx_free(coarse_ctx *c) {
   avg_ctx_free(&c->a);
+  etd_table_free(&c->strang);
   free(c->back);
   free(c->dhalf);
 }
@@ -705,6 +708,12 @@ static void coarse_one(const orc_params *p, const coarse_ctx *c, int scheme, dou
                        double T0, const cplx *u, cplx *out) {
   const int n = p->n;
   const size_t L = state_len(n);
+  if (scheme == ORC_COARSE_STRANG) {
+    /* standard parareal: the coarse solver solves the full equation with one Strang step of size
+       ΔT (Alg.3 with m = 1; "we use Strang splitting for the coarse solver") */
+    fine_one(p, ORC_FINE_STRANG, 0, &c->strang, dT, 1, u, out);
+    return;
+  }
   cplx *v = malloc(sizeof(cplx) * L * 7);
   cplx *k1 = v + L, *k2 = v + 2 * L, *k3 = v + 3 * L, *k4 = v + 4 * L, *y = v + 5 * L,
        *t = v + 6 * L;
@@ -739,7 +748,8 @@ int oracle_coarse_propagate(const orc_params *p, int32_t coarse_scheme, double d
                             int32_t M, int32_t n_states, const double *u_in, double *u_out) {
   if (!params_ok(p) || !(dT > 0) || !(T0 > 0) || M < 2 || n_states < 0 || !u_in || !u_out)
     return ORC_ERR_CONFIG;
-  if (coarse_scheme != ORC_COARSE_RK4 && coarse_scheme != ORC_COARSE_MIDPOINT)
+  if (coarse_scheme != ORC_COARSE_RK4 && coarse_scheme != ORC_COARSE_MIDPOINT &&
+      coarse_scheme != ORC_COARSE_STRANG)
     return ORC_ERR_CONFIG;
   coarse_ctx c;
   coarse_ctx_init(&c, p, dT, M);

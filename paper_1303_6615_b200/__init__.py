@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("RSW_LIB") or os.path.join(_HERE, "librsw.so")
 
 RSW_OK, RSW_ERR_CONFIG, RSW_NOT_CONVERGED, RSW_ERR_DIVERGED, RSW_ERR_CUDA, RSW_ERR_NCCL = range(6)
 FINE_ETDRK4, FINE_STRANG = 0, 1
-COARSE_RK4, COARSE_MIDPOINT = 0, 1
+COARSE_RK4, COARSE_MIDPOINT, COARSE_STRANG = 0, 1, 2
 FLAG_LINEAR_ONLY = 1
 
 # names exported by include/rsw.h (checked by tests/test_capi_load.py)

@@ -257,7 +257,7 @@ cudaError_t get_coarse(const rsw_params* p, double dT, CoarseTables** out) {
 // Workspace (per device), grown on demand
 // ---------------------------------------------------------------------------------------------
 struct Workspace {
-  DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof;
+  DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof, Gnew;
   double* rhost = nullptr;
   std::vector<cudaEvent_t> ev;
   ~Workspace() {
@@ -381,6 +381,20 @@ rsw_status run_chain(const Chain& ch, Workspace* ws, double* r_out, cudaStream_t
       fprintf(stderr, "[rsw coarse n=%d grid=%d] per stage (ns): samples %.0f  barrier1 %.0f  update %.0f  barrier2 %.0f\n",
               ch.p->n, grid, a / cnt, b / cnt, c / cnt, d / cnt);
   }
+  return RSW_OK;
+}
+
+// Standard parareal's serial sweep (NEXT-1): one Strang step of size ΔT per slice, one CTA.
+rsw_status run_strang_chain(const rsw_params* p, double dT, Workspace* ws, double* U, double* G, const double* F,
+                            int S, double* r_out, cudaStream_t st, int64_t* launches) {
+  GeomTables* g;
+  FineTables* ft;
+  CUDA_TRY(get_geom(p, &g));
+  CUDA_TRY(get_fine(p, dT, &ft));
+  CUDA_TRY(ensure(ws->Gnew, sizeof(double) * state_doubles(p->n)));
+  rsw::FineTab tab{geom_of(g), (const double2*)ft->cp.p, (const double*)ft->c0.p, (const double2*)g->tw.p};
+  CUDA_TRY(rsw::launch_strang_sweep(p->n, tab, dT, U, G, F, (double*)ws->Gnew.p, S, r_out, st));
+  if (launches) *launches += 1;
   return RSW_OK;
 }
 
@@ -515,7 +529,8 @@ rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, doub
                                 int32_t n_states, const double* u_in, double* u_out, void* stream) {
   rsw_status s = check_params(p);
   if (s != RSW_OK) return s;
-  if (coarse_scheme != RSW_COARSE_RK4 && coarse_scheme != RSW_COARSE_MIDPOINT)
+  if (coarse_scheme != RSW_COARSE_RK4 && coarse_scheme != RSW_COARSE_MIDPOINT &&
+      coarse_scheme != RSW_COARSE_STRANG)
     return fail(RSW_ERR_CONFIG, "unknown coarse scheme");
   if (!finite_pos(dT) || !finite_pos(T0)) return fail(RSW_ERR_CONFIG, "dT and T0 must be finite and > 0");
   if (M < 2) return fail(RSW_ERR_CONFIG, "M must be >= 2");
@@ -530,11 +545,16 @@ rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, doub
   CUDA_TRY(ensure(ws->Gbuf, sizeof(double) * L));
   double* Ut = (double*)ws->Ubuf.p;
   Chain ch;
-  s = setup_chain(ch, p, coarse_scheme, dT, T0, M, ws, Ut, (double*)ws->Gbuf.p, nullptr, nullptr, 1);
-  if (s != RSW_OK) return s;
+  if (coarse_scheme != RSW_COARSE_STRANG) {
+    s = setup_chain(ch, p, coarse_scheme, dT, T0, M, ws, Ut, (double*)ws->Gbuf.p, nullptr, nullptr, 1);
+    if (s != RSW_OK) return s;
+  }
   for (int i = 0; i < n_states; ++i) {
     CUDA_TRY(cudaMemcpyAsync(Ut, u_in + i * L, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
-    s = run_chain(ch, ws, nullptr, st, nullptr);
+    if (coarse_scheme == RSW_COARSE_STRANG)
+      s = run_strang_chain(p, dT, ws, Ut, (double*)ws->Gbuf.p, nullptr, 1, nullptr, st, nullptr);
+    else
+      s = run_chain(ch, ws, nullptr, st, nullptr);
     if (s != RSW_OK) return s;
     CUDA_TRY(cudaMemcpyAsync(u_out + i * L, Ut + L, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
   }
@@ -556,7 +576,8 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   if (cfg->max_iters < 0 || cfg->max_iters > S) return fail(RSW_ERR_CONFIG, "need 0 <= max_iters <= n_slices");
   if (cfg->fine_scheme != RSW_FINE_ETDRK4 && cfg->fine_scheme != RSW_FINE_STRANG)
     return fail(RSW_ERR_CONFIG, "unknown fine scheme");
-  if (cfg->coarse_scheme != RSW_COARSE_RK4 && cfg->coarse_scheme != RSW_COARSE_MIDPOINT)
+  if (cfg->coarse_scheme != RSW_COARSE_RK4 && cfg->coarse_scheme != RSW_COARSE_MIDPOINT &&
+      cfg->coarse_scheme != RSW_COARSE_STRANG)
     return fail(RSW_ERR_CONFIG, "unknown coarse scheme");
   if (!u0 || !U || !iters_done || (cfg->max_iters > 0 && !resid_hist))
     return fail(RSW_ERR_CONFIG, "NULL pointer argument");
@@ -589,11 +610,17 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
 
   // k = 0: U_0 = u0, U_{n+1} = G(U_n)   (Alg.4)
   if (U != u0) CUDA_TRY(cudaMemcpyAsync(U, u0, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
+  const bool strang_coarse = cfg->coarse_scheme == RSW_COARSE_STRANG;
   Chain ch0;
-  if ((s = setup_chain(ch0, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, nullptr, nullptr, S)))
+  if (!strang_coarse &&
+      (s = setup_chain(ch0, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, nullptr, nullptr, S)))
     return s;
   CUDA_TRY(cudaEventRecord(ev[0], st));
-  if ((s = run_chain(ch0, ws, nullptr, st, &launches))) return s;
+  if (strang_coarse) {
+    if ((s = run_strang_chain(p, cfg->dT, ws, U, G, nullptr, S, nullptr, st, &launches))) return s;
+  } else if ((s = run_chain(ch0, ws, nullptr, st, &launches))) {
+    return s;
+  }
   CUDA_TRY(cudaEventRecord(ev[1], st));
   {
     float ms;
@@ -602,8 +629,8 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     coarse_ms += ms;
   }
   Chain ch;
-  if ((s = setup_chain(ch, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, F, (double*)ws->rparts.p,
-                       S)))
+  if (!strang_coarse && (s = setup_chain(ch, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, F,
+                                         (double*)ws->rparts.p, S)))
     return s;
   rsw_status status = (cfg->tol > 0 && cfg->max_iters > 0) ? RSW_NOT_CONVERGED : RSW_OK;
   int done = 0;
@@ -638,7 +665,11 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     }
     CUDA_TRY(cudaEventRecord(ev[2], st));
     // serial sweep: U^k_{n+1} = G(U^k_n) + (F_n - G_n)
-    if ((s = run_chain(ch, ws, (double*)ws->rdev.p, st, &launches))) return s;
+    if (strang_coarse) {
+      if ((s = run_strang_chain(p, cfg->dT, ws, U, G, F, S, (double*)ws->rdev.p, st, &launches))) return s;
+    } else if ((s = run_chain(ch, ws, (double*)ws->rdev.p, st, &launches))) {
+      return s;
+    }
     CUDA_TRY(cudaEventRecord(ev[3], st));
     CUDA_TRY(cudaMemcpyAsync(ws->rhost, ws->rdev.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));

@@ -54,6 +54,8 @@ cudaError_t launch_avg_states(int n, const double* in, double* out, int S, int M
                               cudaStream_t st);
 cudaError_t launch_coarse_sweep(int n, const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar, double* r_out,
                                 int* grid_used, cudaStream_t st);
+cudaError_t launch_strang_sweep(int n, const FineTab& tab, double h, double* U, double* G, const double* F,
+                                double* Gnew, int S, double* r_out, cudaStream_t st);
 cudaError_t launch_dfma_peak(double* out, int blocks, int iters, cudaStream_t st);
 
 }  // namespace rsw

@@ -693,6 +693,102 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Standard parareal (NEXT-1): the coarse solver is ONE Strang step of size ΔT on the
+// full equation (Alg.3 with m = 1).  The serial sweep is a single CTA: per slice one Strang step
+// (2 N-evals, the state in the real lane of the packed pair), the parareal update
+// U_{n+1} = G + (F_n - G_n), G_n <- G, and the per-slice residual; r_k = max_n at the end.
+// ---------------------------------------------------------------------------------------------
+template <int N, int T>
+__global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h, double* U, double* G,
+                                                     const double* F, double* Gnew, int S, double* r_out) {
+  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
+  constexpr double invN = 1.0 / N;
+  extern __shared__ double2 smem[];
+  double2* W = smem;
+  double2* S1 = W + 3 * WL<N>::NP;
+  __shared__ double red[2][T];
+  __shared__ double rmax;
+  if (threadIdx.x == 0) rmax = 0.0;
+  const size_t L = (size_t)3 * NH * 2;
+  for (int n = 0; n < S; ++n) {
+    load_pair_eigen<N, T>(U + (size_t)n * L, nullptr, tab.g, S1);
+    __syncthreads();
+    for (int j = threadIdx.x; j < Kc; j += T) {  // v = E2 c
+      const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+#pragma unroll
+      for (int al = 0; al < 3; ++al)
+        S1[al * Kc + j] = dmul(al - 1, __ldg(tab.cp + 1 * (K + 1) + ak), __ldg(tab.c0 + 1 * (K + 1) + ak),
+                               S1[al * Kc + j]);
+    }
+    __syncthreads();
+    prologue_from<N, T>(W, S1, tab.g);
+    __syncthreads();
+    for (int st = 0; st < 2; ++st) {
+      nl_physical<N, T, radix_for<N>()>(W, tab.tw);
+      for (int j = threadIdx.x; j < Kc; j += T) {
+        const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+        const int kf = full_index(kap, N);
+        const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
+        const double p = __ldg(tab.g.p + ak), q = __ldg(tab.g.q + ak);
+        double2 nh[3], nn[3], x[3];
+        get_output<N>(W, kf, (double)kap, invN, nh);
+        to_eigen(as, p, q, nh, nn);
+#pragma unroll
+        for (int al = 0; al < 3; ++al) {
+          const int e = al * Kc + j;
+          if (st == 0) {
+            x[al] = caxpy(0.5 * h, nn[al], S1[e]);  // midpoint input v + (h/2) N(v)
+          } else {
+            const double2 w = caxpy(h, nn[al], S1[e]);  // w = v + h N(mid)
+            S1[e] = dmul(al - 1, __ldg(tab.cp + 1 * (K + 1) + ak), __ldg(tab.c0 + 1 * (K + 1) + ak), w);
+          }
+        }
+        if (st == 0) {
+          double2 u[3];
+          to_prim(as, p, q, x, u);
+          put_input<N>(W, kf, (double)kap, u);
+        }
+      }
+      if (st == 0) zero_tail<N, T>(W);
+      __syncthreads();
+    }
+    store_pair_prim<N, T>(S1, tab.g, Gnew, nullptr);
+    __syncthreads();
+    // parareal update and residual (R12) over the half spectrum
+    const double2* gn = reinterpret_cast<const double2*>(Gnew);
+    double2* Go = reinterpret_cast<double2*>(G) + (size_t)n * 3 * NH;
+    double2* Uo = reinterpret_cast<double2*>(U) + (size_t)(n + 1) * 3 * NH;
+    const double2* Fn = F ? reinterpret_cast<const double2*>(F) + (size_t)n * 3 * NH : nullptr;
+    double num = 0.0, den = 0.0;
+    for (int i = threadIdx.x; i < 3 * NH; i += T) {
+      const int k = i % NH;
+      const double2 g = gn[i];
+      const double2 un = Fn ? cadd(g, csub(Fn[i], Go[i])) : g;
+      const double2 d = csub(un, Uo[i]);
+      const double wk = (k == 0 || 2 * k == N) ? 1.0 : 2.0;
+      num += wk * (d.x * d.x + d.y * d.y);
+      den += wk * (un.x * un.x + un.y * un.y);
+      Go[i] = g;
+      Uo[i] = un;
+    }
+    red[0][threadIdx.x] = num;
+    red[1][threadIdx.x] = den;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0;
+      for (int t = 0; t < T; ++t) {
+        a += red[0][t];
+        b += red[1][t];
+      }
+      const double r = sqrt(a / b);
+      rmax = (r != r || rmax != rmax) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(rmax, r);
+    }
+    __syncthreads();
+  }
+  if (r_out && threadIdx.x == 0) *r_out = rmax;
+}
+
 // M0: DFMA peak probe — independent FMA chains, every SM
 __global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters) {
   double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
@@ -820,6 +916,18 @@ static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab
   return cudaErrorInvalidConfiguration;
 }
 
+template <int N>
+static cudaError_t launch_strang_sweep_n(const FineTab& tab, double h, double* U, double* G, const double* F,
+                                         double* Gnew, int S, double* r_out, cudaStream_t st) {
+  constexpr int T = threads_for<N>();
+  auto kfn = k_strang_sweep<N, T>;
+  const size_t sm = nl_smem<N>();
+  cudaError_t e = set_smem(kfn, sm);
+  if (e != cudaSuccess) return e;
+  kfn<<<1, T, sm, st>>>(tab, h, U, G, F, Gnew, S, r_out);
+  return cudaGetLastError();
+}
+
 #define RSW_DISPATCH(n, CALL)                  \
   switch (n) {                                 \
     case 16: return CALL(16);                  \
@@ -852,6 +960,12 @@ cudaError_t launch_avg_states(int n, const double* in, double* out, int S, int M
 cudaError_t launch_coarse_sweep(int n, const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar, double* r_out,
                                 int* grid_used, cudaStream_t st) {
 #define C(NN) launch_coarse_sweep_n<NN>(ca, tab, M, bar, r_out, grid_used, st)
+  RSW_DISPATCH(n, C)
+#undef C
+}
+cudaError_t launch_strang_sweep(int n, const FineTab& tab, double h, double* U, double* G, const double* F,
+                                double* Gnew, int S, double* r_out, cudaStream_t st) {
+#define C(NN) launch_strang_sweep_n<NN>(tab, h, U, G, F, Gnew, S, r_out, st)
   RSW_DISPATCH(n, C)
 #undef C
 }

@@ -115,6 +115,34 @@ def initial_state(w: Workload, seed: int = 0) -> np.ndarray:
     raise KeyError(w.name)
 
 
+def paper_initial_state(n: int) -> np.ndarray:
+    """The paper's initial condition (Eq. initial condition 1-1): v1 = v2 = 0,
+    h = c1 (e^{-4(x-π/2)^2} sin(3(x-π/2)) + e^{-2(x-π)^2} sin(8(x-π))) + c0 with c0, c1 chosen so that
+    ∫h = 0 and max|h| = 1 (on the grid; P:1151 writes "c1 and c2", read as c1, c0 — R17)."""
+    x = 2.0 * np.pi * np.arange(n) / n
+    g = (np.exp(-4.0 * (x - np.pi / 2) ** 2) * np.sin(3.0 * (x - np.pi / 2))
+         + np.exp(-2.0 * (x - np.pi) ** 2) * np.sin(8.0 * (x - np.pi)))
+    g = g - g.mean()
+    h = g / np.abs(g).max()
+    c = np.zeros((3, n // 2 + 1), complex)
+    c[2] = np.fft.rfft(h) / n
+    c[2, n // 3 + 1:] = 0.0
+    c[2, 0] = 0.0
+    return _pack(c)
+
+
+# The paper's experiments (P:1196-1331) as parareal workloads; grid n = 128 (not stated in the
+# paper; SPEC's default).  T = number of slices x ΔT with the paper's slice counts.
+PAPER_EXPERIMENTS = {
+    "eps1e-2": dict(eps=1e-2, dT=0.5, dt=1.0 / 2500, n_slices=1250, T0=1.5, M=450,
+                    standard_dT=(4e-2, 5e-2)),                      # P:1196-1234 (T0 = 150 ε, R4/R17)
+    "eps1e-1": dict(eps=1e-1, dT=0.3, dt=1.0 / 250, n_slices=150, T0=0.5, M=10,
+                    standard_dT=(0.1, 0.2)),                        # P:1293-1319
+    "eps1": dict(eps=1.0, dT=0.3, dt=1.0 / 200, n_slices=60, T0=0.3, M=10,
+                 standard_dT=(0.3, 0.4)),                           # P:1321-1331
+}
+
+
 def random_states(n: int, batch: int, seed: int = 0, kmax: int | None = None,
                   decay: float = 3.0, zero_mean_uv: bool = True, scale: float = 1.0) -> np.ndarray:
     """û_{b,f,k} = scale (1+k)^-decay (z0 + i z1), k = 1..kmax;  k = 0: v1, v2 = 0, h = z (C4 recipe)."""

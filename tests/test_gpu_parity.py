@@ -242,3 +242,35 @@ def test_small_M(rsw_gpu, orc, M):
 def test_fp64_peak_probe(rsw_gpu):
     v = rsw_gpu.fp64_peak_tflops()
     assert 10.0 < v < 45.0  # B200 FP64: 148 SMs x 64 FMA/clk x 2 x <= 1.965 GHz = 37.2 TFLOP/s
+
+
+# ------------------------------------------------------ NEXT-1: standard parareal, Strang coarse
+@pytest.mark.parametrize("k", [1, 3])
+def test_standard_parareal_strang_coarse(rsw_gpu, orc, k):
+    """Standard parareal: coarse = one Strang step of size ΔT on the full equation."""
+    w = inputs.C1
+    u0 = inputs.initial_state(w)
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=k, coarse_scheme=2)
+    g = rsw_gpu.parareal_iterate(P(rsw_gpu, w.eps, w.F, w.mu, w.n), dev(u0), want_FG=True, **kw)
+    r = orc.parareal(u0, w.eps, w.F, w.mu, w.n, want_FG=True, **kw)
+    assert rel_l2(to_np(g["U"]), r["U"], w.n)[1:].max() < TOL
+    assert rel_l2(to_np(g["G"]), r["G"], w.n).max() < TOL
+    assert np.allclose(g["resid"], r["resid"], rtol=1e-8, atol=0)
+    gc = to_np(rsw_gpu.coarse_propagate(P(rsw_gpu, w.eps, w.F, w.mu, w.n), dev(u0[None]), w.dT, w.T0, w.M, 2))
+    assert rel_l2(gc, orc.coarse_propagate(u0[None], w.eps, w.F, w.mu, w.n, w.dT, w.T0, w.M, 2), w.n).max() < TOL
+
+
+# ------------------------------------------------ NEXT-2: the paper's experiments (truncated)
+@pytest.mark.parametrize("name,coarse", [("eps1e-1", 1), ("eps1e-1", 2), ("eps1", 1)])
+def test_paper_experiment_prefix(rsw_gpu, orc, name, coarse):
+    """The paper's IC and parameters, first 12 slices, 2 iterations:
+    GPU = oracle for the paper's midpoint slow solver (Alg.2) and for standard parareal."""
+    cfg = inputs.PAPER_EXPERIMENTS[name]
+    n = 64
+    u0 = inputs.paper_initial_state(n)
+    dT = cfg["dT"] if coarse != 2 else cfg["standard_dT"][0]
+    kw = dict(dT=dT, dt=cfg["dt"], T0=cfg["T0"], M=cfg["M"], n_slices=12, max_iters=2, coarse_scheme=coarse)
+    g = rsw_gpu.parareal_iterate(P(rsw_gpu, cfg["eps"], 1.0, 1e-4, n), dev(u0), **kw)
+    r = orc.parareal(u0, cfg["eps"], 1.0, 1e-4, n, **kw)
+    assert rel_l2(to_np(g["U"]), r["U"], n)[1:].max() < TOL
+    assert np.allclose(g["resid"], r["resid"], rtol=1e-8, atol=0)

@@ -401,3 +401,19 @@ def test_parareal_converges_and_stops(orc):
     res = r["resid"]
     assert all(res[i + 1] < 0.3 * res[i] for i in range(len(res) - 1)), res
     assert r["iters"] == 4 and res[-1] < 5e-4 <= res[-2] and r["status"] == 0
+
+
+def test_standard_parareal_exact_after_S(orc):
+    """NEXT-1, standard parareal with a Strang coarse solver: the same telescoping
+    identity holds (U^S_n = serial fine), and the coarse step is one Strang step of the full eqn."""
+    w = inputs.C1
+    u0 = inputs.initial_state(w)
+    S = 4
+    ser = [u0]
+    for _ in range(S):
+        ser.append(orc.fine_propagate(ser[-1], w.eps, w.F, w.mu, w.n, w.dT, w.dt))
+    r = orc.parareal(u0, w.eps, w.F, w.mu, w.n, dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=S, max_iters=S,
+                     coarse_scheme=2)
+    assert rel_l2(r["U"][1:], np.stack(ser[1:]), w.n).max() < 1e-13
+    g = orc.coarse_propagate(u0, w.eps, w.F, w.mu, w.n, w.dT, w.T0, w.M, scheme=2)
+    assert rel_l2(g, orc.fine_propagate(u0, w.eps, w.F, w.mu, w.n, w.dT, w.dT, scheme=1), w.n) == 0.0
