@@ -105,7 +105,7 @@ def cpu_baseline(w, steps_per_slice: int = 0, target_s: float = 15.0):
     u = np.repeat(u0[None], cores, axis=0)
     if not steps_per_slice:
         t0 = time.perf_counter()
-        oracle.fine_propagate(u, w.eps, w.F, w.mu, w.n, w.dt_eff, w.dt_eff * (1 + 1e-12), 0)
+        oracle.fine_propagate(u, w.eps, w.F, w.mu, w.n, w.dt_eff, w.dt_eff, 0)
         steps_per_slice = max(1, int(target_s / max(time.perf_counter() - t0, 1e-6)))
     steps = steps_per_slice
     dT = steps * w.dt_eff
