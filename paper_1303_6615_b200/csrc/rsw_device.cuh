@@ -115,12 +115,50 @@ __device__ __forceinline__ void dft16(double2* v) {
   }
 }
 
+template <int SIGN>
+__device__ __forceinline__ void dft32(double2* v) {
+  // radix-2 split of two 16-point DFTs: X_q = E_q + w32^q O_q, X_{q+16} = E_q - w32^q O_q
+  double2 e[16], o[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    e[i] = v[2 * i];
+    o[i] = v[2 * i + 1];
+  }
+  dft16<SIGN>(e);
+  dft16<SIGN>(o);
+  // cos / sin (2π q/32), q = 0..8
+  const double c[9] = {1.0,
+                       0.98078528040323044912618223613424,
+                       0.92387953251128675612818318939679,
+                       0.83146961230254523707878837761791,
+                       0.70710678118654752440084436210485,
+                       0.55557023301960222474283081394853,
+                       0.38268343236508977172845998403040,
+                       0.19509032201612826784828486847702,
+                       0.0};
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    double2 t;
+    if (q == 0) t = o[0];
+    else if (q == 8) t = rot90<SIGN>(o[8]);
+    else {
+      // w32^q = e^{SIGN 2πi q/32} = (cos, SIGN sin); for q > 8 use cos(θ) = -sin(θ - π/2) symmetry
+      const double cr = q <= 8 ? c[q] : -c[16 - q];
+      const double si = q <= 8 ? c[8 - q] : c[q - 8];
+      t = cmul(o[q], make_double2(cr, SIGN * si));
+    }
+    v[q] = cadd(e[q], t);
+    v[q + 16] = csub(e[q], t);
+  }
+}
+
 template <int R, int SIGN>
 __device__ __forceinline__ void dftR(double2* v) {
   if constexpr (R == 2) dft2<SIGN>(v[0], v[1]);
   else if constexpr (R == 4) dft4<SIGN>(v[0], v[1], v[2], v[3]);
   else if constexpr (R == 8) dft8<SIGN>(v);
-  else dft16<SIGN>(v);
+  else if constexpr (R == 16) dft16<SIGN>(v);
+  else dft32<SIGN>(v);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -245,6 +283,295 @@ __device__ __forceinline__ void nl_physical(double2* W, const double2* __restric
   }
   __syncthreads();
   fft3<N, T, -1, RMAX>(W, tw);  // analysis (unnormalised)
+}
+
+// ---------------------------------------------------------------------------------------------
+// Register-resident FFT core of the N-eval (replaces the smem round trip per pass of fft3):
+//   thread t < 3N/R owns field f = t / (N/R) and column j = t % (N/R) and keeps R values in
+//   registers through every pass; a pass of radix r <= R does R/r butterflies per thread.
+//   Stockham autosort: in every pass thread j reads the index set {j + i N/R + s N/r} and
+//   butterfly jb = j + i N/R writes (jb/NS) NS r + jb%NS + s NS.  Passes are separated by ONE
+//   barrier (ping-pong between X and Y).  The radix sequence is a palindrome (the small radix in
+//   the middle), so synthesis pass q and analysis pass q have the same (r, NS): they share one
+//   twiddle table, packed per pass as [k][s-1] (consecutive k -> odd stride r-1 -> no bank
+//   conflicts), and the last synthesis pass and the first analysis pass have the same radix and
+//   index set, so the products are formed in registers; only v1 is shared with the v2x / h
+//   threads through one barrier-separated copy.
+//   Buffers: double2[3][N], element i of a field at swz(i) (XOR swizzle inside groups of 8:
+//   every exchange pattern of the core is free of bank conflicts, tools/model_conflicts.py).
+//   in : X = (v̂1, iκ v̂2, ĥ) at the retained full indices (others are never read: pruned zeros)
+//   out: X = N * DFT(q_f) at the retained full indices, q = (v1²/2, v1 v2x, h v1) per lane.
+// Barriers: 2 * passes (the last one makes the output visible to the caller's mode loop).
+// ---------------------------------------------------------------------------------------------
+__host__ __device__ __forceinline__ constexpr int swz(int i) { return (i & ~7) | ((i ^ (i >> 3) ^ (i >> 6)) & 7); }
+
+template <int N, int R>
+__host__ __device__ constexpr int fft_npass() {
+  int m = 0;
+  for (int n = 1; n < N; n *= R) ++m;
+  return m;
+}
+template <int N, int R>
+__host__ __device__ constexpr int fft_rad(int p) {  // radix of pass p (palindrome: small radix in the middle)
+  constexpr int m = fft_npass<N, R>();
+  int small = N;
+  for (int q = 0; q < m - 1; ++q) small /= R;
+  return (p == (m - 1) / 2) ? small : R;
+}
+template <int N, int R>
+__host__ __device__ constexpr bool fft_palindrome() {
+  constexpr int m = fft_npass<N, R>();
+  for (int p = 0; p < m; ++p)
+    if (fft_rad<N, R>(p) != fft_rad<N, R>(m - 1 - p)) return false;
+  return true;
+}
+template <int N, int R>
+__host__ __device__ constexpr int fft_ns(int p) {  // product of the radices before pass p
+  int ns = 1;
+  for (int q = 0; q < p; ++q) ns *= fft_rad<N, R>(q);
+  return ns;
+}
+// packed twiddles of pass p >= 1: TW[(NS_p - r_0) + k (r_p - 1) + s - 1] = e^{-2πi s k / (NS_p r_p)}
+template <int N, int R>
+__host__ __device__ constexpr int fft_tw_size() { return N - fft_rad<N, R>(0); }
+
+// fill the packed table from the plain table tw[m] = e^{-2πi m/N} (all threads of the CTA)
+template <int N, int R, int T>
+__device__ __forceinline__ void fill_packed_twiddles(double2* TW, const double2* __restrict__ tw) {
+  constexpr int m = fft_npass<N, R>(), r0 = fft_rad<N, R>(0);
+  for (int i = threadIdx.x; i < fft_tw_size<N, R>(); i += T) {
+    int p = 1;
+    while (p < m - 1 && i >= fft_ns<N, R>(p + 1) - r0) ++p;
+    const int NS = fft_ns<N, R>(p), r = fft_rad<N, R>(p), o = i - (NS - r0);
+    const int k = o / (r - 1), s = o % (r - 1) + 1;
+    TW[i] = __ldg(tw + s * k * (N / (NS * r)));
+  }
+}
+
+template <int N, int R, int r>
+__device__ __forceinline__ int core_idx(int j, int t) {  // index held in v[t] (t = i r + s) by a radix-r pass
+  return j + (t / r) * (N / R) + (t % r) * (N / r);
+}
+
+template <int N, int R, int p, int SIGN>
+__device__ __forceinline__ void core_math(double2 (&v)[R], int j, const double2* TW) {
+  constexpr int r = fft_rad<N, R>(p), NS = fft_ns<N, R>(p);
+#pragma unroll
+  for (int i = 0; i < R / r; ++i) {
+    if constexpr (NS > 1) {
+      const int k = (j + i * (N / R)) & (NS - 1);
+      const double2* tp = TW + (NS - fft_rad<N, R>(0)) + k * (r - 1) - 1;
+#pragma unroll
+      for (int s = 1; s < r; ++s) {
+        const double2 w = tp[s];  // shared-memory table
+        v[i * r + s] = SIGN < 0 ? cmul(v[i * r + s], w) : cmulc(v[i * r + s], w);
+      }
+    }
+    dftR<r, SIGN>(&v[i * r]);
+  }
+}
+
+template <int N, int R, int p>
+__device__ __forceinline__ void core_store(const double2 (&v)[R], double2* B, int j) {
+  constexpr int r = fft_rad<N, R>(p), NS = fft_ns<N, R>(p);
+#pragma unroll
+  for (int i = 0; i < R / r; ++i) {
+    const int jb = j + i * (N / R);
+    const int base = (jb / NS) * NS * r + (jb & (NS - 1));
+#pragma unroll
+    for (int s = 0; s < r; ++s) B[swz(base + s * NS)] = v[i * r + s];
+  }
+}
+
+template <int N, int R, int r>
+__device__ __forceinline__ void core_load(double2 (&v)[R], const double2* B, int j) {
+#pragma unroll
+  for (int t = 0; t < R; ++t) v[t] = B[swz(core_idx<N, R, r>(j, t))];
+}
+
+// synthesis passes p..m-1 (p >= 1): load from B[p%2], compute, store to B[(p+1)%2] unless last
+template <int N, int R, int p>
+__device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* const (&B)[2], int f, int j, bool act,
+                                             const double2* TW) {
+  constexpr int m = fft_npass<N, R>();
+  if constexpr (p < m) {
+    if (act) {
+      core_load<N, R, fft_rad<N, R>(p)>(v, B[p % 2] + f * N, j);
+      core_math<N, R, p, +1>(v, j, TW);
+      if constexpr (p < m - 1) core_store<N, R, p>(v, B[(p + 1) % 2] + f * N, j);
+    }
+    if constexpr (p < m - 1) {
+      __syncthreads();
+      core_inverse<N, R, p + 1>(v, B, f, j, act, TW);
+    }
+  }
+}
+
+// analysis passes q..m-1 (q >= 1; analysis pass q runs the (r, NS) of synthesis pass q): load from
+// Z_{q-1} = B[(m-1+q-1)%2]; the last pass stores the retained outputs to B[0]
+template <int N, int R, int q>
+__device__ __forceinline__ void core_forward(double2 (&v)[R], double2* const (&B)[2], int f, int j, bool act,
+                                             const double2* TW) {
+  constexpr int m = fft_npass<N, R>();
+  if constexpr (q < m) {
+    constexpr int r = fft_rad<N, R>(q);
+    constexpr int K = N / 3;
+    if (act) {
+      core_load<N, R, r>(v, B[(m - 1 + q - 1) % 2] + f * N, j);
+      core_math<N, R, q, -1>(v, j, TW);
+      double2* out = B[(q == m - 1) ? 0 : (m - 1 + q) % 2] + f * N;
+      if constexpr (q < m - 1) {
+        core_store<N, R, q>(v, out, j);
+      } else {  // final pass: NS = N/r, butterfly jb writes jb + s N/r = core_idx; retained modes only
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+          const int o = core_idx<N, R, r>(j, t);
+          if (o <= K || o >= N - K) out[swz(o)] = v[t];
+        }
+      }
+    }
+    __syncthreads();
+    core_forward<N, R, q + 1>(v, B, f, j, act, TW);
+  }
+}
+
+template <int N, int R, int T>
+__device__ __forceinline__ void nl_core(double2* X, double2* Y, const double2* TW) {
+  static_assert(T >= 3 * (N / R), "nl_core: T must cover 3 N/R field-columns");
+  static_assert(fft_palindrome<N, R>(), "nl_core: radix sequence must be a palindrome");
+  constexpr int m = fft_npass<N, R>(), NJ = N / R, K = N / 3;
+  constexpr int r0 = fft_rad<N, R>(0);
+  double2* const B[2] = {X, Y};
+  const int t = threadIdx.x, f = t / NJ, j = t % NJ;
+  const bool act = t < 3 * NJ;
+  double2 v[R];
+  // synthesis pass 0 (NS = 1, no twiddles): retained inputs only, the rest is zero (R10)
+  if (act) {
+    const double2* in = X + f * N;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int i = core_idx<N, R, r0>(j, s);
+      v[s] = (i <= K || i >= N - K) ? in[swz(i)] : make_double2(0.0, 0.0);
+    }
+    core_math<N, R, 0, +1>(v, j, TW);
+    if constexpr (m > 1) core_store<N, R, 0>(v, Y + f * N, j);
+  }
+  if constexpr (m > 1) {
+    __syncthreads();
+    core_inverse<N, R, 1>(v, B, f, j, act, TW);
+  }
+  // products on the grid: v1 shared through B[m%2] (not read by the last synthesis pass);
+  // the last synthesis pass has radix r0 (palindrome) and the index set of analysis pass 0
+  double2* VB = B[m % 2];
+  if (act && f == 0) {
+#pragma unroll
+    for (int s = 0; s < R; ++s) VB[swz(core_idx<N, R, r0>(j, s))] = v[s];
+  }
+  __syncthreads();
+  if (act) {
+    if (f == 0) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) v[s] = make_double2(0.5 * v[s].x * v[s].x, 0.5 * v[s].y * v[s].y);
+    } else {
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const double2 v1 = VB[swz(core_idx<N, R, r0>(j, s))];
+        v[s] = make_double2(v1.x * v[s].x, v1.y * v[s].y);
+      }
+    }
+    // analysis pass 0: radix r0, NS = 1, operands already in registers
+    core_math<N, R, 0, -1>(v, j, TW);
+    double2* out = B[(m == 1) ? 0 : (m - 1) % 2] + f * N;
+    if constexpr (m > 1) {
+      core_store<N, R, 0>(v, out, j);
+    } else {
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int o = core_idx<N, R, r0>(j, s);
+        if (o <= K || o >= N - K) out[swz(o)] = v[s];
+      }
+    }
+  }
+  __syncthreads();
+  if constexpr (m > 1) core_forward<N, R, 1>(v, B, f, j, act, TW);
+}
+
+// N-eval input / output of one retained entry in the swizzled layout of nl_core
+template <int N>
+__device__ __forceinline__ void put_input_z(double2* X, int k_full, double kap, const double2* u) {
+  const int i = swz(k_full);
+  X[i] = u[0];
+  X[N + i] = cmuli(cscale(u[1], kap));
+  X[2 * N + i] = u[2];
+}
+template <int N>
+__device__ __forceinline__ void get_output_z(const double2* X, int k_full, double kap, double invN, double2* nh) {
+  const int i = swz(k_full);
+  const double2 Q0 = cscale(X[i], invN), Q1 = cscale(X[N + i], invN), Q2 = cscale(X[2 * N + i], invN);
+  nh[0] = cmulmi(cscale(Q0, kap));  // -iκ Q0
+  nh[1] = make_double2(-Q1.x, -Q1.y);
+  nh[2] = cmulmi(cscale(Q2, kap));  // -iκ Q2
+}
+
+// ---------------------------------------------------------------------------------------------
+// Tensor memory (TMEM, 512 columns x 128 lanes x 32 bit per SM) used as thread-private storage
+// for the per-mode integrator state: a warp reaches the 32 lanes 32 (warp % 4) .. +31 of its
+// quarter, each thread its own lane, so a (lane, column range) slot is private to one thread.
+// This frees the shared memory the state would take (98 KB per CTA at n = 1024) for the
+// coefficient / twiddle tables.  Shape 32x32b: thread i of the warp moves consecutive 32-bit
+// columns of lane base + i.  All tcgen05 ops below are warp-collective (.sync.aligned).
+// ---------------------------------------------------------------------------------------------
+template <int C>
+__host__ __device__ constexpr int tmem_cols_pow2() {
+  return C <= 32 ? 32 : C <= 64 ? 64 : C <= 128 ? 128 : C <= 256 ? 256 : 512;
+}
+template <int NCOL>
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {  // by one whole warp
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(slot);
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s), "n"(NCOL) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int NCOL>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {  // by the allocating warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOL) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// one complex double = 4 columns; load / store 3 complex (12 columns) starting at taddr
+__device__ __forceinline__ void tmem_ld3(uint32_t taddr, double2 (&x)[3]) {
+  uint32_t r[12];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
+               : "r"(taddr + 8)
+               : "memory");
+  tmem_wait_ld();
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    x[a] = make_double2(__hiloint2double(r[4 * a + 1], r[4 * a]), __hiloint2double(r[4 * a + 3], r[4 * a + 2]));
+}
+__device__ __forceinline__ void tmem_st3(uint32_t taddr, const double2 (&x)[3]) {
+  uint32_t r[12];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    r[4 * a] = __double2loint(x[a].x);
+    r[4 * a + 1] = __double2hiint(x[a].x);
+    r[4 * a + 2] = __double2loint(x[a].y);
+    r[4 * a + 3] = __double2hiint(x[a].y);
+  }
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr + 8), "r"(r[8]),
+               "r"(r[9]), "r"(r[10]), "r"(r[11])
+               : "memory");
 }
 
 // prologue helper: write prim(x) of entry j into W as the N-eval input (v1, iκ v2, h)

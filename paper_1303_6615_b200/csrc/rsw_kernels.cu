@@ -4,6 +4,8 @@
 #include "rsw_internal.h"
 #include "rsw_device.cuh"
 
+#include <cstdlib>
+
 namespace rsw {
 
 // FFT radix and CTA size, T = 3N/R (one radix-R butterfly of each field per thread), chosen from
@@ -21,6 +23,19 @@ template <int N>
 __host__ __device__ constexpr int radix_for() { return RSW_RADIX_FINE ? RSW_RADIX_FINE : (N >= 512 ? 16 : 4); }
 template <int N>
 __host__ __device__ constexpr int threads_for() { return (3 * N / radix_for<N>()) > 96 ? (3 * N / radix_for<N>()) : 96; }
+// register FFT core (nl_core): R values per thread, T = 3N/R threads (>= 32)
+template <int N>
+__host__ __device__ constexpr int fine_radix() { return N <= 32 ? 4 : N <= 256 ? 8 : 16; }  // palindromic
+template <int N, int R>
+__host__ __device__ constexpr int core_threads() { return (3 * (N / R) + 31) / 32 * 32; }
+static int fine_radix_override() {
+  static int r = -1;
+  if (r < 0) {
+    const char* e = getenv("RSW_FINE_RADIX");
+    r = e ? atoi(e) : 0;
+  }
+  return r;
+}
 template <int N>
 __host__ __device__ constexpr int coarse_radix() {
   return RSW_RADIX_COARSE ? RSW_RADIX_COARSE : (N >= 1024 ? 16 : N >= 512 ? 8 : 4);
@@ -130,52 +145,107 @@ __device__ __forceinline__ void prologue_from(double2* W, const double2* X, cons
 //   which is u+ = E u + f1 Nu + f2 (Na + Nb) + f3 Nc with a, b, c' as in Cox–Matthews.
 //   Strang (Alg.3 + R7): v = E2 c;  m = v + (h/2) N(v);  w = v + h N(m);  c+ = E2 w.
 // ---------------------------------------------------------------------------------------------
-template <int N, int T, int SCHEME, bool LIN>
+template <int N, int R, int T>
+struct FineLayout {  // dynamic shared memory of k_fine (double2 units first, then doubles)
+  static constexpr int K = N / 3, KP = K + 1;
+  static constexpr int W = 0, Y = W + 3 * N, TW = Y + 3 * N, CP = TW + fft_tw_size<N, R>(), D = CP + 6 * KP;
+  static constexpr int C0 = 0, GA = C0 + 6 * KP, GP = GA + KP, GQ = GP + KP, ND = GQ + KP;      // double offsets
+  static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
+  static constexpr int Kc = 2 * K + 1, OMAX = (Kc + T - 1) / T, NGRP = (T + 127) / 128;
+  static constexpr int NCOL = tmem_cols_pow2<NGRP * OMAX * 36>();  // TMEM columns (S1, S0, S2 per mode slot)
+};
+
+template <int N, int R, int T, int SCHEME, bool LIN>
 __global__ void __launch_bounds__(T) k_fine(const double* u_in, double* u_out, int n_slices, int m_steps,
                                             double h, const FineTab tab) {
-  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
+  using LY = FineLayout<N, R, T>;
+  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1, KP = K + 1, OMAX = LY::OMAX;
   constexpr double invN = 1.0 / N;
   extern __shared__ double2 smem[];
-  double2* W = smem;
-  double2* S0 = W + 3 * WL<N>::NP;
-  double2* S1 = S0 + 3 * Kc;
-  double2* S2 = S1 + 3 * Kc;
+  double2* W = smem + LY::W;   // N-eval input / output (natural order, padded)
+  double2* Y = smem + LY::Y;   // ping-pong partner of the register FFT core
+  double2* sTW = smem + LY::TW;
+  double2* sCP = smem + LY::CP;
+  double* sd = reinterpret_cast<double*>(smem + LY::D);
+  double* sC0 = sd + LY::C0;
+  double* sGA = sd + LY::GA;
+  double* sGP = sd + LY::GP;
+  double* sGQ = sd + LY::GQ;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<LY::NCOL>(&tslot);
+  // per-configuration tables into shared memory (read every stage)
+  fill_packed_twiddles<N, R, T>(sTW, tab.tw);
+  for (int i = threadIdx.x; i < 6 * KP; i += T) {
+    sCP[i] = __ldg(tab.cp + i);
+    sC0[i] = __ldg(tab.c0 + i);
+  }
+  for (int i = threadIdx.x; i < KP; i += T) {
+    sGA[i] = __ldg(tab.g.a + i);
+    sGP[i] = __ldg(tab.g.p + i);
+    sGQ[i] = __ldg(tab.g.q + i);
+  }
   const int sA = 2 * blockIdx.x, sB = sA + 1;
   const size_t L = (size_t)3 * NH * 2;
   const double* inB = (sB < n_slices) ? u_in + sB * L : nullptr;
-  load_pair_eigen<N, T>(u_in + sA * L, inB, tab.g, S1);
+  load_pair_eigen<N, T>(u_in + sA * L, inB, tab.g, W);  // C[α][j] staged in W
+  tmem_fence_before();
   __syncthreads();
-
-  if (SCHEME == 1) {  // Strang prologue: S1 = v = E2 c
-    for (int j = threadIdx.x; j < Kc; j += T) {
-      const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+  tmem_fence_after();
+  // thread-private TMEM slot of mode slot o: columns o*36 + {S1: 0, S0: 12, S2: 24} + 4α
+  const uint32_t tb = tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * OMAX * 36);
+  double2 c0v[OMAX][3];
 #pragma unroll
-      for (int al = 0; al < 3; ++al)
-        S1[al * Kc + j] = dmul(al - 1, __ldg(tab.cp + 1 * (K + 1) + ak), __ldg(tab.c0 + 1 * (K + 1) + ak),
-                               S1[al * Kc + j]);
+  for (int o = 0; o < OMAX; ++o) {
+    const int j = threadIdx.x + o * T;
+#pragma unroll
+    for (int al = 0; al < 3; ++al) c0v[o][al] = (j < Kc) ? W[al * Kc + j] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();  // C fully read before W receives the first N-eval input
+#pragma unroll
+  for (int o = 0; o < OMAX; ++o) {
+    const int j = threadIdx.x + o * T;
+    const int jj = j < Kc ? j : 0;
+    const int kap = kappa_of(jj, K), ak = kap < 0 ? -kap : kap;
+    if (SCHEME == 1) {  // Strang prologue: S1 = v = E2 c
+#pragma unroll
+      for (int al = 0; al < 3; ++al) c0v[o][al] = dmul(al - 1, sCP[1 * KP + ak], sC0[1 * KP + ak], c0v[o][al]);
     }
-    __syncthreads();
+    tmem_st3(tb + o * 36, c0v[o]);
+    if (!LIN && j < Kc) {
+      const double as = kap < 0 ? -sGA[ak] : sGA[ak];
+      double2 u[3];
+      to_prim(as, sGP[ak], sGQ[ak], c0v[o], u);
+      put_input_z<N>(W, full_index(kap, N), (double)kap, u);
+    }
   }
-  if (!LIN) {
-    prologue_from<N, T>(W, S1, tab.g);
-    __syncthreads();
-  }
+  tmem_wait_st();
+  __syncthreads();
 
   const int nst = (SCHEME == 0) ? 4 : 2;
   for (int step = 0; step < m_steps; ++step) {
     const bool last_step = (step == m_steps - 1);
     for (int st = 0; st < nst; ++st) {
-      if (!LIN) nl_physical<N, T, radix_for<N>()>(W, tab.tw);
+      if (!LIN) nl_core<N, R, T>(W, Y, sTW);
       // epilogue (this stage's update) fused with the prologue of the next N-eval
-      for (int j = threadIdx.x; j < Kc; j += T) {
-        const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+#pragma unroll
+      for (int o = 0; o < OMAX; ++o) {
+        const int j = threadIdx.x + o * T;
+        const bool valid = j < Kc;
+        const int jj = valid ? j : 0;
+        const int kap = kappa_of(jj, K), ak = kap < 0 ? -kap : kap;
         const int kf = full_index(kap, N);
-        const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
-        const double p = __ldg(tab.g.p + ak), q = __ldg(tab.g.q + ak);
+        const uint32_t ts = tb + o * 36;
+        double2 s1[3], s0[3], s2[3];
+        tmem_ld3(ts, s1);                                            // S1 (every stage)
+        if (SCHEME == 0 && st == 1) tmem_ld3(ts + 12, s0);           // S0 = E2 c
+        if (SCHEME == 0 && st == 2) tmem_ld3(ts + 24, s2);           // S2 = E2 a - Q Nu
+        const double as = kap < 0 ? -sGA[ak] : sGA[ak];
+        const double p = sGP[ak], q = sGQ[ak];
         double2 nn[3];
-        if (!LIN) {
+        if (!LIN && valid) {
           double2 nh[3];
-          get_output<N>(W, kf, (double)kap, invN, nh);
+          get_output_z<N>(W, kf, (double)kap, invN, nh);
           to_eigen(as, p, q, nh, nn);
         } else {
 #pragma unroll
@@ -184,56 +254,76 @@ __global__ void __launch_bounds__(T) k_fine(const double* u_in, double* u_out, i
         double2 x[3];
 #pragma unroll
         for (int al = 0; al < 3; ++al) {
-          const int alpha = al - 1, e = al * Kc + j;
+          const int alpha = al - 1;
           // coefficient i of |κ|: 0 E, 1 E2, 2 Q, 3 f1, 4 f2, 5 f3
-#define CP(i) __ldg(tab.cp + (i) * (K + 1) + ak)
-#define C0(i) __ldg(tab.c0 + (i) * (K + 1) + ak)
+#define CP(i) sCP[(i) * KP + ak]
+#define C0(i) sC0[(i) * KP + ak]
           if (SCHEME == 0) {
             if (st == 0) {
-              const double2 c = S1[e];
+              const double2 c = s1[al];
               const double2 e2c = dmul(alpha, CP(1), C0(1), c);
               const double2 qn = dmul(alpha, CP(2), C0(2), nn[al]);
               const double2 a = cadd(e2c, qn);
-              S0[e] = e2c;
-              S1[e] = cadd(dmul(alpha, CP(0), C0(0), c), dmul(alpha, CP(3), C0(3), nn[al]));
-              S2[e] = csub(dmul(alpha, CP(1), C0(1), a), qn);
+              s0[al] = e2c;
+              s1[al] = cadd(dmul(alpha, CP(0), C0(0), c), dmul(alpha, CP(3), C0(3), nn[al]));
+              s2[al] = csub(dmul(alpha, CP(1), C0(1), a), qn);
               x[al] = a;
             } else if (st == 1) {
-              x[al] = cadd(S0[e], dmul(alpha, CP(2), C0(2), nn[al]));
-              S1[e] = cadd(S1[e], dmul(alpha, CP(4), C0(4), nn[al]));
+              x[al] = cadd(s0[al], dmul(alpha, CP(2), C0(2), nn[al]));
+              s1[al] = cadd(s1[al], dmul(alpha, CP(4), C0(4), nn[al]));
             } else if (st == 2) {
-              x[al] = cadd(S2[e], cscale(dmul(alpha, CP(2), C0(2), nn[al]), 2.0));
-              S1[e] = cadd(S1[e], dmul(alpha, CP(4), C0(4), nn[al]));
+              x[al] = cadd(s2[al], cscale(dmul(alpha, CP(2), C0(2), nn[al]), 2.0));
+              s1[al] = cadd(s1[al], dmul(alpha, CP(4), C0(4), nn[al]));
             } else {
-              const double2 c = cadd(S1[e], dmul(alpha, CP(5), C0(5), nn[al]));
-              S1[e] = c;
-              x[al] = c;
+              s1[al] = cadd(s1[al], dmul(alpha, CP(5), C0(5), nn[al]));
+              x[al] = s1[al];
             }
           } else {
             if (st == 0) {
-              x[al] = caxpy(0.5 * h, nn[al], S1[e]);  // m = v + (h/2) N(v)
+              x[al] = caxpy(0.5 * h, nn[al], s1[al]);  // m = v + (h/2) N(v)
             } else {
-              const double2 w = caxpy(h, nn[al], S1[e]);          // w = v + h N(m)
-              const double2 c = dmul(alpha, CP(1), C0(1), w);      // c+ = E2 w
-              const double2 v = last_step ? c : dmul(alpha, CP(1), C0(1), c);  // next v = E2 c+
-              S1[e] = v;
-              x[al] = v;
+              const double2 w = caxpy(h, nn[al], s1[al]);                     // w = v + h N(m)
+              const double2 c = dmul(alpha, CP(1), C0(1), w);                 // c+ = E2 w
+              s1[al] = last_step ? c : dmul(alpha, CP(1), C0(1), c);          // next v = E2 c+
+              x[al] = s1[al];
             }
           }
 #undef CP
 #undef C0
         }
-        if (!LIN) {
+        if (SCHEME == 0 || st == 1) tmem_st3(ts, s1);
+        if (SCHEME == 0 && st == 0) {
+          tmem_st3(ts + 12, s0);
+          tmem_st3(ts + 24, s2);
+        }
+        if (!LIN && valid) {
           double2 u[3];
           to_prim(as, p, q, x, u);
-          put_input<N>(W, kf, (double)kap, u);
+          put_input_z<N>(W, kf, (double)kap, u);
         }
       }
-      if (!LIN) zero_tail<N, T>(W);
+      tmem_wait_st();
       __syncthreads();
     }
   }
-  store_pair_prim<N, T>(S1, tab.g, u_out + sA * L, (sB < n_slices) ? u_out + sB * L : nullptr);
+  // final state S1 -> C[α][j] in Y (W may still hold the last stage's inputs), then store
+#pragma unroll
+  for (int o = 0; o < OMAX; ++o) {
+    const int j = threadIdx.x + o * T;
+    double2 s1[3];
+    tmem_ld3(tb + o * 36, s1);
+    if (j < Kc) {
+#pragma unroll
+      for (int al = 0; al < 3; ++al) Y[al * Kc + j] = s1[al];
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc<LY::NCOL>(tslot);
+  }
+  store_pair_prim<N, T>(Y, tab.g, u_out + sA * L, (sB < n_slices) ? u_out + sB * L : nullptr);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -811,8 +901,6 @@ __global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters) {
 
 
 template <int N>
-constexpr size_t fine_smem() { return sizeof(double2) * (3 * WL<N>::NP + 3 * 3 * (2 * (N / 3) + 1)); }
-template <int N>
 constexpr size_t nl_smem() { return sizeof(double2) * (3 * WL<N>::NP + 3 * (2 * (N / 3) + 1)); }
 template <int N>
 constexpr size_t avg_smem() { return sizeof(double2) * (3 * WL<N>::NP + 2 * 3 * (2 * (N / 3) + 1)); }
@@ -823,16 +911,16 @@ static cudaError_t set_smem(KernelT k, size_t bytes) {
   return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <int N>
-static cudaError_t launch_fine_n(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
-                                 const FineTab& tab, cudaStream_t st) {
-  constexpr int T = threads_for<N>();
+template <int N, int R>
+static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
+                                  const FineTab& tab, cudaStream_t st) {
+  constexpr int T = core_threads<N, R>();
   const int grid = (S + 1) / 2;
-  const size_t sm = fine_smem<N>();
+  const size_t sm = FineLayout<N, R, T>::bytes;
   cudaError_t e;
 #define LAUNCH_FINE(SC, LN)                                                  \
   {                                                                           \
-    auto kfn = k_fine<N, T, SC, LN>;                                          \
+    auto kfn = k_fine<N, R, T, SC, LN>;                                       \
     if ((e = set_smem(kfn, sm)) != cudaSuccess) return e;                     \
     kfn<<<grid, T, sm, st>>>(in, out, S, m, h, tab);                          \
   }
@@ -842,6 +930,21 @@ static cudaError_t launch_fine_n(int scheme, bool lin, const double* in, double*
   else LAUNCH_FINE(1, true)
 #undef LAUNCH_FINE
   return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_fine_n(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
+                                 const FineTab& tab, cudaStream_t st) {
+  const int r = fine_radix_override();
+  if constexpr (N == 256) {  // measured alternatives (RSW_FINE_RADIX, benchmarking only)
+    if (r == 4) return launch_fine_nr<N, 4>(scheme, lin, in, out, S, m, h, tab, st);
+    if (r == 16) return launch_fine_nr<N, 16>(scheme, lin, in, out, S, m, h, tab, st);
+  }
+  if constexpr (N == 1024) {
+    if (r == 4) return launch_fine_nr<N, 4>(scheme, lin, in, out, S, m, h, tab, st);
+    if (r == 32) return launch_fine_nr<N, 32>(scheme, lin, in, out, S, m, h, tab, st);
+  }
+  return launch_fine_nr<N, fine_radix<N>()>(scheme, lin, in, out, S, m, h, tab, st);
 }
 
 template <int N>
