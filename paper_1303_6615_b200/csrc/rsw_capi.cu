@@ -257,7 +257,7 @@ cudaError_t get_coarse(const rsw_params* p, double dT, CoarseTables** out) {
 // Workspace (per device), grown on demand
 // ---------------------------------------------------------------------------------------------
 struct Workspace {
-  DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof, Gnew;
+  DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof, Gnew, yin;
   double* rhost = nullptr;
   std::vector<cudaEvent_t> ev;
   ~Workspace() {
@@ -319,6 +319,7 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   const int K = p->n / 3, Kc = 2 * K + 1, np = coarse_parts(M, p->n);
   CUDA_TRY(ensure(ws->part, sizeof(double2) * (size_t)np * 3 * Kc));
   CUDA_TRY(ensure(ws->vky, sizeof(double2) * 3 * 3 * (size_t)Kc));
+  CUDA_TRY(ensure(ws->yin, sizeof(double2) * 3 * 3 * (size_t)Kc));
   ch.p = p;
   ch.scheme = scheme;
   ch.M = M;
@@ -335,6 +336,7 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   ca.v = (double2*)ws->vky.p;
   ca.ks = ca.v + 3 * Kc;
   ca.y = ca.v + 6 * Kc;
+  ca.yin = (double2*)ws->yin.p;
   ca.U = U;
   ca.G = G;
   ca.F = F;

@@ -39,6 +39,7 @@ struct CoarseArgs {
   double2* v;           // [3][Kc]
   double2* ks;          // [3][Kc]
   double2* y;           // [3][Kc]
+  double2* yin;         // [3][3][Kc] triple-buffered stage input (sentinel = not yet written)
   double* U;            // [S+1][3][N/2+1][2] (chain states)
   double* G;            // [S][3][N/2+1][2]
   const double* F;      // [S][...] or null (k = 0 sweep / plain coarse step)

@@ -37,11 +37,11 @@ static int fine_radix_override() {
   return r;
 }
 template <int N>
-__host__ __device__ constexpr int coarse_radix() {
-  return RSW_RADIX_COARSE ? RSW_RADIX_COARSE : (N >= 1024 ? 16 : N >= 512 ? 8 : 4);
+__host__ __device__ constexpr int coarse_radix() {  // palindromic; latency-bound (one pair per SM)
+  return RSW_RADIX_COARSE ? RSW_RADIX_COARSE : (N <= 32 ? 4 : N <= 256 ? 8 : 16);
 }
 template <int N>
-__host__ __device__ constexpr int coarse_threads() { return (3 * N / coarse_radix<N>()) > 96 ? (3 * N / coarse_radix<N>()) : 96; }
+__host__ __device__ constexpr int coarse_threads() { return core_threads<N, coarse_radix<N>()>() > 192 ? core_threads<N, coarse_radix<N>()>() : 192; }
 
 // ---------------------------------------------------------------------------------------------
 // shared helpers: load a pair of half-spectrum states into packed eigen coordinates, and store
@@ -464,20 +464,46 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int N, int T>
+// Stage input through a triple-buffered shared array (replaces "owners write y -> grid barrier ->
+// everyone loads y"): update phase u writes its owned entries of the next stage input into
+// ybuf[u%3] (each entry once) and resets the same entries of ybuf[(u+2)%3] to the sentinel; the
+// samples phase polls ybuf[u%3] until no entry holds the sentinel.  Safe without fences: each
+// 8-byte half is single-copy atomic; the reset of ybuf[(u+2)%3] happens after every reader of it
+// (samples phase u-1) passed the release/acquire grid barrier before update u, and it is ordered
+// before any reader of ybuf[(u+2)%3] (samples phase u+2) by the grid barrier after samples u+1.
+constexpr unsigned long long YIN_SENTINEL = 0x7FF4DEADBEEF0001ull;  // a signalling-NaN payload arithmetic never produces
+__device__ __forceinline__ double2 ld_relaxed_v2(const double2* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_v2(double2* p, double2 v) {
+  asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ bool is_sentinel(double x) { return (unsigned long long)__double_as_longlong(x) == YIN_SENTINEL; }
+__device__ __forceinline__ double2 yin_sentinel() {
+  const double s = __longlong_as_double((long long)YIN_SENTINEL);
+  return make_double2(s, s);
+}
+
+template <int N, int R, int T>
 __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* part, int M, const AvgTab& tab,
-                                                     double2* W, double2* C, double2* A, const double2* PH,
+                                                     double2* X, double2* Y, const double2* TW, double2* C,
+                                                     double2* A, const double2* PH, const double* SW,
                                                      const double* GA, const double* GP, const double* GQ,
                                                      unsigned long long* cyc = nullptr) {
 #define STAMP(i) \
   if (cyc && threadIdx.x == 0) cyc[i] = clock64();
   STAMP(0)
-  // PH: this CTA's phases e^{iωτ_m} for its first pair, [2][Kc] (null: load from the table);
-  // GA/GP/GQ: geometry a, p, q per |κ| staged in shared memory
-  constexpr int K = N / 3, Kc = 2 * K + 1;
+  // PH: this CTA's phases e^{iωτ_m} for its first pair, [2][K+1] (null: load from the table);
+  // SW: its weights w_mA, w_mB; GA/GP/GQ: geometry a, p, q per |κ| staged in shared memory
+  constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
   constexpr double invN = 1.0 / N;
+  // stage input from this CTA's inbox (y = inbox row): poll, keep, reset to the sentinel
   for (int i = threadIdx.x; i < 3 * Kc; i += T) {
-    C[i] = __ldcg(y + i);
+    double2 v = ld_relaxed_v2(y + i);
+    while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(y + i);
+    C[i] = v;
     A[i] = make_double2(0.0, 0.0);
   }
   __syncthreads();
@@ -489,9 +515,8 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
     for (int j = threadIdx.x; j < Kc; j += T) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
       const double as = kap < 0 ? -GA[ak] : GA[ak];
-      const double2 pA = cached ? PH[j] : __ldg(tab.phase + (size_t)mA * (K + 1) + ak);
-      const double2 pB = !hasB ? make_double2(1.0, 0.0)
-                               : (cached ? PH[Kc + j] : __ldg(tab.phase + (size_t)mB * (K + 1) + ak));
+      const double2 pA = cached ? PH[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
+      const double2 pB = !hasB ? make_double2(1.0, 0.0) : (cached ? PH[KP + ak] : __ldg(tab.phase + (size_t)mB * KP + ak));
       double2 c[3], u[3];
       // packed eigen input: P-_{mA} y + i P-_{mB} y   (P-: α=-1 -> e^{+iωτ}, α=+1 -> e^{-iωτ})
       const double2 ym = C[j], y0 = C[Kc + j], yp = C[2 * Kc + j];
@@ -502,21 +527,20 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       c[1] = cadd(y0, cmuli(b0));
       c[2] = cadd(cmulc(yp, pA), cmuli(bp));
       to_prim(as, GP[ak], GQ[ak], c, u);
-      put_input<N>(W, full_index(kap, N), (double)kap, u);
+      put_input_z<N>(X, full_index(kap, N), (double)kap, u);
     }
-    zero_tail<N, T>(W);
     __syncthreads();
     STAMP(1)
-    nl_physical<N, T, coarse_radix<N>()>(W, tab.tw);
+    nl_core<N, R, T>(X, Y, TW);
     STAMP(2)
-    const double wA = __ldg(tab.w + mA), wB = hasB ? __ldg(tab.w + mB) : 0.0;
+    const double wA = cached ? SW[0] : __ldg(tab.w + mA), wB = hasB ? (cached ? SW[1] : __ldg(tab.w + mB)) : 0.0;
     for (int j = threadIdx.x; j < Kc; j += T) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
       const double as = kap < 0 ? -GA[ak] : GA[ak];
       const double p = GP[ak], q = GQ[ak];
       double2 zp[3], zm[3], na[3], nb[3], ea[3], eb[3];
-      get_output<N>(W, full_index(kap, N), (double)kap, invN, zp);
-      get_output<N>(W, full_index(-kap, N), (double)(-kap), invN, zm);
+      get_output_z<N>(X, full_index(kap, N), (double)kap, invN, zp);
+      get_output_z<N>(X, full_index(-kap, N), (double)(-kap), invN, zm);
 #pragma unroll
       for (int f = 0; f < 3; ++f) {  // unpack: N_A(κ) = (Z(κ) + conj Z(-κ))/2, N_B = (Z - conj Z(-κ))/(2i)
         const double2 zc = cconj(zm[f]);
@@ -525,18 +549,18 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       }
       to_eigen(as, p, q, na, ea);
       to_eigen(as, p, q, nb, eb);
-      const double2 pA = cached ? PH[j] : __ldg(tab.phase + (size_t)mA * (K + 1) + ak);
+      const double2 pA = cached ? PH[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
       A[j] = caxpy(wA, cmulc(ea[0], pA), A[j]);  // P+: α=-1 -> e^{-iωτ}, α=+1 -> e^{+iωτ}
       A[Kc + j] = caxpy(wA, ea[1], A[Kc + j]);
       A[2 * Kc + j] = caxpy(wA, cmul(ea[2], pA), A[2 * Kc + j]);
       if (hasB) {
-        const double2 pB = cached ? PH[Kc + j] : __ldg(tab.phase + (size_t)mB * (K + 1) + ak);
+        const double2 pB = cached ? PH[KP + ak] : __ldg(tab.phase + (size_t)mB * KP + ak);
         A[j] = caxpy(wB, cmulc(eb[0], pB), A[j]);
         A[Kc + j] = caxpy(wB, eb[1], A[Kc + j]);
         A[2 * Kc + j] = caxpy(wB, cmul(eb[2], pB), A[2 * Kc + j]);
       }
     }
-    __syncthreads();  // all mirror reads of W done before the next prologue overwrites it
+    __syncthreads();  // all mirror reads of X done before the next prologue overwrites it
     STAMP(3)
   }
   double2* P = part + (size_t)blockIdx.x * 3 * Kc;
@@ -549,10 +573,20 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
 // items i = o*6 + e, entries e = (α, +κ) for e < 3, (α, -κ) for e >= 3.  The stage base v and the RK
 // accumulator ks of owned modes live in this CTA's shared memory for the whole sweep; the stage
 // input y is published to global memory for the samples phase of every CTA.
+template <int N, int NOWN, int T>
+__device__ __forceinline__ void push_stage_input(const CoarseArgs& ca, const double2* yv, const int* yidx, unsigned u) {
+  constexpr int Kc3 = 3 * (2 * (N / 3) + 1);
+  __syncthreads();
+  if (threadIdx.x < NOWN * 6 && yidx[threadIdx.x] >= 0) {
+    st_relaxed_v2(ca.yin + (size_t)(u % 3) * Kc3 + yidx[threadIdx.x], yv[threadIdx.x]);
+    st_relaxed_v2(ca.yin + (size_t)((u + 2) % 3) * Kc3 + yidx[threadIdx.x], yin_sentinel());
+  }
+}
+
 template <int N, int T, int NOWN>
 __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int stage, int n, double2* Vs,
                                                     double2* KSs, double2* kk, double2* un_s, double* nd_s,
-                                                    double2* red_buf) {
+                                                    double2* red_buf, double2* yv, int* yidx, unsigned ucount) {
   constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1, NW = T / 32;
   const int P = gridDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t Ls = (size_t)3 * NH;
@@ -605,7 +639,8 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
         const double2 k = kk[it];
         double2& V = Vs[it];
         double2& KS = KSs[it];
-        double2* Y = ca.y + al * Kc + j;
+        double2* Y = yv + it;
+        yidx[it] = last ? -1 : al * Kc + j;
         if (ca.scheme == 0) {  // classical RK4 (R6): (k1 + 2k2 + 2k3 + k4) accumulated in this order
           if (stage == 1) {
             KS = k;
@@ -624,10 +659,15 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
           if (stage == 1) *Y = caxpy(0.5 * dT, k, V);
           else V = caxpy(dT, k, V);
         }
+      } else {
+        yidx[it] = -1;
       }
     }
+    if (!last) {
+      push_stage_input<N, NOWN, T>(ca, yv, yidx, ucount);
+      return;
+    }
     __syncthreads();
-    if (!last) return;
     // finalize: D half step, back-transform, primitive G, parareal update (thread per (o, f))
     if (threadIdx.x < NOWN * 3) {
       const int o = threadIdx.x / 3, f = threadIdx.x % 3, ak = blockIdx.x + o * P;
@@ -693,31 +733,53 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
       to_eigen(e < 3 ? a : -a, p, q, u, c);
       const double2 v = cscale(c[al], __ldg(ca.dhalf + ak));
       Vs[it] = v;
-      ca.y[al * Kc + j] = v;
+      yv[it] = v;
+      yidx[it] = al * Kc + j;
+    } else {
+      yidx[it] = -1;
     }
   }
+  push_stage_input<N, NOWN, T>(ca, yv, yidx, ucount);
   __syncthreads();
 }
 
-template <int N, int T, int NOWN>
+template <int N, int R, int T, int NOWN>
+struct CoarseLayout {  // dynamic shared memory of k_coarse_sweep (double2 units, then doubles)
+  static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NR = (T > NOWN * 6 ? T : NOWN * 6);
+  static constexpr int X = 0, Y = X + 3 * N, TW = Y + 3 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc,
+                       VS = A + 3 * Kc, KS = VS + NOWN * 6, KK = KS + NOWN * 6, UN = KK + NOWN * 6,
+                       RDB = UN + NOWN * 3, PH = RDB + T, YV = PH + 2 * KP, D = YV + NOWN * 6;
+  static constexpr int RED = 0, GA = RED + NR, GP = GA + KP, GQ = GP + KP, SW = GQ + KP, YI = SW + 2,
+                       ND = YI + NOWN * 6;  // YI: int entry indices stored in double slots
+  static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
+};
+
+template <int N, int R, int T, int NOWN>
 __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const AvgTab tab, int M, unsigned* bar,
                                                     double* r_out) {
-  constexpr int K = N / 3, Kc = 2 * K + 1;
+  using LY = CoarseLayout<N, R, T, NOWN>;
+  constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
   extern __shared__ double2 smem[];
-  double2* W = smem;
-  double2* C = W + 3 * WL<N>::NP;
-  double2* A = C + 3 * Kc;
-  double2* Vs = A + 3 * Kc;       // [NOWN*6]
-  double2* KSs = Vs + NOWN * 6;   // [NOWN*6]
-  double2* kk = KSs + NOWN * 6;   // [NOWN*6]
-  double2* un_s = kk + NOWN * 6;  // [NOWN*3]
-  double2* rdb = un_s + NOWN * 3; // [T]
-  double2* PH = rdb + T;          // [2][Kc]
-  double* red = reinterpret_cast<double*>(PH + 2 * Kc);  // [max(T, NOWN*6)]
-  double* GA = red + (T > NOWN * 6 ? T : NOWN * 6);      // [K+1] each
-  double* GP = GA + (K + 1);
-  double* GQ = GP + (K + 1);
-  // per-CTA constants for the whole sweep: geometry, and the phases of this CTA's sample pair
+  double2* X = smem + LY::X;
+  double2* Y = smem + LY::Y;
+  double2* TW = smem + LY::TW;
+  double2* C = smem + LY::C;
+  double2* A = smem + LY::A;
+  double2* Vs = smem + LY::VS;    // [NOWN*6]
+  double2* KSs = smem + LY::KS;   // [NOWN*6]
+  double2* kk = smem + LY::KK;    // [NOWN*6]
+  double2* un_s = smem + LY::UN;  // [NOWN*3]
+  double2* rdb = smem + LY::RDB;  // [T]
+  double2* PH = smem + LY::PH;    // [2][K+1]
+  double* sd = reinterpret_cast<double*>(smem + LY::D);
+  double* red = sd + LY::RED;     // [max(T, NOWN*6)]
+  double* GA = sd + LY::GA;       // [K+1] each
+  double* GP = sd + LY::GP;
+  double* GQ = sd + LY::GQ;
+  double* SW = sd + LY::SW;       // [2]
+  // per-CTA constants for the whole sweep: geometry, twiddles, and the phases / weights of this
+  // CTA's sample pair
+  fill_packed_twiddles<N, R, T>(TW, tab.tw);
   for (int k = threadIdx.x; k <= K; k += T) {
     GA[k] = __ldg(tab.g.a + k);
     GP[k] = __ldg(tab.g.p + k);
@@ -726,35 +788,45 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   const bool one_pair = (int)gridDim.x >= M / 2;
   if (one_pair && (int)blockIdx.x < M / 2) {
     const int mA = 2 * blockIdx.x + 1, mB = 2 * blockIdx.x + 2;
-    for (int j = threadIdx.x; j < Kc; j += T) {
-      const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
-      PH[j] = __ldg(tab.phase + (size_t)mA * (K + 1) + ak);
-      PH[Kc + j] = __ldg(tab.phase + (size_t)mB * (K + 1) + ak);
+    for (int k = threadIdx.x; k <= K; k += T) {
+      PH[k] = __ldg(tab.phase + (size_t)mA * KP + k);
+      PH[KP + k] = __ldg(tab.phase + (size_t)mB * KP + k);
+    }
+    if (threadIdx.x == 0) {
+      SW[0] = __ldg(tab.w + mA);
+      SW[1] = mB <= M - 1 ? __ldg(tab.w + mB) : 0.0;
     }
   }
   __syncthreads();
   const double2* PHc = one_pair ? PH : nullptr;
+  double2* yv = smem + LY::YV;
+  int* yidx = reinterpret_cast<int*>(sd + LY::YI);
   const unsigned P = gridDim.x;
+  constexpr int Kc3 = 3 * Kc;
   const int nst = ca.scheme == 0 ? 4 : 2;
-  unsigned epoch = 0;
+  unsigned epoch = 0, ucount = 0;
   const bool prof = ca.prof && blockIdx.x == 0;
   int ps = 0;
-  coarse_update_phase<N, T, NOWN>(ca, 0, 0, Vs, KSs, kk, un_s, red, rdb);  // slice 0: v = e^{ΔT D̂/2} U_0
+  // the three stage-input buffers start empty (sentinel) before anyone writes
+  for (int i = blockIdx.x * T + threadIdx.x; i < 3 * Kc3; i += P * T) st_relaxed_v2(ca.yin + i, yin_sentinel());
   grid_barrier(bar, P, epoch);
+  coarse_update_phase<N, T, NOWN>(ca, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount);  // slice 0: v = e^{ΔT D̂/2} U_0
   for (int n = 0; n < ca.n_end; ++n) {
     for (int st = 1; st <= nst; ++st) {
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 0] = gtimer();
-      coarse_samples_phase<N, T>(ca.y, const_cast<double2*>(ca.part), M, tab, W, C, A, PHc, GA, GP, GQ,
-                                 (prof && ps == 8) ? ca.prof + 256 : nullptr);
+      const double2* inbox = ca.yin + (size_t)(ucount % 3) * Kc3;
+      coarse_samples_phase<N, R, T>(inbox, const_cast<double2*>(ca.part), M, tab, X, Y, TW, C, A, PHc, SW, GA, GP, GQ,
+                                    (prof && ps == 8) ? ca.prof + 256 : nullptr);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 1] = gtimer();
       grid_barrier(bar, P, epoch);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 2] = gtimer();
-      coarse_update_phase<N, T, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red, rdb);
+      ++ucount;
+      coarse_update_phase<N, T, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 3] = gtimer();
-      grid_barrier(bar, P, epoch);
       ++ps;
     }
   }
+  grid_barrier(bar, P, epoch);  // every slice's U, G and residual partials are written
   if (r_out && blockIdx.x == 0) {  // r_k = max_n sqrt(Σ num / Σ den) over slices (fixed order)
     double mx = 0.0;
     bool bad = false;
@@ -967,19 +1039,28 @@ static cudaError_t launch_avg_n(const double* in, double* out, int S, int M, con
   return cudaGetLastError();
 }
 
-template <int N, int NOWN>
-constexpr size_t coarse_smem() {
-  constexpr int T = coarse_threads<N>(), K = N / 3, Kc = 2 * K + 1;
-  return sizeof(double2) * (3 * WL<N>::NP + 2 * 3 * Kc + NOWN * 21 + T + 2 * Kc) +
-         sizeof(double) * ((T > NOWN * 6 ? T : NOWN * 6) + 3 * (K + 1));
+static int coarse_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RSW_COARSE_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
-template <int N, int NOWN>
+template <int N, int NOWN, int R = coarse_radix<N>(), int T = coarse_threads<N>()>
 static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar,
                                             double* r_out, int grid, cudaStream_t st) {
-  constexpr int T = coarse_threads<N>();
-  auto kfn = k_coarse_sweep<N, T, NOWN>;
-  const size_t sm = coarse_smem<N, NOWN>();
+  if constexpr (N == 256 && R == coarse_radix<N>() && T == coarse_threads<N>()) {  // measured alternatives
+    const int v = coarse_variant();
+    if (v == 1) return launch_coarse_sweep_nown<N, NOWN, 8, 96>(ca, tab, M, bar, r_out, grid, st);
+    if (v == 2) return launch_coarse_sweep_nown<N, NOWN, 4, 192>(ca, tab, M, bar, r_out, grid, st);
+    if (v == 3) return launch_coarse_sweep_nown<N, NOWN, 16, 192>(ca, tab, M, bar, r_out, grid, st);
+    if (v == 4) return launch_coarse_sweep_nown<N, NOWN, 8, 256>(ca, tab, M, bar, r_out, grid, st);
+    if (v == 5) return launch_coarse_sweep_nown<N, NOWN, 4, 256>(ca, tab, M, bar, r_out, grid, st);
+  }
+  auto kfn = k_coarse_sweep<N, R, T, NOWN>;
+  const size_t sm = CoarseLayout<N, R, T, NOWN>::bytes;
   cudaError_t e = set_smem(kfn, sm);
   if (e != cudaSuccess) return e;
   int dev, sms, per_sm;
