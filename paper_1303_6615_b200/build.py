@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "librsw.so")
-SOURCES = ["rsw_kernels.cu", "rsw_capi.cu"]
-HEADERS = ["rsw_device.cuh", "rsw_internal.h"]
+SOURCES = ["rsw_k_fine.cu", "rsw_k_coarse.cu", "rsw_k_misc.cu", "rsw_capi.cu"]
+HEADERS = ["rsw_device.cuh", "rsw_internal.h", "rsw_blocks.cuh"]
 
 
 def _host_cxx() -> str:
@@ -18,13 +18,20 @@ def _host_cxx() -> str:
     return "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else (shutil.which("g++") or "g++")
 
 
-def nvcc_cmd(out: str = LIB) -> list[str]:
-    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+def _nvcc() -> str:
+    return shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+
+
+def compile_cmd(src: str, obj: str) -> list[str]:
     return [
-        nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-        "-Xcompiler", "-fPIC", "-shared", "-ccbin", _host_cxx(), f"-I{INCLUDE}",
-        *[os.path.join(CSRC, s) for s in SOURCES], "-o", out, "-ldl",
+        _nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+        "-Xcompiler", "-fPIC", "-ccbin", _host_cxx(), f"-I{INCLUDE}", "-c", src, "-o", obj,
     ]
+
+
+def link_cmd(objs: list[str], out: str) -> list[str]:
+    return [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-ccbin", _host_cxx(),
+            *objs, "-o", out, "-ldl"]
 
 
 def stale() -> bool:
@@ -36,8 +43,21 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Each translation unit compiles in its own nvcc process (in parallel), then one shared link."""
     if force or stale():
-        cmd = nvcc_cmd(LIB + ".tmp")
+        objdir = os.path.join(HERE, "build")
+        os.makedirs(objdir, exist_ok=True)
+        jobs = []
+        for src in SOURCES:
+            obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+            cmd = compile_cmd(os.path.join(CSRC, src), obj)
+            if verbose:
+                print(" ".join(cmd))
+            jobs.append((subprocess.Popen(cmd), cmd, obj))
+        for proc, cmd, _ in jobs:
+            if proc.wait() != 0:
+                raise subprocess.CalledProcessError(proc.returncode, cmd)
+        cmd = link_cmd([o for _, _, o in jobs], LIB + ".tmp")
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

@@ -1,0 +1,652 @@
+// rsw_blocks.cuh — device building blocks shared by the standalone kernels (rsw_kernels.cu) and the
+// pipelined parareal megakernel (rsw_pipeline.cu): radix / thread choices, pair load / store,
+// the fine pair integrator (a2 / a2'), and the coarse-sweep phases (a3 / a4 / a5).
+#pragma once
+#include "rsw_internal.h"
+#include "rsw_device.cuh"
+
+#include <cstdlib>
+
+namespace rsw {
+
+// FFT radix and CTA size, T = 3N/R (one radix-R butterfly of each field per thread), chosen from
+// measurements on B200: large transforms (n >= 512) are shared-memory-traffic bound,
+// so radix 16 (fewest passes) wins for the throughput kernels (C5 fine 5.6 -> 6.3 TFLOP/s, C4 N̄
+// 6.5 -> 7.8); at n <= 256 the kernels are latency bound and radix 4 with more threads wins (C3 fine
+// 5.4 TFLOP/s vs 4.0 at radix 16; C3 coarse stage 7.5 us vs 14.1).
+template <int N>
+#ifndef RSW_RADIX_FINE
+#define RSW_RADIX_FINE 0
+#endif
+#ifndef RSW_RADIX_COARSE
+#define RSW_RADIX_COARSE 0
+#endif
+__host__ __device__ constexpr int radix_for() { return RSW_RADIX_FINE ? RSW_RADIX_FINE : (N >= 512 ? 16 : 4); }
+template <int N>
+__host__ __device__ constexpr int threads_for() { return (3 * N / radix_for<N>()) > 96 ? (3 * N / radix_for<N>()) : 96; }
+// register FFT core (nl_core): R values per thread, T = 3N/R threads (>= 32)
+template <int N>
+__host__ __device__ constexpr int fine_radix() { return N <= 32 ? 4 : N <= 256 ? 8 : 16; }  // palindromic
+template <int N, int R>
+__host__ __device__ constexpr int core_threads() { return (3 * (N / R) + 31) / 32 * 32; }
+template <int N>
+__host__ __device__ constexpr int coarse_radix() {  // palindromic; latency-bound (one pair per SM)
+  return RSW_RADIX_COARSE ? RSW_RADIX_COARSE : (N <= 32 ? 4 : N <= 256 ? 8 : 16);
+}
+template <int N>
+__host__ __device__ constexpr int coarse_threads() { return core_threads<N, coarse_radix<N>()>() > 192 ? core_threads<N, coarse_radix<N>()>() : 192; }
+
+// ---------------------------------------------------------------------------------------------
+// shared helpers: load a pair of half-spectrum states into packed eigen coordinates, and store
+// ---------------------------------------------------------------------------------------------
+template <int N, int T>
+__device__ __forceinline__ void load_pair_eigen(const double* __restrict__ uA, const double* __restrict__ uB,
+                                                const ModeGeom g, double2* C /*[3][Kc]*/, int t0 = -1) {
+  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
+  const double2* A = reinterpret_cast<const double2*>(uA);
+  const double2* B = reinterpret_cast<const double2*>(uB);
+  for (int j = (t0 < 0 ? (int)threadIdx.x : t0); j < Kc; j += T) {
+    const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+    double2 z[3];
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      double2 a = A[f * NH + ak];
+      double2 b = B ? B[f * NH + ak] : make_double2(0.0, 0.0);
+      if (kap < 0) {  // û(-κ) = conj(û(κ)) for real fields (R16)
+        a = cconj(a);
+        b = cconj(b);
+      }
+      z[f] = make_double2(a.x - b.y, a.y + b.x);  // a + i b
+    }
+    const double as = kap < 0 ? -__ldg(g.a + ak) : __ldg(g.a + ak);
+    double2 c[3];
+    to_eigen(as, __ldg(g.p + ak), __ldg(g.q + ak), z, c);
+#pragma unroll
+    for (int al = 0; al < 3; ++al) C[al * Kc + j] = c[al];
+  }
+}
+
+// unpack Z = Û_A + i Û_B (primitive, from eigen C) and store both half spectra (modes > K -> 0)
+template <int N, int T>
+__device__ __forceinline__ void store_pair_prim(const double2* C, const ModeGeom g, double* __restrict__ oA,
+                                                double* __restrict__ oB, int t0 = -1) {
+  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
+  double2* A = reinterpret_cast<double2*>(oA);
+  double2* B = reinterpret_cast<double2*>(oB);
+  for (int k = (t0 < 0 ? (int)threadIdx.x : t0); k < NH; k += T) {
+    double2 ua[3], ub[3];
+    if (k <= K) {
+      const double a = __ldg(g.a + k), p = __ldg(g.p + k), q = __ldg(g.q + k);
+      double2 cp[3], cm[3], zp[3], zm[3];
+      const int jm = (k == 0) ? 0 : Kc - k;  // compact index of -κ
+#pragma unroll
+      for (int al = 0; al < 3; ++al) {
+        cp[al] = C[al * Kc + k];
+        cm[al] = C[al * Kc + jm];
+      }
+      to_prim(a, p, q, cp, zp);
+      to_prim(-a, p, q, cm, zm);
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        const double2 zc = cconj(zm[f]);
+        ua[f] = cscale(cadd(zp[f], zc), 0.5);
+        ub[f] = cscale(cmulmi(csub(zp[f], zc)), 0.5);  // (Z - conj Z(-κ)) / (2i)
+      }
+      if (k == 0) {
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          ua[f].y = 0.0;
+          ub[f].y = 0.0;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int f = 0; f < 3; ++f) ua[f] = ub[f] = make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      A[f * NH + k] = ua[f];
+      if (B) B[f * NH + k] = ub[f];
+    }
+  }
+}
+
+// write prim(x) of every retained entry as the next N-eval input and zero the tail
+template <int N, int T>
+__device__ __forceinline__ void prologue_from(double2* W, const double2* X, const ModeGeom g) {
+  constexpr int K = N / 3, Kc = 2 * K + 1;
+  for (int j = threadIdx.x; j < Kc; j += T) {
+    const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+    const double as = kap < 0 ? -__ldg(g.a + ak) : __ldg(g.a + ak);
+    double2 c[3], u[3];
+#pragma unroll
+    for (int al = 0; al < 3; ++al) c[al] = X[al * Kc + j];
+    to_prim(as, __ldg(g.p + ak), __ldg(g.q + ak), c, u);
+    put_input<N>(W, full_index(kap, N), (double)kap, u);
+  }
+  zero_tail<N, T>(W);
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1/K2: fine propagator.  One CTA = one pair of slices, state resident in shared memory for all
+// m steps; the only global traffic is one load and one store per slice.
+//   ETDRK4 (Cox–Matthews), eigen-diagonal form with three persistent vectors S0, S1, S2:
+//     stage 0 (n0 = N(c)):  S0 = E2 c;  S1 = E c + f1 n0;  a = S0 + Q n0;  S2 = E2 a - Q n0;  x = a
+//     stage 1 (n1 = N(a)):  x = b = S0 + Q n1;  S1 += f2 n1
+//     stage 2 (n2 = N(b)):  x = c' = S2 + 2 Q n2;  S1 += f2 n2
+//     stage 3 (n3 = N(c')): S1 += f3 n3;  x = S1 (next state)
+//   which is u+ = E u + f1 Nu + f2 (Na + Nb) + f3 Nc with a, b, c' as in Cox–Matthews.
+//   Strang (Alg.3 + R7): v = E2 c;  m = v + (h/2) N(v);  w = v + h N(m);  c+ = E2 w.
+// ---------------------------------------------------------------------------------------------
+
+// per-configuration fine tables staged in shared memory (one copy per CTA)
+struct FineSmemTab {
+  const double2* TW;  // packed twiddles of nl_core
+  const double2* CP;  // [6][K+1]
+  const double* C0;   // [6][K+1]
+  const double *GA, *GP, *GQ;
+};
+
+template <int N, int R, int T>
+__device__ __forceinline__ FineSmemTab stage_fine_tables(double2* smem_tw, double2* smem_cp, double* smem_d,
+                                                         const FineTab& tab, int t, int nthr) {
+  constexpr int K = N / 3, KP = K + 1;
+  double* sC0 = smem_d;
+  double* sGA = sC0 + 6 * KP;
+  double* sGP = sGA + KP;
+  double* sGQ = sGP + KP;
+  constexpr int m = fft_npass<N, R>(), r0 = fft_rad<N, R>(0);
+  for (int i = t; i < fft_tw_size<N, R>(); i += nthr) {  // (fill_packed_twiddles with a runtime stride)
+    int p = 1;
+    while (p < m - 1 && i >= fft_ns<N, R>(p + 1) - r0) ++p;
+    const int NS = fft_ns<N, R>(p), r = fft_rad<N, R>(p), o = i - (NS - r0);
+    smem_tw[i] = __ldg(tab.tw + (o % (r - 1) + 1) * (o / (r - 1)) * (N / (NS * r)));
+  }
+  for (int i = t; i < 6 * KP; i += nthr) {
+    smem_cp[i] = __ldg(tab.cp + i);
+    sC0[i] = __ldg(tab.c0 + i);
+  }
+  for (int i = t; i < KP; i += nthr) {
+    sGA[i] = __ldg(tab.g.a + i);
+    sGP[i] = __ldg(tab.g.p + i);
+    sGQ[i] = __ldg(tab.g.q + i);
+  }
+  return FineSmemTab{smem_tw, smem_cp, sC0, sGA, sGP, sGQ};
+}
+
+template <int N, int TG>
+struct FineTmem {  // TMEM columns of one fine pair-group: per mode slot o, S1 / S0 / S2 at o*36 + {0, 12, 24}
+  static constexpr int Kc = 2 * (N / 3) + 1, OMAX = (Kc + TG - 1) / TG, WG = (TG / 32 + 3) / 4;
+  static constexpr int COLS = WG * OMAX * 36;
+};
+
+// One pair of slices advanced by m fine steps (a2 / a2') by a warp-aligned thread group: the state
+// lives in the group's TMEM columns, the N-evals in its X / Y buffers.  Used by k_fine (the whole
+// CTA) and by the fine workers of the pipelined parareal kernel (one of several groups of a CTA).
+template <int N, int R, int TG, int SCHEME, bool LIN, class GRP>
+__device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double2* Y, const FineSmemTab& st_,
+                                              uint32_t tcol, const ModeGeom& gg, const double* uA,
+                                              const double* uB, double* oA, double* oB, int m_steps, double h) {
+  constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, OMAX = FineTmem<N, TG>::OMAX;
+  constexpr double invN = 1.0 / N;
+  const double2* sCP = st_.CP;
+  const double* sC0 = st_.C0;
+  const double* sGA = st_.GA;
+  const double* sGP = st_.GP;
+  const double* sGQ = st_.GQ;
+  const int t = grp.tid();
+  const int warp = threadIdx.x >> 5, gwarp = t >> 5;
+  load_pair_eigen<N, TG>(uA, uB, gg, W, t);  // C[α][j] staged in W
+  grp.sync();
+  // thread-private TMEM slot of mode slot o: columns o*36 + {S1: 0, S0: 12, S2: 24} + 4α
+  const uint32_t tb = tcol + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((gwarp >> 2) * OMAX * 36);
+  double2 c0v[OMAX][3];
+#pragma unroll
+  for (int o = 0; o < OMAX; ++o) {
+    const int j = t + o * TG;
+#pragma unroll
+    for (int al = 0; al < 3; ++al) c0v[o][al] = (j < Kc) ? W[al * Kc + j] : make_double2(0.0, 0.0);
+  }
+  grp.sync();  // C fully read before W receives the first N-eval input
+#pragma unroll
+  for (int o = 0; o < OMAX; ++o) {
+    const int j = t + o * TG;
+    const int jj = j < Kc ? j : 0;
+    const int kap = kappa_of(jj, K), ak = kap < 0 ? -kap : kap;
+    if (SCHEME == 1) {  // Strang prologue: S1 = v = E2 c
+#pragma unroll
+      for (int al = 0; al < 3; ++al) c0v[o][al] = dmul(al - 1, sCP[1 * KP + ak], sC0[1 * KP + ak], c0v[o][al]);
+    }
+    tmem_st3(tb + o * 36, c0v[o]);
+    if (!LIN && j < Kc) {
+      const double as = kap < 0 ? -sGA[ak] : sGA[ak];
+      double2 u[3];
+      to_prim(as, sGP[ak], sGQ[ak], c0v[o], u);
+      put_input_z<N>(W, full_index(kap, N), (double)kap, u);
+    }
+  }
+  tmem_wait_st();
+  grp.sync();
+
+  const int nst = (SCHEME == 0) ? 4 : 2;
+  for (int step = 0; step < m_steps; ++step) {
+    const bool last_step = (step == m_steps - 1);
+    for (int st = 0; st < nst; ++st) {
+      if (!LIN) nl_core<N, R, TG>(W, Y, st_.TW, grp);
+      // epilogue (this stage's update) fused with the prologue of the next N-eval
+#pragma unroll
+      for (int o = 0; o < OMAX; ++o) {
+        const int j = t + o * TG;
+        const bool valid = j < Kc;
+        const int jj = valid ? j : 0;
+        const int kap = kappa_of(jj, K), ak = kap < 0 ? -kap : kap;
+        const int kf = full_index(kap, N);
+        const uint32_t ts = tb + o * 36;
+        double2 s1[3], s0[3], s2[3];
+        tmem_ld3(ts, s1);                                            // S1 (every stage)
+        if (SCHEME == 0 && st == 1) tmem_ld3(ts + 12, s0);           // S0 = E2 c
+        if (SCHEME == 0 && st == 2) tmem_ld3(ts + 24, s2);           // S2 = E2 a - Q Nu
+        const double as = kap < 0 ? -sGA[ak] : sGA[ak];
+        const double p = sGP[ak], q = sGQ[ak];
+        double2 nn[3];
+        if (!LIN && valid) {
+          double2 nh[3];
+          get_output_z<N>(W, kf, (double)kap, invN, nh);
+          to_eigen(as, p, q, nh, nn);
+        } else {
+#pragma unroll
+          for (int al = 0; al < 3; ++al) nn[al] = make_double2(0.0, 0.0);
+        }
+        double2 x[3];
+#pragma unroll
+        for (int al = 0; al < 3; ++al) {
+          const int alpha = al - 1;
+          // coefficient i of |κ|: 0 E, 1 E2, 2 Q, 3 f1, 4 f2, 5 f3
+#define CP(i) sCP[(i) * KP + ak]
+#define C0(i) sC0[(i) * KP + ak]
+          if (SCHEME == 0) {
+            if (st == 0) {
+              const double2 c = s1[al];
+              const double2 e2c = dmul(alpha, CP(1), C0(1), c);
+              const double2 qn = dmul(alpha, CP(2), C0(2), nn[al]);
+              const double2 a = cadd(e2c, qn);
+              s0[al] = e2c;
+              s1[al] = cadd(dmul(alpha, CP(0), C0(0), c), dmul(alpha, CP(3), C0(3), nn[al]));
+              s2[al] = csub(dmul(alpha, CP(1), C0(1), a), qn);
+              x[al] = a;
+            } else if (st == 1) {
+              x[al] = cadd(s0[al], dmul(alpha, CP(2), C0(2), nn[al]));
+              s1[al] = cadd(s1[al], dmul(alpha, CP(4), C0(4), nn[al]));
+            } else if (st == 2) {
+              x[al] = cadd(s2[al], cscale(dmul(alpha, CP(2), C0(2), nn[al]), 2.0));
+              s1[al] = cadd(s1[al], dmul(alpha, CP(4), C0(4), nn[al]));
+            } else {
+              s1[al] = cadd(s1[al], dmul(alpha, CP(5), C0(5), nn[al]));
+              x[al] = s1[al];
+            }
+          } else {
+            if (st == 0) {
+              x[al] = caxpy(0.5 * h, nn[al], s1[al]);  // m = v + (h/2) N(v)
+            } else {
+              const double2 w = caxpy(h, nn[al], s1[al]);                     // w = v + h N(m)
+              const double2 c = dmul(alpha, CP(1), C0(1), w);                 // c+ = E2 w
+              s1[al] = last_step ? c : dmul(alpha, CP(1), C0(1), c);          // next v = E2 c+
+              x[al] = s1[al];
+            }
+          }
+#undef CP
+#undef C0
+        }
+        if (SCHEME == 0 || st == 1) tmem_st3(ts, s1);
+        if (SCHEME == 0 && st == 0) {
+          tmem_st3(ts + 12, s0);
+          tmem_st3(ts + 24, s2);
+        }
+        if (!LIN && valid) {
+          double2 u[3];
+          to_prim(as, p, q, x, u);
+          put_input_z<N>(W, kf, (double)kap, u);
+        }
+      }
+      tmem_wait_st();
+      grp.sync();
+    }
+  }
+  // final state S1 -> C[α][j] in Y (W may still hold the last stage's inputs), then store
+#pragma unroll
+  for (int o = 0; o < OMAX; ++o) {
+    const int j = t + o * TG;
+    double2 s1[3];
+    tmem_ld3(tb + o * 36, s1);
+    if (j < Kc) {
+#pragma unroll
+      for (int al = 0; al < 3; ++al) Y[al * Kc + j] = s1[al];
+    }
+  }
+  grp.sync();
+  store_pair_prim<N, TG>(Y, gg, oA, oB, t);
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// K4: the serial coarse sweep (Alg.4's serial loop P:583-587 over Alg.2 coarse steps) as ONE
+// persistent cooperative kernel.  Per RK stage of slice n:
+//   phase 1 (all CTAs, sample-parallel as Alg.1): CTA b evaluates its sample pairs
+//     (m_A, m_B) = (2p+1, 2p+2), p = b, b+P, ..., packing the two rotated copies P-_m y of the
+//     stage input into one complex field, and writes its partial Σ w_m P+_m N(P-_m y) to part[b];
+//   grid barrier;
+//   phase 2 (distributed over |κ|): CTA b owns |κ| ≡ b (mod P) and reduces part[0..P-1] for its 6
+//     eigen entries (α, ±κ) in a fixed order, then applies the RK4 / midpoint stage update; at the
+//     last stage also the D half step, the back-transform e^{-(ΔT/ε)L̂}, the parareal update
+//     U_{n+1} = G + (F_n - G_n) with the residual partials (R12), and slice n+1's first input;
+//   grid barrier.
+// Cross-CTA data (y, part) is read with ld.global.cg (L2), never through the incoherent L1.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// grid barrier: monotone arrival counter, arrive with a gpu-scope release RMW, spin with
+// gpu-scope acquire loads (1.2 us at 128-148 CTAs on B200, vs 2.2 us for a volatile-flag barrier;
+// tools/micro/barrier_bench.cu).  `epoch` counts this CTA's barriers; the counter is zeroed by the
+// host before the launch.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    const unsigned target = epoch * nblocks;
+    while (ld_acquire_gpu(bar) < target) {
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Stage input through a triple-buffered shared array (replaces "owners write y -> grid barrier ->
+// everyone loads y"): update phase u writes its owned entries of the next stage input into
+// ybuf[u%3] (each entry once) and resets the same entries of ybuf[(u+2)%3] to the sentinel; the
+// samples phase polls ybuf[u%3] until no entry holds the sentinel.  Safe without fences: each
+// 8-byte half is single-copy atomic; the reset of ybuf[(u+2)%3] happens after every reader of it
+// (samples phase u-1) passed the release/acquire grid barrier before update u, and it is ordered
+// before any reader of ybuf[(u+2)%3] (samples phase u+2) by the grid barrier after samples u+1.
+constexpr unsigned long long YIN_SENTINEL = 0x7FF4DEADBEEF0001ull;  // a signalling-NaN payload arithmetic never produces
+__device__ __forceinline__ double2 ld_relaxed_v2(const double2* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_v2(double2* p, double2 v) {
+  asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ bool is_sentinel(double x) { return (unsigned long long)__double_as_longlong(x) == YIN_SENTINEL; }
+__device__ __forceinline__ double2 yin_sentinel() {
+  const double s = __longlong_as_double((long long)YIN_SENTINEL);
+  return make_double2(s, s);
+}
+
+template <int N, int R, int T>
+__device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* part, int M, const AvgTab& tab,
+                                                     double2* X, double2* Y, const double2* TW, double2* C,
+                                                     double2* A, const double2* PH, const double* SW,
+                                                     const double* GA, const double* GP, const double* GQ,
+                                                     unsigned long long* cyc = nullptr) {
+#define STAMP(i) \
+  if (cyc && threadIdx.x == 0) cyc[i] = clock64();
+  STAMP(0)
+  // PH: this CTA's phases e^{iωτ_m} for its first pair, [2][K+1] (null: load from the table);
+  // SW: its weights w_mA, w_mB; GA/GP/GQ: geometry a, p, q per |κ| staged in shared memory
+  constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
+  constexpr double invN = 1.0 / N;
+  // stage input from this CTA's inbox (y = inbox row): poll, keep, reset to the sentinel
+  for (int i = threadIdx.x; i < 3 * Kc; i += T) {
+    double2 v = ld_relaxed_v2(y + i);
+    while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(y + i);
+    C[i] = v;
+    A[i] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int npairs = M / 2;  // samples 1..M-1 -> pairs (1,2), (3,4), ...; last B may be M (w=0)
+  for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+    const int mA = 2 * pr + 1, mB = 2 * pr + 2;
+    const bool hasB = mB <= M - 1;
+    const bool cached = PH && pr == (int)blockIdx.x;
+    for (int j = threadIdx.x; j < Kc; j += T) {
+      const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+      const double as = kap < 0 ? -GA[ak] : GA[ak];
+      const double2 pA = cached ? PH[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
+      const double2 pB = !hasB ? make_double2(1.0, 0.0) : (cached ? PH[KP + ak] : __ldg(tab.phase + (size_t)mB * KP + ak));
+      double2 c[3], u[3];
+      // packed eigen input: P-_{mA} y + i P-_{mB} y   (P-: α=-1 -> e^{+iωτ}, α=+1 -> e^{-iωτ})
+      const double2 ym = C[j], y0 = C[Kc + j], yp = C[2 * Kc + j];
+      const double2 bm = hasB ? cmul(ym, pB) : make_double2(0.0, 0.0);
+      const double2 b0 = hasB ? y0 : make_double2(0.0, 0.0);
+      const double2 bp = hasB ? cmulc(yp, pB) : make_double2(0.0, 0.0);
+      c[0] = cadd(cmul(ym, pA), cmuli(bm));
+      c[1] = cadd(y0, cmuli(b0));
+      c[2] = cadd(cmulc(yp, pA), cmuli(bp));
+      to_prim(as, GP[ak], GQ[ak], c, u);
+      put_input_z<N>(X, full_index(kap, N), (double)kap, u);
+    }
+    __syncthreads();
+    STAMP(1)
+    nl_core<N, R, T>(X, Y, TW);
+    STAMP(2)
+    const double wA = cached ? SW[0] : __ldg(tab.w + mA), wB = hasB ? (cached ? SW[1] : __ldg(tab.w + mB)) : 0.0;
+    for (int j = threadIdx.x; j < Kc; j += T) {
+      const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+      const double as = kap < 0 ? -GA[ak] : GA[ak];
+      const double p = GP[ak], q = GQ[ak];
+      double2 zp[3], zm[3], na[3], nb[3], ea[3], eb[3];
+      get_output_z<N>(X, full_index(kap, N), (double)kap, invN, zp);
+      get_output_z<N>(X, full_index(-kap, N), (double)(-kap), invN, zm);
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {  // unpack: N_A(κ) = (Z(κ) + conj Z(-κ))/2, N_B = (Z - conj Z(-κ))/(2i)
+        const double2 zc = cconj(zm[f]);
+        na[f] = cscale(cadd(zp[f], zc), 0.5);
+        nb[f] = cscale(cmulmi(csub(zp[f], zc)), 0.5);
+      }
+      to_eigen(as, p, q, na, ea);
+      to_eigen(as, p, q, nb, eb);
+      const double2 pA = cached ? PH[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
+      A[j] = caxpy(wA, cmulc(ea[0], pA), A[j]);  // P+: α=-1 -> e^{-iωτ}, α=+1 -> e^{+iωτ}
+      A[Kc + j] = caxpy(wA, ea[1], A[Kc + j]);
+      A[2 * Kc + j] = caxpy(wA, cmul(ea[2], pA), A[2 * Kc + j]);
+      if (hasB) {
+        const double2 pB = cached ? PH[KP + ak] : __ldg(tab.phase + (size_t)mB * KP + ak);
+        A[j] = caxpy(wB, cmulc(eb[0], pB), A[j]);
+        A[Kc + j] = caxpy(wB, eb[1], A[Kc + j]);
+        A[2 * Kc + j] = caxpy(wB, cmul(eb[2], pB), A[2 * Kc + j]);
+      }
+    }
+    __syncthreads();  // all mirror reads of X done before the next prologue overwrites it
+    STAMP(3)
+  }
+  double2* P = part + (size_t)blockIdx.x * 3 * Kc;
+  for (int i = threadIdx.x; i < 3 * Kc; i += T) P[i] = A[i];
+  STAMP(4)
+#undef STAMP
+}
+
+// phase 2 of one RK stage, thread-parallel over the CTA's owned modes |κ| = b + o P (o < NOWN):
+// items i = o*6 + e, entries e = (α, +κ) for e < 3, (α, -κ) for e >= 3.  The stage base v and the RK
+// accumulator ks of owned modes live in this CTA's shared memory for the whole sweep; the stage
+// input y is published to global memory for the samples phase of every CTA.
+template <int N, int NOWN, int T>
+__device__ __forceinline__ void push_stage_input(const CoarseArgs& ca, const double2* yv, const int* yidx, unsigned u) {
+  constexpr int Kc3 = 3 * (2 * (N / 3) + 1);
+  __syncthreads();
+  if (threadIdx.x < NOWN * 6 && yidx[threadIdx.x] >= 0) {
+    st_relaxed_v2(ca.yin + (size_t)(u % 3) * Kc3 + yidx[threadIdx.x], yv[threadIdx.x]);
+    st_relaxed_v2(ca.yin + (size_t)((u + 2) % 3) * Kc3 + yidx[threadIdx.x], yin_sentinel());
+  }
+}
+
+template <int N, int T, int NOWN>
+__device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int stage, int n, double2* Vs,
+                                                    double2* KSs, double2* kk, double2* un_s, double* nd_s,
+                                                    double2* red_buf, double2* yv, int* yidx, unsigned ucount) {
+  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
+  const int P = gridDim.x;
+  const size_t Ls = (size_t)3 * NH;
+  const double dT = ca.dT;
+  auto entry = [&](int o, int e, int& ak, int& al, int& j) {
+    ak = blockIdx.x + o * P;
+    al = e % 3;
+    j = (e < 3) ? ak : ((ak == 0) ? 0 : Kc - ak);
+  };
+  const bool last = (ca.scheme == 0) ? (stage == 4) : (stage == 2);
+  // prefetch the finalize operands (F_n, old G_n, old U_{n+1}) before the reduction's L2 round trip
+  double2 pf_F = make_double2(0.0, 0.0), pf_G = make_double2(0.0, 0.0), pf_U = make_double2(0.0, 0.0);
+  if (stage > 0 && last && threadIdx.x < NOWN * 3) {
+    const int o = threadIdx.x / 3, f = threadIdx.x % 3, ak = blockIdx.x + o * P;
+    if (ak <= K) {
+      if (ca.F) pf_F = __ldcg(reinterpret_cast<const double2*>(ca.F) + (size_t)n * Ls + f * NH + ak);
+      pf_G = reinterpret_cast<const double2*>(ca.G)[(size_t)n * Ls + f * NH + ak];
+      pf_U = reinterpret_cast<const double2*>(ca.U)[(size_t)(n + 1) * Ls + f * NH + ak];
+    }
+  }
+  if (stage > 0) {
+    // deterministic reduction of the partials: TQ threads per item issue all their loads at once,
+    // then a fixed-order tree in shared memory
+    constexpr int ITEMS = NOWN * 6;
+    constexpr int TQ0 = T / ITEMS;
+    constexpr int TQ = TQ0 >= 32 ? 32 : TQ0 >= 16 ? 16 : TQ0 >= 8 ? 8 : TQ0 >= 4 ? 4 : TQ0 >= 2 ? 2 : 1;
+    double2* rd = reinterpret_cast<double2*>(red_buf);
+    const int it = threadIdx.x / TQ, qd = threadIdx.x % TQ;
+    if (it < ITEMS) {
+      int ak, al, j;
+      entry(it / 6, it % 6, ak, al, j);
+      double2 sacc = make_double2(0.0, 0.0);
+      if (ak <= K)
+        for (int b = qd; b < ca.nparts; b += TQ) sacc = cadd(sacc, __ldcg(ca.part + (size_t)b * 3 * Kc + al * Kc + j));
+      rd[threadIdx.x] = sacc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = TQ / 2; w > 0; w >>= 1) {
+      if (it < ITEMS && qd < w) rd[threadIdx.x] = cadd(rd[threadIdx.x], rd[threadIdx.x + w]);
+      __syncthreads();
+    }
+    if (it < ITEMS && qd == 0) kk[it] = rd[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x < NOWN * 6) {
+      int ak, al, j;
+      const int it = threadIdx.x;
+      entry(it / 6, it % 6, ak, al, j);
+      if (ak <= K && !(ak == 0 && it % 6 >= 3)) {
+        const double2 k = kk[it];
+        double2& V = Vs[it];
+        double2& KS = KSs[it];
+        double2* Y = yv + it;
+        yidx[it] = last ? -1 : al * Kc + j;
+        if (ca.scheme == 0) {  // classical RK4 (R6): (k1 + 2k2 + 2k3 + k4) accumulated in this order
+          if (stage == 1) {
+            KS = k;
+            *Y = caxpy(0.5 * dT, k, V);
+          } else if (stage == 2) {
+            KS = caxpy(2.0, k, KS);
+            *Y = caxpy(0.5 * dT, k, V);
+          } else if (stage == 3) {
+            KS = caxpy(2.0, k, KS);
+            *Y = caxpy(dT, k, V);
+          } else {
+            KS = cadd(KS, k);
+            V = caxpy(dT / 6.0, KS, V);
+          }
+        } else {  // midpoint (Alg.2, R7): v + ΔT N̄(v + ΔT/2 N̄(v))
+          if (stage == 1) *Y = caxpy(0.5 * dT, k, V);
+          else V = caxpy(dT, k, V);
+        }
+      } else {
+        yidx[it] = -1;
+      }
+    }
+    if (!last) {
+      push_stage_input<N, NOWN, T>(ca, yv, yidx, ucount);
+      return;
+    }
+    __syncthreads();
+    // finalize: D half step, back-transform, primitive G, parareal update (thread per (o, f))
+    if (threadIdx.x < NOWN * 3) {
+      const int o = threadIdx.x / 3, f = threadIdx.x % 3, ak = blockIdx.x + o * P;
+      if (ak <= K) {
+        const double a = __ldg(ca.g.a + ak), p = __ldg(ca.g.p + ak), q = __ldg(ca.g.q + ak);
+        const double dh = __ldg(ca.dhalf + ak);
+        const double2 bt = __ldg(ca.back + ak);  // e^{-iωΔT/ε}: α=+1 entry of e^{-(ΔT/ε)L̂} (R3)
+        double2 cg[3], G[3];
+#pragma unroll
+        for (int al = 0; al < 3; ++al) {
+          const double2 c = cscale(Vs[o * 6 + al], dh);  // e^{(ΔT/2) D̂} (Alg.2)
+          cg[al] = (al == 1) ? c : (al == 2 ? cmul(c, bt) : cmulc(c, bt));
+        }
+        to_prim(a, p, q, cg, G);
+        double2 g = G[f];
+        if (ak == 0) g.y = 0.0;
+        double2* Gst = reinterpret_cast<double2*>(ca.G) + (size_t)n * Ls + f * NH + ak;
+        double2* Uo = reinterpret_cast<double2*>(ca.U) + (size_t)(n + 1) * Ls + f * NH + ak;
+        double2 un = g;
+        if (ca.F) un = cadd(g, csub(pf_F, pf_G));  // U^k_{n+1} = G(U^k_n) + (F_n - G_n)
+        const double2 d = csub(un, pf_U);
+        const double wk = (ak == 0 || 2 * ak == N) ? 1.0 : 2.0;
+        nd_s[threadIdx.x * 2] = wk * (d.x * d.x + d.y * d.y);
+        nd_s[threadIdx.x * 2 + 1] = wk * (un.x * un.x + un.y * un.y);
+        *Gst = g;
+        *Uo = un;
+        un_s[threadIdx.x] = un;
+        if (ak == K)  // modes K < k <= N/2 stay zero
+          for (int k = K + 1; k < NH; ++k) {
+            Uo[k - K] = make_double2(0.0, 0.0);
+            Gst[k - K] = make_double2(0.0, 0.0);
+          }
+      }
+    }
+    __syncthreads();
+    if (ca.rparts && threadIdx.x < NOWN) {
+      const int ak = blockIdx.x + threadIdx.x * P;
+      if (ak <= K) {
+        const double* t = nd_s + threadIdx.x * 6;
+        ca.rparts[((size_t)n * (K + 1) + ak) * 2 + 0] = t[0] + t[2] + t[4];
+        ca.rparts[((size_t)n * (K + 1) + ak) * 2 + 1] = t[1] + t[3] + t[5];
+      }
+    }
+    if (n + 1 >= ca.n_end) return;  // no next slice
+  } else {
+    // stage 0: load U_0 of owned modes
+    if (threadIdx.x < NOWN * 3) {
+      const int o = threadIdx.x / 3, f = threadIdx.x % 3, ak = blockIdx.x + o * P;
+      if (ak <= K) un_s[threadIdx.x] = reinterpret_cast<const double2*>(ca.U)[(size_t)n * Ls + f * NH + ak];
+    }
+    __syncthreads();
+  }
+  // first stage input of the next slice: v = e^{ΔT D̂/2} u (Alg.2), eigen, both signs of κ
+  if (threadIdx.x < NOWN * 6) {
+    int ak, al, j;
+    const int it = threadIdx.x, o = it / 6, e = it % 6;
+    entry(o, e, ak, al, j);
+    if (ak <= K && !(ak == 0 && e >= 3)) {
+      const double a = __ldg(ca.g.a + ak), p = __ldg(ca.g.p + ak), q = __ldg(ca.g.q + ak);
+      double2 u[3], c[3];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) u[f] = (e < 3) ? un_s[o * 3 + f] : cconj(un_s[o * 3 + f]);
+      to_eigen(e < 3 ? a : -a, p, q, u, c);
+      const double2 v = cscale(c[al], __ldg(ca.dhalf + ak));
+      Vs[it] = v;
+      yv[it] = v;
+      yidx[it] = al * Kc + j;
+    } else {
+      yidx[it] = -1;
+    }
+  }
+  push_stage_input<N, NOWN, T>(ca, yv, yidx, ucount);
+  __syncthreads();
+}
+
+}  // namespace rsw

@@ -303,6 +303,17 @@ __device__ __forceinline__ void nl_physical(double2* W, const double2* __restric
 //   out: X = N * DFT(q_f) at the retained full indices, q = (v1²/2, v1 v2x, h v1) per lane.
 // Barriers: 2 * passes (the last one makes the output visible to the caller's mode loop).
 // ---------------------------------------------------------------------------------------------
+// thread-group policies: the whole CTA, or a warp-aligned group of a CTA with its own named barrier
+struct CtaGroup {
+  __device__ __forceinline__ int tid() const { return threadIdx.x; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+struct NamedGroup {
+  int base, id, nthr;  // first thread, barrier id (1..15), thread count (multiple of 32)
+  __device__ __forceinline__ int tid() const { return threadIdx.x - base; }
+  __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory"); }
+};
+
 __host__ __device__ __forceinline__ constexpr int swz(int i) { return (i & ~7) | ((i ^ (i >> 3) ^ (i >> 6)) & 7); }
 
 template <int N, int R>
@@ -337,9 +348,9 @@ __host__ __device__ constexpr int fft_tw_size() { return N - fft_rad<N, R>(0); }
 
 // fill the packed table from the plain table tw[m] = e^{-2πi m/N} (all threads of the CTA)
 template <int N, int R, int T>
-__device__ __forceinline__ void fill_packed_twiddles(double2* TW, const double2* __restrict__ tw) {
+__device__ __forceinline__ void fill_packed_twiddles(double2* TW, const double2* __restrict__ tw, int t0 = -1) {
   constexpr int m = fft_npass<N, R>(), r0 = fft_rad<N, R>(0);
-  for (int i = threadIdx.x; i < fft_tw_size<N, R>(); i += T) {
+  for (int i = (t0 < 0 ? (int)threadIdx.x : t0); i < fft_tw_size<N, R>(); i += T) {
     int p = 1;
     while (p < m - 1 && i >= fft_ns<N, R>(p + 1) - r0) ++p;
     const int NS = fft_ns<N, R>(p), r = fft_rad<N, R>(p), o = i - (NS - r0);
@@ -390,9 +401,9 @@ __device__ __forceinline__ void core_load(double2 (&v)[R], const double2* B, int
 }
 
 // synthesis passes p..m-1 (p >= 1): load from B[p%2], compute, store to B[(p+1)%2] unless last
-template <int N, int R, int p>
+template <int N, int R, int p, class GRP>
 __device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* const (&B)[2], int f, int j, bool act,
-                                             const double2* TW) {
+                                             const double2* TW, const GRP& grp) {
   constexpr int m = fft_npass<N, R>();
   if constexpr (p < m) {
     if (act) {
@@ -401,17 +412,17 @@ __device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* const (&B
       if constexpr (p < m - 1) core_store<N, R, p>(v, B[(p + 1) % 2] + f * N, j);
     }
     if constexpr (p < m - 1) {
-      __syncthreads();
-      core_inverse<N, R, p + 1>(v, B, f, j, act, TW);
+      grp.sync();
+      core_inverse<N, R, p + 1>(v, B, f, j, act, TW, grp);
     }
   }
 }
 
 // analysis passes q..m-1 (q >= 1; analysis pass q runs the (r, NS) of synthesis pass q): load from
 // Z_{q-1} = B[(m-1+q-1)%2]; the last pass stores the retained outputs to B[0]
-template <int N, int R, int q>
+template <int N, int R, int q, class GRP>
 __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* const (&B)[2], int f, int j, bool act,
-                                             const double2* TW) {
+                                             const double2* TW, const GRP& grp) {
   constexpr int m = fft_npass<N, R>();
   if constexpr (q < m) {
     constexpr int r = fft_rad<N, R>(q);
@@ -430,19 +441,19 @@ __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* const (&B
         }
       }
     }
-    __syncthreads();
-    core_forward<N, R, q + 1>(v, B, f, j, act, TW);
+    grp.sync();
+    core_forward<N, R, q + 1>(v, B, f, j, act, TW, grp);
   }
 }
 
-template <int N, int R, int T>
-__device__ __forceinline__ void nl_core(double2* X, double2* Y, const double2* TW) {
+template <int N, int R, int T, class GRP = CtaGroup>
+__device__ __forceinline__ void nl_core(double2* X, double2* Y, const double2* TW, const GRP& grp = GRP()) {
   static_assert(T >= 3 * (N / R), "nl_core: T must cover 3 N/R field-columns");
   static_assert(fft_palindrome<N, R>(), "nl_core: radix sequence must be a palindrome");
   constexpr int m = fft_npass<N, R>(), NJ = N / R, K = N / 3;
   constexpr int r0 = fft_rad<N, R>(0);
   double2* const B[2] = {X, Y};
-  const int t = threadIdx.x, f = t / NJ, j = t % NJ;
+  const int t = grp.tid(), f = t / NJ, j = t % NJ;
   const bool act = t < 3 * NJ;
   double2 v[R];
   // synthesis pass 0 (NS = 1, no twiddles): retained inputs only, the rest is zero (R10)
@@ -457,8 +468,8 @@ __device__ __forceinline__ void nl_core(double2* X, double2* Y, const double2* T
     if constexpr (m > 1) core_store<N, R, 0>(v, Y + f * N, j);
   }
   if constexpr (m > 1) {
-    __syncthreads();
-    core_inverse<N, R, 1>(v, B, f, j, act, TW);
+    grp.sync();
+    core_inverse<N, R, 1>(v, B, f, j, act, TW, grp);
   }
   // products on the grid: v1 shared through B[m%2] (not read by the last synthesis pass);
   // the last synthesis pass has radix r0 (palindrome) and the index set of analysis pass 0
@@ -467,7 +478,7 @@ __device__ __forceinline__ void nl_core(double2* X, double2* Y, const double2* T
 #pragma unroll
     for (int s = 0; s < R; ++s) VB[swz(core_idx<N, R, r0>(j, s))] = v[s];
   }
-  __syncthreads();
+  grp.sync();
   if (act) {
     if (f == 0) {
 #pragma unroll
@@ -492,8 +503,8 @@ __device__ __forceinline__ void nl_core(double2* X, double2* Y, const double2* T
       }
     }
   }
-  __syncthreads();
-  if constexpr (m > 1) core_forward<N, R, 1>(v, B, f, j, act, TW);
+  grp.sync();
+  if constexpr (m > 1) core_forward<N, R, 1>(v, B, f, j, act, TW, grp);
 }
 
 // N-eval input / output of one retained entry in the swizzled layout of nl_core

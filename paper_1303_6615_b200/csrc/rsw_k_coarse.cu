@@ -1,0 +1,314 @@
+// rsw_k_coarse.cu — the persistent cooperative coarse sweep (a3-a5) and the Strang-coarse serial sweep (NEXT-1).
+#include "rsw_blocks.cuh"
+
+namespace rsw {
+
+template <typename KernelT>
+static cudaError_t set_smem(KernelT k, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+#define RSW_DISPATCH(n, CALL)                  \
+  switch (n) {                                 \
+    case 16: return CALL(16);                  \
+    case 32: return CALL(32);                  \
+    case 64: return CALL(64);                  \
+    case 128: return CALL(128);                \
+    case 256: return CALL(256);                \
+    case 512: return CALL(512);                \
+    case 1024: return CALL(1024);              \
+    default: return cudaErrorInvalidValue;     \
+  }
+
+template <int N, int R, int T, int NOWN>
+struct CoarseLayout {  // dynamic shared memory of k_coarse_sweep (double2 units, then doubles)
+  static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NR = (T > NOWN * 6 ? T : NOWN * 6);
+  static constexpr int X = 0, Y = X + 3 * N, TW = Y + 3 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc,
+                       VS = A + 3 * Kc, KS = VS + NOWN * 6, KK = KS + NOWN * 6, UN = KK + NOWN * 6,
+                       RDB = UN + NOWN * 3, PH = RDB + T, YV = PH + 2 * KP, D = YV + NOWN * 6;
+  static constexpr int RED = 0, GA = RED + NR, GP = GA + KP, GQ = GP + KP, SW = GQ + KP, YI = SW + 2,
+                       ND = YI + NOWN * 6;  // YI: int entry indices stored in double slots
+  static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
+};
+
+template <int N, int R, int T, int NOWN>
+__global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const AvgTab tab, int M, unsigned* bar,
+                                                    double* r_out) {
+  using LY = CoarseLayout<N, R, T, NOWN>;
+  constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
+  extern __shared__ double2 smem[];
+  double2* X = smem + LY::X;
+  double2* Y = smem + LY::Y;
+  double2* TW = smem + LY::TW;
+  double2* C = smem + LY::C;
+  double2* A = smem + LY::A;
+  double2* Vs = smem + LY::VS;    // [NOWN*6]
+  double2* KSs = smem + LY::KS;   // [NOWN*6]
+  double2* kk = smem + LY::KK;    // [NOWN*6]
+  double2* un_s = smem + LY::UN;  // [NOWN*3]
+  double2* rdb = smem + LY::RDB;  // [T]
+  double2* PH = smem + LY::PH;    // [2][K+1]
+  double* sd = reinterpret_cast<double*>(smem + LY::D);
+  double* red = sd + LY::RED;     // [max(T, NOWN*6)]
+  double* GA = sd + LY::GA;       // [K+1] each
+  double* GP = sd + LY::GP;
+  double* GQ = sd + LY::GQ;
+  double* SW = sd + LY::SW;       // [2]
+  // per-CTA constants for the whole sweep: geometry, twiddles, and the phases / weights of this
+  // CTA's sample pair
+  fill_packed_twiddles<N, R, T>(TW, tab.tw);
+  for (int k = threadIdx.x; k <= K; k += T) {
+    GA[k] = __ldg(tab.g.a + k);
+    GP[k] = __ldg(tab.g.p + k);
+    GQ[k] = __ldg(tab.g.q + k);
+  }
+  const bool one_pair = (int)gridDim.x >= M / 2;
+  if (one_pair && (int)blockIdx.x < M / 2) {
+    const int mA = 2 * blockIdx.x + 1, mB = 2 * blockIdx.x + 2;
+    for (int k = threadIdx.x; k <= K; k += T) {
+      PH[k] = __ldg(tab.phase + (size_t)mA * KP + k);
+      PH[KP + k] = __ldg(tab.phase + (size_t)mB * KP + k);
+    }
+    if (threadIdx.x == 0) {
+      SW[0] = __ldg(tab.w + mA);
+      SW[1] = mB <= M - 1 ? __ldg(tab.w + mB) : 0.0;
+    }
+  }
+  __syncthreads();
+  const double2* PHc = one_pair ? PH : nullptr;
+  double2* yv = smem + LY::YV;
+  int* yidx = reinterpret_cast<int*>(sd + LY::YI);
+  const unsigned P = gridDim.x;
+  constexpr int Kc3 = 3 * Kc;
+  const int nst = ca.scheme == 0 ? 4 : 2;
+  unsigned epoch = 0, ucount = 0;
+  const bool prof = ca.prof && blockIdx.x == 0;
+  int ps = 0;
+  // the three stage-input buffers start empty (sentinel) before anyone writes
+  for (int i = blockIdx.x * T + threadIdx.x; i < 3 * Kc3; i += P * T) st_relaxed_v2(ca.yin + i, yin_sentinel());
+  grid_barrier(bar, P, epoch);
+  coarse_update_phase<N, T, NOWN>(ca, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount);  // slice 0: v = e^{ΔT D̂/2} U_0
+  for (int n = 0; n < ca.n_end; ++n) {
+    for (int st = 1; st <= nst; ++st) {
+      if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 0] = gtimer();
+      const double2* inbox = ca.yin + (size_t)(ucount % 3) * Kc3;
+      coarse_samples_phase<N, R, T>(inbox, const_cast<double2*>(ca.part), M, tab, X, Y, TW, C, A, PHc, SW, GA, GP, GQ,
+                                    (prof && ps == 8) ? ca.prof + 256 : nullptr);
+      if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 1] = gtimer();
+      grid_barrier(bar, P, epoch);
+      if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 2] = gtimer();
+      ++ucount;
+      coarse_update_phase<N, T, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount);
+      if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 3] = gtimer();
+      ++ps;
+    }
+  }
+  grid_barrier(bar, P, epoch);  // every slice's U, G and residual partials are written
+  if (r_out && blockIdx.x == 0) {  // r_k = max_n sqrt(Σ num / Σ den) over slices (fixed order)
+    double mx = 0.0;
+    bool bad = false;
+    for (int s = threadIdx.x; s < ca.n_end; s += T) {
+      double num = 0.0, den = 0.0;
+      for (int k = 0; k <= K; ++k) {
+        num += __ldcg(ca.rparts + ((size_t)s * (K + 1) + k) * 2);
+        den += __ldcg(ca.rparts + ((size_t)s * (K + 1) + k) * 2 + 1);
+      }
+      const double r = sqrt(num / den);
+      if (!(r == r) || isinf(r)) bad = true;
+      mx = fmax(mx, r);
+    }
+    double* rr = red;
+    rr[threadIdx.x] = bad ? __longlong_as_double(0x7ff8000000000000LL) : mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      bool nan = false;
+      for (int t = 0; t < T; ++t) {
+        if (rr[t] != rr[t]) nan = true;
+        m = fmax(m, rr[t]);
+      }
+      *r_out = nan ? __longlong_as_double(0x7ff8000000000000LL) : m;
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Standard parareal (NEXT-1): the coarse solver is ONE Strang step of size ΔT on the
+// full equation (Alg.3 with m = 1).  The serial sweep is a single CTA: per slice one Strang step
+// (2 N-evals, the state in the real lane of the packed pair), the parareal update
+// U_{n+1} = G + (F_n - G_n), G_n <- G, and the per-slice residual; r_k = max_n at the end.
+// ---------------------------------------------------------------------------------------------
+template <int N, int T>
+__global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h, double* U, double* G,
+                                                     const double* F, double* Gnew, int S, double* r_out) {
+  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
+  constexpr double invN = 1.0 / N;
+  extern __shared__ double2 smem[];
+  double2* W = smem;
+  double2* S1 = W + 3 * WL<N>::NP;
+  __shared__ double red[2][T];
+  __shared__ double rmax;
+  if (threadIdx.x == 0) rmax = 0.0;
+  const size_t L = (size_t)3 * NH * 2;
+  for (int n = 0; n < S; ++n) {
+    load_pair_eigen<N, T>(U + (size_t)n * L, nullptr, tab.g, S1);
+    __syncthreads();
+    for (int j = threadIdx.x; j < Kc; j += T) {  // v = E2 c
+      const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+#pragma unroll
+      for (int al = 0; al < 3; ++al)
+        S1[al * Kc + j] = dmul(al - 1, __ldg(tab.cp + 1 * (K + 1) + ak), __ldg(tab.c0 + 1 * (K + 1) + ak),
+                               S1[al * Kc + j]);
+    }
+    __syncthreads();
+    prologue_from<N, T>(W, S1, tab.g);
+    __syncthreads();
+    for (int st = 0; st < 2; ++st) {
+      nl_physical<N, T, radix_for<N>()>(W, tab.tw);
+      for (int j = threadIdx.x; j < Kc; j += T) {
+        const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+        const int kf = full_index(kap, N);
+        const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
+        const double p = __ldg(tab.g.p + ak), q = __ldg(tab.g.q + ak);
+        double2 nh[3], nn[3], x[3];
+        get_output<N>(W, kf, (double)kap, invN, nh);
+        to_eigen(as, p, q, nh, nn);
+#pragma unroll
+        for (int al = 0; al < 3; ++al) {
+          const int e = al * Kc + j;
+          if (st == 0) {
+            x[al] = caxpy(0.5 * h, nn[al], S1[e]);  // midpoint input v + (h/2) N(v)
+          } else {
+            const double2 w = caxpy(h, nn[al], S1[e]);  // w = v + h N(mid)
+            S1[e] = dmul(al - 1, __ldg(tab.cp + 1 * (K + 1) + ak), __ldg(tab.c0 + 1 * (K + 1) + ak), w);
+          }
+        }
+        if (st == 0) {
+          double2 u[3];
+          to_prim(as, p, q, x, u);
+          put_input<N>(W, kf, (double)kap, u);
+        }
+      }
+      if (st == 0) zero_tail<N, T>(W);
+      __syncthreads();
+    }
+    store_pair_prim<N, T>(S1, tab.g, Gnew, nullptr);
+    __syncthreads();
+    // parareal update and residual (R12) over the half spectrum
+    const double2* gn = reinterpret_cast<const double2*>(Gnew);
+    double2* Go = reinterpret_cast<double2*>(G) + (size_t)n * 3 * NH;
+    double2* Uo = reinterpret_cast<double2*>(U) + (size_t)(n + 1) * 3 * NH;
+    const double2* Fn = F ? reinterpret_cast<const double2*>(F) + (size_t)n * 3 * NH : nullptr;
+    double num = 0.0, den = 0.0;
+    for (int i = threadIdx.x; i < 3 * NH; i += T) {
+      const int k = i % NH;
+      const double2 g = gn[i];
+      const double2 un = Fn ? cadd(g, csub(Fn[i], Go[i])) : g;
+      const double2 d = csub(un, Uo[i]);
+      const double wk = (k == 0 || 2 * k == N) ? 1.0 : 2.0;
+      num += wk * (d.x * d.x + d.y * d.y);
+      den += wk * (un.x * un.x + un.y * un.y);
+      Go[i] = g;
+      Uo[i] = un;
+    }
+    red[0][threadIdx.x] = num;
+    red[1][threadIdx.x] = den;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0;
+      for (int t = 0; t < T; ++t) {
+        a += red[0][t];
+        b += red[1][t];
+      }
+      const double r = sqrt(a / b);
+      rmax = (r != r || rmax != rmax) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(rmax, r);
+    }
+    __syncthreads();
+  }
+  if (r_out && threadIdx.x == 0) *r_out = rmax;
+}
+
+// M0: DFMA peak probe — independent FMA chains, every SM
+
+template <int N>
+constexpr size_t nl_smem() { return sizeof(double2) * (3 * WL<N>::NP + 3 * (2 * (N / 3) + 1)); }
+template <int N>
+constexpr size_t avg_smem() { return sizeof(double2) * (3 * WL<N>::NP + 2 * 3 * (2 * (N / 3) + 1)); }
+
+
+
+template <int N, int NOWN, int R = coarse_radix<N>(), int T = coarse_threads<N>()>
+static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar,
+                                            double* r_out, int grid, cudaStream_t st) {
+  auto kfn = k_coarse_sweep<N, R, T, NOWN>;
+  const size_t sm = CoarseLayout<N, R, T, NOWN>::bytes;
+  cudaError_t e = set_smem(kfn, sm);
+  if (e != cudaSuccess) return e;
+  int dev, sms, per_sm;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, T, sm)) != cudaSuccess) return e;
+  if (grid > per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
+  CoarseArgs c2 = ca;
+  c2.nparts = grid;
+  if ((e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st)) != cudaSuccess) return e;
+  void* args[] = {(void*)&c2, (void*)&tab, (void*)&M, (void*)&bar, (void*)&r_out};
+  return cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(T), args, sm, st);
+}
+
+template <int N>
+static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar,
+                                         double* r_out, int* grid_used, cudaStream_t st) {
+  int dev, sms;
+  cudaError_t e;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  constexpr int K = N / 3;
+  // one sample pair per CTA, but enough CTAs that each owns <= 16 modes in the update phase;
+  // at most one CTA per SM (co-residency of the cooperative launch)
+  int grid = M / 2;
+  if (grid < (K + 1 + 15) / 16) grid = (K + 1 + 15) / 16;
+  if (grid > sms) grid = sms;
+  if (grid > ca.nparts) grid = ca.nparts;
+  if (grid < 1) grid = 1;
+  const int nown = (K + 1 + grid - 1) / grid;  // owned modes per CTA in the update phase
+  if (grid_used) *grid_used = grid;
+  if (nown <= 1) return launch_coarse_sweep_nown<N, 1>(ca, tab, M, bar, r_out, grid, st);
+  if (nown <= 2) return launch_coarse_sweep_nown<N, 2>(ca, tab, M, bar, r_out, grid, st);
+  if (nown <= 4) return launch_coarse_sweep_nown<N, 4>(ca, tab, M, bar, r_out, grid, st);
+  if (nown <= 8) return launch_coarse_sweep_nown<N, 8>(ca, tab, M, bar, r_out, grid, st);
+  if (nown <= 16) return launch_coarse_sweep_nown<N, 16>(ca, tab, M, bar, r_out, grid, st);
+  return cudaErrorInvalidConfiguration;
+}
+
+
+template <int N>
+static cudaError_t launch_strang_sweep_n(const FineTab& tab, double h, double* U, double* G, const double* F,
+                                         double* Gnew, int S, double* r_out, cudaStream_t st) {
+  constexpr int T = threads_for<N>();
+  auto kfn = k_strang_sweep<N, T>;
+  const size_t sm = nl_smem<N>();
+  cudaError_t e = set_smem(kfn, sm);
+  if (e != cudaSuccess) return e;
+  kfn<<<1, T, sm, st>>>(tab, h, U, G, F, Gnew, S, r_out);
+  return cudaGetLastError();
+}
+
+
+cudaError_t launch_coarse_sweep(int n, const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar, double* r_out,
+                                int* grid_used, cudaStream_t st) {
+#define C(NN) launch_coarse_sweep_n<NN>(ca, tab, M, bar, r_out, grid_used, st)
+  RSW_DISPATCH(n, C)
+#undef C
+}
+
+cudaError_t launch_strang_sweep(int n, const FineTab& tab, double h, double* U, double* G, const double* F,
+                                double* Gnew, int S, double* r_out, cudaStream_t st) {
+#define C(NN) launch_strang_sweep_n<NN>(tab, h, U, G, F, Gnew, S, r_out, st)
+  RSW_DISPATCH(n, C)
+#undef C
+}
+
+}  // namespace rsw
