@@ -203,16 +203,56 @@ def main():
     total_slice_steps = iters * w.n_slices * w.m_fine  # all ranks together
     value = total_slice_steps / (ms_max * 1e-3)
 
-    # fine kernel roofline (dominant-by-FLOP kernel; its share of the step is reported beside it)
-    fine_ms = statistics.median(s["fine_ms"] for s in stats) / max(iters, 1)   # per launch
+    # roofline of the dominant kernel of the timed region.  Pipelined schedule (1 GPU): ONE launch of
+    # k_parareal_pipe per solve (coarse sweeps + fine solves); its algorithmic flops = the fine
+    # slice-steps x F_step + every sweep's N-bar sample evaluations x F_sample.
+    # Bulk schedule (N > 1): the fine kernel k_fine, one launch per iteration.
+    pipelined = bool(stats[-1].get("pipelined"))
+    f_step = rsw.flops_per_unit(w.n, "etdrk4" if args.fine_scheme == 0 else "strang")
+    f_sample = rsw.flops_per_unit(w.n, "sample")
+    nominal_peak = 148 * 64 * 2 * 1965e6 / 1e12  # FP64 FMA units x clock (DESIGN.md §6)
+    measured_peak = rsw.fp64_peak_tflops()
+    local_slices = w.n_slices // world
+    fine_flops_iter = local_slices * w.m_fine * f_step
+    coarse_flops_sweep = w.n_slices * 4 * (w.M - 1) * f_sample  # averaged RK4: 4 N-bar per coarse step
+    if pipelined:
+        step_flops = iters * fine_flops_iter + (iters + 1) * coarse_flops_sweep
+        kern_ms = ms_max
+        roof = {"bound": "alu", "kernel": "k_parareal_pipe (pipelined sweeps + fine solves, 1 launch/step)",
+                "achieved": step_flops / (kern_ms * 1e-3) / 1e12, "flops_per_launch": step_flops,
+                "flops_fine": iters * fine_flops_iter, "flops_coarse": (iters + 1) * coarse_flops_sweep,
+                "share_of_step": 1.0}
+    else:
+        fine_ms = statistics.median(s["fine_ms"] for s in stats) / max(iters, 1)   # per launch
+        roof = {"bound": "alu", "kernel": "k_fine (ETDRK4 fine sweep)", "achieved": fine_flops_iter / (fine_ms * 1e-3) / 1e12,
+                "flops_per_launch": fine_flops_iter,
+                "share_of_step": statistics.median(s["fine_ms"] for s in stats) / ms_max}
+    roof.update({"peak": nominal_peak, "unit": "TFLOP/s", "frac": roof["achieved"] / nominal_peak, "traffic": None,
+                 "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz",
+                 "peak_measured_dfma": measured_peak, "frac_of_measured": roof["achieved"] / measured_peak})
     coarse_ms = statistics.median(s["coarse_ms"] for s in stats)
     comm_ms = statistics.median(s["comm_ms"] for s in stats)
-    f_step = rsw.flops_per_unit(w.n, "etdrk4" if args.fine_scheme == 0 else "strang")
-    local_slices = w.n_slices // world
-    fine_flops = local_slices * w.m_fine * f_step
-    achieved_tf = fine_flops / (fine_ms * 1e-3) / 1e12
-    nominal_peak = 148 * 64 * 2 * 1965e6 / 1e12  # FP64 FMA units x clock (DESIGN.md §7)
-    measured_peak = rsw.fp64_peak_tflops()
+
+    # the fine kernel alone on this rank's slices of the workload (same launch configuration as the
+    # bulk schedule's fine sweep): CUDA events around each launch, L2 flushed before each
+    uf = torch.from_numpy(inputs.random_states(w.n, local_slices, seed=0, kmax=32)).cuda()
+    of = torch.empty_like(uf)
+    fk = []
+    for r in range(4):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rsw.fine_propagate(p, uf, w.dT, w.dt, args.fine_scheme, out=of)
+        e1.record(stream)
+        e1.synchronize()
+        if r:
+            fk.append(e0.elapsed_time(e1))
+    fine_ms = statistics.median(fk)
+    fine_tf = fine_flops_iter / (fine_ms * 1e-3) / 1e12
+    roof_fine = {"bound": "alu", "kernel": "k_fine (ETDRK4 fine sweep, standalone)", "achieved": fine_tf,
+                 "peak": nominal_peak, "unit": "TFLOP/s", "frac": fine_tf / nominal_peak, "traffic": None,
+                 "frac_of_measured": fine_tf / measured_peak, "ms_per_launch": fine_ms,
+                 "flops_per_launch": fine_flops_iter, "slices": local_slices, "steps": w.m_fine}
 
     # ---- e2e: same solve through the C-ABI from pinned host buffers, H2D + D2H inside the region
     U_host = torch.empty(U.shape, dtype=torch.float64).pin_memory()
@@ -240,18 +280,17 @@ def main():
             "config": {"workload": w.name, "n": w.n, "slices": w.n_slices, "fine_steps_per_slice": w.m_fine,
                        "dt_eff": w.dt_eff, "iterations": iters, "M": w.M, "T0": w.T0, "eps": w.eps,
                        "fine_scheme": "ETDRK4" if args.fine_scheme == 0 else "Strang",
-                       "parallelism": f"slices sharded over {world} GPU(s), NCCL all-gather, replicated coarse",
+                       "parallelism": (f"1 GPU, pipelined parareal megakernel" if world == 1 else
+                                       f"slices sharded over {world} GPUs, NCCL all-gather, replicated coarse"),
                        "l2": "flushed (256 MB write) before every timed step"},
             "time_to_solution_ms": ms_max,
-            "phases_ms": {"fine": statistics.median(s["fine_ms"] for s in stats), "allgather": comm_ms,
-                          "coarse": coarse_ms, "total_library": statistics.median(s["total_ms"] for s in stats)},
+            "schedule": "pipelined (one persistent launch per solve)" if pipelined else "bulk (fine sweep + coarse sweep per iteration)",
+            "phases_ms": ({"pipelined_total": statistics.median(s["total_ms"] for s in stats)} if pipelined else
+                          {"fine": statistics.median(s["fine_ms"] for s in stats), "allgather": comm_ms,
+                           "coarse": coarse_ms, "total_library": statistics.median(s["total_ms"] for s in stats)}),
             "fine_kernel_slice_steps_per_s": local_slices * w.m_fine / (fine_ms * 1e-3) * world,
-            "roofline": {"bound": "alu", "kernel": "k_fine (ETDRK4 fine sweep)", "achieved": achieved_tf,
-                         "peak": nominal_peak, "unit": "TFLOP/s", "frac": achieved_tf / nominal_peak,
-                         "traffic": None, "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz",
-                         "peak_measured_dfma": measured_peak, "frac_of_measured": achieved_tf / measured_peak,
-                         "flops_per_launch": fine_flops,
-                         "share_of_step": statistics.median(s["fine_ms"] for s in stats) / ms_max},
+            "roofline": roof,
+            "roofline_fine": roof_fine,
             "clocks": clk.summary(),
             "e2e": {"value": total_slice_steps / (e2e_ms * 1e-3), "unit": UNIT, "ms": e2e_ms,
                     "h2d_bytes_per_step": u0_host.numel() * 8, "d2h_bytes_per_step": U_host.numel() * 8},

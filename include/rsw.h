@@ -91,9 +91,20 @@ rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, doub
                                 int32_t M, int32_t n_states, const double* u_in, double* u_out,
                                 void* stream);
 
+/* Schedule of the parareal iteration (results are bitwise identical; only the order of the work
+   differs):
+     RSW_SCHEDULE_AUTO      pipelined when supported (single GPU, n in {64, 128, 256}, coarse RK4 or
+                            midpoint), bulk otherwise;
+     RSW_SCHEDULE_BULK      per iteration: the fine sweep over all slices, then the serial coarse sweep;
+     RSW_SCHEDULE_PIPELINED one persistent kernel in which sweep k trails sweep k-1 slice by slice and
+                            each fine solve F(U^k_n) starts as soon as U^k_n exists (SURVEY
+                            NEXT-3); RSW_ERR_CONFIG if the configuration is not supported. */
+enum { RSW_SCHEDULE_AUTO = 0, RSW_SCHEDULE_BULK = 1, RSW_SCHEDULE_PIPELINED = 2 };
+
 typedef struct {
   double dT, dt, T0, tol;
   int32_t M, n_slices, max_iters, fine_scheme, coarse_scheme;
+  int32_t schedule; /* RSW_SCHEDULE_* */
 } parareal_config;
 
 typedef struct rsw_comm rsw_comm; /* opaque; NULL = single GPU */
@@ -103,6 +114,8 @@ typedef struct {
   double fine_ms, comm_ms, coarse_ms, total_ms;
   int64_t fine_slice_steps; /* slice-steps advanced by THIS rank's fine sweeps */
   int64_t kernel_launches;  /* kernels this library launched during the call */
+  int32_t pipelined;        /* 1: the pipelined schedule ran (fine / coarse times overlap: only
+                               total_ms is meaningful, fine_ms = coarse_ms = total_ms) */
 } rsw_parareal_stats;
 
 /* The asymptotic parareal iteration (Eq. HMM parareal iteration P:428-430; Alg.4):

@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("RSW_LIB") or os.path.join(_HERE, "librsw.so")
 RSW_OK, RSW_ERR_CONFIG, RSW_NOT_CONVERGED, RSW_ERR_DIVERGED, RSW_ERR_CUDA, RSW_ERR_NCCL = range(6)
 FINE_ETDRK4, FINE_STRANG = 0, 1
 COARSE_RK4, COARSE_MIDPOINT, COARSE_STRANG = 0, 1, 2
+SCHEDULE_AUTO, SCHEDULE_BULK, SCHEDULE_PIPELINED = 0, 1, 2
 FLAG_LINEAR_ONLY = 1
 
 # names exported by include/rsw.h (checked by tests/test_capi_load.py)
@@ -47,13 +48,14 @@ class _PararealConfig(ctypes.Structure):
     _fields_ = [("dT", ctypes.c_double), ("dt", ctypes.c_double), ("T0", ctypes.c_double),
                 ("tol", ctypes.c_double), ("M", ctypes.c_int32), ("n_slices", ctypes.c_int32),
                 ("max_iters", ctypes.c_int32), ("fine_scheme", ctypes.c_int32),
-                ("coarse_scheme", ctypes.c_int32)]
+                ("coarse_scheme", ctypes.c_int32), ("schedule", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
     _fields_ = [("fine_ms", ctypes.c_double), ("comm_ms", ctypes.c_double),
                 ("coarse_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
-                ("fine_slice_steps", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
+                ("fine_slice_steps", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("pipelined", ctypes.c_int32)]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -202,7 +204,7 @@ def shard_range(n_slices: int, rank: int, world: int):
 
 def parareal_iterate(p: Params, u0, *, dT, dt, T0, M, n_slices, max_iters, tol=0.0,
                      fine_scheme=FINE_ETDRK4, coarse_scheme=COARSE_RK4, comm: Comm | None = None,
-                     U=None, want_FG=False, allow_diverged=False):
+                     U=None, want_FG=False, allow_diverged=False, schedule=None):
     """Asymptotic parareal (Eq. HMM parareal iteration P:428-430, Alg.4).
     Returns dict(U, resid, iters, status, stats[, F, G])."""
     import torch
@@ -214,7 +216,9 @@ def parareal_iterate(p: Params, u0, *, dT, dt, T0, M, n_slices, max_iters, tol=0
     resid = (ctypes.c_double * max(max_iters, 1))()
     it = ctypes.c_int32(0)
     st = _Stats()
-    cfg = _PararealConfig(dT, dt, T0, tol, M, n_slices, max_iters, fine_scheme, coarse_scheme)
+    if schedule is None:
+        schedule = SCHEDULE_AUTO
+    cfg = _PararealConfig(dT, dt, T0, tol, M, n_slices, max_iters, fine_scheme, coarse_scheme, schedule)
     rc = load().parareal_iterate_ex(ctypes.byref(p._c()), ctypes.byref(cfg), a, ctypes.c_void_p(U.data_ptr()),
                                     resid, ctypes.byref(it), comm.handle if comm else None, _stream(),
                                     ctypes.c_void_p(F.data_ptr()) if want_FG else None,
@@ -223,7 +227,7 @@ def parareal_iterate(p: Params, u0, *, dT, dt, T0, M, n_slices, max_iters, tol=0
     out = dict(U=U, resid=[resid[i] for i in range(it.value)], iters=it.value, status=rc,
                stats=dict(fine_ms=st.fine_ms, comm_ms=st.comm_ms, coarse_ms=st.coarse_ms,
                           total_ms=st.total_ms, fine_slice_steps=st.fine_slice_steps,
-                          kernel_launches=st.kernel_launches))
+                          kernel_launches=st.kernel_launches, pipelined=bool(st.pipelined)))
     if want_FG:
         out["F"], out["G"] = F, G
     return out

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "librsw.so")
-SOURCES = ["rsw_k_fine.cu", "rsw_k_coarse.cu", "rsw_k_misc.cu", "rsw_capi.cu"]
+SOURCES = ["rsw_k_fine.cu", "rsw_k_coarse.cu", "rsw_k_misc.cu", "rsw_pipeline.cu", "rsw_capi.cu"]
 HEADERS = ["rsw_device.cuh", "rsw_internal.h", "rsw_blocks.cuh"]
 
 

@@ -370,6 +370,30 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// bounded spins (pipelined parareal): acquire loads, back off, give up after ~4 s or when another
+// CTA raised the watchdog flag wd (a dependency that never completes is a bug: the kernel then
+// reports an error instead of hanging the GPU)
+__device__ __forceinline__ bool watchdog_expired(unsigned long long t0, unsigned* wd) {
+  if (gtimer() - t0 > 4000000000ull) {
+    if (wd) atomicExch(wd, 1u);
+    return true;
+  }
+  return wd && *(volatile unsigned*)wd != 0;
+}
+// stopk / kself: give up as well once the run stopped before iteration kself (the waiting sweep is
+// discarded: its remaining work only has to reach the next group barrier, where it aborts)
+__device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target, unsigned* wd,
+                                               const int* stopk = nullptr, int kself = 0) {
+  if (ld_acquire_gpu(p) >= target) return;
+  const unsigned long long t0 = gtimer();
+  for (unsigned it = 0;; ++it) {
+    if (ld_acquire_gpu(p) >= target) return;
+    if (stopk && *(volatile const int*)stopk < kself) return;
+    if ((it & 63) == 63 && watchdog_expired(t0, wd)) return;
+    __nanosleep(64);
+  }
+}
+
 // Stage input through a triple-buffered shared array (replaces "owners write y -> grid barrier ->
 // everyone loads y"): update phase u writes its owned entries of the next stage input into
 // ybuf[u%3] (each entry once) and resets the same entries of ybuf[(u+2)%3] to the sentinel; the
@@ -392,37 +416,46 @@ __device__ __forceinline__ double2 yin_sentinel() {
   return make_double2(s, s);
 }
 
-template <int N, int R, int T>
+template <int N, int R, int T, class GRP = CtaGroup, int NPC = 1>
 __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* part, int M, const AvgTab& tab,
                                                      double2* X, double2* Y, const double2* TW, double2* C,
                                                      double2* A, const double2* PH, const double* SW,
                                                      const double* GA, const double* GP, const double* GQ,
-                                                     unsigned long long* cyc = nullptr) {
+                                                     unsigned long long* cyc = nullptr, int rank = -1, int P = -1,
+                                                     const GRP& grp = GRP()) {
+  const int tid_ = grp.tid();
+  if (rank < 0) {
+    rank = blockIdx.x;
+    P = gridDim.x;
+  }
 #define STAMP(i) \
-  if (cyc && threadIdx.x == 0) cyc[i] = clock64();
+  if (cyc && tid_ == 0) cyc[i] = clock64();
   STAMP(0)
   // PH: this CTA's phases e^{iωτ_m} for its first pair, [2][K+1] (null: load from the table);
   // SW: its weights w_mA, w_mB; GA/GP/GQ: geometry a, p, q per |κ| staged in shared memory
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
   constexpr double invN = 1.0 / N;
   // stage input from this CTA's inbox (y = inbox row): poll, keep, reset to the sentinel
-  for (int i = threadIdx.x; i < 3 * Kc; i += T) {
+  for (int i = tid_; i < 3 * Kc; i += T) {
     double2 v = ld_relaxed_v2(y + i);
     while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(y + i);
     C[i] = v;
     A[i] = make_double2(0.0, 0.0);
   }
-  __syncthreads();
+  grp.sync();
   const int npairs = M / 2;  // samples 1..M-1 -> pairs (1,2), (3,4), ...; last B may be M (w=0)
-  for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+  for (int pr = rank; pr < npairs; pr += P) {
     const int mA = 2 * pr + 1, mB = 2 * pr + 2;
     const bool hasB = mB <= M - 1;
-    const bool cached = PH && pr == (int)blockIdx.x;
-    for (int j = threadIdx.x; j < Kc; j += T) {
+    const int q = (pr - rank) / P;  // this CTA's q-th pair: phases / weights cached when q < NPC
+    const bool cached = PH && q < NPC;
+    const double2* PHq = PH + (size_t)q * 2 * KP;
+    const double* SWq = SW + 2 * q;
+    for (int j = tid_; j < Kc; j += T) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
       const double as = kap < 0 ? -GA[ak] : GA[ak];
-      const double2 pA = cached ? PH[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
-      const double2 pB = !hasB ? make_double2(1.0, 0.0) : (cached ? PH[KP + ak] : __ldg(tab.phase + (size_t)mB * KP + ak));
+      const double2 pA = cached ? PHq[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
+      const double2 pB = !hasB ? make_double2(1.0, 0.0) : (cached ? PHq[KP + ak] : __ldg(tab.phase + (size_t)mB * KP + ak));
       double2 c[3], u[3];
       // packed eigen input: P-_{mA} y + i P-_{mB} y   (P-: α=-1 -> e^{+iωτ}, α=+1 -> e^{-iωτ})
       const double2 ym = C[j], y0 = C[Kc + j], yp = C[2 * Kc + j];
@@ -435,12 +468,12 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       to_prim(as, GP[ak], GQ[ak], c, u);
       put_input_z<N>(X, full_index(kap, N), (double)kap, u);
     }
-    __syncthreads();
+    grp.sync();
     STAMP(1)
-    nl_core<N, R, T>(X, Y, TW);
+    nl_core<N, R, T>(X, Y, TW, grp);
     STAMP(2)
-    const double wA = cached ? SW[0] : __ldg(tab.w + mA), wB = hasB ? (cached ? SW[1] : __ldg(tab.w + mB)) : 0.0;
-    for (int j = threadIdx.x; j < Kc; j += T) {
+    const double wA = cached ? SWq[0] : __ldg(tab.w + mA), wB = hasB ? (cached ? SWq[1] : __ldg(tab.w + mB)) : 0.0;
+    for (int j = tid_; j < Kc; j += T) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
       const double as = kap < 0 ? -GA[ak] : GA[ak];
       const double p = GP[ak], q = GQ[ak];
@@ -455,22 +488,27 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       }
       to_eigen(as, p, q, na, ea);
       to_eigen(as, p, q, nb, eb);
-      const double2 pA = cached ? PH[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
+      const double2 pA = cached ? PHq[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
       A[j] = caxpy(wA, cmulc(ea[0], pA), A[j]);  // P+: α=-1 -> e^{-iωτ}, α=+1 -> e^{+iωτ}
       A[Kc + j] = caxpy(wA, ea[1], A[Kc + j]);
       A[2 * Kc + j] = caxpy(wA, cmul(ea[2], pA), A[2 * Kc + j]);
       if (hasB) {
-        const double2 pB = cached ? PH[KP + ak] : __ldg(tab.phase + (size_t)mB * KP + ak);
+        const double2 pB = cached ? PHq[KP + ak] : __ldg(tab.phase + (size_t)mB * KP + ak);
         A[j] = caxpy(wB, cmulc(eb[0], pB), A[j]);
         A[Kc + j] = caxpy(wB, eb[1], A[Kc + j]);
         A[2 * Kc + j] = caxpy(wB, cmul(eb[2], pB), A[2 * Kc + j]);
       }
     }
-    __syncthreads();  // all mirror reads of X done before the next prologue overwrites it
+    grp.sync();  // all mirror reads of X done before the next prologue overwrites it
     STAMP(3)
+    // one partial per sample pair (not per CTA): the owners' reduction order is then the same for
+    // every CTA count (bulk sweep, pipelined groups), so all schedules agree bitwise
+    double2* Pp = part + (size_t)pr * 3 * Kc;
+    for (int i = tid_; i < 3 * Kc; i += T) {
+      Pp[i] = A[i];
+      A[i] = make_double2(0.0, 0.0);
+    }
   }
-  double2* P = part + (size_t)blockIdx.x * 3 * Kc;
-  for (int i = threadIdx.x; i < 3 * Kc; i += T) P[i] = A[i];
   STAMP(4)
 #undef STAMP
 }
@@ -479,67 +517,85 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
 // items i = o*6 + e, entries e = (α, +κ) for e < 3, (α, -κ) for e >= 3.  The stage base v and the RK
 // accumulator ks of owned modes live in this CTA's shared memory for the whole sweep; the stage
 // input y is published to global memory for the samples phase of every CTA.
-template <int N, int NOWN, int T>
-__device__ __forceinline__ void push_stage_input(const CoarseArgs& ca, const double2* yv, const int* yidx, unsigned u) {
+template <int N, int NOWN, int T, class GRP = CtaGroup>
+__device__ __forceinline__ void push_stage_input(const CoarseArgs& ca, const double2* yv, const int* yidx, unsigned u,
+                                                 const GRP& grp = GRP()) {
+  const int tid_ = grp.tid();
   constexpr int Kc3 = 3 * (2 * (N / 3) + 1);
-  __syncthreads();
-  if (threadIdx.x < NOWN * 6 && yidx[threadIdx.x] >= 0) {
-    st_relaxed_v2(ca.yin + (size_t)(u % 3) * Kc3 + yidx[threadIdx.x], yv[threadIdx.x]);
-    st_relaxed_v2(ca.yin + (size_t)((u + 2) % 3) * Kc3 + yidx[threadIdx.x], yin_sentinel());
+  grp.sync();
+  if (tid_ < NOWN * 6 && yidx[tid_] >= 0) {
+    st_relaxed_v2(ca.yin + (size_t)(u % 3) * Kc3 + yidx[tid_], yv[tid_]);
+    st_relaxed_v2(ca.yin + (size_t)((u + 2) % 3) * Kc3 + yidx[tid_], yin_sentinel());
   }
 }
 
-template <int N, int T, int NOWN>
+template <int N, int T, int NOWN, class GRP = CtaGroup>
 __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int stage, int n, double2* Vs,
                                                     double2* KSs, double2* kk, double2* un_s, double* nd_s,
-                                                    double2* red_buf, double2* yv, int* yidx, unsigned ucount) {
+                                                    double2* red_buf, double2* yv, int* yidx, unsigned ucount,
+                                                    int rank = -1, int P = -1, const GRP& grp = GRP()) {
+  const int tid_ = grp.tid();
   constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
-  const int P = gridDim.x;
+  if (rank < 0) {
+    rank = blockIdx.x;
+    P = gridDim.x;
+  }
   const size_t Ls = (size_t)3 * NH;
   const double dT = ca.dT;
   auto entry = [&](int o, int e, int& ak, int& al, int& j) {
-    ak = blockIdx.x + o * P;
+    ak = rank + o * P;
     al = e % 3;
     j = (e < 3) ? ak : ((ak == 0) ? 0 : Kc - ak);
   };
   const bool last = (ca.scheme == 0) ? (stage == 4) : (stage == 2);
   // prefetch the finalize operands (F_n, old G_n, old U_{n+1}) before the reduction's L2 round trip
   double2 pf_F = make_double2(0.0, 0.0), pf_G = make_double2(0.0, 0.0), pf_U = make_double2(0.0, 0.0);
-  if (stage > 0 && last && threadIdx.x < NOWN * 3) {
-    const int o = threadIdx.x / 3, f = threadIdx.x % 3, ak = blockIdx.x + o * P;
+  if (stage > 0 && last && tid_ < NOWN * 3) {
+    const int o = tid_ / 3, f = tid_ % 3, ak = rank + o * P;
     if (ak <= K) {
+      // pipelined parareal: F(U^{k-1}_n) and the previous sweep's slice n must be complete
+      if (ca.wF) spin_until_geq(ca.wF + n / 2, 1u, ca.wd, ca.stopk, ca.kself);
+      if (ca.wprog) spin_until_geq(ca.wprog, ca.wunit * (unsigned)(n + 1), ca.wd, ca.stopk, ca.kself);
       if (ca.F) pf_F = __ldcg(reinterpret_cast<const double2*>(ca.F) + (size_t)n * Ls + f * NH + ak);
-      pf_G = reinterpret_cast<const double2*>(ca.G)[(size_t)n * Ls + f * NH + ak];
-      pf_U = reinterpret_cast<const double2*>(ca.U)[(size_t)(n + 1) * Ls + f * NH + ak];
+      pf_G = __ldcg(reinterpret_cast<const double2*>(ca.Gprev) + (size_t)n * Ls + f * NH + ak);
+      pf_U = __ldcg(reinterpret_cast<const double2*>(ca.Uprev) + (size_t)(n + 1) * Ls + f * NH + ak);
     }
   }
   if (stage > 0) {
-    // deterministic reduction of the partials: TQ threads per item issue all their loads at once,
-    // then a fixed-order tree in shared memory
-    constexpr int ITEMS = NOWN * 6;
-    constexpr int TQ0 = T / ITEMS;
-    constexpr int TQ = TQ0 >= 32 ? 32 : TQ0 >= 16 ? 16 : TQ0 >= 8 ? 8 : TQ0 >= 4 ? 4 : TQ0 >= 2 ? 2 : 1;
-    double2* rd = reinterpret_cast<double2*>(red_buf);
-    const int it = threadIdx.x / TQ, qd = threadIdx.x % TQ;
-    if (it < ITEMS) {
-      int ak, al, j;
-      entry(it / 6, it % 6, ak, al, j);
+    // deterministic reduction of the per-pair partials in a fixed order that does not depend on the
+    // CTA size or the owned-mode count: RQ = 8 lanes per item, lane q sums partials q, q+8, ...
+    // ascending, then a fixed xor tree over the 8 lanes (shuffles inside one warp)
+    constexpr int ITEMS = NOWN * 6, RQ = 8, IPR = T / RQ;  // items per round
+    static_assert(T % 32 == 0 && T >= RQ, "reduction layout");
+    for (int it0 = 0; it0 < ITEMS; it0 += IPR) {
+      const int it = it0 + tid_ / RQ, qd = tid_ % RQ;
       double2 sacc = make_double2(0.0, 0.0);
-      if (ak <= K)
-        for (int b = qd; b < ca.nparts; b += TQ) sacc = cadd(sacc, __ldcg(ca.part + (size_t)b * 3 * Kc + al * Kc + j));
-      rd[threadIdx.x] = sacc;
-    }
-    __syncthreads();
+      int ak = 0, al = 0, j = 0;
+      if (it < ITEMS) entry(it / 6, it % 6, ak, al, j);
+      if (it < ITEMS && ak <= K) {
+        const double2* src = ca.part + al * Kc + j;
+        for (int b0 = qd; b0 < ca.nparts; b0 += 8 * RQ) {  // 8 independent L2 loads in flight, summed in order
+          double2 buf[8];
 #pragma unroll
-    for (int w = TQ / 2; w > 0; w >>= 1) {
-      if (it < ITEMS && qd < w) rd[threadIdx.x] = cadd(rd[threadIdx.x], rd[threadIdx.x + w]);
-      __syncthreads();
+          for (int u = 0; u < 8; ++u) {
+            const int b = b0 + u * RQ;
+            buf[u] = b < ca.nparts ? __ldcg(src + (size_t)b * 3 * Kc) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sacc = cadd(sacc, buf[u]);
+        }
+      }
+#pragma unroll
+      for (int w = RQ / 2; w > 0; w >>= 1) {
+        sacc.x += __shfl_xor_sync(0xffffffffu, sacc.x, w);
+        sacc.y += __shfl_xor_sync(0xffffffffu, sacc.y, w);
+      }
+      if (it < ITEMS && qd == 0) kk[it] = sacc;
     }
-    if (it < ITEMS && qd == 0) kk[it] = rd[threadIdx.x];
-    __syncthreads();
-    if (threadIdx.x < NOWN * 6) {
+    grp.sync();
+    if (tid_ < NOWN * 6) {
       int ak, al, j;
-      const int it = threadIdx.x;
+      const int it = tid_;
       entry(it / 6, it % 6, ak, al, j);
       if (ak <= K && !(ak == 0 && it % 6 >= 3)) {
         const double2 k = kk[it];
@@ -570,13 +626,13 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
       }
     }
     if (!last) {
-      push_stage_input<N, NOWN, T>(ca, yv, yidx, ucount);
+      push_stage_input<N, NOWN, T>(ca, yv, yidx, ucount, grp);
       return;
     }
-    __syncthreads();
+    grp.sync();
     // finalize: D half step, back-transform, primitive G, parareal update (thread per (o, f))
-    if (threadIdx.x < NOWN * 3) {
-      const int o = threadIdx.x / 3, f = threadIdx.x % 3, ak = blockIdx.x + o * P;
+    if (tid_ < NOWN * 3) {
+      const int o = tid_ / 3, f = tid_ % 3, ak = rank + o * P;
       if (ak <= K) {
         const double a = __ldg(ca.g.a + ak), p = __ldg(ca.g.p + ak), q = __ldg(ca.g.q + ak);
         const double dh = __ldg(ca.dhalf + ak);
@@ -596,11 +652,11 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
         if (ca.F) un = cadd(g, csub(pf_F, pf_G));  // U^k_{n+1} = G(U^k_n) + (F_n - G_n)
         const double2 d = csub(un, pf_U);
         const double wk = (ak == 0 || 2 * ak == N) ? 1.0 : 2.0;
-        nd_s[threadIdx.x * 2] = wk * (d.x * d.x + d.y * d.y);
-        nd_s[threadIdx.x * 2 + 1] = wk * (un.x * un.x + un.y * un.y);
+        nd_s[tid_ * 2] = wk * (d.x * d.x + d.y * d.y);
+        nd_s[tid_ * 2 + 1] = wk * (un.x * un.x + un.y * un.y);
         *Gst = g;
         *Uo = un;
-        un_s[threadIdx.x] = un;
+        un_s[tid_] = un;
         if (ak == K)  // modes K < k <= N/2 stay zero
           for (int k = K + 1; k < NH; ++k) {
             Uo[k - K] = make_double2(0.0, 0.0);
@@ -608,11 +664,11 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
           }
       }
     }
-    __syncthreads();
-    if (ca.rparts && threadIdx.x < NOWN) {
-      const int ak = blockIdx.x + threadIdx.x * P;
+    grp.sync();
+    if (ca.rparts && tid_ < NOWN) {
+      const int ak = rank + tid_ * P;
       if (ak <= K) {
-        const double* t = nd_s + threadIdx.x * 6;
+        const double* t = nd_s + tid_ * 6;
         ca.rparts[((size_t)n * (K + 1) + ak) * 2 + 0] = t[0] + t[2] + t[4];
         ca.rparts[((size_t)n * (K + 1) + ak) * 2 + 1] = t[1] + t[3] + t[5];
       }
@@ -620,16 +676,16 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
     if (n + 1 >= ca.n_end) return;  // no next slice
   } else {
     // stage 0: load U_0 of owned modes
-    if (threadIdx.x < NOWN * 3) {
-      const int o = threadIdx.x / 3, f = threadIdx.x % 3, ak = blockIdx.x + o * P;
-      if (ak <= K) un_s[threadIdx.x] = reinterpret_cast<const double2*>(ca.U)[(size_t)n * Ls + f * NH + ak];
+    if (tid_ < NOWN * 3) {
+      const int o = tid_ / 3, f = tid_ % 3, ak = rank + o * P;
+      if (ak <= K) un_s[tid_] = reinterpret_cast<const double2*>(ca.U)[(size_t)n * Ls + f * NH + ak];
     }
-    __syncthreads();
+    grp.sync();
   }
   // first stage input of the next slice: v = e^{ΔT D̂/2} u (Alg.2), eigen, both signs of κ
-  if (threadIdx.x < NOWN * 6) {
+  if (tid_ < NOWN * 6) {
     int ak, al, j;
-    const int it = threadIdx.x, o = it / 6, e = it % 6;
+    const int it = tid_, o = it / 6, e = it % 6;
     entry(o, e, ak, al, j);
     if (ak <= K && !(ak == 0 && e >= 3)) {
       const double a = __ldg(ca.g.a + ak), p = __ldg(ca.g.p + ak), q = __ldg(ca.g.q + ak);
@@ -645,8 +701,19 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
       yidx[it] = -1;
     }
   }
-  push_stage_input<N, NOWN, T>(ca, yv, yidx, ucount);
-  __syncthreads();
+  push_stage_input<N, NOWN, T>(ca, yv, yidx, ucount, grp);
+  grp.sync();
 }
+
+template <int N, int R, int T, int NOWN, int NPC = 1>
+struct CoarseLayout {  // dynamic shared memory of a coarse-sweep CTA (double2 units, then doubles); NPC cached pairs
+  static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NR = (T > NOWN * 6 ? T : NOWN * 6);
+  static constexpr int X = 0, Y = X + 3 * N, TW = Y + 3 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc,
+                       VS = A + 3 * Kc, KS = VS + NOWN * 6, KK = KS + NOWN * 6, UN = KK + NOWN * 6,
+                       RDB = UN + NOWN * 3, PH = RDB + T, YV = PH + NPC * 2 * KP, D = YV + NOWN * 6;
+  static constexpr int RED = 0, GA = RED + NR, GP = GA + KP, GQ = GP + KP, SW = GQ + KP, YI = SW + 2 * NPC,
+                       ND = YI + NOWN * 6;  // YI: int entry indices stored in double slots
+  static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
+};
 
 }  // namespace rsw

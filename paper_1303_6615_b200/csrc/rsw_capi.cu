@@ -258,6 +258,7 @@ cudaError_t get_coarse(const rsw_params* p, double dT, CoarseTables** out) {
 // ---------------------------------------------------------------------------------------------
 struct Workspace {
   DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof, Gnew, yin;
+  DevBuf pU, pG, pF, prp, pres, pctl, pyb, ppart;  // pipelined schedule
   double* rhost = nullptr;
   std::vector<cudaEvent_t> ev;
   ~Workspace() {
@@ -317,7 +318,7 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   CUDA_TRY(get_avg(p, T0, M, &at));
   CUDA_TRY(get_coarse(p, dT, &ct));
   const int K = p->n / 3, Kc = 2 * K + 1, np = coarse_parts(M, p->n);
-  CUDA_TRY(ensure(ws->part, sizeof(double2) * (size_t)np * 3 * Kc));
+  CUDA_TRY(ensure(ws->part, sizeof(double2) * (size_t)std::max(np, M / 2) * 3 * Kc));
   CUDA_TRY(ensure(ws->vky, sizeof(double2) * 3 * 3 * (size_t)Kc));
   CUDA_TRY(ensure(ws->yin, sizeof(double2) * 3 * 3 * (size_t)Kc));
   ch.p = p;
@@ -328,7 +329,7 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   rsw::CoarseArgs& ca = ch.ca;
   ca.g = geom_of(g);
   ca.part = (const double2*)ws->part.p;
-  ca.nparts = np;
+  ca.nparts = std::max(M / 2, 1);
   ca.scheme = scheme;
   ca.dT = dT;
   ca.dhalf = (const double*)ct->dhalf.p;
@@ -339,7 +340,15 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   ca.yin = (double2*)ws->yin.p;
   ca.U = U;
   ca.G = G;
+  ca.Uprev = U;
+  ca.Gprev = G;
   ca.F = F;
+  ca.wprog = nullptr;
+  ca.wunit = 0;
+  ca.wF = nullptr;
+  ca.wd = nullptr;
+  ca.stopk = nullptr;
+  ca.kself = 0;
   ca.rparts = rparts;
   ca.n_end = nsteps;
   ca.prof = nullptr;
@@ -563,6 +572,164 @@ rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, doub
   return RSW_OK;
 }
 
+// Pipelined schedule (rsw_pipeline.cu): one cooperative launch runs every sweep and
+// every fine solve as soon as its inputs exist.  Same arithmetic as the bulk schedule, so U, the
+// residual history and the iteration count are bitwise identical (tests/test_gpu_parity.py).
+rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
+                         double* resid_hist, int32_t* iters_done, cudaStream_t st, double* F_out, double* G_out,
+                         rsw_parareal_stats* stats, Workspace* ws) {
+  const int n = p->n, Km = n / 3, Kc = 2 * Km + 1, S = cfg->n_slices, K = cfg->max_iters, M = cfg->M;
+  const size_t L = state_doubles(n);
+  const int m = n_fine_steps(cfg->dT, cfg->dt);
+  const double h = cfg->dT / m;
+  GeomTables* g;
+  FineTables* ft;
+  AvgTables* at;
+  CoarseTables* ct;
+  CUDA_TRY(get_geom(p, &g));
+  CUDA_TRY(get_fine(p, h, &ft));
+  CUDA_TRY(get_avg(p, cfg->T0, M, &at));
+  CUDA_TRY(get_coarse(p, cfg->dT, &ct));
+  rsw::PipeArgs a{};
+  a.ft = rsw::FineTab{geom_of(g), (const double2*)ft->cp.p, (const double*)ft->c0.p, (const double2*)g->tw.p};
+  a.at = rsw::AvgTab{geom_of(g), (const double*)at->w.p, (const double2*)at->phase.p, (const double2*)g->tw.p};
+  a.base.g = geom_of(g);
+  a.base.scheme = cfg->coarse_scheme;
+  a.base.dT = cfg->dT;
+  a.base.dhalf = (const double*)ct->dhalf.p;
+  a.base.back = (const double2*)ct->back.p;
+  a.S = S;
+  a.K = K;
+  a.M = M;
+  a.m_fine = m;
+  a.h = h;
+  a.tol = cfg->tol;
+  a.npairs = (S + 1) / 2;
+  // roles: coarse groups of GC CTAs (one sample pair each when GC = M/2), fine workers on the rest
+  size_t cap = 0;
+  // every CTA hosts a coarse sub-CTA and fine groups: NG groups of GC sub-CTAs run NG sweeps at once.
+  // Two sample pairs per coarse sub-CTA (GC = M/4) measured best on C3 (50 ms vs 60 ms at GC = M/2:
+  // more concurrent sweeps outweigh the longer stage)
+  a.GC = std::min(std::max(M / 4, 1), 64);
+  const char* eg = getenv("RSW_PIPE_GC");
+  if (eg) a.GC = std::max(1, atoi(eg));
+  while ((Km + 1 + a.GC - 1) / a.GC > 8 || (M / 2 + a.GC - 1) / a.GC > 8) a.GC *= 2;  // <= 8 modes / pairs per CTA
+  CUDA_TRY(rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, 0, &cap, st));
+  const char* egr = getenv("RSW_PIPE_GRID");
+  const int grid = egr ? atoi(egr) : (int)cap;
+  if (a.GC > grid) return fail(RSW_ERR_CONFIG, "pipelined schedule: not enough co-resident CTAs");
+  int ng = grid / a.GC;
+  const char* en = getenv("RSW_PIPE_NG");
+  if (en) ng = atoi(en);
+  a.NG = std::max(1, std::min(std::min(ng, K + 1), grid / a.GC));
+  // buffers
+  const size_t nU = (size_t)(K + 1) * (S + 1) * L, nG = (size_t)(K + 1) * S * L, nF = (size_t)std::max(K, 1) * S * L;
+  CUDA_TRY(ensure(ws->pU, sizeof(double) * nU));
+  CUDA_TRY(ensure(ws->pG, sizeof(double) * nG));
+  CUDA_TRY(ensure(ws->pF, sizeof(double) * nF));
+  CUDA_TRY(ensure(ws->prp, sizeof(double) * 2 * (size_t)(K + 1) * S * (Km + 1)));
+  CUDA_TRY(ensure(ws->pres, sizeof(double) * (K + 1)));
+  const size_t nctl = (size_t)(K + 1) + (size_t)std::max(K, 1) * a.npairs + std::max(K, 1) + 4 + (size_t)a.NG * 32;
+  CUDA_TRY(ensure(ws->pctl, sizeof(unsigned) * nctl));
+  CUDA_TRY(ensure(ws->pyb, sizeof(double2) * (size_t)a.NG * 3 * 3 * Kc));
+  CUDA_TRY(ensure(ws->ppart, sizeof(double2) * (size_t)a.NG * std::max(M / 2, 1) * 3 * Kc));
+  a.Uall = (double*)ws->pU.p;
+  a.Gall = (double*)ws->pG.p;
+  a.Fall = (double*)ws->pF.p;
+  a.rparts = (double*)ws->prp.p;
+  a.resid = (double*)ws->pres.p;
+  unsigned* ctl = (unsigned*)ws->pctl.p;
+  a.prog = ctl;
+  a.doneF = a.prog + (K + 1);
+  a.next = a.doneF + (size_t)std::max(K, 1) * a.npairs;
+  a.stopk = (int*)(a.next + std::max(K, 1));
+  a.wd = (unsigned*)(a.stopk + 1);
+  a.ticket = a.wd + 1;
+  a.gbar = a.ticket + 2;
+  a.ybuf = (double2*)ws->pyb.p;
+  a.part = (double2*)ws->ppart.p;
+  a.trace = nullptr;
+  static const bool trace = getenv("RSW_PIPE_TRACE") != nullptr;
+  const size_t ntr = 2 * (size_t)(K + 1) + (size_t)(K + 1) * S + 2 * (size_t)std::max(K, 1) * a.npairs;
+  if (trace) {
+    CUDA_TRY(ensure(ws->prof, sizeof(unsigned long long) * ntr));
+    CUDA_TRY(cudaMemsetAsync(ws->prof.p, 0, sizeof(unsigned long long) * ntr, st));
+    a.trace = (unsigned long long*)ws->prof.p;
+  }
+  cudaEvent_t* ev = ws->ev.data();
+  CUDA_TRY(cudaEventRecord(ev[6], st));
+  CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * nctl, st));
+  const int stop_init = K + 1;
+  CUDA_TRY(cudaMemcpyAsync(a.stopk, &stop_init, sizeof(int), cudaMemcpyHostToDevice, st));
+  for (int k = 0; k <= K; ++k)  // U^k_0 = u0 for every iteration
+    CUDA_TRY(cudaMemcpyAsync(a.Uall + (size_t)k * (S + 1) * L, u0, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, grid, nullptr, st));
+  int stopk = 0;
+  unsigned wd = 0;
+  std::vector<double> res(K + 1, 0.0);
+  CUDA_TRY(cudaMemcpyAsync(&stopk, a.stopk, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&wd, a.wd, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(res.data(), a.resid, sizeof(double) * (K + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (trace) {  // debug timeline to stderr (ms since the first sweep start)
+    std::vector<unsigned long long> tr(ntr);
+    CUDA_TRY(cudaMemcpy(tr.data(), a.trace, sizeof(unsigned long long) * ntr, cudaMemcpyDeviceToHost));
+    const double t0 = (double)tr[0];
+    auto ms = [&](unsigned long long t) { return t ? (t - t0) * 1e-6 : -1.0; };
+    fprintf(stderr, "[rsw pipe] grid %d NG %d GC %d npairs %d\n", grid, a.NG, a.GC, a.npairs);
+    for (int k = 0; k <= K; ++k) {
+      const unsigned long long* sl = tr.data() + 2 * (K + 1) + (size_t)k * S;
+      fprintf(stderr, "[rsw pipe] sweep %d: start %.3f end %.3f | slice 0 %.3f, S/4 %.3f, S/2 %.3f, S-1 %.3f\n", k,
+              ms(tr[2 * k]), ms(tr[2 * k + 1]), ms(sl[0]), ms(sl[S / 4]), ms(sl[S / 2]), ms(sl[S - 1]));
+    }
+    for (int k = 0; k < K; ++k) {
+      const unsigned long long* fk = tr.data() + 2 * (K + 1) + (size_t)(K + 1) * S + (size_t)k * a.npairs * 2;
+      double lat = 0, first = 1e30, last = 0;
+      int cnt = 0;
+      for (int q = 0; q < a.npairs; ++q)
+        if (fk[2 * q] && fk[2 * q + 1]) {
+          lat += (fk[2 * q + 1] - fk[2 * q]) * 1e-6;
+          first = std::min(first, ms(fk[2 * q]));
+          last = std::max(last, ms(fk[2 * q + 1]));
+          ++cnt;
+        }
+      fprintf(stderr, "[rsw pipe] fine k=%d: %d tasks, mean latency %.3f ms, first start %.3f, last end %.3f\n", k, cnt,
+              cnt ? lat / cnt : 0.0, first, last);
+    }
+  }
+  if (wd) return fail(RSW_ERR_CUDA, "pipelined parareal: a dependency wait timed out (watchdog)");
+  const int kout = stopk <= K ? stopk : K;
+  for (int k = 1; k <= kout; ++k) resid_hist[k - 1] = res[k];
+  *iters_done = kout;
+  CUDA_TRY(cudaMemcpyAsync(U, a.Uall + (size_t)kout * (S + 1) * L, sizeof(double) * L * (S + 1),
+                           cudaMemcpyDeviceToDevice, st));
+  if (F_out && kout >= 1)
+    CUDA_TRY(cudaMemcpyAsync(F_out, a.Fall + (size_t)(kout - 1) * S * L, sizeof(double) * L * S,
+                             cudaMemcpyDeviceToDevice, st));
+  if (G_out)
+    CUDA_TRY(cudaMemcpyAsync(G_out, a.Gall + (size_t)kout * S * L, sizeof(double) * L * S, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaEventRecord(ev[7], st));
+  if (stats) {
+    float tot;
+    CUDA_TRY(cudaEventSynchronize(ev[7]));
+    CUDA_TRY(cudaEventElapsedTime(&tot, ev[6], ev[7]));
+    stats->fine_ms = tot;
+    stats->comm_ms = 0;
+    stats->coarse_ms = tot;
+    stats->total_ms = tot;
+    stats->fine_slice_steps = (int64_t)kout * S * m;
+    stats->kernel_launches = 1;
+    stats->pipelined = 1;
+  }
+  if (kout >= 1 && (!std::isfinite(res[kout]) || res[kout] > 1e6))
+    return fail(RSW_ERR_DIVERGED, "parareal residual non-finite or > 1e6");
+  if (cfg->tol > 0 && K > 0 && !(stopk <= K)) {
+    g_err = "parareal: tolerance not reached within max_iters";
+    return RSW_NOT_CONVERGED;
+  }
+  return RSW_OK;
+}
+
 rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
                                double* resid_hist, int32_t* iters_done, rsw_comm* comm, void* stream,
                                double* F_out, double* G_out, rsw_parareal_stats* stats) {
@@ -590,6 +757,21 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   std::lock_guard<std::mutex> lk(g_mu);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace* ws = workspace();
+  if (stats) stats->pipelined = 0;
+  {
+    const char* vwe = getenv("RSW_VIRTUAL_WORLD");
+    const bool can_pipe = !comm && rsw::pipeline_supported(p->n) && cfg->coarse_scheme != RSW_COARSE_STRANG &&
+                          !(vwe && atoi(vwe) > 1);
+    const char* pe = getenv("RSW_PIPELINE");
+    const bool auto_pipe = cfg->schedule == RSW_SCHEDULE_AUTO && !(pe && pe[0] == '0');
+    if (cfg->schedule == RSW_SCHEDULE_PIPELINED && !can_pipe)
+      return fail(RSW_ERR_CONFIG, "pipelined schedule needs one GPU, n in {64,128,256} and an averaged coarse solver");
+    if (cfg->schedule != RSW_SCHEDULE_AUTO && cfg->schedule != RSW_SCHEDULE_BULK &&
+        cfg->schedule != RSW_SCHEDULE_PIPELINED)
+      return fail(RSW_ERR_CONFIG, "unknown schedule");
+    if (can_pipe && (auto_pipe || cfg->schedule == RSW_SCHEDULE_PIPELINED))
+      return run_pipelined(p, cfg, u0, U, resid_hist, iters_done, st, F_out, G_out, stats, ws);
+  }
   const int n = p->n, K = n / 3;
   const size_t L = state_doubles(n);
   const int m = n_fine_steps(cfg->dT, cfg->dt);

@@ -30,8 +30,8 @@ struct AvgTab {
 // Arguments of the coarse combine kernel (one state chain)
 struct CoarseArgs {
   ModeGeom g;
-  const double2* part;  // [nparts][3][Kc]
-  int nparts;
+  const double2* part;  // [nparts][3][Kc]  one partial per sample pair
+  int nparts;           // sample pairs M/2
   int scheme;           // 0 RK4, 1 midpoint
   double dT;
   const double* dhalf;  // e^{-μκ^4 ΔT/2}
@@ -40,13 +40,47 @@ struct CoarseArgs {
   double2* ks;          // [3][Kc]
   double2* y;           // [3][Kc]
   double2* yin;         // [3][3][Kc] triple-buffered stage input (sentinel = not yet written)
-  double* U;            // [S+1][3][N/2+1][2] (chain states)
-  double* G;            // [S][3][N/2+1][2]
+  double* U;            // [S+1][3][N/2+1][2] (chain states, written)
+  double* G;            // [S][3][N/2+1][2] (G(U_n) of this sweep, written)
+  const double* Uprev;  // previous iterate U^{k-1} (residual); == U for the in-place classic sweep
+  const double* Gprev;  // G(U^{k-1}_n) of the previous sweep; == G for the in-place classic sweep
   const double* F;      // [S][...] or null (k = 0 sweep / plain coarse step)
+  const unsigned* wprog;  // pipelined: progress counter of the previous sweep (>= wunit*(n+1): slice n done), or null
+  unsigned wunit;
+  const unsigned* wF;     // pipelined: done flags of the previous iteration's fine pairs, or null
+  unsigned* wd;           // pipelined: watchdog flag (set when a wait times out), or null
+  const int* stopk;       // pipelined: first stopped iteration (waits of sweep kself > *stopk give up), or null
+  int kself;
   double* rparts;       // [S][K+1][2] residual partials or null
   int n_end;            // number of chain steps (S)
   unsigned long long* prof;  // optional phase timestamps (CTA 0; RSW_PROFILE_COARSE=1), else null
 };
+
+// Pipelined parareal (rsw_pipeline.cu): every iteration's buffers stay resident
+struct PipeArgs {
+  CoarseArgs base;      // geometry, scheme, dT, D half step, back-transform (per-sweep pointers set in-kernel)
+  AvgTab at;
+  FineTab ft;
+  int S, K, M, m_fine, NG, GC, npairs;
+  double h, tol;
+  double* Uall;         // [K+1][S+1][state]   U^k (row 0 = u0)
+  double* Gall;         // [K+1][S][state]     G(U^k_n)
+  double* Fall;         // [K][S][state]       F(U^k_n)
+  double* rparts;       // [K+1][S][K_modes+1][2]
+  double* resid;        // [K+1]               r_k
+  unsigned* prog;       // [K+1]   sweep progress (CTA-slices finalized)
+  unsigned* doneF;      // [K][npairs] fine pair done flags
+  unsigned* next;       // [K]     next unclaimed fine pair per iteration
+  int* stopk;           // first iteration that stopped the run (K+1: none)
+  unsigned* wd;         // watchdog flag
+  unsigned* ticket;     // role tickets
+  unsigned* gbar;       // [NG][32] group barrier counters
+  double2* ybuf;        // [NG][3][3Kc] stage inputs
+  double2* part;        // [NG][GC][3Kc] partial sums
+  unsigned long long* trace;  // optional timeline (RSW_PIPE_TRACE): sweep [K+1][2], slice [K+1][S], fine [K][npairs][2]
+};
+bool pipeline_supported(int n);
+cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);
 
 cudaError_t launch_fine(int n, int scheme, bool lin, const double* in, double* out, int S, int m, double h,
                         const FineTab& tab, cudaStream_t st);

@@ -21,16 +21,6 @@ static cudaError_t set_smem(KernelT k, size_t bytes) {
     default: return cudaErrorInvalidValue;     \
   }
 
-template <int N, int R, int T, int NOWN>
-struct CoarseLayout {  // dynamic shared memory of k_coarse_sweep (double2 units, then doubles)
-  static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NR = (T > NOWN * 6 ? T : NOWN * 6);
-  static constexpr int X = 0, Y = X + 3 * N, TW = Y + 3 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc,
-                       VS = A + 3 * Kc, KS = VS + NOWN * 6, KK = KS + NOWN * 6, UN = KK + NOWN * 6,
-                       RDB = UN + NOWN * 3, PH = RDB + T, YV = PH + 2 * KP, D = YV + NOWN * 6;
-  static constexpr int RED = 0, GA = RED + NR, GP = GA + KP, GQ = GP + KP, SW = GQ + KP, YI = SW + 2,
-                       ND = YI + NOWN * 6;  // YI: int entry indices stored in double slots
-  static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
-};
 
 template <int N, int R, int T, int NOWN>
 __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const AvgTab tab, int M, unsigned* bar,
@@ -252,7 +242,6 @@ static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& 
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, T, sm)) != cudaSuccess) return e;
   if (grid > per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
   CoarseArgs c2 = ca;
-  c2.nparts = grid;
   if ((e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st)) != cudaSuccess) return e;
   void* args[] = {(void*)&c2, (void*)&tab, (void*)&M, (void*)&bar, (void*)&r_out};
   return cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(T), args, sm, st);
@@ -271,7 +260,6 @@ static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab
   int grid = M / 2;
   if (grid < (K + 1 + 15) / 16) grid = (K + 1 + 15) / 16;
   if (grid > sms) grid = sms;
-  if (grid > ca.nparts) grid = ca.nparts;
   if (grid < 1) grid = 1;
   const int nown = (K + 1 + grid - 1) / grid;  // owned modes per CTA in the update phase
   if (grid_used) *grid_used = grid;

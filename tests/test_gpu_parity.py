@@ -3,6 +3,7 @@ relative weighted L2 (R12) <= 1e-10 per state / slice endpoint / iterate, identi
 counts.  Every call goes through the C-ABI (paper_1303_6615_b200 is a ctypes binding)."""
 import numpy as np
 import pytest
+import torch
 
 from paper_1303_6615_b200 import inputs
 from tests.helpers import rel_l2, to_np
@@ -274,3 +275,43 @@ def test_paper_experiment_prefix(rsw_gpu, orc, name, coarse):
     r = orc.parareal(u0, cfg["eps"], 1.0, 1e-4, n, **kw)
     assert rel_l2(to_np(g["U"]), r["U"], n)[1:].max() < TOL
     assert np.allclose(g["resid"], r["resid"], rtol=1e-8, atol=0)
+
+
+# ---- pipelined schedule (NEXT-3): same arithmetic as the bulk schedule, so results are bitwise equal
+@pytest.mark.parametrize("wname,fine_scheme,coarse_scheme", [("C1", 0, 0), ("C1", 1, 1), ("C2", 0, 0)])
+def test_pipelined_schedule_bitwise_equals_bulk(rsw_gpu, wname, fine_scheme, coarse_scheme):
+    w = getattr(inputs, wname)
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=w.max_iters, tol=w.tol,
+              fine_scheme=fine_scheme, coarse_scheme=coarse_scheme, want_FG=True)
+    a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
+    assert b["stats"]["pipelined"] and not a["stats"]["pipelined"]
+    assert a["iters"] == b["iters"] and a["resid"] == b["resid"]
+    assert torch.equal(a["U"], b["U"])
+    assert torch.equal(a["F"], b["F"]) and torch.equal(a["G"], b["G"])
+
+
+@pytest.mark.parametrize("gc,ng", [(32, 4), (16, 6), (64, 2)])
+def test_pipelined_group_layouts_bitwise(rsw_gpu, gc, ng, monkeypatch):
+    """C3 (the bench workload, 2 iterations) under several coarse-group layouts: per-pair partials
+    and a fixed reduction order make the result independent of how the sweeps are spread."""
+    w = inputs.C3
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=2)
+    a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    monkeypatch.setenv("RSW_PIPE_GC", str(gc))
+    monkeypatch.setenv("RSW_PIPE_NG", str(ng))
+    b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
+    assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
+
+
+def test_pipelined_rejects_unsupported(rsw_gpu):
+    w = inputs.C1
+    p = P(rsw_gpu, w.eps, w.F, w.mu, 512)
+    u0 = dev(inputs.random_states(512, 1, seed=0)[0])
+    with pytest.raises(rsw_gpu.RSWError):
+        rsw_gpu.parareal_iterate(p, u0, dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=4, max_iters=1,
+                                 schedule=rsw_gpu.SCHEDULE_PIPELINED)

@@ -1,0 +1,2 @@
+RSW_PIPE_TRACE=1 timeout 120 python tools/pipe_check.py C1 C2 C3 2>&1 | grep -v "dyn \|sweep\|fine k" | tail -16
+for cfg in "32 4" "16 6"; do set -- $cfg; echo "== GC=$1 NG=$2"; RSW_PIPE_GC=$1 RSW_PIPE_NG=$2 RSW_PIPE_TRACE=1 timeout 120 python tools/pipe_check.py C3 2>&1 | grep -v "dyn " | tail -16; done

@@ -1,0 +1,3 @@
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 120 python tools/pipe_check.py C1 C2 C3 2>&1 | grep -v "dyn \|sweep\|fine k"
+for cfg in "32 4" "16 6"; do set -- $cfg; echo "== GC=$1 NG=$2"; RSW_PIPE_GC=$1 RSW_PIPE_NG=$2 timeout 120 python tools/pipe_check.py C2 C3 2>&1 | grep "identical\|schedule=2"; done
