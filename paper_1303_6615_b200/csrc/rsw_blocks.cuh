@@ -416,13 +416,20 @@ __device__ __forceinline__ double2 yin_sentinel() {
   return make_double2(s, s);
 }
 
-template <int N, int R, int T, class GRP = CtaGroup, int NPC = 1>
+// Samples phase of one RK stage (Alg.1): poll the stage input y into C, then evaluate this
+// CTA's sample pairs (m_A, m_B) = (2p+1, 2p+2), p = rank, rank + P, ..., SPLIT pairs at a time on
+// SPLIT thread halves (each with its own X/Y at X + h*6N and named barrier 12 + h), writing one
+// partial Σ_{m in pair} w_m P+_m N(P-_m y) per pair to part[p] (per-pair partials: the owners'
+// reduction order is then independent of the CTA count, so every schedule agrees bitwise).
+template <int N, int R, int T, class GRP = CtaGroup, int NPC = 1, int SPLIT = 1>
 __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* part, int M, const AvgTab& tab,
-                                                     double2* X, double2* Y, const double2* TW, double2* C,
-                                                     double2* A, const double2* PH, const double* SW,
-                                                     const double* GA, const double* GP, const double* GQ,
-                                                     unsigned long long* cyc = nullptr, int rank = -1, int P = -1,
-                                                     const GRP& grp = GRP()) {
+                                                     double2* X, double2* /*Y (= X + 3N)*/, const double2* TW,
+                                                     double2* C, double2* /*A (unused)*/, const double2* PH,
+                                                     const double* SW, const double* GA, const double* GP,
+                                                     const double* GQ, unsigned long long* cyc = nullptr,
+                                                     int rank = -1, int P = -1, const GRP& grp = GRP()) {
+  static_assert(SPLIT == 1 || SPLIT == 2, "SPLIT");
+  constexpr int TH = T / SPLIT;
   const int tid_ = grp.tid();
   if (rank < 0) {
     rank = blockIdx.x;
@@ -431,27 +438,30 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
 #define STAMP(i) \
   if (cyc && tid_ == 0) cyc[i] = clock64();
   STAMP(0)
-  // PH: this CTA's phases e^{iωτ_m} for its first pair, [2][K+1] (null: load from the table);
-  // SW: its weights w_mA, w_mB; GA/GP/GQ: geometry a, p, q per |κ| staged in shared memory
+  // PH: phases e^{iωτ_m} of this CTA's first NPC pairs, [NPC][2][K+1] (null: load from the table);
+  // SW: their weights; GA/GP/GQ: geometry a, p, q per |κ| staged in shared memory
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
   constexpr double invN = 1.0 / N;
-  // stage input from this CTA's inbox (y = inbox row): poll, keep, reset to the sentinel
+  // stage input (triple-buffered, sentinel = not yet written): poll, keep
   for (int i = tid_; i < 3 * Kc; i += T) {
     double2 v = ld_relaxed_v2(y + i);
     while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(y + i);
     C[i] = v;
-    A[i] = make_double2(0.0, 0.0);
   }
   grp.sync();
+  const int h = SPLIT > 1 ? tid_ / TH : 0, th = tid_ - h * TH;
+  const NamedGroup hg{grp.base() + h * TH, 12 + h, TH};
+  double2* Xh = X + (size_t)h * 6 * N;
+  double2* Yh = Xh + 3 * N;
   const int npairs = M / 2;  // samples 1..M-1 -> pairs (1,2), (3,4), ...; last B may be M (w=0)
-  for (int pr = rank; pr < npairs; pr += P) {
+  for (int pr = rank + h * P; pr < npairs; pr += SPLIT * P) {
     const int mA = 2 * pr + 1, mB = 2 * pr + 2;
     const bool hasB = mB <= M - 1;
     const int q = (pr - rank) / P;  // this CTA's q-th pair: phases / weights cached when q < NPC
     const bool cached = PH && q < NPC;
     const double2* PHq = PH + (size_t)q * 2 * KP;
     const double* SWq = SW + 2 * q;
-    for (int j = tid_; j < Kc; j += T) {
+    for (int j = th; j < Kc; j += TH) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
       const double as = kap < 0 ? -GA[ak] : GA[ak];
       const double2 pA = cached ? PHq[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
@@ -466,20 +476,21 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       c[1] = cadd(y0, cmuli(b0));
       c[2] = cadd(cmulc(yp, pA), cmuli(bp));
       to_prim(as, GP[ak], GQ[ak], c, u);
-      put_input_z<N>(X, full_index(kap, N), (double)kap, u);
+      put_input_z<N>(Xh, full_index(kap, N), (double)kap, u);
     }
-    grp.sync();
+    if (SPLIT > 1) hg.sync(); else grp.sync();
     STAMP(1)
-    nl_core<N, R, T>(X, Y, TW, grp);
+    if (SPLIT > 1) nl_core<N, R, TH>(Xh, Yh, TW, hg); else nl_core<N, R, T>(Xh, Yh, TW, grp);
     STAMP(2)
     const double wA = cached ? SWq[0] : __ldg(tab.w + mA), wB = hasB ? (cached ? SWq[1] : __ldg(tab.w + mB)) : 0.0;
-    for (int j = tid_; j < Kc; j += T) {
+    double2* Pp = part + (size_t)pr * 3 * Kc;
+    for (int j = th; j < Kc; j += TH) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
       const double as = kap < 0 ? -GA[ak] : GA[ak];
       const double p = GP[ak], q = GQ[ak];
       double2 zp[3], zm[3], na[3], nb[3], ea[3], eb[3];
-      get_output_z<N>(X, full_index(kap, N), (double)kap, invN, zp);
-      get_output_z<N>(X, full_index(-kap, N), (double)(-kap), invN, zm);
+      get_output_z<N>(Xh, full_index(kap, N), (double)kap, invN, zp);
+      get_output_z<N>(Xh, full_index(-kap, N), (double)(-kap), invN, zm);
 #pragma unroll
       for (int f = 0; f < 3; ++f) {  // unpack: N_A(κ) = (Z(κ) + conj Z(-κ))/2, N_B = (Z - conj Z(-κ))/(2i)
         const double2 zc = cconj(zm[f]);
@@ -489,26 +500,24 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       to_eigen(as, p, q, na, ea);
       to_eigen(as, p, q, nb, eb);
       const double2 pA = cached ? PHq[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
-      A[j] = caxpy(wA, cmulc(ea[0], pA), A[j]);  // P+: α=-1 -> e^{-iωτ}, α=+1 -> e^{+iωτ}
-      A[Kc + j] = caxpy(wA, ea[1], A[Kc + j]);
-      A[2 * Kc + j] = caxpy(wA, cmul(ea[2], pA), A[2 * Kc + j]);
+      const double2 z0 = make_double2(0.0, 0.0);
+      double2 am = caxpy(wA, cmulc(ea[0], pA), z0);  // P+: α=-1 -> e^{-iωτ}, α=+1 -> e^{+iωτ}
+      double2 a0 = caxpy(wA, ea[1], z0);
+      double2 ap = caxpy(wA, cmul(ea[2], pA), z0);
       if (hasB) {
         const double2 pB = cached ? PHq[KP + ak] : __ldg(tab.phase + (size_t)mB * KP + ak);
-        A[j] = caxpy(wB, cmulc(eb[0], pB), A[j]);
-        A[Kc + j] = caxpy(wB, eb[1], A[Kc + j]);
-        A[2 * Kc + j] = caxpy(wB, cmul(eb[2], pB), A[2 * Kc + j]);
+        am = caxpy(wB, cmulc(eb[0], pB), am);
+        a0 = caxpy(wB, eb[1], a0);
+        ap = caxpy(wB, cmul(eb[2], pB), ap);
       }
+      Pp[j] = am;
+      Pp[Kc + j] = a0;
+      Pp[2 * Kc + j] = ap;
     }
-    grp.sync();  // all mirror reads of X done before the next prologue overwrites it
+    if (SPLIT > 1) hg.sync(); else grp.sync();  // all mirror reads of X done before the next prologue
     STAMP(3)
-    // one partial per sample pair (not per CTA): the owners' reduction order is then the same for
-    // every CTA count (bulk sweep, pipelined groups), so all schedules agree bitwise
-    double2* Pp = part + (size_t)pr * 3 * Kc;
-    for (int i = tid_; i < 3 * Kc; i += T) {
-      Pp[i] = A[i];
-      A[i] = make_double2(0.0, 0.0);
-    }
   }
+  if (SPLIT > 1) grp.sync();
   STAMP(4)
 #undef STAMP
 }
@@ -705,10 +714,10 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
   grp.sync();
 }
 
-template <int N, int R, int T, int NOWN, int NPC = 1>
+template <int N, int R, int T, int NOWN, int NPC = 1, int SPLIT = 1>
 struct CoarseLayout {  // dynamic shared memory of a coarse-sweep CTA (double2 units, then doubles); NPC cached pairs
   static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NR = (T > NOWN * 6 ? T : NOWN * 6);
-  static constexpr int X = 0, Y = X + 3 * N, TW = Y + 3 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc,
+  static constexpr int X = 0, Y = X + 3 * N, TW = X + SPLIT * 6 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc,
                        VS = A + 3 * Kc, KS = VS + NOWN * 6, KK = KS + NOWN * 6, UN = KK + NOWN * 6,
                        RDB = UN + NOWN * 3, PH = RDB + T, YV = PH + NPC * 2 * KP, D = YV + NOWN * 6;
   static constexpr int RED = 0, GA = RED + NR, GP = GA + KP, GQ = GP + KP, SW = GQ + KP, YI = SW + 2 * NPC,

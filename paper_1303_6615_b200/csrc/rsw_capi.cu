@@ -607,10 +607,17 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   a.npairs = (S + 1) / 2;
   // roles: coarse groups of GC CTAs (one sample pair each when GC = M/2), fine workers on the rest
   size_t cap = 0;
-  // every CTA hosts a coarse sub-CTA and fine groups: NG groups of GC sub-CTAs run NG sweeps at once.
-  // Two sample pairs per coarse sub-CTA (GC = M/4) measured best on C3 (50 ms vs 60 ms at GC = M/2:
-  // more concurrent sweeps outweigh the longer stage)
-  a.GC = std::min(std::max(M / 4, 1), 64);
+  // every CTA hosts a coarse sub-CTA and a fine group: NG groups of GC sub-CTAs run NG sweeps at once.
+  // Prefer running every sweep concurrently (NG = K+1) as long as a sub-CTA evaluates at most 4 sample
+  // pairs (two rounds of two concurrent halves): C3 measured 43.9 ms at GC = 24 / NG = 6, 45.0 at
+  // 32 / 4, 58.3 at 64 / 2.
+  {
+    int smc = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&smc, cudaDevAttrMultiProcessorCount, dev);
+    const int pairs = std::max(M / 2, 1);
+    a.GC = std::max((pairs + 3) / 4, std::min(pairs, smc / (K + 1)));
+  }
   const char* eg = getenv("RSW_PIPE_GC");
   if (eg) a.GC = std::max(1, atoi(eg));
   while ((Km + 1 + a.GC - 1) / a.GC > 8 || (M / 2 + a.GC - 1) / a.GC > 8) a.GC *= 2;  // <= 8 modes / pairs per CTA

@@ -305,12 +305,14 @@ __device__ __forceinline__ void nl_physical(double2* W, const double2* __restric
 // ---------------------------------------------------------------------------------------------
 // thread-group policies: the whole CTA, or a warp-aligned group of a CTA with its own named barrier
 struct CtaGroup {
+  __device__ __forceinline__ int base() const { return 0; }
   __device__ __forceinline__ int tid() const { return threadIdx.x; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
 };
 struct NamedGroup {
-  int base, id, nthr;  // first thread, barrier id (1..15), thread count (multiple of 32)
-  __device__ __forceinline__ int tid() const { return threadIdx.x - base; }
+  int b0, id, nthr;  // first thread, barrier id (1..15), thread count (multiple of 32)
+  __device__ __forceinline__ int base() const { return b0; }
+  __device__ __forceinline__ int tid() const { return threadIdx.x - b0; }
   __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory"); }
 };
 

@@ -74,7 +74,8 @@ __device__ __forceinline__ bool group_barrier(unsigned* bar, unsigned P, unsigne
 // the CTA rather than spread over CTAs.
 template <int N, int RC, int TC, int NOWN, int NPC, int RF, int TG, int NPG>
 struct PipeLayout {
-  using CL = CoarseLayout<N, RC, TC, NOWN, NPC>;
+  static constexpr int SPLIT = (NPC >= 2 && TC / 2 >= 3 * N / RC) ? 2 : 1;  // pairs evaluated concurrently
+  using CL = CoarseLayout<N, RC, TC, NOWN, NPC, SPLIT>;
   static constexpr int K = N / 3, KP = K + 1;
   static constexpr int C0 = 0, F0 = (int)((CL::bytes + 15) / 16);  // double2 offsets of the coarse / fine regions
   static constexpr int F_TW = F0, F_CP = F_TW + fft_tw_size<N, RF>(), F_D = F_CP + 6 * KP, F_ND = 9 * KP,
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         bool aborted = false;
         for (int n = 0; n < S && !aborted; ++n) {
           for (int st = 1; st <= nst; ++st) {
-            coarse_samples_phase<N, RC, TC, NamedGroup, NPC>(yb + (size_t)(ucount % 3) * Kc3, part, M, tab, X, Y, TW,
+            coarse_samples_phase<N, RC, TC, NamedGroup, NPC, LY::SPLIT>(yb + (size_t)(ucount % 3) * Kc3, part, M, tab, X, Y, TW,
                                                              C, A, PH, SW, GA, GP, GQ, nullptr, c, P, cg);
             const bool raise = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
             if (group_barrier(bar, P, epoch, raise, a.wd, &s_flag, cg)) {
