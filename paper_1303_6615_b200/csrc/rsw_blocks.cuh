@@ -418,7 +418,7 @@ __device__ __forceinline__ double2 yin_sentinel() {
 
 // Samples phase of one RK stage (Alg.1): poll the stage input y into C, then evaluate this
 // CTA's sample pairs (m_A, m_B) = (2p+1, 2p+2), p = rank, rank + P, ..., SPLIT pairs at a time on
-// SPLIT thread halves (each with its own X/Y at X + h*6N and named barrier 12 + h), writing one
+// SPLIT thread parts (each with its own X/Y at X + h*6N and named barrier 8 + h), writing one
 // partial Σ_{m in pair} w_m P+_m N(P-_m y) per pair to part[p] (per-pair partials: the owners'
 // reduction order is then independent of the CTA count, so every schedule agrees bitwise).
 template <int N, int R, int T, class GRP = CtaGroup, int NPC = 1, int SPLIT = 1>
@@ -428,7 +428,8 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
                                                      const double* SW, const double* GA, const double* GP,
                                                      const double* GQ, unsigned long long* cyc = nullptr,
                                                      int rank = -1, int P = -1, const GRP& grp = GRP()) {
-  static_assert(SPLIT == 1 || SPLIT == 2, "SPLIT");
+  static_assert(T % SPLIT == 0 && (T / SPLIT) % 32 == 0, "parts must be whole warps (bar.sync counts)");
+  static_assert(3 * (N / R) <= T / SPLIT, "each part must cover 3N/R FFT threads");
   constexpr int TH = T / SPLIT;
   const int tid_ = grp.tid();
   if (rank < 0) {
@@ -450,7 +451,7 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
   }
   grp.sync();
   const int h = SPLIT > 1 ? tid_ / TH : 0, th = tid_ - h * TH;
-  const NamedGroup hg{grp.base() + h * TH, 12 + h, TH};
+  const NamedGroup hg{grp.base() + h * TH, 8 + h, TH};  // named barriers 8..11
   double2* Xh = X + (size_t)h * 6 * N;
   double2* Yh = Xh + 3 * N;
   const int npairs = M / 2;  // samples 1..M-1 -> pairs (1,2), (3,4), ...; last B may be M (w=0)

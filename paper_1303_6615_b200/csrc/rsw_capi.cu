@@ -608,15 +608,14 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   // roles: coarse groups of GC CTAs (one sample pair each when GC = M/2), fine workers on the rest
   size_t cap = 0;
   // every CTA hosts a coarse sub-CTA and a fine group: NG groups of GC sub-CTAs run NG sweeps at once.
-  // Prefer running every sweep concurrently (NG = K+1) as long as a sub-CTA evaluates at most 4 sample
-  // pairs (two rounds of two concurrent halves): C3 measured 43.9 ms at GC = 24 / NG = 6, 45.0 at
-  // 32 / 4, 58.3 at 64 / 2.
+  // Prefer running every sweep concurrently (NG = K+1) as long as a sub-CTA evaluates at most 3 sample
+  // pairs (one round on its three 64-thread parts).
   {
     int smc = 148;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&smc, cudaDevAttrMultiProcessorCount, dev);
     const int pairs = std::max(M / 2, 1);
-    a.GC = std::max((pairs + 3) / 4, std::min(pairs, smc / (K + 1)));
+    a.GC = std::max((pairs + 2) / 3, std::min(pairs, smc / (K + 1)));  // <= 3 pairs: one concurrent round
   }
   const char* eg = getenv("RSW_PIPE_GC");
   if (eg) a.GC = std::max(1, atoi(eg));
@@ -657,7 +656,8 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   a.part = (double2*)ws->ppart.p;
   a.trace = nullptr;
   static const bool trace = getenv("RSW_PIPE_TRACE") != nullptr;
-  const size_t ntr = 2 * (size_t)(K + 1) + (size_t)(K + 1) * S + 2 * (size_t)std::max(K, 1) * a.npairs;
+  const size_t ntr0 = 2 * (size_t)(K + 1) + (size_t)(K + 1) * S + 2 * (size_t)std::max(K, 1) * a.npairs;
+  const size_t ntr = ntr0 + 16 * 4 * 4;  // + stage-phase stamps (16 slices x 4 stages x 4)
   if (trace) {
     CUDA_TRY(ensure(ws->prof, sizeof(unsigned long long) * ntr));
     CUDA_TRY(cudaMemsetAsync(ws->prof.p, 0, sizeof(unsigned long long) * ntr, st));
@@ -703,6 +703,20 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
       fprintf(stderr, "[rsw pipe] fine k=%d: %d tasks, mean latency %.3f ms, first start %.3f, last end %.3f\n", k, cnt,
               cnt ? lat / cnt : 0.0, first, last);
     }
+    double ph[3] = {0, 0, 0}, cyc = 0;
+    int cs = 0;
+    const unsigned long long* sp = tr.data() + ntr0;
+    for (int i = 0; i + 1 < 64; ++i) {
+      if (!sp[i * 4] || !sp[(i + 1) * 4]) continue;
+      ph[0] += (sp[i * 4 + 1] - sp[i * 4]) * 1e-3;
+      ph[1] += (sp[i * 4 + 2] - sp[i * 4 + 1]) * 1e-3;
+      ph[2] += (sp[i * 4 + 3] - sp[i * 4 + 2]) * 1e-3;
+      cyc += (sp[(i + 1) * 4] - sp[i * 4]) * 1e-3;
+      ++cs;
+    }
+    if (cs)
+      fprintf(stderr, "[rsw pipe] sweep 0 stage (us): samples+poll %.2f  barrier %.2f  update %.2f  total %.2f\n",
+              ph[0] / cs, ph[1] / cs, ph[2] / cs, cyc / cs);
   }
   if (wd) return fail(RSW_ERR_CUDA, "pipelined parareal: a dependency wait timed out (watchdog)");
   const int kout = stopk <= K ? stopk : K;

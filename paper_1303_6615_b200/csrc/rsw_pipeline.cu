@@ -72,9 +72,25 @@ __device__ __forceinline__ bool group_barrier(unsigned* bar, unsigned P, unsigne
 // latency-critical sweep wins issue slots over the throughput-bound fine solves).  The tcgen05
 // allocation limits a cooperative launch to one CTA per SM, so the roles are warp-specialized inside
 // the CTA rather than spread over CTAs.
-template <int N, int RC, int TC, int NOWN, int NPC, int RF, int TG, int NPG>
+// smallest palindromic radix whose FFT core fits in `threads` threads
+template <int N>
+__host__ __device__ constexpr int radix_for_threads(int threads) {
+  return (3 * (N / 4) <= threads && fft_palindrome<N, 4>()) ? 4
+       : (3 * (N / 8) <= threads && fft_palindrome<N, 8>()) ? 8
+       : (3 * (N / 16) <= threads && fft_palindrome<N, 16>()) ? 16 : 32;
+}
+template <int N, int TC, int NPC, int RC0>
+__host__ __device__ constexpr int pipe_split() {  // sample pairs a coarse sub-CTA evaluates concurrently
+  // parts must be whole warps (named-barrier thread counts) and must run the bulk sweep's radix RC0
+  // (another radix rounds differently: the schedules would no longer agree bitwise)
+  return (NPC >= 3 && (TC / 3) % 32 == 0 && 3 * (N / RC0) <= TC / 3) ? 3
+       : (NPC >= 2 && (TC / 2) % 32 == 0 && 3 * (N / RC0) <= TC / 2) ? 2 : 1;
+}
+
+template <int N, int RC0, int TC, int NOWN, int NPC, int RF, int TG, int NPG>
 struct PipeLayout {
-  static constexpr int SPLIT = (NPC >= 2 && TC / 2 >= 3 * N / RC) ? 2 : 1;  // pairs evaluated concurrently
+  static constexpr int SPLIT = pipe_split<N, TC, NPC, RC0>();
+  static constexpr int RC = RC0;
   using CL = CoarseLayout<N, RC, TC, NOWN, NPC, SPLIT>;
   static constexpr int K = N / 3, KP = K + 1;
   static constexpr int C0 = 0, F0 = (int)((CL::bytes + 15) / 16);  // double2 offsets of the coarse / fine regions
@@ -90,7 +106,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
   using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG>;
   using CL = typename LY::CL;
   static_assert(NPG * LY::CPG <= 512, "fine groups must fit in TMEM");
-  static_assert(NPG <= 13, "named barrier ids");
+  static_assert(NPG <= 7, "named barrier ids (fine 1..7, split parts 8..11, staging 14, coarse 15)");
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NH = N / 2 + 1, Kc3 = 3 * Kc;
   constexpr size_t L = (size_t)3 * NH * 2;  // doubles per state
   extern __shared__ double2 smem[];
@@ -135,7 +151,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
       int* yidx = reinterpret_cast<int*>(sd + CL::YI);
       const AvgTab& tab = a.at;
       const int M = a.M;
-      fill_packed_twiddles<N, RC, TC>(TW, tab.tw, ct);
+      fill_packed_twiddles<N, LY::RC, TC>(TW, tab.tw, ct);
       for (int k = ct; k <= K; k += TC) {
         GA[k] = __ldg(tab.g.a + k);
         GP[k] = __ldg(tab.g.p + k);
@@ -189,15 +205,24 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         bool aborted = false;
         for (int n = 0; n < S && !aborted; ++n) {
           for (int st = 1; st <= nst; ++st) {
-            coarse_samples_phase<N, RC, TC, NamedGroup, NPC, LY::SPLIT>(yb + (size_t)(ucount % 3) * Kc3, part, M, tab, X, Y, TW,
+            // optional stage-phase stamps (trace, group 0 rank 0, slices 8..23 of sweep g): samples / barrier / update
+            unsigned long long* stp = (a.trace && g == 0 && c == 0 && ct == 0 && n >= 8 && n < 24 && k == g)
+                                          ? a.trace + 2 * (Kit + 1) + (size_t)(Kit + 1) * S + 2 * (size_t)(Kit > 0 ? Kit : 1) * a.npairs +
+                                                ((n - 8) * nst + st - 1) * 4
+                                          : nullptr;
+            if (stp) stp[0] = gtimer();
+            coarse_samples_phase<N, LY::RC, TC, NamedGroup, NPC, LY::SPLIT>(yb + (size_t)(ucount % 3) * Kc3, part, M, tab, X, Y, TW,
                                                              C, A, PH, SW, GA, GP, GQ, nullptr, c, P, cg);
+            if (stp) stp[1] = gtimer();
             const bool raise = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
             if (group_barrier(bar, P, epoch, raise, a.wd, &s_flag, cg)) {
               aborted = true;
               break;
             }
+            if (stp) stp[2] = gtimer();
             ++ucount;
             coarse_update_phase<N, TC, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, c, P, cg);
+            if (stp) stp[3] = gtimer();
           }
           if (!aborted) {
             cg.sync();  // this CTA's part of U^k_{n+1}, G^k_n is written
@@ -341,7 +366,8 @@ static cudaError_t launch_pipe_n(const PipeArgs& a, int fine_scheme, int grid, s
                                                        : launch_pipe_nf<N, NW, NP, 1>(a, grid, out, st);
   PIPE_CFG(2, 1)
   PIPE_CFG(2, 2)
-  PIPE_CFG(4, 4)
+  PIPE_CFG(4, 2)
+  PIPE_CFG(8, 4)
   PIPE_CFG(8, 8)
 #undef PIPE_CFG
   return cudaErrorInvalidConfiguration;

@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+RSW_PIPE_TRACE=1 timeout 120 python tools/pipe_check.py C3 2>&1 | grep "stage\|identical\|schedule=2\|grid" | tail -4
+for cfg in "16 9" "16 6" "32 4"; do set -- $cfg; echo "== GC=$1 NG=$2"; RSW_PIPE_TRACE=1 RSW_PIPE_GC=$1 RSW_PIPE_NG=$2 timeout 120 python tools/pipe_check.py C3 2>&1 | grep "stage (us)\|identical\|schedule=2" | tail -3; done
