@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 ORC_OK, ORC_ERR_CONFIG, ORC_NOT_CONVERGED, ORC_ERR_DIVERGED = 0, 1, 2, 3
-FINE_ETDRK4, FINE_STRANG = 0, 1
+FINE_ETDRK4, FINE_STRANG, FINE_IFRK4 = 0, 1, 2
 COARSE_RK4, COARSE_MIDPOINT, COARSE_STRANG = 0, 1, 2
 FLAG_LINEAR_ONLY = 1
 

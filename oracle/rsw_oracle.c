@@ -52,7 +52,7 @@ typedef struct {
 } orc_parareal_config;
 
 enum { ORC_OK = 0, ORC_ERR_CONFIG = 1, ORC_NOT_CONVERGED = 2, ORC_ERR_DIVERGED = 3 };
-enum { ORC_FINE_ETDRK4 = 0, ORC_FINE_STRANG = 1 };
+enum { ORC_FINE_ETDRK4 = 0, ORC_FINE_STRANG = 1, ORC_FINE_IFRK4 = 2 };
 enum { ORC_COARSE_RK4 = 0, ORC_COARSE_MIDPOINT = 1, ORC_COARSE_STRANG = 2 };
 enum { ORC_FLAG_LINEAR_ONLY = 1u };
 
@@ -514,6 +514,85 @@ static void strang_step(const etd_table *t, double h, int linear_only, cplx *u, 
   realify_k0(n, u);
 }
 
+/* Integrating-factor baseline ("the operator integrating factor method (cf.
+   Kassam-Trefethen)"; SPEC S:350 reading: factor e^{-tA}, classical RK4 on the
+   transformed system).  With v(t) = e^{-tA} u(t), v' = g(t, v) = e^{-tA} N(e^{tA} v); one step of
+   classical RK4 for v from v0 = u_n, then u_{n+1} = e^{hA} v1:
+     K1 = g(0, v0), K2 = g(h/2, v0 + h/2 K1), K3 = g(h/2, v0 + h/2 K2), K4 = g(h, v0 + h K3),
+     v1 = v0 + h/6 (K1 + 2K2 + 2K3 + K4).
+   Written literally (the transforms e^{±(h/2)A}, e^{±hA} are separate per-mode matrices from the
+   numeric eigendecomposition), not in the factored forward-only form the GPU uses. */
+typedef struct {
+  int n, K;
+  cplx (*Ep)[3][3], (*Em)[3][3], (*E2p)[3][3], (*E2m)[3][3]; /* e^{hA}, e^{-hA}, e^{hA/2}, e^{-hA/2} */
+} if_table;
+
+static void if_table_init(if_table *t, const orc_params *p, double h) {
+  t->n = p->n;
+  t->K = k_max(p->n);
+  size_t m = (size_t)(t->K + 1);
+  t->Ep = malloc(sizeof(*t->Ep) * m);
+  t->Em = malloc(sizeof(*t->Em) * m);
+  t->E2p = malloc(sizeof(*t->E2p) * m);
+  t->E2m = malloc(sizeof(*t->E2m) * m);
+  for (int k = 0; k <= t->K; ++k) {
+    mode_eig e;
+    mode_eigen((double)k, p->F, &e);
+    cplx nu[3], nu2[3], mnu[3], mnu2[3];
+    hA_eigs(p, &e, (double)k, h, nu);
+    hA_eigs(p, &e, (double)k, 0.5 * h, nu2);
+    for (int j = 0; j < 3; ++j) {
+      mnu[j] = -nu[j];
+      mnu2[j] = -nu2[j];
+    }
+    matfun(&e, nu, f_exp, NULL, t->Ep[k]);
+    matfun(&e, mnu, f_exp, NULL, t->Em[k]);
+    matfun(&e, nu2, f_exp, NULL, t->E2p[k]);
+    matfun(&e, mnu2, f_exp, NULL, t->E2m[k]);
+  }
+}
+static void if_table_free(if_table *t) {
+  free(t->Ep);
+  free(t->Em);
+  free(t->E2p);
+  free(t->E2m);
+}
+
+/* g(τ, v) = e^{-τA} N(e^{τA} v) for τ = 0 (P = M = NULL), h/2 or h */
+static void if_rhs(int n, int linear_only, const cplx (*P)[3][3], const cplx (*Mi)[3][3], const cplx *v,
+                   cplx *out, nl_work *w, cplx *tmp) {
+  const size_t L = state_len(n);
+  if (linear_only) {
+    memset(out, 0, sizeof(cplx) * L);
+    return;
+  }
+  if (!P) {
+    nonlinear(n, v, out, w);
+    return;
+  }
+  apply_modes(n, P, v, tmp);
+  nonlinear(n, tmp, out, w);
+  memcpy(tmp, out, sizeof(cplx) * L);
+  apply_modes(n, Mi, tmp, out);
+}
+
+static void ifrk4_step(const if_table *t, double h, int linear_only, cplx *u, nl_work *w, cplx *buf) {
+  const int n = t->n;
+  const size_t L = state_len(n);
+  cplx *K1 = buf, *K2 = buf + L, *K3 = buf + 2 * L, *K4 = buf + 3 * L, *vs = buf + 4 * L,
+       *tmp = buf + 5 * L;
+  if_rhs(n, linear_only, NULL, NULL, u, K1, w, tmp);
+  for (size_t i = 0; i < L; ++i) vs[i] = u[i] + 0.5 * h * K1[i];
+  if_rhs(n, linear_only, (const cplx(*)[3][3])t->E2p, (const cplx(*)[3][3])t->E2m, vs, K2, w, tmp);
+  for (size_t i = 0; i < L; ++i) vs[i] = u[i] + 0.5 * h * K2[i];
+  if_rhs(n, linear_only, (const cplx(*)[3][3])t->E2p, (const cplx(*)[3][3])t->E2m, vs, K3, w, tmp);
+  for (size_t i = 0; i < L; ++i) vs[i] = u[i] + h * K3[i];
+  if_rhs(n, linear_only, (const cplx(*)[3][3])t->Ep, (const cplx(*)[3][3])t->Em, vs, K4, w, tmp);
+  for (size_t i = 0; i < L; ++i) vs[i] = u[i] + (h / 6.0) * (K1[i] + 2.0 * K2[i] + 2.0 * K3[i] + K4[i]);
+  apply_modes(n, (const cplx(*)[3][3])t->Ep, vs, u);
+  realify_k0(n, u);
+}
+
 static void fine_one(const orc_params *p, int scheme, int linear_only, const etd_table *t,
                      double h, int m, const cplx *in, cplx *out) {
   const size_t L = state_len(p->n);
@@ -522,10 +601,14 @@ static void fine_one(const orc_params *p, int scheme, int linear_only, const etd
   cplx *buf = malloc(sizeof(cplx) * 9 * L);
   cplx *u = malloc(sizeof(cplx) * L);
   memcpy(u, in, sizeof(cplx) * L);
+  if_table it = {0};
+  if (scheme == ORC_FINE_IFRK4) if_table_init(&it, p, h);
   for (int s = 0; s < m; ++s) {
     if (scheme == ORC_FINE_STRANG) strang_step(t, h, linear_only, u, &w, buf);
+    else if (scheme == ORC_FINE_IFRK4) ifrk4_step(&it, h, linear_only, u, &w, buf);
     else etdrk4_step(t, linear_only, u, &w, buf);
   }
+  if (scheme == ORC_FINE_IFRK4) if_table_free(&it);
   memcpy(out, u, sizeof(cplx) * L);
   free(u);
   free(buf);
@@ -545,7 +628,7 @@ int oracle_fine_propagate(const orc_params *p, int32_t scheme, uint32_t flags, d
                           double dt, int32_t n_slices, const double *u_in, double *u_out) {
   if (!params_ok(p) || !(dT > 0) || !(dt > 0) || dt > dT || n_slices < 0 || !u_in || !u_out)
     return ORC_ERR_CONFIG;
-  if (scheme != ORC_FINE_ETDRK4 && scheme != ORC_FINE_STRANG) return ORC_ERR_CONFIG;
+  if (scheme != ORC_FINE_ETDRK4 && scheme != ORC_FINE_STRANG && scheme != ORC_FINE_IFRK4) return ORC_ERR_CONFIG;
   const int m = n_fine_steps(dT, dt);
   const double h = dT / (double)m;
   etd_table t;
