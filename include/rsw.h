@@ -52,7 +52,10 @@ typedef enum {
   RSW_ERR_NCCL = 5
 } rsw_status;
 
-enum { RSW_FINE_ETDRK4 = 0, RSW_FINE_STRANG = 1 };
+enum { RSW_FINE_ETDRK4 = 0, RSW_FINE_STRANG = 1, RSW_FINE_IFRK4 = 2 };
+/* RSW_FINE_IFRK4: integrating-factor baseline ("operator integrating factor method",
+   P:1215-1219): classical RK4 on v = e^{-tA} u (Lawson form, forward factors only),
+   u+ = E u + h/6 (E k1 + 2 E2 k2 + 2 E2 k3 + k4). */
 enum { RSW_COARSE_RK4 = 0, RSW_COARSE_MIDPOINT = 1, RSW_COARSE_STRANG = 2 };
 /* RSW_COARSE_STRANG: standard parareal — the coarse solver is one Strang step of
    size dT on the full equation (Alg.3 with m = 1); T0 and M are then ignored. */

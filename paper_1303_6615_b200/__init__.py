@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RSW_LIB") or os.path.join(_HERE, "librsw.so")
 
 RSW_OK, RSW_ERR_CONFIG, RSW_NOT_CONVERGED, RSW_ERR_DIVERGED, RSW_ERR_CUDA, RSW_ERR_NCCL = range(6)
-FINE_ETDRK4, FINE_STRANG = 0, 1
+FINE_ETDRK4, FINE_STRANG, FINE_IFRK4 = 0, 1, 2
 COARSE_RK4, COARSE_MIDPOINT, COARSE_STRANG = 0, 1, 2
 SCHEDULE_AUTO, SCHEDULE_BULK, SCHEDULE_PIPELINED = 0, 1, 2
 FLAG_LINEAR_ONLY = 1

@@ -228,7 +228,8 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
   tmem_wait_st();
   grp.sync();
 
-  const int nst = (SCHEME == 0) ? 4 : 2;
+  constexpr bool RK = (SCHEME == 0 || SCHEME == 2);  // four-stage schemes with S0 / S2 in TMEM
+  const int nst = RK ? 4 : 2;
   for (int step = 0; step < m_steps; ++step) {
     const bool last_step = (step == m_steps - 1);
     for (int st = 0; st < nst; ++st) {
@@ -244,8 +245,8 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
         const uint32_t ts = tb + o * 36;
         double2 s1[3], s0[3], s2[3];
         tmem_ld3(ts, s1);                                            // S1 (every stage)
-        if (SCHEME == 0 && st == 1) tmem_ld3(ts + 12, s0);           // S0 = E2 c
-        if (SCHEME == 0 && st == 2) tmem_ld3(ts + 24, s2);           // S2 = E2 a - Q Nu
+        if (RK && st == 1) tmem_ld3(ts + 12, s0);                    // S0 = E2 c
+        if (RK && st == 2) tmem_ld3(ts + 24, s2);                    // S2 = E2 a - Q Nu (IF: E c)
         const double as = kap < 0 ? -sGA[ak] : sGA[ak];
         const double p = sGP[ak], q = sGQ[ak];
         double2 nn[3];
@@ -284,6 +285,30 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
               s1[al] = cadd(s1[al], dmul(alpha, CP(5), C0(5), nn[al]));
               x[al] = s1[al];
             }
+          } else if (SCHEME == 2) {
+            // integrating-factor RK4 (Lawson form of RK4 on v = e^{-tA}u, forward factors only):
+            //   k1 = N(u); a = E2 (u + h/2 k1); k2 = N(a); b = E2 u + h/2 k2; k3 = N(b);
+            //   c = E u + h E2 k3; k4 = N(c); u+ = E u + h/6 (E k1 + 2 E2 k2 + 2 E2 k3 + k4)
+            // S0 = E2 u, S2 = E u, S1 accumulates u+
+            if (st == 0) {
+              const double2 c = s1[al];
+              const double2 e2c = dmul(alpha, CP(1), C0(1), c);
+              const double2 ec = dmul(alpha, CP(0), C0(0), c);
+              s0[al] = e2c;
+              s2[al] = ec;
+              s1[al] = caxpy(h / 6.0, dmul(alpha, CP(0), C0(0), nn[al]), ec);
+              x[al] = caxpy(0.5 * h, dmul(alpha, CP(1), C0(1), nn[al]), e2c);
+            } else if (st == 1) {
+              x[al] = caxpy(0.5 * h, nn[al], s0[al]);
+              s1[al] = caxpy(h / 3.0, dmul(alpha, CP(1), C0(1), nn[al]), s1[al]);
+            } else if (st == 2) {
+              const double2 e2k = dmul(alpha, CP(1), C0(1), nn[al]);
+              x[al] = caxpy(h, e2k, s2[al]);
+              s1[al] = caxpy(h / 3.0, e2k, s1[al]);
+            } else {
+              s1[al] = caxpy(h / 6.0, nn[al], s1[al]);
+              x[al] = s1[al];
+            }
           } else {
             if (st == 0) {
               x[al] = caxpy(0.5 * h, nn[al], s1[al]);  // m = v + (h/2) N(v)
@@ -297,8 +322,8 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
 #undef CP
 #undef C0
         }
-        if (SCHEME == 0 || st == 1) tmem_st3(ts, s1);
-        if (SCHEME == 0 && st == 0) {
+        if (RK || st == 1) tmem_st3(ts, s1);
+        if (RK && st == 0) {
           tmem_st3(ts + 12, s0);
           tmem_st3(ts + 24, s2);
         }

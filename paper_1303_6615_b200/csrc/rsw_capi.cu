@@ -497,7 +497,8 @@ rsw_status rsw_fine_propagate(const rsw_params* p, int32_t scheme, uint32_t flag
                               int32_t n_slices, const double* u_in, double* u_out, void* stream) {
   rsw_status s = check_params(p);
   if (s != RSW_OK) return s;
-  if (scheme != RSW_FINE_ETDRK4 && scheme != RSW_FINE_STRANG) return fail(RSW_ERR_CONFIG, "unknown fine scheme");
+  if (scheme != RSW_FINE_ETDRK4 && scheme != RSW_FINE_STRANG && scheme != RSW_FINE_IFRK4)
+    return fail(RSW_ERR_CONFIG, "unknown fine scheme");
   if (flags & ~(uint32_t)RSW_FLAG_LINEAR_ONLY) return fail(RSW_ERR_CONFIG, "unknown flags");
   if (!finite_pos(dT) || !finite_pos(dt) || dt > dT) return fail(RSW_ERR_CONFIG, "need 0 < dt <= dT");
   if (n_slices < 0) return fail(RSW_ERR_CONFIG, "n_slices < 0");
@@ -764,7 +765,7 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   const int S = cfg->n_slices;
   if (S < 1) return fail(RSW_ERR_CONFIG, "n_slices must be >= 1");
   if (cfg->max_iters < 0 || cfg->max_iters > S) return fail(RSW_ERR_CONFIG, "need 0 <= max_iters <= n_slices");
-  if (cfg->fine_scheme != RSW_FINE_ETDRK4 && cfg->fine_scheme != RSW_FINE_STRANG)
+  if (cfg->fine_scheme != RSW_FINE_ETDRK4 && cfg->fine_scheme != RSW_FINE_STRANG && cfg->fine_scheme != RSW_FINE_IFRK4)
     return fail(RSW_ERR_CONFIG, "unknown fine scheme");
   if (cfg->coarse_scheme != RSW_COARSE_RK4 && cfg->coarse_scheme != RSW_COARSE_MIDPOINT &&
       cfg->coarse_scheme != RSW_COARSE_STRANG)

@@ -21,14 +21,6 @@ static cudaError_t set_smem(KernelT k, size_t bytes) {
     default: return cudaErrorInvalidValue;     \
   }
 
-static int fine_radix_override() {
-  static int r = -1;
-  if (r < 0) {
-    const char* e = getenv("RSW_FINE_RADIX");
-    r = e ? atoi(e) : 0;
-  }
-  return r;
-}
 
 
 template <int N, int R, int T>
@@ -83,7 +75,9 @@ static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double
   if (scheme == 0 && !lin) LAUNCH_FINE(0, false)
   else if (scheme == 0 && lin) LAUNCH_FINE(0, true)
   else if (scheme == 1 && !lin) LAUNCH_FINE(1, false)
-  else LAUNCH_FINE(1, true)
+  else if (scheme == 1 && lin) LAUNCH_FINE(1, true)
+  else if (scheme == 2 && !lin) LAUNCH_FINE(2, false)
+  else LAUNCH_FINE(2, true)
 #undef LAUNCH_FINE
   return cudaGetLastError();
 }
@@ -91,15 +85,6 @@ static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double
 template <int N>
 static cudaError_t launch_fine_n(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
                                  const FineTab& tab, cudaStream_t st) {
-  const int r = fine_radix_override();
-  if constexpr (N == 256) {  // measured alternatives (RSW_FINE_RADIX, benchmarking only)
-    if (r == 4) return launch_fine_nr<N, 4>(scheme, lin, in, out, S, m, h, tab, st);
-    if (r == 16) return launch_fine_nr<N, 16>(scheme, lin, in, out, S, m, h, tab, st);
-  }
-  if constexpr (N == 1024) {
-    if (r == 4) return launch_fine_nr<N, 4>(scheme, lin, in, out, S, m, h, tab, st);
-    if (r == 32) return launch_fine_nr<N, 32>(scheme, lin, in, out, S, m, h, tab, st);
-  }
   return launch_fine_nr<N, fine_radix<N>()>(scheme, lin, in, out, S, m, h, tab, st);
 }
 

@@ -363,7 +363,8 @@ static cudaError_t launch_pipe_n(const PipeArgs& a, int fine_scheme, int grid, s
   const int npc = (a.M / 2 + a.GC - 1) / a.GC;  // sample pairs per coarse CTA
 #define PIPE_CFG(NW, NP)                                                                            \
   if (nown <= NW && npc <= NP) return fine_scheme == 0 ? launch_pipe_nf<N, NW, NP, 0>(a, grid, out, st) \
-                                                       : launch_pipe_nf<N, NW, NP, 1>(a, grid, out, st);
+                                    : fine_scheme == 1 ? launch_pipe_nf<N, NW, NP, 1>(a, grid, out, st) \
+                                                       : launch_pipe_nf<N, NW, NP, 2>(a, grid, out, st);
   PIPE_CFG(2, 1)
   PIPE_CFG(2, 2)
   PIPE_CFG(4, 2)

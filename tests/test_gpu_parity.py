@@ -32,7 +32,7 @@ def test_nonlinear(rsw_gpu, orc, n):
     assert np.all(got[:, :, 0, 1] == 0.0)
 
 
-@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("scheme", [0, 1, 2])
 def test_fine_c1(rsw_gpu, orc, scheme):
     w = inputs.C1
     u = np.stack([inputs.initial_state(w, seed=s) for s in range(5)])
@@ -42,7 +42,7 @@ def test_fine_c1(rsw_gpu, orc, scheme):
     assert err.max() < TOL, err
 
 
-@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("scheme", [0, 1, 2])
 @pytest.mark.parametrize("n,eps,mu,dt,steps", [(128, 1e-2, 1e-4, 5e-4, 40), (256, 1e-3, 1e-5, 1e-4, 25),
                                                (512, 1e-3, 1e-5, 1e-4, 6), (1024, 1e-4, 1e-6, 2e-5, 4)])
 def test_fine_sizes(rsw_gpu, orc, scheme, n, eps, mu, dt, steps):
@@ -54,12 +54,13 @@ def test_fine_sizes(rsw_gpu, orc, scheme, n, eps, mu, dt, steps):
     assert err.max() < TOL, err
 
 
-def test_fine_linear_only(rsw_gpu, orc):
+@pytest.mark.parametrize("scheme", [0, 1, 2])
+def test_fine_linear_only(rsw_gpu, orc, scheme):
     n = 128
     u = inputs.random_states(n, 4, seed=3)
-    got = to_np(rsw_gpu.fine_propagate(P(rsw_gpu, 1e-2, 1.0, 1e-4, n), dev(u), 0.1, 1e-3, 0,
+    got = to_np(rsw_gpu.fine_propagate(P(rsw_gpu, 1e-2, 1.0, 1e-4, n), dev(u), 0.1, 1e-3, scheme,
                                        flags=rsw_gpu.FLAG_LINEAR_ONLY))
-    ref = orc.fine_propagate(u, 1e-2, 1.0, 1e-4, n, 0.1, 1e-3, 0, flags=1)
+    ref = orc.fine_propagate(u, 1e-2, 1.0, 1e-4, n, 0.1, 1e-3, scheme, flags=1)
     assert rel_l2(got, ref, n).max() < 1e-12
 
 
@@ -278,7 +279,7 @@ def test_paper_experiment_prefix(rsw_gpu, orc, name, coarse):
 
 
 # ---- pipelined schedule (NEXT-3): same arithmetic as the bulk schedule, so results are bitwise equal
-@pytest.mark.parametrize("wname,fine_scheme,coarse_scheme", [("C1", 0, 0), ("C1", 1, 1), ("C2", 0, 0)])
+@pytest.mark.parametrize("wname,fine_scheme,coarse_scheme", [("C1", 0, 0), ("C1", 1, 1), ("C1", 2, 0), ("C2", 0, 0)])
 def test_pipelined_schedule_bitwise_equals_bulk(rsw_gpu, wname, fine_scheme, coarse_scheme):
     w = getattr(inputs, wname)
     p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
@@ -315,3 +316,16 @@ def test_pipelined_rejects_unsupported(rsw_gpu):
     with pytest.raises(rsw_gpu.RSWError):
         rsw_gpu.parareal_iterate(p, u0, dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=4, max_iters=1,
                                  schedule=rsw_gpu.SCHEDULE_PIPELINED)
+
+
+def test_parareal_c1_ifrk4_fine(rsw_gpu, orc):
+    """Asymptotic parareal with the integrating-factor fine solver (NEXT-4) vs the oracle."""
+    w = inputs.C1
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = inputs.initial_state(w)
+    g = rsw_gpu.parareal_iterate(p, dev(u0), dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices,
+                                 max_iters=3, fine_scheme=rsw_gpu.FINE_IFRK4)
+    r = orc.parareal(u0, w.eps, w.F, w.mu, w.n, dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices,
+                     max_iters=3, fine_scheme=2)
+    assert rel_l2(to_np(g["U"]), r["U"], w.n)[1:].max() < TOL
+    assert np.allclose(g["resid"], r["resid"], rtol=1e-8, atol=0)
