@@ -6,7 +6,13 @@ solver at the paper's two smaller ΔT, iterations k = 0..5, agains
 (ETDRK4) reference at the slice boundaries.  Error = max_n relative L∞ on the grid.
 The paper's figures are placeholders, so this reproduces the experiments, not its numbers.
 
+NEXT-4 (--serial): the paper's serial-accuracy comparison: each serial
+integrator of the full equation — ETDRK4, the integrating-factor method (IF-RK4) and Strang splitting
+— at Δt = ε/m over the whole interval, error (same metric) against an ETDRK4 solution at Δt = ε/100,
+and the largest Δt whose error is at most the asymptotic parareal's error after 5 iterations.
+
   python tools/paper_experiments.py [--out docs/paper_experiments.json]
+  python tools/paper_experiments.py --serial [--out docs/paper_serial_accuracy.json]
 """
 import argparse
 import json
@@ -29,11 +35,11 @@ def grid(U):
     return np.fft.irfft(c * N_GRID, N_GRID, axis=-1)  # [.., 3, n]
 
 
-def serial_reference(p, u0, dT, dt, S):
+def serial_reference(p, u0, dT, dt, S, scheme=0):
     ref = [u0]
     x = u0[None].contiguous()
     for _ in range(S):
-        x = rsw.fine_propagate(p, x, dT, dt)
+        x = rsw.fine_propagate(p, x, dT, dt, scheme)
         ref.append(x[0])
     return torch.stack(ref).cpu().numpy()
 
@@ -79,13 +85,53 @@ def run(name, cfg, kmax=5):
     return out
 
 
+SERIAL_SCHEMES = {"ETDRK4": 0, "IF-RK4": 2, "Strang": 1}
+
+
+def serial_accuracy(name, cfg, targets, divisors=(5, 10, 20, 25, 50)):
+    p = rsw.Params(cfg["eps"], F, MU, N_GRID)
+    u0 = torch.from_numpy(inputs.paper_initial_state(N_GRID)).cuda()
+    eps, dT, S = cfg["eps"], cfg["dT"], cfg["n_slices"]
+    t = time.time()
+    ref = serial_reference(p, u0, dT, eps / 100, S, 0)
+    out = {"eps": eps, "T": S * dT, "reference": "ETDRK4, dt = eps/100", "targets": targets, "schemes": {}}
+    for sname, sch in SERIAL_SCHEMES.items():
+        errs = {}
+        for m in divisors:
+            U = serial_reference(p, u0, dT, eps / m, S, sch)
+            e = max_rel_linf(U, ref)
+            errs[f"eps/{m}"] = e if np.isfinite(e) else None
+            print(name, sname, f"dt=eps/{m}", "%.2e" % e, flush=True)
+        best = {}
+        for tname, tval in targets.items():
+            ok = [m for m in divisors if errs[f"eps/{m}"] is not None and errs[f"eps/{m}"] <= tval]
+            best[tname] = f"eps/{min(ok)}" if ok else None
+        out["schemes"][sname] = {"max_rel_linf_error": errs, "largest_dt_reaching": best}
+    out["wall_s"] = time.time() - t
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                                   "docs", "paper_experiments.json"))
     ap.add_argument("--only", default="")
+    ap.add_argument("--serial", action="store_true")
     a = ap.parse_args()
     res = {}
+    if a.serial:
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        prev = json.load(open(os.path.join(root, "docs", "paper_experiments.json")))
+        out = a.out if a.out.endswith("serial_accuracy.json") else os.path.join(root, "docs", "paper_serial_accuracy.json")
+        for name, cfg in inputs.PAPER_EXPERIMENTS.items():
+            if a.only and name != a.only:
+                continue
+            targets = {lab: v["max_rel_linf_error_k0..k5"][5] for lab, v in prev[name].items()
+                       if isinstance(v, dict) and lab.startswith("asymptotic") and v["max_rel_linf_error_k0..k5"][5] == v["max_rel_linf_error_k0..k5"][5]}
+            res[name] = serial_accuracy(name, cfg, {f"{k} (k=5)": t for k, t in targets.items()})
+        with open(out, "w") as f:
+            json.dump(res, f, indent=1)
+        return
     for name, cfg in inputs.PAPER_EXPERIMENTS.items():
         if a.only and name != a.only:
             continue
