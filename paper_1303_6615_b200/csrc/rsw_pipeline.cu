@@ -27,8 +27,11 @@
 
 #include <cstdio>
 
-#ifndef RSW_PIPE_THREADS
-#define RSW_PIPE_THREADS 288  // coarse sub-CTA (192) + one fine group: measured best on C3 (two groups slow the sweeps)
+#ifndef RSW_PIPE_COARSE_THREADS
+#define RSW_PIPE_COARSE_THREADS 288  // coarse sub-CTA: three 96-thread parts evaluate three sample pairs at once
+#endif
+#ifndef RSW_PIPE_FINE_GROUPS
+#define RSW_PIPE_FINE_GROUPS 1  // fine worker groups per CTA (two slowed the sweeps on C3)
 #endif
 
 namespace rsw {
@@ -93,13 +96,67 @@ struct PipeLayout {
   static constexpr int RC = RC0;
   using CL = CoarseLayout<N, RC, TC, NOWN, NPC, SPLIT>;
   static constexpr int K = N / 3, KP = K + 1;
-  static constexpr int C0 = 0, F0 = (int)((CL::bytes + 15) / 16);  // double2 offsets of the coarse / fine regions
+  // coarse region: the coarse sub-CTA's layout, or (CTAs without a coarse role) TC/TG extra fine groups' X/Y
+  static constexpr int XG = TC / TG;
+  static constexpr size_t CREG = CL::bytes > sizeof(double2) * XG * 6 * N ? CL::bytes : sizeof(double2) * XG * 6 * N;
+  static constexpr int C0 = 0, F0 = (int)((CREG + 15) / 16);  // double2 offsets of the coarse / fine regions
   static constexpr int F_TW = F0, F_CP = F_TW + fft_tw_size<N, RF>(), F_D = F_CP + 6 * KP, F_ND = 9 * KP,
                        F_G = F_D + (F_ND + 1) / 2;  // first fine group's X
   static constexpr size_t bytes = sizeof(double2) * (F_G + NPG * 6 * N);
   static constexpr int CPG = (FineTmem<N, TG>::COLS + 31) / 32 * 32;  // TMEM columns per fine group
   static constexpr int T = TC + NPG * TG;
 };
+
+// fine worker group: claim the lowest-iteration ready pair task (k, p) — slices 2p, 2p+1 of U^k, ready
+// when prog[k] covers them — run the fine pair integrator, write F^k, set doneF[k][p] (release)
+template <int N, int RF, int TG, int FSCHEME>
+__device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedGroup grp, double2* W,
+                                                 const FineSmemTab& ft, uint32_t tcol, int* task) {
+  constexpr size_t L = (size_t)3 * (N / 2 + 1) * 2;
+  const int S = a.S, Kit = a.K, npairs = a.npairs;
+  double2* Yb = W + 3 * N;
+  for (;;) {
+    if (grp.tid() == 0) {
+      int tk = -1, tp = -1;
+      const unsigned long long t0 = gtimer();
+      for (unsigned it = 0;; ++it) {
+        const int lim = min(Kit, *(volatile int*)a.stopk) - 1;  // F^k is needed by sweep k+1 <= stop
+        bool all_claimed = true;
+        for (int k = 0; k <= lim && tk < 0; ++k) {
+          const unsigned t = *(volatile unsigned*)(a.next + k);
+          if ((int)t >= npairs) continue;
+          all_claimed = false;
+          const int need = (2 * (int)t + 1 < S) ? 2 * (int)t + 1 : 2 * (int)t;  // U^k_{2t}, U^k_{2t+1}
+          if (ld_acquire_gpu(a.prog + k) >= (unsigned)(a.GC * need) && atomicCAS(a.next + k, t, t + 1) == t) {
+            tk = k;
+            tp = (int)t;
+          }
+        }
+        if (tk >= 0 || all_claimed) break;
+        if ((it & 63) == 63 && watchdog_expired(t0, a.wd)) break;
+        __nanosleep(128);
+      }
+      task[0] = tk;
+      task[1] = tp;
+    }
+    grp.sync();
+    const int tk = task[0], tp = task[1];
+    if (tk < 0) break;
+    const int nA = 2 * tp, nB = nA + 1;
+    unsigned long long* tf =
+        a.trace ? a.trace + 2 * (Kit + 1) + (size_t)(Kit + 1) * S + ((size_t)tk * npairs + tp) * 2 : nullptr;
+    if (tf && grp.tid() == 0) tf[0] = gtimer();
+    const double* Uk = a.Uall + (size_t)tk * (S + 1) * L;
+    double* Fk = a.Fall + (size_t)tk * S * L;
+    fine_pair_run<N, RF, TG, FSCHEME, false>(grp, W, Yb, ft, tcol, a.ft.g, Uk + nA * L, nB < S ? Uk + nB * L : nullptr,
+                                             Fk + nA * L, nB < S ? Fk + nB * L : nullptr, a.m_fine, a.h);
+    grp.sync();  // the whole pair's F is written
+    if (grp.tid() == 0) {
+      st_release_u32(a.doneF + (size_t)tk * npairs + tp, 1u);
+      if (tf) tf[1] = gtimer();
+    }
+  }
+}
 
 template <int N, int RC, int TC, int NOWN, int NPC, int RF, int TG, int NPG, int FSCHEME>
 __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeArgs a) {
@@ -112,7 +169,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
   extern __shared__ double2 smem[];
   __shared__ uint32_t tslot;
   __shared__ unsigned s_ticket, s_flag;
-  __shared__ int s_task[NPG][2];
+  __shared__ int s_task[NPG + TC / TG][2];
   const int warp = threadIdx.x >> 5;
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1u);
@@ -121,13 +178,25 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
   tmem_fence_after();
   const int ticket = (int)s_ticket;
   const int S = a.S, Kit = a.K;
+  // fine tables (shared by every fine group of the CTA), staged by all threads
+  const FineSmemTab ft = stage_fine_tables<N, RF, TC + NPG * TG>(
+      smem + LY::F_TW, smem + LY::F_CP, reinterpret_cast<double*>(smem + LY::F_D), a.ft, threadIdx.x, TC + NPG * TG);
+  __syncthreads();
 
   constexpr int FT = NPG * TG;  // fine groups take the low warps, the coarse sub-CTA the high ones
   if ((int)threadIdx.x >= FT) {
     // ===================================== coarse sub-CTA =====================================
     const NamedGroup cg{FT, 15, TC};
     const int ct = (int)threadIdx.x - FT;
-    if (ticket < a.NG * a.GC) {
+    if (ticket >= a.NG * a.GC) {
+      // no coarse role: the coarse threads run XG more fine groups (in the coarse region of smem)
+      constexpr int XG = TC / TG;
+      const int xi = ct / TG;
+      if (xi < XG && (NPG + XG) * LY::CPG <= 512)
+        fine_worker_loop<N, RF, TG, FSCHEME>(a, NamedGroup{FT + xi * TG, 1 + NPG + xi, TG},
+                                            smem + LY::C0 + (size_t)xi * 6 * N, ft,
+                                            tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi]);
+    } else {
       const int g = ticket / a.GC, c = ticket % a.GC, P = a.GC;
       double2* cs = smem + LY::C0;
       double2* X = cs + CL::X;
@@ -263,60 +332,10 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
       }
     }
   } else {
-    // ======================================= fine worker groups =======================================
-    const int ft0 = threadIdx.x;  // 0 .. NPG*TG-1
-    double* sdd = reinterpret_cast<double*>(smem + LY::F_D);
-    const FineSmemTab ft =
-        stage_fine_tables<N, RF, TC>(smem + LY::F_TW, smem + LY::F_CP, sdd, a.ft, ft0, NPG * TG);
-    asm volatile("bar.sync 14, %0;" ::"r"(NPG * TG) : "memory");
-    const int gi = ft0 / TG;
-    const NamedGroup grp{gi * TG, 1 + gi, TG};
-    double2* W = smem + LY::F_G + (size_t)gi * 6 * N;
-    double2* Yb = W + 3 * N;
-    const uint32_t tcol = tslot + (uint32_t)(gi * LY::CPG);
-    const int npairs = a.npairs;
-    for (;;) {
-      if (grp.tid() == 0) {
-        int tk = -1, tp = -1;
-        const unsigned long long t0 = gtimer();
-        for (unsigned it = 0;; ++it) {
-          const int lim = min(Kit, *(volatile int*)a.stopk) - 1;  // F^k is needed by sweep k+1 <= stop
-          bool all_claimed = true;
-          for (int k = 0; k <= lim && tk < 0; ++k) {
-            const unsigned t = *(volatile unsigned*)(a.next + k);
-            if ((int)t >= npairs) continue;
-            all_claimed = false;
-            const int need = (2 * (int)t + 1 < S) ? 2 * (int)t + 1 : 2 * (int)t;  // U^k_{2t}, U^k_{2t+1}
-            if (ld_acquire_gpu(a.prog + k) >= (unsigned)(a.GC * need) && atomicCAS(a.next + k, t, t + 1) == t) {
-              tk = k;
-              tp = (int)t;
-            }
-          }
-          if (tk >= 0 || all_claimed) break;
-          if ((it & 63) == 63 && watchdog_expired(t0, a.wd)) break;
-          __nanosleep(128);
-        }
-        s_task[gi][0] = tk;
-        s_task[gi][1] = tp;
-      }
-      grp.sync();
-      const int tk = s_task[gi][0], tp = s_task[gi][1];
-      if (tk < 0) break;
-      const int nA = 2 * tp, nB = nA + 1;
-      unsigned long long* tf =
-          a.trace ? a.trace + 2 * (Kit + 1) + (size_t)(Kit + 1) * S + ((size_t)tk * npairs + tp) * 2 : nullptr;
-      if (tf && grp.tid() == 0) tf[0] = gtimer();
-      const double* Uk = a.Uall + (size_t)tk * (S + 1) * L;
-      double* Fk = a.Fall + (size_t)tk * S * L;
-      fine_pair_run<N, RF, TG, FSCHEME, false>(grp, W, Yb, ft, tcol, a.ft.g, Uk + nA * L,
-                                               nB < S ? Uk + nB * L : nullptr, Fk + nA * L,
-                                               nB < S ? Fk + nB * L : nullptr, a.m_fine, a.h);
-      grp.sync();  // the whole pair's F is written
-      if (grp.tid() == 0) {
-        st_release_u32(a.doneF + (size_t)tk * npairs + tp, 1u);
-        if (tf) tf[1] = gtimer();
-      }
-    }
+    // ======================================= fine worker group 0 =======================================
+    const int gi = threadIdx.x / TG;
+    fine_worker_loop<N, RF, TG, FSCHEME>(a, NamedGroup{gi * TG, 1 + gi, TG}, smem + LY::F_G + (size_t)gi * 6 * N,
+                                        ft, tslot + (uint32_t)(gi * LY::CPG), s_task[gi]);
   }
   tmem_fence_before();
   __syncthreads();
@@ -331,11 +350,11 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
 // ---------------------------------------------------------------------------------------------
 template <int N, int NOWN, int NPC, int FSCHEME>
 static cudaError_t launch_pipe_nf(const PipeArgs& a, int grid, size_t* out, cudaStream_t st) {
-  constexpr int RC = coarse_radix<N>(), TC = coarse_threads<N>();
+  constexpr int RC = coarse_radix<N>();
+  constexpr int TC = RSW_PIPE_COARSE_THREADS > coarse_threads<N>() ? RSW_PIPE_COARSE_THREADS : coarse_threads<N>();
   constexpr int RF = fine_radix<N>(), TG = core_threads<N, RF>();
   constexpr int CPG = (FineTmem<N, TG>::COLS + 31) / 32 * 32;
-  constexpr int NPG0 = (RSW_PIPE_THREADS - TC) / TG > 0 ? (RSW_PIPE_THREADS - TC) / TG : 1;
-  constexpr int NPG = NPG0 * CPG <= 512 ? NPG0 : 512 / CPG;
+  constexpr int NPG = RSW_PIPE_FINE_GROUPS * CPG <= 512 ? RSW_PIPE_FINE_GROUPS : 512 / CPG;
   using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG>;
   auto kfn = k_parareal_pipe<N, RC, TC, NOWN, NPC, RF, TG, NPG, FSCHEME>;
   const size_t sm = LY::bytes;
