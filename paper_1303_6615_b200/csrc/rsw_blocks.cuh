@@ -1,4 +1,4 @@
-// rsw_blocks.cuh — device building blocks shared by the standalone kernels (rsw_kernels.cu) and the
+// rsw_blocks.cuh — device building blocks shared by the standalone kernels (rsw_k_*.cu) and the
 // pipelined parareal megakernel (rsw_pipeline.cu): radix / thread choices, pair load / store,
 // the fine pair integrator (a2 / a2'), and the coarse-sweep phases (a3 / a4 / a5).
 #pragma once
@@ -9,30 +9,17 @@
 
 namespace rsw {
 
-// FFT radix and CTA size, T = 3N/R (one radix-R butterfly of each field per thread), chosen from
-// measurements on B200: large transforms (n >= 512) are shared-memory-traffic bound,
-// so radix 16 (fewest passes) wins for the throughput kernels (C5 fine 5.6 -> 6.3 TFLOP/s, C4 N̄
-// 6.5 -> 7.8); at n <= 256 the kernels are latency bound and radix 4 with more threads wins (C3 fine
-// 5.4 TFLOP/s vs 4.0 at radix 16; C3 coarse stage 7.5 us vs 14.1).
-template <int N>
-#ifndef RSW_RADIX_FINE
-#define RSW_RADIX_FINE 0
-#endif
-#ifndef RSW_RADIX_COARSE
-#define RSW_RADIX_COARSE 0
-#endif
-__host__ __device__ constexpr int radix_for() { return RSW_RADIX_FINE ? RSW_RADIX_FINE : (N >= 512 ? 16 : 4); }
-template <int N>
-__host__ __device__ constexpr int threads_for() { return (3 * N / radix_for<N>()) > 96 ? (3 * N / radix_for<N>()) : 96; }
-// register FFT core (nl_core): R values per thread, T = 3N/R threads (>= 32)
+// Radix / thread choices of the register FFT core (nl_core), measured on B200:
+// R values per thread, T = 3N/R threads rounded up to whole warps.  Fine and batched-N̄ kernels:
+// radix 8 up to n = 256 (C3 fine 8.5 TFLOP/s vs 7.1 at radix 4 / 16), radix 16 above (C5 10.4 vs 7.6 /
+// 6.1 at radix 4 / 32).  Coarse sweep (latency bound, one sample pair per CTA): radix 8 with 192
+// threads (the extra threads speed up the mode loops; C3 stage 6.7 us vs 8.3 at 96 threads).
 template <int N>
 __host__ __device__ constexpr int fine_radix() { return N <= 32 ? 4 : N <= 256 ? 8 : 16; }  // palindromic
 template <int N, int R>
 __host__ __device__ constexpr int core_threads() { return (3 * (N / R) + 31) / 32 * 32; }
 template <int N>
-__host__ __device__ constexpr int coarse_radix() {  // palindromic; latency-bound (one pair per SM)
-  return RSW_RADIX_COARSE ? RSW_RADIX_COARSE : (N <= 32 ? 4 : N <= 256 ? 8 : 16);
-}
+__host__ __device__ constexpr int coarse_radix() { return N <= 32 ? 4 : N <= 256 ? 8 : 16; }  // palindromic
 template <int N>
 __host__ __device__ constexpr int coarse_threads() { return core_threads<N, coarse_radix<N>()>() > 192 ? core_threads<N, coarse_radix<N>()>() : 192; }
 
@@ -112,20 +99,6 @@ __device__ __forceinline__ void store_pair_prim(const double2* C, const ModeGeom
 }
 
 // write prim(x) of every retained entry as the next N-eval input and zero the tail
-template <int N, int T>
-__device__ __forceinline__ void prologue_from(double2* W, const double2* X, const ModeGeom g) {
-  constexpr int K = N / 3, Kc = 2 * K + 1;
-  for (int j = threadIdx.x; j < Kc; j += T) {
-    const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
-    const double as = kap < 0 ? -__ldg(g.a + ak) : __ldg(g.a + ak);
-    double2 c[3], u[3];
-#pragma unroll
-    for (int al = 0; al < 3; ++al) c[al] = X[al * Kc + j];
-    to_prim(as, __ldg(g.p + ak), __ldg(g.q + ak), c, u);
-    put_input<N>(W, full_index(kap, N), (double)kap, u);
-  }
-  zero_tail<N, T>(W);
-}
 
 // ---------------------------------------------------------------------------------------------
 // K1/K2: fine propagator.  One CTA = one pair of slices, state resident in shared memory for all

@@ -162,75 +162,6 @@ __device__ __forceinline__ void dftR(double2* v) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Padded work-buffer layout: element i of a field lives at i + i/8, field stride NP = N + N/8.
-// Every access pattern of the path (Stockham loads, the stride-R stores of the first pass,
-// grid-point and mode loops) is then free of shared-memory bank conflicts for 16-byte elements.
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
-template <int N>
-struct WL {
-  static constexpr int NP = N + N / 8;
-};
-
-// ---------------------------------------------------------------------------------------------
-// Stockham autosort FFT over the 3 fields of W (in place: load all, barrier, compute, store).
-// Pass with radix R after NS = product of previous radices (natural order in and out):
-//   for j in [0, N/R): k = j mod NS; v_r = W[j + r N/R] * w^{r k N/(NS R)}; DFT_R;
-//                      W[(j/NS) NS R + k + r NS] = v_r.
-// tw[m] = e^{-2πi m/N} (forward, SIGN=-1); the inverse (SIGN=+1) uses conj(tw).
-// ---------------------------------------------------------------------------------------------
-template <int N, int T, int R, int NS, int SIGN>
-__device__ __forceinline__ void stockham_pass(double2* W, const double2* __restrict__ tw) {
-  constexpr int NB = 3 * (N / R);  // butterflies over the 3 fields
-  constexpr int BPT = (NB + T - 1) / T;
-  double2 v[BPT][R];
-#pragma unroll
-  for (int i = 0; i < BPT; ++i) {
-    const int b = threadIdx.x + i * T;
-    if (NB % T == 0 || b < NB) {
-      const int f = b / (N / R), j = b % (N / R);
-      const double2* in = W + f * WL<N>::NP;
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[i][r] = in[pad(j + r * (N / R))];
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < BPT; ++i) {
-    const int b = threadIdx.x + i * T;
-    if (NB % T == 0 || b < NB) {
-      const int f = b / (N / R), j = b % (N / R);
-      const int k = j % NS;
-      if constexpr (NS > 1) {
-#pragma unroll
-        for (int r = 1; r < R; ++r) {
-          const double2 w = __ldg(tw + r * k * (N / (NS * R)));
-          v[i][r] = SIGN < 0 ? cmul(v[i][r], w) : cmulc(v[i][r], w);
-        }
-      }
-      dftR<R, SIGN>(v[i]);
-      double2* out = W + f * WL<N>::NP;
-      const int base = (j / NS) * NS * R + k;
-#pragma unroll
-      for (int r = 0; r < R; ++r) out[pad(base + r * NS)] = v[i][r];
-    }
-  }
-  __syncthreads();
-}
-
-// RMAX: largest radix (8: fewer shared-memory passes, best for throughput; 4: twice the threads,
-// best for latency-bound launches such as the serial coarse sweep)
-template <int N, int T, int SIGN, int RMAX, int NS = 1>
-__device__ __forceinline__ void fft3(double2* W, const double2* __restrict__ tw) {
-  if constexpr (NS < N) {
-    constexpr int rem = N / NS;
-    constexpr int R = (rem % RMAX == 0) ? RMAX : rem;
-    stockham_pass<N, T, R, NS, SIGN>(W, tw);
-    fft3<N, T, SIGN, RMAX, NS * R>(W, tw);
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
 // Closed-form eigenbasis of L̂(κ) = [[0,-1,ia],[1,0,0],[ia,0,0]], a = κ/√F:
 //   r^- = (-iω, 1, ia)/(√2ω),  r^0 = (0, ia, 1)/ω,  r^+ = (iω, 1, ia)/(√2ω),  ω = √(1+a²),
 //   L̂ r^α = iαω r^α.  Per |κ| the host stores a, p = 1/(√2ω), q = 1/ω.
@@ -263,46 +194,6 @@ __device__ __forceinline__ void to_prim(double as, double p, double q, const dou
   u[2] = cadd(qc0, cmuli(cscale(pe, as)));
 }
 
-// ---------------------------------------------------------------------------------------------
-// N(u) on the packed work buffer W (3 fields, full spectrum in, full spectrum out, unscaled):
-//   in:  W[0] = v̂1, W[1] = iκ v̂2, W[2] = ĥ  (prepared by the caller's prologue)
-//   out: W[f] = N * DFT(q_f),  q = (v1²/2, v1 v2x, h v1)   (products per real/imag lane)
-// The caller's epilogue applies 1/N, the derivative factors (-iκ, -1, -iκ) and the 2/3 mask:
-//   N(u) = -(∂x(v1²/2), v1 ∂x v2, ∂x(h v1))   (P:1090-1094 with R1; v1 v1x = ∂x(v1²/2))
-// ---------------------------------------------------------------------------------------------
-template <int N, int T, int RMAX>
-__device__ __forceinline__ void nl_physical(double2* W, const double2* __restrict__ tw) {
-  fft3<N, T, +1, RMAX>(W, tw);  // synthesis: u(x_n) = Σ_κ Z_κ e^{iκ x_n}
-  constexpr int NP = WL<N>::NP;
-  for (int n = threadIdx.x; n < N; n += T) {
-    const int i = pad(n);
-    const double2 v1 = W[i], v2x = W[NP + i], h = W[2 * NP + i];
-    W[i] = make_double2(0.5 * v1.x * v1.x, 0.5 * v1.y * v1.y);
-    W[NP + i] = make_double2(v1.x * v2x.x, v1.y * v2x.y);
-    W[2 * NP + i] = make_double2(h.x * v1.x, h.y * v1.y);
-  }
-  __syncthreads();
-  fft3<N, T, -1, RMAX>(W, tw);  // analysis (unnormalised)
-}
-
-// ---------------------------------------------------------------------------------------------
-// Register-resident FFT core of the N-eval (replaces the smem round trip per pass of fft3):
-//   thread t < 3N/R owns field f = t / (N/R) and column j = t % (N/R) and keeps R values in
-//   registers through every pass; a pass of radix r <= R does R/r butterflies per thread.
-//   Stockham autosort: in every pass thread j reads the index set {j + i N/R + s N/r} and
-//   butterfly jb = j + i N/R writes (jb/NS) NS r + jb%NS + s NS.  Passes are separated by ONE
-//   barrier (ping-pong between X and Y).  The radix sequence is a palindrome (the small radix in
-//   the middle), so synthesis pass q and analysis pass q have the same (r, NS): they share one
-//   twiddle table, packed per pass as [k][s-1] (consecutive k -> odd stride r-1 -> no bank
-//   conflicts), and the last synthesis pass and the first analysis pass have the same radix and
-//   index set, so the products are formed in registers; only v1 is shared with the v2x / h
-//   threads through one barrier-separated copy.
-//   Buffers: double2[3][N], element i of a field at swz(i) (XOR swizzle inside groups of 8:
-//   every exchange pattern of the core is free of bank conflicts, tools/model_conflicts.py).
-//   in : X = (v̂1, iκ v̂2, ĥ) at the retained full indices (others are never read: pruned zeros)
-//   out: X = N * DFT(q_f) at the retained full indices, q = (v1²/2, v1 v2x, h v1) per lane.
-// Barriers: 2 * passes (the last one makes the output visible to the caller's mode loop).
-// ---------------------------------------------------------------------------------------------
 // thread-group policies: the whole CTA, or a warp-aligned group of a CTA with its own named barrier
 struct CtaGroup {
   __device__ __forceinline__ int base() const { return 0; }
@@ -585,37 +476,6 @@ __device__ __forceinline__ void tmem_st3(uint32_t taddr, const double2 (&x)[3]) 
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr + 8), "r"(r[8]),
                "r"(r[9]), "r"(r[10]), "r"(r[11])
                : "memory");
-}
-
-// prologue helper: write prim(x) of entry j into W as the N-eval input (v1, iκ v2, h)
-template <int N>
-__device__ __forceinline__ void put_input(double2* W, int k_full, double kap, const double2* u) {
-  constexpr int NP = WL<N>::NP;
-  const int i = pad(k_full);
-  W[i] = u[0];
-  W[NP + i] = cmuli(cscale(u[1], kap));
-  W[2 * NP + i] = u[2];
-}
-
-// epilogue helper: read the N-eval output of entry k_full, return N̂ (primitive)
-template <int N>
-__device__ __forceinline__ void get_output(const double2* W, int k_full, double kap, double invN, double2* nh) {
-  constexpr int NP = WL<N>::NP;
-  const int i = pad(k_full);
-  const double2 Q0 = cscale(W[i], invN), Q1 = cscale(W[NP + i], invN), Q2 = cscale(W[2 * NP + i], invN);
-  nh[0] = cmulmi(cscale(Q0, kap));  // -iκ Q0
-  nh[1] = make_double2(-Q1.x, -Q1.y);
-  nh[2] = cmulmi(cscale(Q2, kap));  // -iκ Q2
-}
-
-// zero the non-retained full-spectrum entries K < k < N-K of the 3 fields
-template <int N, int T>
-__device__ __forceinline__ void zero_tail(double2* W) {
-  constexpr int K = N / 3, NZ = N - (2 * K + 1);
-  for (int i = threadIdx.x; i < 3 * NZ; i += T) {
-    const int f = i / NZ, k = K + 1 + i % NZ;
-    W[f * WL<N>::NP + pad(k)] = make_double2(0.0, 0.0);
-  }
 }
 
 __device__ __forceinline__ int full_index(int kap, int N) { return kap >= 0 ? kap : kap + N; }

@@ -130,14 +130,17 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
 // (2 N-evals, the state in the real lane of the packed pair), the parareal update
 // U_{n+1} = G + (F_n - G_n), G_n <- G, and the per-slice residual; r_k = max_n at the end.
 // ---------------------------------------------------------------------------------------------
-template <int N, int T>
+template <int N, int R, int T>
 __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h, double* U, double* G,
                                                      const double* F, double* Gnew, int S, double* r_out) {
   constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
   constexpr double invN = 1.0 / N;
   extern __shared__ double2 smem[];
-  double2* W = smem;
-  double2* S1 = W + 3 * WL<N>::NP;
+  double2* W = smem;              // nl_core X (swizzled)
+  double2* Yb = W + 3 * N;        // nl_core Y
+  double2* TW = Yb + 3 * N;       // packed twiddles
+  double2* S1 = TW + fft_tw_size<N, R>();
+  fill_packed_twiddles<N, R, T>(TW, tab.tw);
   __shared__ double red[2][T];
   __shared__ double rmax;
   if (threadIdx.x == 0) rmax = 0.0;
@@ -153,17 +156,24 @@ __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h,
                                S1[al * Kc + j]);
     }
     __syncthreads();
-    prologue_from<N, T>(W, S1, tab.g);
+    for (int j = threadIdx.x; j < Kc; j += T) {  // first N-eval input: prim(v)
+      const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+      double2 c[3], u[3];
+#pragma unroll
+      for (int al = 0; al < 3; ++al) c[al] = S1[al * Kc + j];
+      to_prim(kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak), __ldg(tab.g.p + ak), __ldg(tab.g.q + ak), c, u);
+      put_input_z<N>(W, full_index(kap, N), (double)kap, u);
+    }
     __syncthreads();
     for (int st = 0; st < 2; ++st) {
-      nl_physical<N, T, radix_for<N>()>(W, tab.tw);
+      nl_core<N, R, T>(W, Yb, TW);
       for (int j = threadIdx.x; j < Kc; j += T) {
         const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
         const int kf = full_index(kap, N);
         const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
         const double p = __ldg(tab.g.p + ak), q = __ldg(tab.g.q + ak);
         double2 nh[3], nn[3], x[3];
-        get_output<N>(W, kf, (double)kap, invN, nh);
+        get_output_z<N>(W, kf, (double)kap, invN, nh);
         to_eigen(as, p, q, nh, nn);
 #pragma unroll
         for (int al = 0; al < 3; ++al) {
@@ -178,10 +188,9 @@ __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h,
         if (st == 0) {
           double2 u[3];
           to_prim(as, p, q, x, u);
-          put_input<N>(W, kf, (double)kap, u);
+          put_input_z<N>(W, kf, (double)kap, u);
         }
       }
-      if (st == 0) zero_tail<N, T>(W);
       __syncthreads();
     }
     store_pair_prim<N, T>(S1, tab.g, Gnew, nullptr);
@@ -222,10 +231,6 @@ __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h,
 
 // M0: DFMA peak probe — independent FMA chains, every SM
 
-template <int N>
-constexpr size_t nl_smem() { return sizeof(double2) * (3 * WL<N>::NP + 3 * (2 * (N / 3) + 1)); }
-template <int N>
-constexpr size_t avg_smem() { return sizeof(double2) * (3 * WL<N>::NP + 2 * 3 * (2 * (N / 3) + 1)); }
 
 
 
@@ -275,9 +280,9 @@ static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab
 template <int N>
 static cudaError_t launch_strang_sweep_n(const FineTab& tab, double h, double* U, double* G, const double* F,
                                          double* Gnew, int S, double* r_out, cudaStream_t st) {
-  constexpr int T = threads_for<N>();
-  auto kfn = k_strang_sweep<N, T>;
-  const size_t sm = nl_smem<N>();
+  constexpr int R = fine_radix<N>(), T = core_threads<N, R>() > 96 ? core_threads<N, R>() : 96;
+  auto kfn = k_strang_sweep<N, R, T>;
+  constexpr size_t sm = sizeof(double2) * (6 * N + fft_tw_size<N, R>() + 3 * (2 * (N / 3) + 1));
   cudaError_t e = set_smem(kfn, sm);
   if (e != cudaSuccess) return e;
   kfn<<<1, T, sm, st>>>(tab, h, U, G, F, Gnew, S, r_out);

@@ -24,27 +24,60 @@ static cudaError_t set_smem(KernelT k, size_t bytes) {
 // ---------------------------------------------------------------------------------------------
 // K0: standalone N(u) for pairs of states (parity tests of step a1)
 // ---------------------------------------------------------------------------------------------
-template <int N, int T>
+// per-CTA staging of the geometry (a, p, q per |κ|) and the packed twiddles of nl_core
+template <int N, int R, int T>
+__device__ __forceinline__ void stage_geom_tw(const ModeGeom& g, const double2* __restrict__ tw, double2* TW,
+                                              double* GA, double* GP, double* GQ) {
+  fill_packed_twiddles<N, R, T>(TW, tw);
+  for (int k = threadIdx.x; k <= N / 3; k += T) {
+    GA[k] = __ldg(g.a + k);
+    GP[k] = __ldg(g.p + k);
+    GQ[k] = __ldg(g.q + k);
+  }
+}
+
+template <int N, int R, int T>
+struct MiscLayout {  // X, Y (swizzled), packed twiddles, C / A [3][Kc], then doubles GA, GP, GQ
+  static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
+  static constexpr int X = 0, Y = 3 * N, TW = 6 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc, D = A + 3 * Kc;
+  static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * 3 * KP;
+};
+
+// ---------------------------------------------------------------------------------------------
+// K0: standalone N(u) for pairs of states (parity tests of step a1), register FFT core
+// ---------------------------------------------------------------------------------------------
+template <int N, int R, int T>
 __global__ void __launch_bounds__(T) k_nonlinear(const double* u_in, double* out, int n_states,
                                                  const FineTab tab) {
-  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
+  using LY = MiscLayout<N, R, T>;
+  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1, KP = K + 1;
   constexpr double invN = 1.0 / N;
   extern __shared__ double2 smem[];
-  double2* W = smem;
-  double2* C = W + 3 * WL<N>::NP;
+  double2* X = smem + LY::X;
+  double2* C = smem + LY::C;
+  double* GA = reinterpret_cast<double*>(smem + LY::D);
+  double* GP = GA + KP;
+  double* GQ = GP + KP;
+  stage_geom_tw<N, R, T>(tab.g, tab.tw, smem + LY::TW, GA, GP, GQ);
   const int sA = 2 * blockIdx.x, sB = sA + 1;
   const size_t L = (size_t)3 * NH * 2;
   load_pair_eigen<N, T>(u_in + sA * L, (sB < n_states) ? u_in + sB * L : nullptr, tab.g, C);
   __syncthreads();
-  prologue_from<N, T>(W, C, tab.g);
-  __syncthreads();
-  nl_physical<N, T, radix_for<N>()>(W, tab.tw);
   for (int j = threadIdx.x; j < Kc; j += T) {
     const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
-    const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
+    double2 c[3], u[3];
+#pragma unroll
+    for (int al = 0; al < 3; ++al) c[al] = C[al * Kc + j];
+    to_prim(kap < 0 ? -GA[ak] : GA[ak], GP[ak], GQ[ak], c, u);
+    put_input_z<N>(X, full_index(kap, N), (double)kap, u);
+  }
+  __syncthreads();
+  nl_core<N, R, T>(X, smem + LY::Y, smem + LY::TW);
+  for (int j = threadIdx.x; j < Kc; j += T) {
+    const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
     double2 nh[3], nn[3];
-    get_output<N>(W, full_index(kap, N), (double)kap, invN, nh);
-    to_eigen(as, __ldg(tab.g.p + ak), __ldg(tab.g.q + ak), nh, nn);
+    get_output_z<N>(X, full_index(kap, N), (double)kap, invN, nh);
+    to_eigen(kap < 0 ? -GA[ak] : GA[ak], GP[ak], GQ[ak], nh, nn);
 #pragma unroll
     for (int al = 0; al < 3; ++al) C[al * Kc + j] = nn[al];
   }
@@ -53,66 +86,81 @@ __global__ void __launch_bounds__(T) k_nonlinear(const double* u_in, double* out
 }
 
 // ---------------------------------------------------------------------------------------------
-// K3: averaged nonlinearity for pairs of independent states (same sample m for both):
-//   acc = Σ_{m=1}^{M-1} w_m P+_m N(P-_m c), in ascending m; P±_m = diag(e^{±iατ_m ω}) (eigen).
+// K3: averaged nonlinearity for pairs of independent states (same sample m for both), register
+// FFT core; ascending m:  acc = Σ_{m=1}^{M-1} w_m P+_m N(P-_m c),  P±_m = diag(e^{±iατ_m ω}) (eigen).
+// Each thread owns the modes j = t + o T for every sample: the next sample's phases are loaded
+// into registers before the FFT so their L2 latency hides behind it.
 // ---------------------------------------------------------------------------------------------
-
-template <int N, int T>
+template <int N, int R, int T>
 __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* out, int n_states, int M,
                                                   const AvgTab tab) {
-  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
+  using LY = MiscLayout<N, R, T>;
+  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1, KP = K + 1, OMAX = (Kc + T - 1) / T;
   constexpr double invN = 1.0 / N;
   extern __shared__ double2 smem[];
-  double2* W = smem;
-  double2* C = W + 3 * WL<N>::NP;
-  double2* A = C + 3 * Kc;
+  double2* X = smem + LY::X;
+  double2* C = smem + LY::C;
+  double2* A = smem + LY::A;
+  double* GA = reinterpret_cast<double*>(smem + LY::D);
+  double* GP = GA + KP;
+  double* GQ = GP + KP;
+  stage_geom_tw<N, R, T>(tab.g, tab.tw, smem + LY::TW, GA, GP, GQ);
   const int sA = 2 * blockIdx.x, sB = sA + 1;
   const size_t L = (size_t)3 * NH * 2;
   load_pair_eigen<N, T>(u_in + sA * L, (sB < n_states) ? u_in + sB * L : nullptr, tab.g, C);
   for (int i = threadIdx.x; i < 3 * Kc; i += T) A[i] = make_double2(0.0, 0.0);
   __syncthreads();
-  // prologue for m = 1
-  for (int m = 1; m <= M - 1; ++m) {
-    if (m == 1) {
-      for (int j = threadIdx.x; j < Kc; j += T) {
-        const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
-        const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
-        const double2 ph = __ldg(tab.phase + (size_t)m * (K + 1) + ak);  // e^{iωτ_m}
-        double2 c[3], u[3];
-        c[0] = cmul(C[j], ph);            // α=-1: e^{+iωτ}
-        c[1] = C[Kc + j];                 // α=0
-        c[2] = cmulc(C[2 * Kc + j], ph);  // α=+1: e^{-iωτ}
-        to_prim(as, __ldg(tab.g.p + ak), __ldg(tab.g.q + ak), c, u);
-        put_input<N>(W, full_index(kap, N), (double)kap, u);
-      }
-      zero_tail<N, T>(W);
-      __syncthreads();
-    }
-    nl_physical<N, T, radix_for<N>()>(W, tab.tw);
-    const double wm = __ldg(tab.w + m);
-    for (int j = threadIdx.x; j < Kc; j += T) {
+  double2 ph[OMAX];
+#pragma unroll
+  for (int o = 0; o < OMAX; ++o) {  // prologue for m = 1
+    const int j = threadIdx.x + o * T;
+    if (j < Kc) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
-      const int kf = full_index(kap, N);
-      const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
-      const double p = __ldg(tab.g.p + ak), q = __ldg(tab.g.q + ak);
-      double2 nh[3], nn[3];
-      get_output<N>(W, kf, (double)kap, invN, nh);
-      to_eigen(as, p, q, nh, nn);
-      const double2 ph = __ldg(tab.phase + (size_t)m * (K + 1) + ak);
-      A[j] = caxpy(wm, cmulc(nn[0], ph), A[j]);               // α=-1: e^{-iωτ}
-      A[Kc + j] = caxpy(wm, nn[1], A[Kc + j]);                // α=0
-      A[2 * Kc + j] = caxpy(wm, cmul(nn[2], ph), A[2 * Kc + j]);  // α=+1: e^{+iωτ}
-      if (m + 1 <= M - 1) {
-        const double2 ph2 = __ldg(tab.phase + (size_t)(m + 1) * (K + 1) + ak);
-        double2 c[3], u[3];
-        c[0] = cmul(C[j], ph2);
-        c[1] = C[Kc + j];
-        c[2] = cmulc(C[2 * Kc + j], ph2);
-        to_prim(as, p, q, c, u);
-        put_input<N>(W, kf, (double)kap, u);
-      }
+      ph[o] = __ldg(tab.phase + (size_t)1 * KP + ak);  // e^{iωτ_1}
+      double2 c[3], u[3];
+      c[0] = cmul(C[j], ph[o]);            // α=-1: e^{+iωτ}
+      c[1] = C[Kc + j];                    // α=0
+      c[2] = cmulc(C[2 * Kc + j], ph[o]);  // α=+1: e^{-iωτ}
+      to_prim(kap < 0 ? -GA[ak] : GA[ak], GP[ak], GQ[ak], c, u);
+      put_input_z<N>(X, full_index(kap, N), (double)kap, u);
     }
-    zero_tail<N, T>(W);
+  }
+  __syncthreads();
+  for (int m = 1; m <= M - 1; ++m) {
+    double2 phn[OMAX];  // next sample's phases, in flight during the FFT
+#pragma unroll
+    for (int o = 0; o < OMAX; ++o) {
+      const int j = threadIdx.x + o * T;
+      const int kap = kappa_of(j < Kc ? j : 0, K), ak = kap < 0 ? -kap : kap;
+      phn[o] = (j < Kc && m + 1 <= M - 1) ? __ldg(tab.phase + (size_t)(m + 1) * KP + ak) : make_double2(1.0, 0.0);
+    }
+    nl_core<N, R, T>(X, smem + LY::Y, smem + LY::TW);
+    const double wm = __ldg(tab.w + m);
+#pragma unroll
+    for (int o = 0; o < OMAX; ++o) {
+      const int j = threadIdx.x + o * T;
+      if (j < Kc) {
+        const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+        const int kf = full_index(kap, N);
+        const double as = kap < 0 ? -GA[ak] : GA[ak];
+        const double p = GP[ak], q = GQ[ak];
+        double2 nh[3], nn[3];
+        get_output_z<N>(X, kf, (double)kap, invN, nh);
+        to_eigen(as, p, q, nh, nn);
+        A[j] = caxpy(wm, cmulc(nn[0], ph[o]), A[j]);                  // α=-1: e^{-iωτ}
+        A[Kc + j] = caxpy(wm, nn[1], A[Kc + j]);                      // α=0
+        A[2 * Kc + j] = caxpy(wm, cmul(nn[2], ph[o]), A[2 * Kc + j]);  // α=+1: e^{+iωτ}
+        if (m + 1 <= M - 1) {
+          double2 c[3], u[3];
+          c[0] = cmul(C[j], phn[o]);
+          c[1] = C[Kc + j];
+          c[2] = cmulc(C[2 * Kc + j], phn[o]);
+          to_prim(as, p, q, c, u);
+          put_input_z<N>(X, kf, (double)kap, u);
+        }
+      }
+      ph[o] = phn[o];
+    }
     __syncthreads();
   }
   store_pair_prim<N, T>(A, tab.g, out + sA * L, (sB < n_states) ? out + sB * L : nullptr);
@@ -137,32 +185,26 @@ __global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters) {
 
 
 template <int N>
-constexpr size_t nl_smem() { return sizeof(double2) * (3 * WL<N>::NP + 3 * (2 * (N / 3) + 1)); }
-template <int N>
-constexpr size_t avg_smem() { return sizeof(double2) * (3 * WL<N>::NP + 2 * 3 * (2 * (N / 3) + 1)); }
-
-
-template <int N>
 static cudaError_t launch_nl_n(const double* in, double* out, int S, const FineTab& tab, cudaStream_t st) {
-  constexpr int T = threads_for<N>();
-  auto kfn = k_nonlinear<N, T>;
-  cudaError_t e = set_smem(kfn, nl_smem<N>());
+  constexpr int R = fine_radix<N>(), T = core_threads<N, R>();
+  auto kfn = k_nonlinear<N, R, T>;
+  constexpr size_t sm = MiscLayout<N, R, T>::bytes;
+  cudaError_t e = set_smem(kfn, sm);
   if (e != cudaSuccess) return e;
-  kfn<<<(S + 1) / 2, T, nl_smem<N>(), st>>>(in, out, S, tab);
+  kfn<<<(S + 1) / 2, T, sm, st>>>(in, out, S, tab);
   return cudaGetLastError();
 }
-
 
 template <int N>
 static cudaError_t launch_avg_n(const double* in, double* out, int S, int M, const AvgTab& tab, cudaStream_t st) {
-  constexpr int T = threads_for<N>();
-  auto kfn = k_avg_states<N, T>;
-  cudaError_t e = set_smem(kfn, avg_smem<N>());
+  constexpr int R = fine_radix<N>(), T = core_threads<N, R>();
+  auto kfn = k_avg_states<N, R, T>;
+  constexpr size_t sm = MiscLayout<N, R, T>::bytes;
+  cudaError_t e = set_smem(kfn, sm);
   if (e != cudaSuccess) return e;
-  kfn<<<(S + 1) / 2, T, avg_smem<N>(), st>>>(in, out, S, M, tab);
+  kfn<<<(S + 1) / 2, T, sm, st>>>(in, out, S, M, tab);
   return cudaGetLastError();
 }
-
 
 cudaError_t launch_nonlinear(int n, const double* in, double* out, int S, const FineTab& tab, cudaStream_t st) {
 #define C(NN) launch_nl_n<NN>(in, out, S, tab, st)
