@@ -7,15 +7,21 @@
 
 #include <cstdlib>
 
+#ifndef RSW_FINE_R8_MAX
+#define RSW_FINE_R8_MAX 1024  // radix 8 up to n = 1024 (C5 fine 10.95 vs 10.34 TFLOP/s at radix 16)
+#endif
+
 namespace rsw {
 
 // Radix / thread choices of the register FFT core (nl_core), measured on B200:
 // R values per thread, T = 3N/R threads rounded up to whole warps.  Fine and batched-N̄ kernels:
-// radix 8 up to n = 256 (C3 fine 8.5 TFLOP/s vs 7.1 at radix 4 / 16), radix 16 above (C5 10.4 vs 7.6 /
-// 6.1 at radix 4 / 32).  Coarse sweep (latency bound, one sample pair per CTA): radix 8 with 192
-// threads (the extra threads speed up the mode loops; C3 stage 6.7 us vs 8.3 at 96 threads).
+// radix 8 up to n = 1024 (C3 fine 8.5 TFLOP/s vs 7.1 at radix 4 / 16; C5 10.95 vs 10.33 at 16.4.16 and
+// 6.1 at 32.32; C4 N̄ 12.2 vs 11.3 at 16.2.16).  Coarse sweep (latency bound, one sample pair per CTA):
+// radix 8 with 192 threads (the extra threads speed up the mode loops; C3 stage 6.7 us vs 8.3 at 96).
 template <int N>
-__host__ __device__ constexpr int fine_radix() { return N <= 32 ? 4 : N <= 256 ? 8 : 16; }  // palindromic
+__host__ __device__ constexpr int fine_radix() {  // palindromic plans: 256 = 8.4.8, 512 = 8.8.8, 1024 = 8.4.4.8
+  return N <= 32 ? 4 : (N <= RSW_FINE_R8_MAX ? 8 : 16);
+}
 template <int N, int R>
 __host__ __device__ constexpr int core_threads() { return (3 * (N / R) + 31) / 32 * 32; }
 template <int N>

@@ -209,19 +209,37 @@ struct NamedGroup {
 
 __host__ __device__ __forceinline__ constexpr int swz(int i) { return (i & ~7) | ((i ^ (i >> 3) ^ (i >> 6)) & 7); }
 
+// Palindromic plan: a = floor(log_R N) full passes, rem = N / R^a.  rem == 1: a passes of R.  a even:
+// R^(a/2) . rem . R^(a/2).  a odd: R^((a-1)/2) . q . q . R^((a-1)/2) with q^2 = rem R (1024 = 8.4.4.8).
 template <int N, int R>
-__host__ __device__ constexpr int fft_npass() {
-  int m = 0;
-  for (int n = 1; n < N; n *= R) ++m;
-  return m;
+__host__ __device__ constexpr int fft_plan(int p, bool count) {
+  int a = 0, x = 1;
+  while (x * R <= N) {
+    x *= R;
+    ++a;
+  }
+  const int rem = N / x;
+  int m = 0, mid0 = 0, mid1 = 0;
+  if (rem == 1) {
+    m = a;
+  } else if (a % 2 == 0) {
+    m = a + 1;
+    mid0 = mid1 = rem;
+  } else {
+    int q = 1;
+    while (q * q < rem * R) q *= 2;
+    m = a + 1;  // (a-1) R passes + two middle passes
+    mid0 = mid1 = (q * q == rem * R) ? q : -1;
+  }
+  if (count) return m;
+  if (rem == 1) return R;
+  if (a % 2 == 0) return p == a / 2 ? mid0 : R;
+  return (p == (a - 1) / 2 || p == (a + 1) / 2) ? mid0 : R;
 }
 template <int N, int R>
-__host__ __device__ constexpr int fft_rad(int p) {  // radix of pass p (palindrome: small radix in the middle)
-  constexpr int m = fft_npass<N, R>();
-  int small = N;
-  for (int q = 0; q < m - 1; ++q) small /= R;
-  return (p == (m - 1) / 2) ? small : R;
-}
+__host__ __device__ constexpr int fft_npass() { return fft_plan<N, R>(0, true); }
+template <int N, int R>
+__host__ __device__ constexpr int fft_rad(int p) { return fft_plan<N, R>(p, false); }
 template <int N, int R>
 __host__ __device__ constexpr bool fft_palindrome() {
   constexpr int m = fft_npass<N, R>();

@@ -1,6 +1,8 @@
 // rsw_k_fine.cu — fine propagator kernels (a2 ETDRK4 / a2' Strang) and their launcher.
 #include "rsw_blocks.cuh"
 
+#include <cstdlib>
+
 namespace rsw {
 
 template <typename KernelT>
@@ -85,6 +87,10 @@ static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double
 template <int N>
 static cudaError_t launch_fine_n(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
                                  const FineTab& tab, cudaStream_t st) {
+  if constexpr (N == 1024 || N == 512) {  // measurement knob: the radix-16 plans (16.4.16, 16.2.16)
+    static const char* e = getenv("RSW_FINE_R16");
+    if (e && atoi(e) == 1) return launch_fine_nr<N, 16>(scheme, lin, in, out, S, m, h, tab, st);
+  }
   return launch_fine_nr<N, fine_radix<N>()>(scheme, lin, in, out, S, m, h, tab, st);
 }
 
