@@ -7,25 +7,21 @@
 
 #include <cstdlib>
 
-#ifndef RSW_FINE_R8_MAX
-#define RSW_FINE_R8_MAX 1024  // radix 8 up to n = 1024 (C5 fine 10.95 vs 10.34 TFLOP/s at radix 16)
-#endif
-
 namespace rsw {
 
-// Radix / thread choices of the register FFT core (nl_core), measured on B200:
-// R values per thread, T = 3N/R threads rounded up to whole warps.  Fine and batched-N̄ kernels:
-// radix 8 up to n = 1024 (C3 fine 8.5 TFLOP/s vs 7.1 at radix 4 / 16; C5 10.95 vs 10.33 at 16.4.16 and
-// 6.1 at 32.32; C4 N̄ 12.2 vs 11.3 at 16.2.16).  Coarse sweep (latency bound, one sample pair per CTA):
-// radix 8 with 192 threads (the extra threads speed up the mode loops; C3 stage 6.7 us vs 8.3 at 96).
+// Radix / thread choices of the in-place register FFT core (nl_core), R values per thread, T = 3N/R
+// threads rounded up to whole warps.  Plans (passes): 1024 = 4.16.16 at R = 16 (8: 2.8.8.8),
+// 512 = 8.8.8, 256 = 4.8.8, 128 = 2.8.8.  Fine kernel at n = 1024: two 192-thread pair-groups per
+// CTA sharing the tables (fine_groups).  Coarse sweep (latency bound, one sample pair per CTA):
+// radix 8 with 192 threads (the extra threads speed up the mode loops).
 template <int N>
-__host__ __device__ constexpr int fine_radix() {  // palindromic plans: 256 = 8.4.8, 512 = 8.8.8, 1024 = 8.4.4.8
-  return N <= 32 ? 4 : (N <= RSW_FINE_R8_MAX ? 8 : 16);
-}
+__host__ __device__ constexpr int fine_radix() { return N <= 32 ? 4 : (N <= 512 ? 8 : 16); }
+template <int N>
+__host__ __device__ constexpr int fine_groups() { return N >= 1024 ? 2 : 1; }
 template <int N, int R>
 __host__ __device__ constexpr int core_threads() { return (3 * (N / R) + 31) / 32 * 32; }
 template <int N>
-__host__ __device__ constexpr int coarse_radix() { return N <= 32 ? 4 : N <= 256 ? 8 : 16; }  // palindromic
+__host__ __device__ constexpr int coarse_radix() { return N <= 32 ? 4 : N <= 256 ? 8 : 16; }
 template <int N>
 __host__ __device__ constexpr int coarse_threads() { return core_threads<N, coarse_radix<N>()>() > 192 ? core_threads<N, coarse_radix<N>()>() : 192; }
 
@@ -134,13 +130,7 @@ __device__ __forceinline__ FineSmemTab stage_fine_tables(double2* smem_tw, doubl
   double* sGA = sC0 + 6 * KP;
   double* sGP = sGA + KP;
   double* sGQ = sGP + KP;
-  constexpr int m = fft_npass<N, R>(), r0 = fft_rad<N, R>(0);
-  for (int i = t; i < fft_tw_size<N, R>(); i += nthr) {  // (fill_packed_twiddles with a runtime stride)
-    int p = 1;
-    while (p < m - 1 && i >= fft_ns<N, R>(p + 1) - r0) ++p;
-    const int NS = fft_ns<N, R>(p), r = fft_rad<N, R>(p), o = i - (NS - r0);
-    smem_tw[i] = __ldg(tab.tw + (o % (r - 1) + 1) * (o / (r - 1)) * (N / (NS * r)));
-  }
+  fill_packed_twiddles<N, R, T>(smem_tw, tab.tw, t, nthr);
   for (int i = t; i < 6 * KP; i += nthr) {
     smem_cp[i] = __ldg(tab.cp + i);
     sC0[i] = __ldg(tab.c0 + i);
@@ -162,7 +152,10 @@ struct FineTmem {  // TMEM columns of one fine pair-group: per mode slot o, S1 /
 // One pair of slices advanced by m fine steps (a2 / a2') by a warp-aligned thread group: the state
 // lives in the group's TMEM columns, the N-evals in its X / Y buffers.  Used by k_fine (the whole
 // CTA) and by the fine workers of the pipelined parareal kernel (one of several groups of a CTA).
-template <int N, int R, int TG, int SCHEME, bool LIN, class GRP>
+// TMEM layout of the group's thread-private slots: lane quarter = (CTA warp) mod 4; column block =
+// (group warp) / 4 (TBLK = false: groups own disjoint column ranges starting at tcol) or (CTA warp) / 4
+// (TBLK = true: tcol is the CTA's base and the groups of a CTA interleave, 3 blocks for 12 warps).
+template <int N, int R, int TG, int SCHEME, bool LIN, class GRP, bool TBLK = false>
 __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double2* Y, const FineSmemTab& st_,
                                               uint32_t tcol, const ModeGeom& gg, const double* uA,
                                               const double* uB, double* oA, double* oB, int m_steps, double h) {
@@ -178,7 +171,7 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
   load_pair_eigen<N, TG>(uA, uB, gg, W, t);  // C[α][j] staged in W
   grp.sync();
   // thread-private TMEM slot of mode slot o: columns o*36 + {S1: 0, S0: 12, S2: 24} + 4α
-  const uint32_t tb = tcol + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((gwarp >> 2) * OMAX * 36);
+  const uint32_t tb = tcol + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(((TBLK ? warp : gwarp) >> 2) * OMAX * 36);
   double2 c0v[OMAX][3];
 #pragma unroll
   for (int o = 0; o < OMAX; ++o) {
@@ -213,8 +206,9 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
     const bool last_step = (step == m_steps - 1);
     for (int st = 0; st < nst; ++st) {
       if (!LIN) nl_core<N, R, TG>(W, Y, st_.TW, grp);
-      // epilogue (this stage's update) fused with the prologue of the next N-eval
-#pragma unroll
+      // epilogue (this stage's update) fused with the prologue of the next N-eval (rolled when a
+      // thread owns many modes: an unrolled body of 4 modes spills at 168 registers)
+#pragma unroll (OMAX > 2 ? 1 : OMAX)
       for (int o = 0; o < OMAX; ++o) {
         const int j = t + o * TG;
         const bool valid = j < Kc;
@@ -316,7 +310,8 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
       grp.sync();
     }
   }
-  // final state S1 -> C[α][j] in Y (W may still hold the last stage's inputs), then store
+  // final state S1 -> C[α][j] in W (the last stage's N-eval inputs are dead; every thread is past
+  // its last W read at the barrier above), then store
 #pragma unroll
   for (int o = 0; o < OMAX; ++o) {
     const int j = t + o * TG;
@@ -324,11 +319,11 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
     tmem_ld3(tb + o * 36, s1);
     if (j < Kc) {
 #pragma unroll
-      for (int al = 0; al < 3; ++al) Y[al * Kc + j] = s1[al];
+      for (int al = 0; al < 3; ++al) W[al * Kc + j] = s1[al];
     }
   }
   grp.sync();
-  store_pair_prim<N, TG>(Y, gg, oA, oB, t);
+  store_pair_prim<N, TG>(W, gg, oA, oB, t);
 }
 
 

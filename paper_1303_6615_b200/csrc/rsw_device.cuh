@@ -209,185 +209,185 @@ struct NamedGroup {
 
 __host__ __device__ __forceinline__ constexpr int swz(int i) { return (i & ~7) | ((i ^ (i >> 3) ^ (i >> 6)) & 7); }
 
-// Palindromic plan: a = floor(log_R N) full passes, rem = N / R^a.  rem == 1: a passes of R.  a even:
-// R^(a/2) . rem . R^(a/2).  a odd: R^((a-1)/2) . q . q . R^((a-1)/2) with q^2 = rem R (1024 = 8.4.4.8).
+// ---------------------------------------------------------------------------------------------
+// In-place mixed-radix FFT core (nl_core).  Plan for (N, R): pass 0 has radix rem = N / R^a when
+// N is not a power of R, every other pass radix R (1024 = 4.16.16, 512 = 2.16.16, 256 = 16.16 at
+// R = 16).  Pass p works on blocks of length L_p = N / (r_0 ... r_{p-1}) with stride d_p = L_p / r_p:
+// butterfly b = (block, k1) = divmod(b, d_p) owns the elements block·L_p + k1 + d_p·s, s < r_p.
+//  * synthesis (inverse transform, sign +): decimation in frequency (Gentleman–Sande) — r-point DFT,
+//    then the twiddles ω_L^{s k1} — written back to the positions it was read from.  The grid
+//    values come out in digit-reversed order, which the pointwise products do not care about;
+//  * analysis (forward transform, sign −): the conjugate transpose, passes in reverse order —
+//    twiddles e^{-2πi s k1/L} on the inputs, then the r-point DFT, again in place — which returns
+//    the natural spectral order.  No reordering pass is ever needed.
+// Because a butterfly writes back exactly the elements it read, a pass needs no barrier between its
+// loads and its stores: ONE barrier per pass and a single buffer of 3N values (plus N for the v1
+// copy of the products).  Thread t of the group owns field f = t / (N/R) and column j = t mod (N/R);
+// its butterflies in a pass of radix r are b = j + i N/R, i < R/r.  Storage index swz(e): conflict-
+// free for every pass pattern of these plans (tools/fft_model.py), and the identity inside each
+// aligned group of 8 (so the natural-order epilogue accesses stay conflict-free).
+// ---------------------------------------------------------------------------------------------
 template <int N, int R>
-__host__ __device__ constexpr int fft_plan(int p, bool count) {
+__host__ __device__ constexpr int fft_npass() {
   int a = 0, x = 1;
   while (x * R <= N) {
     x *= R;
     ++a;
   }
-  const int rem = N / x;
-  int m = 0, mid0 = 0, mid1 = 0;
-  if (rem == 1) {
-    m = a;
-  } else if (a % 2 == 0) {
-    m = a + 1;
-    mid0 = mid1 = rem;
-  } else {
-    int q = 1;
-    while (q * q < rem * R) q *= 2;
-    m = a + 1;  // (a-1) R passes + two middle passes
-    mid0 = mid1 = (q * q == rem * R) ? q : -1;
-  }
-  if (count) return m;
-  if (rem == 1) return R;
-  if (a % 2 == 0) return p == a / 2 ? mid0 : R;
-  return (p == (a - 1) / 2 || p == (a + 1) / 2) ? mid0 : R;
+  return (N / x > 1) ? a + 1 : a;
 }
 template <int N, int R>
-__host__ __device__ constexpr int fft_npass() { return fft_plan<N, R>(0, true); }
-template <int N, int R>
-__host__ __device__ constexpr int fft_rad(int p) { return fft_plan<N, R>(p, false); }
-template <int N, int R>
-__host__ __device__ constexpr bool fft_palindrome() {
-  constexpr int m = fft_npass<N, R>();
-  for (int p = 0; p < m; ++p)
-    if (fft_rad<N, R>(p) != fft_rad<N, R>(m - 1 - p)) return false;
-  return true;
+__host__ __device__ constexpr int fft_rad(int p) {
+  int x = 1;
+  while (x * R <= N) x *= R;
+  return (N / x > 1 && p == 0) ? N / x : R;
 }
 template <int N, int R>
-__host__ __device__ constexpr int fft_ns(int p) {  // product of the radices before pass p
-  int ns = 1;
-  for (int q = 0; q < p; ++q) ns *= fft_rad<N, R>(q);
-  return ns;
+__host__ __device__ constexpr int fft_len(int p) {  // block length L_p
+  int L = N;
+  for (int q = 0; q < p; ++q) L /= fft_rad<N, R>(q);
+  return L;
 }
-// packed twiddles of pass p >= 1: TW[(NS_p - r_0) + k (r_p - 1) + s - 1] = e^{-2πi s k / (NS_p r_p)}
 template <int N, int R>
-__host__ __device__ constexpr int fft_tw_size() { return N - fft_rad<N, R>(0); }
+__host__ __device__ constexpr int fft_tw_off(int p) {  // offset of pass p's twiddle bases
+  int o = 0;
+  for (int q = 0; q < p; ++q) o += fft_len<N, R>(q) / fft_rad<N, R>(q);
+  return o;
+}
+// twiddle bases TW[off_p + k1] = e^{-2πi k1 / L_p}, k1 < d_p, for the passes p < m-1 (the last pass
+// has d = 1 and no twiddles)
+template <int N, int R>
+__host__ __device__ constexpr int fft_tw_size() { return fft_tw_off<N, R>(fft_npass<N, R>() - 1) > 0 ? fft_tw_off<N, R>(fft_npass<N, R>() - 1) : 1; }
 
-// fill the packed table from the plain table tw[m] = e^{-2πi m/N} (all threads of the CTA)
+// fill the twiddle bases from the plain table tw[m] = e^{-2πi m/N} (threads t0, t0 + T, ...)
 template <int N, int R, int T>
-__device__ __forceinline__ void fill_packed_twiddles(double2* TW, const double2* __restrict__ tw, int t0 = -1) {
-  constexpr int m = fft_npass<N, R>(), r0 = fft_rad<N, R>(0);
-  for (int i = (t0 < 0 ? (int)threadIdx.x : t0); i < fft_tw_size<N, R>(); i += T) {
-    int p = 1;
-    while (p < m - 1 && i >= fft_ns<N, R>(p + 1) - r0) ++p;
-    const int NS = fft_ns<N, R>(p), r = fft_rad<N, R>(p), o = i - (NS - r0);
-    const int k = o / (r - 1), s = o % (r - 1) + 1;
-    TW[i] = __ldg(tw + s * k * (N / (NS * r)));
+__device__ __forceinline__ void fill_packed_twiddles(double2* TW, const double2* __restrict__ tw, int t0 = -1, int nthr = T) {
+  constexpr int m = fft_npass<N, R>();
+  for (int i = (t0 < 0 ? (int)threadIdx.x : t0); i < fft_tw_off<N, R>(m - 1); i += nthr) {
+    int p = 0;
+    while (p < m - 2 && i >= fft_tw_off<N, R>(p + 1)) ++p;
+    TW[i] = __ldg(tw + (i - fft_tw_off<N, R>(p)) * (N / fft_len<N, R>(p)));
   }
 }
 
-template <int N, int R, int r>
-__device__ __forceinline__ int core_idx(int j, int t) {  // index held in v[t] (t = i r + s) by a radix-r pass
-  return j + (t / r) * (N / R) + (t % r) * (N / r);
+__device__ __forceinline__ double2 csqr(double2 a) {  // a^2
+  return make_double2((a.x + a.y) * (a.x - a.y), (a.x + a.x) * a.y);
 }
 
-template <int N, int R, int p, int SIGN>
-__device__ __forceinline__ void core_math(double2 (&v)[R], int j, const double2* TW) {
-  constexpr int r = fft_rad<N, R>(p), NS = fft_ns<N, R>(p);
+// v[s] *= w^s (CONJ: conj(w)^s), s = 1..r-1, for a twiddle base w read from the shared table; the
+// powers are formed in registers as they are needed (w^2 = w·w, w^3 = w^2·w, w^4 = (w^2)^2, ...,
+// w^{8+s} = w^8·w^s: at most 5 roundings deep, error ≲ 5 ulp): the shared-memory pipe is the binding
+// resource of the FFT core (ncu, n = 1024: 80% of peak wavefronts, twiddle loads ~23% of them),
+// while the FP64 pipe has room.
+template <int r, bool CONJ>
+__device__ __forceinline__ void apply_twiddles(double2* v, const double2 w1) {
+#define TWM(s, w) v[s] = CONJ ? cmulc(v[s], w) : cmul(v[s], w)
+  if constexpr (r >= 2) TWM(1, w1);
+  if constexpr (r >= 4) {
+    const double2 w2 = csqr(w1), w3 = cmul(w2, w1);
+    TWM(2, w2);
+    TWM(3, w3);
+    if constexpr (r >= 8) {
+      const double2 w4 = csqr(w2), w5 = cmul(w4, w1), w6 = csqr(w3), w7 = cmul(w4, w3);
+      TWM(4, w4);
+      TWM(5, w5);
+      TWM(6, w6);
+      TWM(7, w7);
+      if constexpr (r >= 16) {
+        const double2 w8 = csqr(w4);
+        const double2 ws[8] = {make_double2(1.0, 0.0), w1, w2, w3, w4, w5, w6, w7};
+        TWM(8, w8);
 #pragma unroll
-  for (int i = 0; i < R / r; ++i) {
-    if constexpr (NS > 1) {
-      const int k = (j + i * (N / R)) & (NS - 1);
-      const double2* tp = TW + (NS - fft_rad<N, R>(0)) + k * (r - 1) - 1;
-#pragma unroll
-      for (int s = 1; s < r; ++s) {
-        const double2 w = tp[s];  // shared-memory table
-        v[i * r + s] = SIGN < 0 ? cmul(v[i * r + s], w) : cmulc(v[i * r + s], w);
+        for (int s = 9; s < 16; ++s) TWM(s, cmul(w8, ws[s - 8]));
+        static_assert(r <= 16, "apply_twiddles: radix <= 16");
       }
     }
-    dftR<r, SIGN>(&v[i * r]);
   }
+#undef TWM
 }
 
 template <int N, int R, int p>
-__device__ __forceinline__ void core_store(const double2 (&v)[R], double2* B, int j) {
-  constexpr int r = fft_rad<N, R>(p), NS = fft_ns<N, R>(p);
-#pragma unroll
-  for (int i = 0; i < R / r; ++i) {
-    const int jb = j + i * (N / R);
-    const int base = (jb / NS) * NS * r + (jb & (NS - 1));
-#pragma unroll
-    for (int s = 0; s < r; ++s) B[swz(base + s * NS)] = v[i * r + s];
-  }
+__device__ __forceinline__ int fft_elem0(int b) {  // first element of butterfly b in pass p
+  constexpr int L = fft_len<N, R>(p), d = L / fft_rad<N, R>(p);
+  return (b / d) * L + (b % d);
 }
 
-template <int N, int R, int r>
-__device__ __forceinline__ void core_load(double2 (&v)[R], const double2* B, int j) {
-#pragma unroll
-  for (int t = 0; t < R; ++t) v[t] = B[swz(core_idx<N, R, r>(j, t))];
-}
-
-// synthesis passes p..m-1 (p >= 1): load from B[p%2], compute, store to B[(p+1)%2] unless last
+// synthesis passes p..m-1 of field buffer Xf (sign +); the last pass leaves its outputs in v
 template <int N, int R, int p, class GRP>
-__device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* const (&B)[2], int f, int j, bool act,
-                                             const double2* TW, const GRP& grp) {
-  constexpr int m = fft_npass<N, R>();
-  if constexpr (p < m) {
-    if (act) {
-      core_load<N, R, fft_rad<N, R>(p)>(v, B[p % 2] + f * N, j);
-      core_math<N, R, p, +1>(v, j, TW);
-      if constexpr (p < m - 1) core_store<N, R, p>(v, B[(p + 1) % 2] + f * N, j);
+__device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* Xf, int j, bool act, const double2* TW,
+                                             const GRP& grp) {
+  constexpr int m = fft_npass<N, R>(), r = fft_rad<N, R>(p), L = fft_len<N, R>(p), d = L / r, NJ = N / R;
+  constexpr int K = N / 3;
+  if (act) {
+#pragma unroll
+    for (int i = 0; i < R / r; ++i) {
+      const int b = j + i * NJ, e0 = fft_elem0<N, R, p>(b);
+#pragma unroll
+      for (int s = 0; s < r; ++s) {
+        const int e = e0 + d * s;
+        if constexpr (p == 0) v[i * r + s] = (e <= K || e >= N - K) ? Xf[swz(e)] : make_double2(0.0, 0.0);  // R10
+        else v[i * r + s] = Xf[swz(e)];
+      }
+      dftR<r, +1>(&v[i * r]);
+      if constexpr (p < m - 1) {
+        apply_twiddles<r, true>(&v[i * r], TW[fft_tw_off<N, R>(p) + (b % d)]);  // ω_L^{+s k1}
+#pragma unroll
+        for (int s = 0; s < r; ++s) Xf[swz(e0 + d * s)] = v[i * r + s];
+      }
     }
-    if constexpr (p < m - 1) {
-      grp.sync();
-      core_inverse<N, R, p + 1>(v, B, f, j, act, TW, grp);
-    }
+  }
+  if constexpr (p < m - 1) {
+    grp.sync();
+    core_inverse<N, R, p + 1>(v, Xf, j, act, TW, grp);
   }
 }
 
-// analysis passes q..m-1 (q >= 1; analysis pass q runs the (r, NS) of synthesis pass q): load from
-// Z_{q-1} = B[(m-1+q-1)%2]; the last pass stores the retained outputs to B[0]
-template <int N, int R, int q, class GRP>
-__device__ __forceinline__ void core_forward(double2 (&v)[R], double2* const (&B)[2], int f, int j, bool act,
-                                             const double2* TW, const GRP& grp) {
-  constexpr int m = fft_npass<N, R>();
-  if constexpr (q < m) {
-    constexpr int r = fft_rad<N, R>(q);
+// analysis passes p, p-1, ..., 0 (sign -); pass 0 stores the retained modes only
+template <int N, int R, int p, class GRP>
+__device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j, bool act, const double2* TW,
+                                             const GRP& grp) {
+  if constexpr (p >= 0) {
+    constexpr int r = fft_rad<N, R>(p), L = fft_len<N, R>(p), d = L / r, NJ = N / R;
     constexpr int K = N / 3;
     if (act) {
-      core_load<N, R, r>(v, B[(m - 1 + q - 1) % 2] + f * N, j);
-      core_math<N, R, q, -1>(v, j, TW);
-      double2* out = B[(q == m - 1) ? 0 : (m - 1 + q) % 2] + f * N;
-      if constexpr (q < m - 1) {
-        core_store<N, R, q>(v, out, j);
-      } else {  // final pass: NS = N/r, butterfly jb writes jb + s N/r = core_idx; retained modes only
 #pragma unroll
-        for (int t = 0; t < R; ++t) {
-          const int o = core_idx<N, R, r>(j, t);
-          if (o <= K || o >= N - K) out[swz(o)] = v[t];
+      for (int i = 0; i < R / r; ++i) {
+        const int b = j + i * NJ, e0 = fft_elem0<N, R, p>(b);
+#pragma unroll
+        for (int s = 0; s < r; ++s) v[i * r + s] = Xf[swz(e0 + d * s)];
+        apply_twiddles<r, false>(&v[i * r], TW[fft_tw_off<N, R>(p) + (b % d)]);  // e^{-2πi s k1/L}
+        dftR<r, -1>(&v[i * r]);
+#pragma unroll
+        for (int s = 0; s < r; ++s) {
+          const int e = e0 + d * s;
+          if (p > 0 || e <= K || e >= N - K) Xf[swz(e)] = v[i * r + s];
         }
       }
     }
     grp.sync();
-    core_forward<N, R, q + 1>(v, B, f, j, act, TW, grp);
+    core_forward<N, R, p - 1>(v, Xf, j, act, TW, grp);
   }
 }
 
+// N(u) core on the packed pair: X = double2[3][N] (swizzled) holds the retained spectra of
+// (v1, i κ v2, h) on entry and the retained spectra of (v1²/2, v1 v2x, h v1) (unnormalised) on exit;
+// V = double2[N] scratch for the v1 copy.  2m barriers (m = passes), the last one on exit.
 template <int N, int R, int T, class GRP = CtaGroup>
-__device__ __forceinline__ void nl_core(double2* X, double2* Y, const double2* TW, const GRP& grp = GRP()) {
+__device__ __forceinline__ void nl_core(double2* X, double2* V, const double2* TW, const GRP& grp = GRP()) {
   static_assert(T >= 3 * (N / R), "nl_core: T must cover 3 N/R field-columns");
-  static_assert(fft_palindrome<N, R>(), "nl_core: radix sequence must be a palindrome");
   constexpr int m = fft_npass<N, R>(), NJ = N / R, K = N / 3;
-  constexpr int r0 = fft_rad<N, R>(0);
-  double2* const B[2] = {X, Y};
+  constexpr int rl = fft_rad<N, R>(m - 1), Ll = fft_len<N, R>(m - 1), dl = Ll / rl;
+  static_assert(dl == 1 && rl == R, "nl_core: the last pass must have radix R and stride 1");
   const int t = grp.tid(), f = t / NJ, j = t % NJ;
   const bool act = t < 3 * NJ;
+  double2* Xf = X + (act ? f : 0) * N;
   double2 v[R];
-  // synthesis pass 0 (NS = 1, no twiddles): retained inputs only, the rest is zero (R10)
-  if (act) {
-    const double2* in = X + f * N;
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      const int i = core_idx<N, R, r0>(j, s);
-      v[s] = (i <= K || i >= N - K) ? in[swz(i)] : make_double2(0.0, 0.0);
-    }
-    core_math<N, R, 0, +1>(v, j, TW);
-    if constexpr (m > 1) core_store<N, R, 0>(v, Y + f * N, j);
-  }
-  if constexpr (m > 1) {
-    grp.sync();
-    core_inverse<N, R, 1>(v, B, f, j, act, TW, grp);
-  }
-  // products on the grid: v1 shared through B[m%2] (not read by the last synthesis pass);
-  // the last synthesis pass has radix r0 (palindrome) and the index set of analysis pass 0
-  double2* VB = B[m % 2];
+  core_inverse<N, R, 0>(v, Xf, j, act, TW, grp);
+  // grid products (R1, R10): the last synthesis pass left the grid values of positions j R + s in
+  // registers; v1 is shared with the v2x / h threads through V
   if (act && f == 0) {
 #pragma unroll
-    for (int s = 0; s < R; ++s) VB[swz(core_idx<N, R, r0>(j, s))] = v[s];
+    for (int s = 0; s < R; ++s) V[swz(j * R + s)] = v[s];
   }
   grp.sync();
   if (act) {
@@ -397,25 +397,20 @@ __device__ __forceinline__ void nl_core(double2* X, double2* Y, const double2* T
     } else {
 #pragma unroll
       for (int s = 0; s < R; ++s) {
-        const double2 v1 = VB[swz(core_idx<N, R, r0>(j, s))];
+        const double2 v1 = V[swz(j * R + s)];
         v[s] = make_double2(v1.x * v[s].x, v1.y * v[s].y);
       }
     }
-    // analysis pass 0: radix r0, NS = 1, operands already in registers
-    core_math<N, R, 0, -1>(v, j, TW);
-    double2* out = B[(m == 1) ? 0 : (m - 1) % 2] + f * N;
-    if constexpr (m > 1) {
-      core_store<N, R, 0>(v, out, j);
-    } else {
+    // analysis pass m-1: stride 1, no twiddles, operands already in registers
+    dftR<R, -1>(v);
 #pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int o = core_idx<N, R, r0>(j, s);
-        if (o <= K || o >= N - K) out[swz(o)] = v[s];
-      }
+    for (int s = 0; s < R; ++s) {
+      const int e = j * R + s;
+      if (m > 1 || e <= K || e >= N - K) Xf[swz(e)] = v[s];
     }
   }
   grp.sync();
-  if constexpr (m > 1) core_forward<N, R, 1>(v, B, f, j, act, TW, grp);
+  core_forward<N, R, m - 2>(v, Xf, j, act, TW, grp);
 }
 
 // N-eval input / output of one retained entry in the swizzled layout of nl_core

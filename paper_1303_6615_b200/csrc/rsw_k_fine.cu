@@ -25,33 +25,51 @@ static cudaError_t set_smem(KernelT k, size_t bytes) {
 
 
 
-template <int N, int R, int T>
+// k_fine: NPG pair-groups of TG threads per CTA (named barriers 1..NPG, or the whole CTA when
+// NPG = 1); group g advances slices 2(NPG b + g), +1.  Shared memory: per group the N-eval buffer W
+// (3N) and the v1 copy V (N), then the tables shared by the groups (twiddle bases, ETDRK4 / Strang
+// coefficients, geometry).  TMEM: the groups' thread-private state slots interleave (TBLK layout).
+template <int N, int R, int TG, int NPG>
 struct FineLayout {  // dynamic shared memory of k_fine (double2 units first, then doubles)
-  static constexpr int K = N / 3, KP = K + 1;
-  static constexpr int W = 0, Y = W + 3 * N, TW = Y + 3 * N, CP = TW + fft_tw_size<N, R>(), D = CP + 6 * KP;
-  static constexpr int C0 = 0, GA = C0 + 6 * KP, GP = GA + KP, GQ = GP + KP, ND = GQ + KP;      // double offsets
+  static constexpr int K = N / 3, KP = K + 1, Kc = 2 * K + 1;
+  static constexpr int GS = 4 * N;  // per-group stride: W (3N) + V (N)
+  static constexpr int TW = NPG * GS, CP = TW + fft_tw_size<N, R>(), D = CP + 6 * KP;
+  static constexpr int ND = 9 * KP;  // C0 [6][KP], GA, GP, GQ
   static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
-  static constexpr int NCOL = tmem_cols_pow2<FineTmem<N, T>::COLS>();
+  static constexpr int T = NPG * TG, OMAX = (Kc + TG - 1) / TG, BLKS = (T / 32 + 3) / 4;
+  static constexpr int NCOL = tmem_cols_pow2<BLKS * OMAX * 36>();
+  static_assert(BLKS * OMAX * 36 <= 512, "k_fine: TMEM state does not fit");
 };
 
-template <int N, int R, int T, int SCHEME, bool LIN>
-__global__ void __launch_bounds__(T) k_fine(const double* u_in, double* u_out, int n_slices, int m_steps,
-                                            double h, const FineTab tab) {
-  using LY = FineLayout<N, R, T>;
+template <int N, int R, int TG, int NPG, int SCHEME, bool LIN>
+__global__ void __launch_bounds__(NPG * TG) k_fine(const double* u_in, double* u_out, int n_slices, int m_steps,
+                                                   double h, const FineTab tab) {
+  using LY = FineLayout<N, R, TG, NPG>;
   constexpr int NH = N / 2 + 1;
   extern __shared__ double2 smem[];
   __shared__ uint32_t tslot;
   if ((threadIdx.x >> 5) == 0) tmem_alloc<LY::NCOL>(&tslot);
-  const FineSmemTab st_ = stage_fine_tables<N, R, T>(smem + LY::TW, smem + LY::CP,
-                                                     reinterpret_cast<double*>(smem + LY::D), tab, threadIdx.x, T);
+  const FineSmemTab st_ = stage_fine_tables<N, R, LY::T>(smem + LY::TW, smem + LY::CP,
+                                                         reinterpret_cast<double*>(smem + LY::D), tab, threadIdx.x, LY::T);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const int sA = 2 * blockIdx.x, sB = sA + 1;
+  const int g = (NPG == 1) ? 0 : (int)threadIdx.x / TG;
+  const int sA = 2 * (NPG * blockIdx.x + g), sB = sA + 1;
   const size_t L = (size_t)3 * NH * 2;
-  fine_pair_run<N, R, T, SCHEME, LIN>(CtaGroup(), smem + LY::W, smem + LY::Y, st_, tslot, tab.g, u_in + sA * L,
-                                      (sB < n_slices) ? u_in + sB * L : nullptr, u_out + sA * L,
-                                      (sB < n_slices) ? u_out + sB * L : nullptr, m_steps, h);
+  if (sA < n_slices) {
+    double2* W = smem + g * LY::GS;
+    const double* uA = u_in + sA * L;
+    const double* uB = (sB < n_slices) ? u_in + sB * L : nullptr;
+    double* oA = u_out + sA * L;
+    double* oB = (sB < n_slices) ? u_out + sB * L : nullptr;
+    if constexpr (NPG == 1)
+      fine_pair_run<N, R, TG, SCHEME, LIN, CtaGroup, true>(CtaGroup(), W, W + 3 * N, st_, tslot, tab.g, uA, uB, oA, oB,
+                                                           m_steps, h);
+    else
+      fine_pair_run<N, R, TG, SCHEME, LIN, NamedGroup, true>(NamedGroup{g * TG, 1 + g, TG}, W, W + 3 * N, st_, tslot,
+                                                             tab.g, uA, uB, oA, oB, m_steps, h);
+  }
   tmem_fence_before();
   __syncthreads();
   if ((threadIdx.x >> 5) == 0) {
@@ -61,18 +79,18 @@ __global__ void __launch_bounds__(T) k_fine(const double* u_in, double* u_out, i
 }
 
 
-template <int N, int R>
+template <int N, int R, int NPG>
 static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
                                   const FineTab& tab, cudaStream_t st) {
-  constexpr int T = core_threads<N, R>();
-  const int grid = (S + 1) / 2;
-  const size_t sm = FineLayout<N, R, T>::bytes;
+  constexpr int TG = core_threads<N, R>();
+  const int grid = ((S + 1) / 2 + NPG - 1) / NPG;
+  const size_t sm = FineLayout<N, R, TG, NPG>::bytes;
   cudaError_t e;
 #define LAUNCH_FINE(SC, LN)                                                  \
   {                                                                           \
-    auto kfn = k_fine<N, R, T, SC, LN>;                                       \
+    auto kfn = k_fine<N, R, TG, NPG, SC, LN>;                                 \
     if ((e = set_smem(kfn, sm)) != cudaSuccess) return e;                     \
-    kfn<<<grid, T, sm, st>>>(in, out, S, m, h, tab);                          \
+    kfn<<<grid, NPG * TG, sm, st>>>(in, out, S, m, h, tab);                   \
   }
   if (scheme == 0 && !lin) LAUNCH_FINE(0, false)
   else if (scheme == 0 && lin) LAUNCH_FINE(0, true)
@@ -87,11 +105,11 @@ static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double
 template <int N>
 static cudaError_t launch_fine_n(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
                                  const FineTab& tab, cudaStream_t st) {
-  if constexpr (N == 1024 || N == 512) {  // measurement knob: the radix-16 plans (16.4.16, 16.2.16)
+  if constexpr (N == 256 || N == 512) {  // measurement knob: radix 16 (256 = 16.16, 512 = 2.16.16)
     static const char* e = getenv("RSW_FINE_R16");
-    if (e && atoi(e) == 1) return launch_fine_nr<N, 16>(scheme, lin, in, out, S, m, h, tab, st);
+    if (e && atoi(e) == 1) return launch_fine_nr<N, 16, 1>(scheme, lin, in, out, S, m, h, tab, st);
   }
-  return launch_fine_nr<N, fine_radix<N>()>(scheme, lin, in, out, S, m, h, tab, st);
+  return launch_fine_nr<N, fine_radix<N>(), fine_groups<N>()>(scheme, lin, in, out, S, m, h, tab, st);
 }
 
 

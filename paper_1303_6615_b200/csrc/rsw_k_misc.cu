@@ -37,9 +37,9 @@ __device__ __forceinline__ void stage_geom_tw(const ModeGeom& g, const double2* 
 }
 
 template <int N, int R, int T>
-struct MiscLayout {  // X, Y (swizzled), packed twiddles, C / A [3][Kc], then doubles GA, GP, GQ
+struct MiscLayout {  // X (swizzled), V (v1 copy of nl_core), twiddle bases, C / A [3][Kc], then GA, GP, GQ
   static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
-  static constexpr int X = 0, Y = 3 * N, TW = 6 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc, D = A + 3 * Kc;
+  static constexpr int X = 0, Y = 3 * N, TW = 4 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc, D = A + 3 * Kc;
   static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * 3 * KP;
 };
 

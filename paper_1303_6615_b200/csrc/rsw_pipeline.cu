@@ -75,12 +75,10 @@ __device__ __forceinline__ bool group_barrier(unsigned* bar, unsigned P, unsigne
 // latency-critical sweep wins issue slots over the throughput-bound fine solves).  The tcgen05
 // allocation limits a cooperative launch to one CTA per SM, so the roles are warp-specialized inside
 // the CTA rather than spread over CTAs.
-// smallest palindromic radix whose FFT core fits in `threads` threads
+// smallest radix whose FFT core fits in `threads` threads
 template <int N>
 __host__ __device__ constexpr int radix_for_threads(int threads) {
-  return (3 * (N / 4) <= threads && fft_palindrome<N, 4>()) ? 4
-       : (3 * (N / 8) <= threads && fft_palindrome<N, 8>()) ? 8
-       : (3 * (N / 16) <= threads && fft_palindrome<N, 16>()) ? 16 : 32;
+  return (3 * (N / 4) <= threads) ? 4 : (3 * (N / 8) <= threads) ? 8 : (3 * (N / 16) <= threads) ? 16 : 32;
 }
 template <int N, int TC, int NPC, int RC0>
 __host__ __device__ constexpr int pipe_split() {  // sample pairs a coarse sub-CTA evaluates concurrently
