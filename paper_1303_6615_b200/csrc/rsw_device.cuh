@@ -378,7 +378,12 @@ __device__ __forceinline__ void nl_core(double2* X, double2* V, const double2* T
   constexpr int m = fft_npass<N, R>(), NJ = N / R, K = N / 3;
   constexpr int rl = fft_rad<N, R>(m - 1), Ll = fft_len<N, R>(m - 1), dl = Ll / rl;
   static_assert(dl == 1 && rl == R, "nl_core: the last pass must have radix R and stride 1");
-  const int t = grp.tid(), f = t / NJ, j = t % NJ;
+  // at R = 16 the thread index is laundered so the per-element swizzled offsets are recomputed
+  // (integer pipe) in every call instead of being hoisted out of the callers' time-step loops and
+  // spilled (n = 1024 fine kernel at 168 registers); smaller R keep them (latency-bound n <= 256)
+  int t = grp.tid();
+  if constexpr (R >= 16) asm volatile("mov.b32 %0, %0;" : "+r"(t));
+  const int f = t / NJ, j = t % NJ;
   const bool act = t < 3 * NJ;
   double2* Xf = X + (act ? f : 0) * N;
   double2 v[R];

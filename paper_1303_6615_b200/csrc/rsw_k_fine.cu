@@ -105,9 +105,10 @@ static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double
 template <int N>
 static cudaError_t launch_fine_n(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
                                  const FineTab& tab, cudaStream_t st) {
-  if constexpr (N == 256 || N == 512) {  // measurement knob: radix 16 (256 = 16.16, 512 = 2.16.16)
-    static const char* e = getenv("RSW_FINE_R16");
-    if (e && atoi(e) == 1) return launch_fine_nr<N, 16, 1>(scheme, lin, in, out, S, m, h, tab, st);
+  if constexpr (N == 256 || N == 512) {  // measurement knob: RSW_FINE_R = 4 or 16
+    static const char* e = getenv("RSW_FINE_R");
+    if (e && atoi(e) == 16) return launch_fine_nr<N, 16, 1>(scheme, lin, in, out, S, m, h, tab, st);
+    if (e && atoi(e) == 4) return launch_fine_nr<N, 4, 1>(scheme, lin, in, out, S, m, h, tab, st);
   }
   return launch_fine_nr<N, fine_radix<N>(), fine_groups<N>()>(scheme, lin, in, out, S, m, h, tab, st);
 }
