@@ -254,6 +254,38 @@ def main():
                  "frac_of_measured": fine_tf / measured_peak, "ms_per_launch": fine_ms,
                  "flops_per_launch": fine_flops_iter, "slices": local_slices, "steps": w.m_fine}
 
+    # ---- the fine sweep of the large configuration (C5, BASELINE configs[4]: 4096 slices, n = 1024,
+    # 391 ETDRK4 steps), sharded over the ranks: the throughput-bound kernel whose scaling the north
+    # star targets (the C3 time-to-solution above is bounded by the serial coarse chain).  Max over
+    # ranks of the per-launch CUDA-event time, L2 flushed before each launch.
+    w5 = inputs.C5
+    p5 = rsw.Params(w5.eps, w5.F, w5.mu, w5.n)
+    s5 = w5.n_slices // world
+    u5 = torch.from_numpy(inputs.random_states(w5.n, s5, seed=rank, kmax=64)).cuda()
+    o5 = torch.empty_like(u5)
+    f5 = []
+    for r in range(4):
+        flush.fill_(1.0)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rsw.fine_propagate(p5, u5, w5.dT, w5.dt, 0, out=o5)
+        e1.record(stream)
+        e1.synchronize()
+        if r:
+            f5.append(e0.elapsed_time(e1))
+    t = torch.tensor([statistics.median(f5)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    c5_ms = float(t.item())
+    c5_tf = w5.n_slices * w5.m_fine * rsw.flops_per_unit(w5.n, "etdrk4") / (c5_ms * 1e-3) / 1e12
+    fine_c5 = {"workload": "C5 fine sweep (ETDRK4, n=1024, 391 steps)", "slices_total": w5.n_slices,
+               "slices_per_rank": s5, "ms_max_over_ranks": c5_ms,
+               "slice_steps_per_s": w5.n_slices * w5.m_fine / (c5_ms * 1e-3), "achieved_tflops": c5_tf,
+               "frac": c5_tf / (nominal_peak * world), "frac_of_measured": c5_tf / (measured_peak * world),
+               "kernel": "k_fine<1024,16,192,2> (two pair-groups per CTA)"}
+    del u5, o5
+
     # ---- e2e: same solve through the C-ABI from pinned host buffers, H2D + D2H inside the region
     U_host = torch.empty(U.shape, dtype=torch.float64).pin_memory()
     e2e = []
@@ -291,6 +323,7 @@ def main():
             "fine_kernel_slice_steps_per_s": local_slices * w.m_fine / (fine_ms * 1e-3) * world,
             "roofline": roof,
             "roofline_fine": roof_fine,
+            "fine_c5": fine_c5,
             "clocks": clk.summary(),
             "e2e": {"value": total_slice_steps / (e2e_ms * 1e-3), "unit": UNIT, "ms": e2e_ms,
                     "h2d_bytes_per_step": u0_host.numel() * 8, "d2h_bytes_per_step": U_host.numel() * 8},

@@ -194,7 +194,7 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
       const double as = kap < 0 ? -sGA[ak] : sGA[ak];
       double2 u[3];
       to_prim(as, sGP[ak], sGQ[ak], c0v[o], u);
-      put_input_z<N>(W, full_index(kap, N), (double)kap, u);
+      put_input_z<N, R>(W, full_index(kap, N), (double)kap, u);
     }
   }
   tmem_wait_st();
@@ -225,7 +225,7 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
         double2 nn[3];
         if (!LIN && valid) {
           double2 nh[3];
-          get_output_z<N>(W, kf, (double)kap, invN, nh);
+          get_output_z<N, R>(W, kf, (double)kap, invN, nh);
           to_eigen(as, p, q, nh, nn);
         } else {
 #pragma unroll
@@ -303,7 +303,7 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
         if (!LIN && valid) {
           double2 u[3];
           to_prim(as, p, q, x, u);
-          put_input_z<N>(W, kf, (double)kap, u);
+          put_input_z<N, R>(W, kf, (double)kap, u);
         }
       }
       tmem_wait_st();
@@ -476,7 +476,7 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       c[1] = cadd(y0, cmuli(b0));
       c[2] = cadd(cmulc(yp, pA), cmuli(bp));
       to_prim(as, GP[ak], GQ[ak], c, u);
-      put_input_z<N>(Xh, full_index(kap, N), (double)kap, u);
+      put_input_z<N, R>(Xh, full_index(kap, N), (double)kap, u);
     }
     if (SPLIT > 1) hg.sync(); else grp.sync();
     STAMP(1)
@@ -489,8 +489,8 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       const double as = kap < 0 ? -GA[ak] : GA[ak];
       const double p = GP[ak], q = GQ[ak];
       double2 zp[3], zm[3], na[3], nb[3], ea[3], eb[3];
-      get_output_z<N>(Xh, full_index(kap, N), (double)kap, invN, zp);
-      get_output_z<N>(Xh, full_index(-kap, N), (double)(-kap), invN, zm);
+      get_output_z<N, R>(Xh, full_index(kap, N), (double)kap, invN, zp);
+      get_output_z<N, R>(Xh, full_index(-kap, N), (double)(-kap), invN, zm);
 #pragma unroll
       for (int f = 0; f < 3; ++f) {  // unpack: N_A(κ) = (Z(κ) + conj Z(-κ))/2, N_B = (Z - conj Z(-κ))/(2i)
         const double2 zc = cconj(zm[f]);

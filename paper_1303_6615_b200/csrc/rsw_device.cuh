@@ -207,7 +207,20 @@ struct NamedGroup {
   __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory"); }
 };
 
-__host__ __device__ __forceinline__ constexpr int swz(int i) { return (i & ~7) | ((i ^ (i >> 3) ^ (i >> 6)) & 7); }
+// Padded storage of the FFT buffers: element e of a field lives at fpad(e) = e + e / R (one pad slot
+// per R elements), fields FS = N + N/R apart; nl_core's buffer is X[3 FS] followed by V[FS].  The
+// pad is conflict-free for every pass of the plans below at R >= 8 (quarter-warp of 8 threads on 8
+// distinct 16-byte bank groups; tools/fft_model.py) and it is additive over disjoint bit fields:
+// a butterfly's elements e0 + d s have e0 and d s in disjoint bits, so fpad(e0 + d s) =
+// fpad(e0) + fpad(d s) — one base register per butterfly plus compile-time immediate offsets.
+template <int R>
+__host__ __device__ __forceinline__ constexpr int fpad(int e) {
+  return e + (e >> (R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : R == 16 ? 4 : 5));
+}
+template <int N, int R>
+__host__ __device__ constexpr int fft_fs() { return N + N / R; }
+template <int N, int R>
+__host__ __device__ constexpr int nl_buf() { return 4 * fft_fs<N, R>(); }  // X (3 fields) + V
 
 // ---------------------------------------------------------------------------------------------
 // In-place mixed-radix FFT core (nl_core).  Plan for (N, R): pass 0 has radix rem = N / R^a when
@@ -223,9 +236,8 @@ __host__ __device__ __forceinline__ constexpr int swz(int i) { return (i & ~7) |
 // Because a butterfly writes back exactly the elements it read, a pass needs no barrier between its
 // loads and its stores: ONE barrier per pass and a single buffer of 3N values (plus N for the v1
 // copy of the products).  Thread t of the group owns field f = t / (N/R) and column j = t mod (N/R);
-// its butterflies in a pass of radix r are b = j + i N/R, i < R/r.  Storage index swz(e): conflict-
-// free for every pass pattern of these plans (tools/fft_model.py), and the identity inside each
-// aligned group of 8 (so the natural-order epilogue accesses stay conflict-free).
+// its butterflies in a pass of radix r are b = j + i N/R, i < R/r.  Storage: the padded layout fpad
+// (below), conflict-free for every pass of these plans at R >= 8.
 // ---------------------------------------------------------------------------------------------
 template <int N, int R>
 __host__ __device__ constexpr int fft_npass() {
@@ -322,17 +334,18 @@ __device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* Xf, int j
 #pragma unroll
     for (int i = 0; i < R / r; ++i) {
       const int b = j + i * NJ, e0 = fft_elem0<N, R, p>(b);
+      const double2* xb = Xf + fpad<R>(e0);
 #pragma unroll
       for (int s = 0; s < r; ++s) {
         const int e = e0 + d * s;
-        if constexpr (p == 0) v[i * r + s] = (e <= K || e >= N - K) ? Xf[swz(e)] : make_double2(0.0, 0.0);  // R10
-        else v[i * r + s] = Xf[swz(e)];
+        if constexpr (p == 0) v[i * r + s] = (e <= K || e >= N - K) ? xb[fpad<R>(d * s)] : make_double2(0.0, 0.0);  // R10
+        else v[i * r + s] = xb[fpad<R>(d * s)];
       }
       dftR<r, +1>(&v[i * r]);
       if constexpr (p < m - 1) {
         apply_twiddles<r, true>(&v[i * r], TW[fft_tw_off<N, R>(p) + (b % d)]);  // ω_L^{+s k1}
 #pragma unroll
-        for (int s = 0; s < r; ++s) Xf[swz(e0 + d * s)] = v[i * r + s];
+        for (int s = 0; s < r; ++s) Xf[fpad<R>(e0) + fpad<R>(d * s)] = v[i * r + s];
       }
     }
   }
@@ -353,14 +366,15 @@ __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j
 #pragma unroll
       for (int i = 0; i < R / r; ++i) {
         const int b = j + i * NJ, e0 = fft_elem0<N, R, p>(b);
+        double2* xb = Xf + fpad<R>(e0);
 #pragma unroll
-        for (int s = 0; s < r; ++s) v[i * r + s] = Xf[swz(e0 + d * s)];
+        for (int s = 0; s < r; ++s) v[i * r + s] = xb[fpad<R>(d * s)];
         apply_twiddles<r, false>(&v[i * r], TW[fft_tw_off<N, R>(p) + (b % d)]);  // e^{-2πi s k1/L}
         dftR<r, -1>(&v[i * r]);
 #pragma unroll
         for (int s = 0; s < r; ++s) {
           const int e = e0 + d * s;
-          if (p > 0 || e <= K || e >= N - K) Xf[swz(e)] = v[i * r + s];
+          if (p > 0 || e <= K || e >= N - K) xb[fpad<R>(d * s)] = v[i * r + s];
         }
       }
     }
@@ -369,30 +383,30 @@ __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j
   }
 }
 
-// N(u) core on the packed pair: X = double2[3][N] (swizzled) holds the retained spectra of
-// (v1, i κ v2, h) on entry and the retained spectra of (v1²/2, v1 v2x, h v1) (unnormalised) on exit;
-// V = double2[N] scratch for the v1 copy.  2m barriers (m = passes), the last one on exit.
+// N(u) core on the packed pair: X = double2[nl_buf<N, R>()] — fields (v1, i κ v2, h) at f FS in the
+// padded layout, then V (the v1 copy) at 3 FS — holds the retained spectra of (v1, iκ v2, h) on entry
+// and the retained spectra of (v1²/2, v1 v2x, h v1) (unnormalised) on exit.  The second argument is
+// unused (kept for the callers' layouts, which reserve >= nl_buf entries from X).  2m barriers
+// (m = passes), the last one on exit.
 template <int N, int R, int T, class GRP = CtaGroup>
-__device__ __forceinline__ void nl_core(double2* X, double2* V, const double2* TW, const GRP& grp = GRP()) {
+__device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const double2* TW, const GRP& grp = GRP()) {
   static_assert(T >= 3 * (N / R), "nl_core: T must cover 3 N/R field-columns");
   constexpr int m = fft_npass<N, R>(), NJ = N / R, K = N / 3;
   constexpr int rl = fft_rad<N, R>(m - 1), Ll = fft_len<N, R>(m - 1), dl = Ll / rl;
   static_assert(dl == 1 && rl == R, "nl_core: the last pass must have radix R and stride 1");
-  // at R = 16 the thread index is laundered so the per-element swizzled offsets are recomputed
-  // (integer pipe) in every call instead of being hoisted out of the callers' time-step loops and
-  // spilled (n = 1024 fine kernel at 168 registers); smaller R keep them (latency-bound n <= 256)
-  int t = grp.tid();
-  if constexpr (R >= 16) asm volatile("mov.b32 %0, %0;" : "+r"(t));
+  const int t = grp.tid();
   const int f = t / NJ, j = t % NJ;
   const bool act = t < 3 * NJ;
-  double2* Xf = X + (act ? f : 0) * N;
+  constexpr int FS = fft_fs<N, R>();
+  double2* Xf = X + (act ? f : 0) * FS;
+  double2* V = X + 3 * FS + fpad<R>(j * R);
   double2 v[R];
   core_inverse<N, R, 0>(v, Xf, j, act, TW, grp);
   // grid products (R1, R10): the last synthesis pass left the grid values of positions j R + s in
   // registers; v1 is shared with the v2x / h threads through V
   if (act && f == 0) {
 #pragma unroll
-    for (int s = 0; s < R; ++s) V[swz(j * R + s)] = v[s];
+    for (int s = 0; s < R; ++s) V[fpad<R>(s)] = v[s];
   }
   grp.sync();
   if (act) {
@@ -402,34 +416,37 @@ __device__ __forceinline__ void nl_core(double2* X, double2* V, const double2* T
     } else {
 #pragma unroll
       for (int s = 0; s < R; ++s) {
-        const double2 v1 = V[swz(j * R + s)];
+        const double2 v1 = V[fpad<R>(s)];
         v[s] = make_double2(v1.x * v[s].x, v1.y * v[s].y);
       }
     }
     // analysis pass m-1: stride 1, no twiddles, operands already in registers
     dftR<R, -1>(v);
+    double2* xb = Xf + fpad<R>(j * R);
 #pragma unroll
     for (int s = 0; s < R; ++s) {
       const int e = j * R + s;
-      if (m > 1 || e <= K || e >= N - K) Xf[swz(e)] = v[s];
+      if (m > 1 || e <= K || e >= N - K) xb[fpad<R>(s)] = v[s];
     }
   }
   grp.sync();
   core_forward<N, R, m - 2>(v, Xf, j, act, TW, grp);
 }
 
-// N-eval input / output of one retained entry in the swizzled layout of nl_core
-template <int N>
+// N-eval input / output of one retained entry in the padded layout of nl_core
+template <int N, int R>
 __device__ __forceinline__ void put_input_z(double2* X, int k_full, double kap, const double2* u) {
-  const int i = swz(k_full);
+  constexpr int FS = fft_fs<N, R>();
+  const int i = fpad<R>(k_full);
   X[i] = u[0];
-  X[N + i] = cmuli(cscale(u[1], kap));
-  X[2 * N + i] = u[2];
+  X[FS + i] = cmuli(cscale(u[1], kap));
+  X[2 * FS + i] = u[2];
 }
-template <int N>
+template <int N, int R>
 __device__ __forceinline__ void get_output_z(const double2* X, int k_full, double kap, double invN, double2* nh) {
-  const int i = swz(k_full);
-  const double2 Q0 = cscale(X[i], invN), Q1 = cscale(X[N + i], invN), Q2 = cscale(X[2 * N + i], invN);
+  constexpr int FS = fft_fs<N, R>();
+  const int i = fpad<R>(k_full);
+  const double2 Q0 = cscale(X[i], invN), Q1 = cscale(X[FS + i], invN), Q2 = cscale(X[2 * FS + i], invN);
   nh[0] = cmulmi(cscale(Q0, kap));  // -iκ Q0
   nh[1] = make_double2(-Q1.x, -Q1.y);
   nh[2] = cmulmi(cscale(Q2, kap));  // -iκ Q2

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h,
 #pragma unroll
       for (int al = 0; al < 3; ++al) c[al] = S1[al * Kc + j];
       to_prim(kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak), __ldg(tab.g.p + ak), __ldg(tab.g.q + ak), c, u);
-      put_input_z<N>(W, full_index(kap, N), (double)kap, u);
+      put_input_z<N, R>(W, full_index(kap, N), (double)kap, u);
     }
     __syncthreads();
     for (int st = 0; st < 2; ++st) {
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h,
         const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
         const double p = __ldg(tab.g.p + ak), q = __ldg(tab.g.q + ak);
         double2 nh[3], nn[3], x[3];
-        get_output_z<N>(W, kf, (double)kap, invN, nh);
+        get_output_z<N, R>(W, kf, (double)kap, invN, nh);
         to_eigen(as, p, q, nh, nn);
 #pragma unroll
         for (int al = 0; al < 3; ++al) {
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h,
         if (st == 0) {
           double2 u[3];
           to_prim(as, p, q, x, u);
-          put_input_z<N>(W, kf, (double)kap, u);
+          put_input_z<N, R>(W, kf, (double)kap, u);
         }
       }
       __syncthreads();

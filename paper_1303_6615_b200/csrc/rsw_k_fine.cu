@@ -32,7 +32,7 @@ static cudaError_t set_smem(KernelT k, size_t bytes) {
 template <int N, int R, int TG, int NPG>
 struct FineLayout {  // dynamic shared memory of k_fine (double2 units first, then doubles)
   static constexpr int K = N / 3, KP = K + 1, Kc = 2 * K + 1;
-  static constexpr int GS = 4 * N;  // per-group stride: W (3N) + V (N)
+  static constexpr int GS = nl_buf<N, R>();  // per-group stride: the N-eval buffer (padded fields + V)
   static constexpr int TW = NPG * GS, CP = TW + fft_tw_size<N, R>(), D = CP + 6 * KP;
   static constexpr int ND = 9 * KP;  // C0 [6][KP], GA, GP, GQ
   static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
@@ -64,10 +64,10 @@ __global__ void __launch_bounds__(NPG * TG) k_fine(const double* u_in, double* u
     double* oA = u_out + sA * L;
     double* oB = (sB < n_slices) ? u_out + sB * L : nullptr;
     if constexpr (NPG == 1)
-      fine_pair_run<N, R, TG, SCHEME, LIN, CtaGroup, true>(CtaGroup(), W, W + 3 * N, st_, tslot, tab.g, uA, uB, oA, oB,
+      fine_pair_run<N, R, TG, SCHEME, LIN, CtaGroup, true>(CtaGroup(), W, nullptr, st_, tslot, tab.g, uA, uB, oA, oB,
                                                            m_steps, h);
     else
-      fine_pair_run<N, R, TG, SCHEME, LIN, NamedGroup, true>(NamedGroup{g * TG, 1 + g, TG}, W, W + 3 * N, st_, tslot,
+      fine_pair_run<N, R, TG, SCHEME, LIN, NamedGroup, true>(NamedGroup{g * TG, 1 + g, TG}, W, nullptr, st_, tslot,
                                                              tab.g, uA, uB, oA, oB, m_steps, h);
   }
   tmem_fence_before();

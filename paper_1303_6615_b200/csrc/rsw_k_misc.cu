@@ -37,9 +37,9 @@ __device__ __forceinline__ void stage_geom_tw(const ModeGeom& g, const double2* 
 }
 
 template <int N, int R, int T>
-struct MiscLayout {  // X (swizzled), V (v1 copy of nl_core), twiddle bases, C / A [3][Kc], then GA, GP, GQ
+struct MiscLayout {  // X (nl_core buffer), twiddle bases, C / A [3][Kc], then GA, GP, GQ
   static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
-  static constexpr int X = 0, Y = 3 * N, TW = 4 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc, D = A + 3 * Kc;
+  static constexpr int X = 0, Y = 0, TW = nl_buf<N, R>(), C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc, D = A + 3 * Kc;
   static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * 3 * KP;
 };
 
@@ -69,14 +69,14 @@ __global__ void __launch_bounds__(T) k_nonlinear(const double* u_in, double* out
 #pragma unroll
     for (int al = 0; al < 3; ++al) c[al] = C[al * Kc + j];
     to_prim(kap < 0 ? -GA[ak] : GA[ak], GP[ak], GQ[ak], c, u);
-    put_input_z<N>(X, full_index(kap, N), (double)kap, u);
+    put_input_z<N, R>(X, full_index(kap, N), (double)kap, u);
   }
   __syncthreads();
   nl_core<N, R, T>(X, smem + LY::Y, smem + LY::TW);
   for (int j = threadIdx.x; j < Kc; j += T) {
     const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
     double2 nh[3], nn[3];
-    get_output_z<N>(X, full_index(kap, N), (double)kap, invN, nh);
+    get_output_z<N, R>(X, full_index(kap, N), (double)kap, invN, nh);
     to_eigen(kap < 0 ? -GA[ak] : GA[ak], GP[ak], GQ[ak], nh, nn);
 #pragma unroll
     for (int al = 0; al < 3; ++al) C[al * Kc + j] = nn[al];
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
       c[1] = C[Kc + j];                    // α=0
       c[2] = cmulc(C[2 * Kc + j], ph[o]);  // α=+1: e^{-iωτ}
       to_prim(kap < 0 ? -GA[ak] : GA[ak], GP[ak], GQ[ak], c, u);
-      put_input_z<N>(X, full_index(kap, N), (double)kap, u);
+      put_input_z<N, R>(X, full_index(kap, N), (double)kap, u);
     }
   }
   __syncthreads();
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
         const double as = kap < 0 ? -GA[ak] : GA[ak];
         const double p = GP[ak], q = GQ[ak];
         double2 nh[3], nn[3];
-        get_output_z<N>(X, kf, (double)kap, invN, nh);
+        get_output_z<N, R>(X, kf, (double)kap, invN, nh);
         to_eigen(as, p, q, nh, nn);
         A[j] = caxpy(wm, cmulc(nn[0], ph[o]), A[j]);                  // α=-1: e^{-iωτ}
         A[Kc + j] = caxpy(wm, nn[1], A[Kc + j]);                      // α=0
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
           c[1] = C[Kc + j];
           c[2] = cmulc(C[2 * Kc + j], phn[o]);
           to_prim(as, p, q, c, u);
-          put_input_z<N>(X, kf, (double)kap, u);
+          put_input_z<N, R>(X, kf, (double)kap, u);
         }
       }
       ph[o] = phn[o];

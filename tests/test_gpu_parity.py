@@ -54,6 +54,18 @@ def test_fine_sizes(rsw_gpu, orc, scheme, n, eps, mu, dt, steps):
     assert err.max() < TOL, err
 
 
+@pytest.mark.parametrize("S", [1, 5, 7])
+def test_fine_pair_groups_tail(rsw_gpu, orc, S):
+    """n = 1024 runs two pair-groups per CTA: S = 1 (one group with a dummy slice), 5 (the second
+    CTA's second group idle), 7 (last pair with a dummy slice) against the oracle."""
+    n, eps, mu, dt = 1024, 1e-4, 1e-6, 2e-5
+    u = inputs.random_states(n, S, seed=13, kmax=64)
+    got = to_np(rsw_gpu.fine_propagate(P(rsw_gpu, eps, 1.0, mu, n), dev(u), 2 * dt, dt, 0))
+    ref = orc.fine_propagate(u, eps, 1.0, mu, n, 2 * dt, dt, 0)
+    err = rel_l2(got, ref, n)
+    assert err.max() < TOL, err
+
+
 @pytest.mark.parametrize("scheme", [0, 1, 2])
 def test_fine_linear_only(rsw_gpu, orc, scheme):
     n = 128
