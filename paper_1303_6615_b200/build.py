@@ -47,17 +47,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
         objdir = os.path.join(HERE, "build")
         os.makedirs(objdir, exist_ok=True)
-        jobs = []
+        jobs, objs = [], []
+        hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
+        hdr_t = max(hdr_t, os.path.getmtime(os.path.join(INCLUDE, "rsw.h")))
         for src in SOURCES:
             obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
-            cmd = compile_cmd(os.path.join(CSRC, src), obj)
+            objs.append(obj)
+            srcp = os.path.join(CSRC, src)
+            if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(srcp)):
+                continue  # object newer than its source and every shared header
+            cmd = compile_cmd(srcp, obj)
             if verbose:
                 print(" ".join(cmd))
             jobs.append((subprocess.Popen(cmd), cmd, obj))
         for proc, cmd, _ in jobs:
             if proc.wait() != 0:
                 raise subprocess.CalledProcessError(proc.returncode, cmd)
-        cmd = link_cmd([o for _, _, o in jobs], LIB + ".tmp")
+        cmd = link_cmd(objs, LIB + ".tmp")
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

@@ -88,42 +88,82 @@ __global__ void __launch_bounds__(T) k_nonlinear(const double* u_in, double* out
 // ---------------------------------------------------------------------------------------------
 // K3: averaged nonlinearity for pairs of independent states (same sample m for both), register
 // FFT core; ascending m:  acc = Σ_{m=1}^{M-1} w_m P+_m N(P-_m c),  P±_m = diag(e^{±iατ_m ω}) (eigen).
-// Each thread owns the modes j = t + o T for every sample: the next sample's phases are loaded
-// into registers before the FFT so their L2 latency hides behind it.
+// Each thread owns the modes j = t + o T for every sample; their state c and accumulator acc live
+// in the thread's private TMEM slots (columns o*24 + {c: 0..11, acc: 12..23}, lane quarter = warp
+// mod 4, column block = warp / 4), which takes their read-modify-write traffic off the shared-memory
+// pipe (the binding resource: ncu 81% of peak wavefronts with them in smem).  The next sample's
+// phases are loaded into registers before the FFT so their L2 latency hides behind it.
 // ---------------------------------------------------------------------------------------------
+#ifndef RSW_AVG_MINB
+#define RSW_AVG_MINB 1
+#endif
+template <int N, int T>
+struct AvgTmem {
+  static constexpr int Kc = 2 * (N / 3) + 1, OMAX = (Kc + T - 1) / T, BLKS = (T / 32 + 3) / 4;
+  static constexpr int NCOL = tmem_cols_pow2<BLKS * OMAX * 24>();
+  static_assert(BLKS * OMAX * 24 <= 512, "k_avg_states: TMEM slots do not fit");
+};
+
 template <int N, int R, int T>
-__global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* out, int n_states, int M,
+struct AvgLayout {  // X (nl_core buffer; also stages C in and acc out), twiddle bases, then GA, GP, GQ
+  static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
+  static_assert(3 * Kc <= nl_buf<N, R>(), "AvgLayout: staging does not fit in X");
+  static constexpr int X = 0, TW = nl_buf<N, R>(), D = TW + fft_tw_size<N, R>();
+  static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * 3 * KP;
+};
+
+template <int N, int R, int T>
+__global__ void __launch_bounds__(T, RSW_AVG_MINB) k_avg_states(const double* u_in, double* out, int n_states, int M,
                                                   const AvgTab tab) {
-  using LY = MiscLayout<N, R, T>;
-  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1, KP = K + 1, OMAX = (Kc + T - 1) / T;
+  using LY = AvgLayout<N, R, T>;
+  using TM = AvgTmem<N, T>;
+  constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1, KP = K + 1, OMAX = TM::OMAX;
   constexpr double invN = 1.0 / N;
   extern __shared__ double2 smem[];
+  __shared__ uint32_t tslot;
   double2* X = smem + LY::X;
-  double2* C = smem + LY::C;
-  double2* A = smem + LY::A;
+  double2* C = X;  // staging of the eigen state, then of the accumulator
   double* GA = reinterpret_cast<double*>(smem + LY::D);
   double* GP = GA + KP;
   double* GQ = GP + KP;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<TM::NCOL>(&tslot);
   stage_geom_tw<N, R, T>(tab.g, tab.tw, smem + LY::TW, GA, GP, GQ);
   const int sA = 2 * blockIdx.x, sB = sA + 1;
   const size_t L = (size_t)3 * NH * 2;
   load_pair_eigen<N, T>(u_in + sA * L, (sB < n_states) ? u_in + sB * L : nullptr, tab.g, C);
-  for (int i = threadIdx.x; i < 3 * Kc; i += T) A[i] = make_double2(0.0, 0.0);
+  tmem_fence_before();
   __syncthreads();
+  tmem_fence_after();
+  const uint32_t tb = tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * OMAX * 24);
   double2 ph[OMAX];
+  {
+    double2 cc[OMAX][3];
 #pragma unroll
-  for (int o = 0; o < OMAX; ++o) {  // prologue for m = 1
-    const int j = threadIdx.x + o * T;
-    if (j < Kc) {
-      const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
-      ph[o] = __ldg(tab.phase + (size_t)1 * KP + ak);  // e^{iωτ_1}
-      double2 c[3], u[3];
-      c[0] = cmul(C[j], ph[o]);            // α=-1: e^{+iωτ}
-      c[1] = C[Kc + j];                    // α=0
-      c[2] = cmulc(C[2 * Kc + j], ph[o]);  // α=+1: e^{-iωτ}
-      to_prim(kap < 0 ? -GA[ak] : GA[ak], GP[ak], GQ[ak], c, u);
-      put_input_z<N, R>(X, full_index(kap, N), (double)kap, u);
+    for (int o = 0; o < OMAX; ++o) {
+      const int j = threadIdx.x + o * T;
+#pragma unroll
+      for (int al = 0; al < 3; ++al) cc[o][al] = (j < Kc) ? C[al * Kc + j] : make_double2(0.0, 0.0);
     }
+    __syncthreads();  // C read before X receives the first N-eval input
+    const double2 z[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+#pragma unroll
+    for (int o = 0; o < OMAX; ++o) {  // prologue for m = 1
+      const int j = threadIdx.x + o * T;
+      tmem_st3(tb + o * 24, cc[o]);
+      tmem_st3(tb + o * 24 + 12, z);
+      if (j < Kc) {
+        const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+        ph[o] = __ldg(tab.phase + (size_t)1 * KP + ak);  // e^{iωτ_1}
+        double2 c[3], u[3];
+        c[0] = cmul(cc[o][0], ph[o]);   // α=-1: e^{+iωτ}
+        c[1] = cc[o][1];                // α=0
+        c[2] = cmulc(cc[o][2], ph[o]);  // α=+1: e^{-iωτ}
+        to_prim(kap < 0 ? -GA[ak] : GA[ak], GP[ak], GQ[ak], c, u);
+        put_input_z<N, R>(X, full_index(kap, N), (double)kap, u);
+      }
+    }
+    tmem_wait_st();
   }
   __syncthreads();
   for (int m = 1; m <= M - 1; ++m) {
@@ -134,11 +174,14 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
       const int kap = kappa_of(j < Kc ? j : 0, K), ak = kap < 0 ? -kap : kap;
       phn[o] = (j < Kc && m + 1 <= M - 1) ? __ldg(tab.phase + (size_t)(m + 1) * KP + ak) : make_double2(1.0, 0.0);
     }
-    nl_core<N, R, T>(X, smem + LY::Y, smem + LY::TW);
+    nl_core<N, R, T>(X, nullptr, smem + LY::TW);
     const double wm = __ldg(tab.w + m);
 #pragma unroll
     for (int o = 0; o < OMAX; ++o) {
       const int j = threadIdx.x + o * T;
+      double2 cc[3], acc[3];
+      tmem_ld3(tb + o * 24, cc);
+      tmem_ld3(tb + o * 24 + 12, acc);
       if (j < Kc) {
         const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
         const int kf = full_index(kap, N);
@@ -147,23 +190,42 @@ __global__ void __launch_bounds__(T) k_avg_states(const double* u_in, double* ou
         double2 nh[3], nn[3];
         get_output_z<N, R>(X, kf, (double)kap, invN, nh);
         to_eigen(as, p, q, nh, nn);
-        A[j] = caxpy(wm, cmulc(nn[0], ph[o]), A[j]);                  // α=-1: e^{-iωτ}
-        A[Kc + j] = caxpy(wm, nn[1], A[Kc + j]);                      // α=0
-        A[2 * Kc + j] = caxpy(wm, cmul(nn[2], ph[o]), A[2 * Kc + j]);  // α=+1: e^{+iωτ}
+        acc[0] = caxpy(wm, cmulc(nn[0], ph[o]), acc[0]);  // α=-1: e^{-iωτ}
+        acc[1] = caxpy(wm, nn[1], acc[1]);                // α=0
+        acc[2] = caxpy(wm, cmul(nn[2], ph[o]), acc[2]);   // α=+1: e^{+iωτ}
         if (m + 1 <= M - 1) {
           double2 c[3], u[3];
-          c[0] = cmul(C[j], phn[o]);
-          c[1] = C[Kc + j];
-          c[2] = cmulc(C[2 * Kc + j], phn[o]);
+          c[0] = cmul(cc[0], phn[o]);
+          c[1] = cc[1];
+          c[2] = cmulc(cc[2], phn[o]);
           to_prim(as, p, q, c, u);
           put_input_z<N, R>(X, kf, (double)kap, u);
         }
       }
+      tmem_st3(tb + o * 24 + 12, acc);
       ph[o] = phn[o];
     }
+    tmem_wait_st();
     __syncthreads();
   }
-  store_pair_prim<N, T>(A, tab.g, out + sA * L, (sB < n_states) ? out + sB * L : nullptr);
+  // accumulator -> C[α][j] staging in X (all N-eval reads are done), then store
+#pragma unroll
+  for (int o = 0; o < OMAX; ++o) {
+    const int j = threadIdx.x + o * T;
+    double2 acc[3];
+    tmem_ld3(tb + o * 24 + 12, acc);
+    if (j < Kc) {
+#pragma unroll
+      for (int al = 0; al < 3; ++al) C[al * Kc + j] = acc[al];
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  store_pair_prim<N, T>(C, tab.g, out + sA * L, (sB < n_states) ? out + sB * L : nullptr);
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc<TM::NCOL>(tslot);
+  }
 }
 
 
@@ -199,7 +261,7 @@ template <int N>
 static cudaError_t launch_avg_n(const double* in, double* out, int S, int M, const AvgTab& tab, cudaStream_t st) {
   constexpr int R = fine_radix<N>(), T = core_threads<N, R>();
   auto kfn = k_avg_states<N, R, T>;
-  constexpr size_t sm = MiscLayout<N, R, T>::bytes;
+  constexpr size_t sm = AvgLayout<N, R, T>::bytes;
   cudaError_t e = set_smem(kfn, sm);
   if (e != cudaSuccess) return e;
   kfn<<<(S + 1) / 2, T, sm, st>>>(in, out, S, M, tab);
