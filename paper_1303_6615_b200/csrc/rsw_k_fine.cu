@@ -79,10 +79,10 @@ __global__ void __launch_bounds__(NPG * TG) k_fine(const double* u_in, double* u
 }
 
 
-template <int N, int R, int NPG>
+template <int N, int R, int NPG, int TMUL = 1>
 static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
                                   const FineTab& tab, cudaStream_t st) {
-  constexpr int TG = core_threads<N, R>();
+  constexpr int TG = TMUL * core_threads<N, R>();
   const int grid = ((S + 1) / 2 + NPG - 1) / NPG;
   const size_t sm = FineLayout<N, R, TG, NPG>::bytes;
   cudaError_t e;
@@ -109,6 +109,19 @@ static cudaError_t launch_fine_n(int scheme, bool lin, const double* in, double*
     static const char* e = getenv("RSW_FINE_R");
     if (e && atoi(e) == 16) return launch_fine_nr<N, 16, 1>(scheme, lin, in, out, S, m, h, tab, st);
     if (e && atoi(e) == 4) return launch_fine_nr<N, 4, 1>(scheme, lin, in, out, S, m, h, tab, st);
+    if (e && atoi(e) == 82) return launch_fine_nr<N, 8, 1, 2>(scheme, lin, in, out, S, m, h, tab, st);  // 2x threads
+  }
+  if constexpr (N >= 64 && N <= 256) {
+    // latency regime (at most ~2 pairs per SM, e.g. C3's 256 pairs): twice the threads per pair (the
+    // extra warps split the mode loops and fill the schedulers): C3 3.16 -> 2.90 ms; throughput
+    // regime keeps 3N/R threads (C3-size 4736 slices: 17.9 vs 22.0 ms)
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        sms = 148;
+    }
+    if ((S + 1) / 2 <= 2 * sms) return launch_fine_nr<N, fine_radix<N>(), 1, 2>(scheme, lin, in, out, S, m, h, tab, st);
   }
   return launch_fine_nr<N, fine_radix<N>(), fine_groups<N>()>(scheme, lin, in, out, S, m, h, tab, st);
 }

@@ -30,6 +30,9 @@
 #ifndef RSW_PIPE_COARSE_THREADS
 #define RSW_PIPE_COARSE_THREADS 288  // coarse sub-CTA: three 96-thread parts evaluate three sample pairs at once
 #endif
+#ifndef RSW_PIPE_FINE_TMUL
+#define RSW_PIPE_FINE_TMUL 1  // threads per fine group = TMUL x 3N/R
+#endif
 #ifndef RSW_PIPE_FINE_GROUPS
 #define RSW_PIPE_FINE_GROUPS 1  // fine worker groups per CTA (two slowed the sweeps on C3)
 #endif
@@ -350,7 +353,7 @@ template <int N, int NOWN, int NPC, int FSCHEME>
 static cudaError_t launch_pipe_nf(const PipeArgs& a, int grid, size_t* out, cudaStream_t st) {
   constexpr int RC = coarse_radix<N>();
   constexpr int TC = RSW_PIPE_COARSE_THREADS > coarse_threads<N>() ? RSW_PIPE_COARSE_THREADS : coarse_threads<N>();
-  constexpr int RF = fine_radix<N>(), TG = core_threads<N, RF>();
+  constexpr int RF = fine_radix<N>(), TG = RSW_PIPE_FINE_TMUL * core_threads<N, RF>();
   constexpr int CPG = (FineTmem<N, TG>::COLS + 31) / 32 * 32;
   constexpr int NPG = RSW_PIPE_FINE_GROUPS * CPG <= 512 ? RSW_PIPE_FINE_GROUPS : 512 / CPG;
   using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG>;

@@ -54,6 +54,20 @@ def test_fine_sizes(rsw_gpu, orc, scheme, n, eps, mu, dt, steps):
     assert err.max() < TOL, err
 
 
+@pytest.mark.parametrize("n", [64, 256])
+def test_fine_throughput_layout(rsw_gpu, orc, n):
+    """n <= 256 with more than 2 pairs per SM runs 3N/R threads per pair (fewer pairs: twice that);
+    601 slices (301 pairs, the last with a dummy slice) take the throughput layout."""
+    S = 601
+    u = inputs.random_states(n, S, seed=17, kmax=min(32, n // 3))
+    eps, mu, dt = 1e-2, 1e-4, 2e-4
+    got = to_np(rsw_gpu.fine_propagate(P(rsw_gpu, eps, 1.0, mu, n), dev(u), 2 * dt, dt, 0))
+    idx = np.r_[0:4, 297:305, S - 4:S]  # both layouts' tails and the dummy-slice pair
+    ref = orc.fine_propagate(u[idx], eps, 1.0, mu, n, 2 * dt, dt, 0)
+    err = rel_l2(got[idx], ref, n)
+    assert err.max() < TOL, err
+
+
 @pytest.mark.parametrize("S", [1, 5, 7])
 def test_fine_pair_groups_tail(rsw_gpu, orc, S):
     """n = 1024 runs two pair-groups per CTA: S = 1 (one group with a dummy slice), 5 (the second
