@@ -31,7 +31,7 @@
 #define RSW_PIPE_COARSE_THREADS 288  // coarse sub-CTA: three 96-thread parts evaluate three sample pairs at once
 #endif
 #ifndef RSW_PIPE_FINE_TMUL
-#define RSW_PIPE_FINE_TMUL 1  // threads per fine group = TMUL x 3N/R
+#define RSW_PIPE_FINE_TMUL 2  // threads per fine group = TMUL x 3N/R
 #endif
 #ifndef RSW_PIPE_FINE_GROUPS
 #define RSW_PIPE_FINE_GROUPS 1  // fine worker groups per CTA (two slowed the sweeps on C3)
