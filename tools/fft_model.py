@@ -4,17 +4,18 @@ Checks, in numpy, for a radix plan and a per-thread value count R:
   * the index / twiddle formulas: inverse of a natural-order spectrum lands in a digit-reversed grid
     order, pointwise products in that order, the conjugate-transposed passes bring the result back
     to natural order (compared with numpy.fft);
-  * shared-memory bank conflicts of every pass for a given swizzle (16-byte accesses: a quarter
-    warp is conflict-free iff the 8 swizzled indices are distinct mod 8).
-Usage: python tools/fft_model.py 1024 16 16,16,4
+  * shared-memory bank conflicts of every pass in the padded layout of nl_core (element e of field f
+    at f (N + N/R) + e + e/R; 16-byte accesses: a quarter warp is conflict-free iff its 8 slot
+    indices are distinct mod 8), over the 3 N/R threads of the three fields.
+Usage: python tools/fft_model.py 1024 16 4,16,16
 """
 import sys
 
 import numpy as np
 
 
-def swz(i):
-    return (i & ~7) | ((i ^ (i >> 3) ^ (i >> 6)) & 7)
+def fpad(e, R):
+    return e + e // R
 
 
 def passes(N, plan):
@@ -70,30 +71,29 @@ def forward_inplace(x, N, R, plan, sign=-1):
     return x
 
 
-def conflicts(N, R, plan, T_field_base=0):
-    NJ = N // R
-    worst = 0
+def conflicts(N, R, plan):
+    NJ, FS, T = N // R, N + N // R, 3 * (N // R)
+    worst = 1
     for p, (r, L, d) in enumerate(passes(N, plan)):
         for i in range(R // r):
             for s in range(r):
-                for q0 in range(0, NJ, 8):  # quarter warps (NJ multiple of 8)
+                for q0 in range(0, T, 8):  # quarter warps over the field-major thread ids
                     ids = []
-                    for j in range(q0, min(q0 + 8, NJ)):
-                        b = j + i * NJ
-                        idx, _ = butterfly_elems(b, r, L, d)
-                        ids.append(swz(idx[s]) % 8)
-                    c = max(ids.count(v) for v in set(ids))
-                    worst = max(worst, c)
-                    if c > 1:
+                    for t in range(q0, min(q0 + 8, T)):
+                        f, j = divmod(t, NJ)
+                        idx, _ = butterfly_elems(j + i * NJ, r, L, d)
+                        ids.append((f * FS + fpad(idx[s], R)) % 8)
+                    c = max(ids.count(v) for v in ids)
+                    if c > worst:
                         print(f"  pass {p} (r={r}, L={L}, d={d}) i={i} s={s} quarter {q0}: {c}-way")
-                        break
+                    worst = max(worst, c)
     return worst
 
 
 def main():
     N = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
     R = int(sys.argv[2]) if len(sys.argv) > 2 else 16
-    plan = [int(t) for t in sys.argv[3].split(",")] if len(sys.argv) > 3 else [16, 16, 4]
+    plan = [int(t) for t in sys.argv[3].split(",")] if len(sys.argv) > 3 else [4, 16, 16]
     rng = np.random.default_rng(0)
     a = rng.standard_normal(N) + 1j * rng.standard_normal(N)
     b = rng.standard_normal(N) + 1j * rng.standard_normal(N)
