@@ -263,27 +263,32 @@ def main():
     s5 = w5.n_slices // world
     u5 = torch.from_numpy(inputs.random_states(w5.n, s5, seed=rank, kmax=64)).cuda()
     o5 = torch.empty_like(u5)
-    f5 = []
-    for r in range(4):
-        flush.fill_(1.0)
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rsw.fine_propagate(p5, u5, w5.dT, w5.dt, 0, out=o5)
-        e1.record(stream)
-        e1.synchronize()
-        if r:
-            f5.append(e0.elapsed_time(e1))
-    t = torch.tensor([statistics.median(f5)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    c5_ms = float(t.item())
-    c5_tf = w5.n_slices * w5.m_fine * rsw.flops_per_unit(w5.n, "etdrk4") / (c5_ms * 1e-3) / 1e12
-    fine_c5 = {"workload": "C5 fine sweep (ETDRK4, n=1024, 391 steps)", "slices_total": w5.n_slices,
-               "slices_per_rank": s5, "ms_max_over_ranks": c5_ms,
-               "slice_steps_per_s": w5.n_slices * w5.m_fine / (c5_ms * 1e-3), "achieved_tflops": c5_tf,
-               "frac": c5_tf / (nominal_peak * world), "frac_of_measured": c5_tf / (measured_peak * world),
-               "kernel": "k_fine<1024,16,192,2> (two pair-groups per CTA)"}
+    def c5_sweep(scheme):
+        f5 = []
+        for r in range(4):
+            flush.fill_(1.0)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rsw.fine_propagate(p5, u5, w5.dT, w5.dt, scheme, out=o5)
+            e1.record(stream)
+            e1.synchronize()
+            if r:
+                f5.append(e0.elapsed_time(e1))
+        t = torch.tensor([statistics.median(f5)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        c5_ms = float(t.item())
+        c5_tf = w5.n_slices * w5.m_fine * rsw.flops_per_unit(w5.n, "etdrk4" if scheme == 0 else "strang") \
+            / (c5_ms * 1e-3) / 1e12
+        return {"workload": f"C5 fine sweep ({'ETDRK4' if scheme == 0 else 'Strang'}, n=1024, 391 steps)",
+                "slices_total": w5.n_slices, "slices_per_rank": s5, "ms_max_over_ranks": c5_ms,
+                "slice_steps_per_s": w5.n_slices * w5.m_fine / (c5_ms * 1e-3), "achieved_tflops": c5_tf,
+                "frac": c5_tf / (nominal_peak * world), "frac_of_measured": c5_tf / (measured_peak * world),
+                "kernel": "k_fine<1024,16,192,2> (two pair-groups per CTA)"}
+
+    fine_c5 = c5_sweep(0)
+    fine_c5["strang"] = c5_sweep(1)  # BASELINE configs[4]: "Strang-splitting variant also run"
     del u5, o5
 
     # ---- e2e: same solve through the C-ABI from pinned host buffers, H2D + D2H inside the region
