@@ -233,7 +233,19 @@ def main():
         roof = {"bound": "alu", "kernel": "k_fine (ETDRK4 fine sweep)", "achieved": fine_flops_iter / (fine_ms * 1e-3) / 1e12,
                 "flops_per_launch": fine_flops_iter,
                 "share_of_step": statistics.median(s["fine_ms"] for s in stats) / ms_max}
-    roof.update({"peak": nominal_peak, "unit": "TFLOP/s", "frac": roof["achieved"] / nominal_peak, "traffic": None,
+    traffic = {}
+    try:  # DRAM bytes per launch from the committed ncu capture of this same workload (profiles/)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh)
+    except (OSError, ValueError):
+        pass
+
+    def traffic_of(key):
+        t = traffic.get(key)
+        return None if not t else t["read"] + t["write"]
+
+    roof_traffic = traffic_of("k_parareal_pipe C3 5 iterations") if (pipelined and w.name == "C3" and iters == 5) else None
+    roof.update({"peak": nominal_peak, "unit": "TFLOP/s", "frac": roof["achieved"] / nominal_peak, "traffic": roof_traffic,
                  "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz",
                  "peak_measured_dfma": measured_peak, "frac_of_measured": roof["achieved"] / measured_peak})
     coarse_ms = statistics.median(s["coarse_ms"] for s in stats)
@@ -291,7 +303,8 @@ def main():
                 "slices_total": w5.n_slices, "slices_per_rank": s5, "ms_max_over_ranks": c5_ms,
                 "slice_steps_per_s": w5.n_slices * w5.m_fine / (c5_ms * 1e-3), "achieved_tflops": c5_tf,
                 "frac": c5_tf / (nominal_peak * world), "frac_of_measured": c5_tf / (measured_peak * world),
-                "kernel": "k_fine<1024,16,192,2> (two pair-groups per CTA)"}
+                "kernel": "k_fine<1024,16,192,2> (two pair-groups per CTA)",
+                "traffic": traffic_of("k_fine C5 4096 slices ETDRK4") if (scheme == 0 and world == 1) else None}
 
     fine_c5 = c5_sweep(0)
     fine_c5["strang"] = c5_sweep(1)  # BASELINE configs[4]: "Strang-splitting variant also run"

@@ -15,6 +15,7 @@ ap.add_argument("--config", default="C5")
 ap.add_argument("--what", default="fine", choices=["fine", "strang", "avg", "coarse", "parareal"])
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--slices", type=int, default=0)
+ap.add_argument("--iters", type=int, default=2, help="parareal: iterations (the bench runs the config's count)")
 a = ap.parse_args()
 w = inputs.WORKLOADS[a.config]
 p = rsw.Params(w.eps, w.F, w.mu, w.n)
@@ -57,5 +58,5 @@ else:
     u0 = torch.from_numpy(inputs.initial_state(w)).cuda()
     for r in range(a.reps):
         res = rsw.parareal_iterate(p, u0, dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices,
-                                   max_iters=min(w.max_iters, 2), tol=w.tol)
+                                   max_iters=min(w.max_iters, a.iters), tol=w.tol)
         print(res["stats"], res["resid"])
