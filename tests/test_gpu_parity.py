@@ -255,6 +255,29 @@ def test_edge_sizes(rsw_gpu, orc):
     assert empty.shape[0] == 0
 
 
+@pytest.mark.parametrize("schedule", ["bulk", "pipelined"])
+@pytest.mark.parametrize("fault", ["nan", "overflow"])
+def test_divergence_guard_fault_injection(rsw_gpu, schedule, fault):
+    """Fault injection: a NaN in one retained mode of u0, or an amplitude that overflows in
+    the first N-evals, must end the solve with RSW_ERR_DIVERGED (non-finite or > 1e6 residual)
+    under both schedules — never a hang on the pipelined schedule's sentinel hand-off."""
+    w = inputs.C1
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = inputs.initial_state(w)
+    if fault == "nan":
+        u0[2, 3, 0] = np.nan
+    else:
+        u0 = u0 * 1e150
+    sched = rsw_gpu.SCHEDULE_BULK if schedule == "bulk" else rsw_gpu.SCHEDULE_PIPELINED
+    g = rsw_gpu.parareal_iterate(p, dev(u0), dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices,
+                                 max_iters=3, schedule=sched, allow_diverged=True)
+    assert g["status"] == rsw_gpu.RSW_ERR_DIVERGED
+    # the library stays usable after the guard fired
+    ok = rsw_gpu.parareal_iterate(p, dev(inputs.initial_state(w)), dT=w.dT, dt=w.dt, T0=w.T0, M=w.M,
+                                  n_slices=w.n_slices, max_iters=1, schedule=sched)
+    assert ok["status"] == rsw_gpu.RSW_OK and np.isfinite(to_np(ok["U"])).all()
+
+
 @pytest.mark.parametrize("M", [2, 3, 5])
 def test_small_M(rsw_gpu, orc, M):
     """M = 2 (one effective sample), odd M (unpaired last sample)."""
