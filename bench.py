@@ -310,6 +310,35 @@ def main():
     fine_c5["strang"] = c5_sweep(1)  # BASELINE configs[4]: "Strang-splitting variant also run"
     del u5, o5
 
+    # ---- the standalone averaged-nonlinearity batch (C4, BASELINE configs[3]: 4096 states, n = 512,
+    # M = 256) sharded over the ranks ("on 1 GPU and sharded across 8"), max over ranks
+    w4 = inputs.C4
+    p4 = rsw.Params(w4.eps, w4.F, w4.mu, w4.n)
+    s4 = 4096 // world
+    u4 = torch.from_numpy(inputs.random_states(w4.n, s4, seed=100 + rank)).cuda()
+    a4 = []
+    for r in range(4):
+        flush.fill_(1.0)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rsw.averaged_rhs(p4, u4, w4.T0, w4.M)
+        e1.record(stream)
+        e1.synchronize()
+        if r:
+            a4.append(e0.elapsed_time(e1))
+    t = torch.tensor([statistics.median(a4)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    c4_ms = float(t.item())
+    c4_tf = 4096 * (w4.M - 1) * rsw.flops_per_unit(w4.n, "sample") / (c4_ms * 1e-3) / 1e12
+    avg_c4 = {"workload": "C4 averaged-nonlinearity batch (4096 states, n=512, M=256)", "states_total": 4096,
+              "states_per_rank": s4, "ms_max_over_ranks": c4_ms,
+              "sample_evals_per_s": 4096 * (w4.M - 1) / (c4_ms * 1e-3), "achieved_tflops": c4_tf,
+              "frac": c4_tf / (nominal_peak * world), "frac_of_measured": c4_tf / (measured_peak * world),
+              "kernel": "k_avg_states<512,8,192> (state and accumulator in TMEM)"}
+    del u4
+
     # ---- e2e: same solve through the C-ABI from pinned host buffers, H2D + D2H inside the region
     U_host = torch.empty(U.shape, dtype=torch.float64).pin_memory()
     e2e = []
@@ -350,6 +379,7 @@ def main():
             "roofline": roof,
             "roofline_fine": roof_fine,
             "fine_c5": fine_c5,
+            "avg_c4": avg_c4,
             "clocks": clk.summary(),
             "e2e": {"value": total_slice_steps / (e2e_ms * 1e-3), "unit": UNIT, "ms": e2e_ms,
                     "h2d_bytes_per_step": u0_host.numel() * 8, "d2h_bytes_per_step": U_host.numel() * 8},
