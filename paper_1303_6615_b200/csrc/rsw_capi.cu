@@ -306,7 +306,7 @@ struct Chain {
   int scheme, M;
   double dT;
   rsw::AvgTab at;
-  rsw::CoarseArgs ca;
+  rsw::CoarseArgs ca{};
 };
 
 rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, double T0, int M, Workspace* ws,
@@ -621,7 +621,26 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   const char* eg = getenv("RSW_PIPE_GC");
   if (eg) a.GC = std::max(1, atoi(eg));
   while ((Km + 1 + a.GC - 1) / a.GC > 8 || (M / 2 + a.GC - 1) / a.GC > 8) a.GC *= 2;  // <= 8 modes / pairs per CTA
-  CUDA_TRY(rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, 0, &cap, st));
+  // cluster mode (one thread-block cluster per sweep, stage communication over DSMEM; opt-in with
+  // RSW_PIPE_CLUSTER=1): bitwise identical, but slower on B200 — at most 7 clusters of 16 one-CTA-per-SM
+  // CTAs are co-resident (112 of 148 SMs) and 16 CTAs per sweep means 4 sample pairs per SM and stage
+  // (C3: 12.9 us per stage, 50.9 ms per solve, vs 10 us / 38.6 ms with 24-CTA global-memory groups)
+  bool use_cl = false;
+  {
+    const char* ec = getenv("RSW_PIPE_CLUSTER");
+    if ((ec && ec[0] == '1') && !eg && rsw::pipeline_cluster_supported(n, M)) {
+      size_t ccap = 0;
+      if (rsw::launch_parareal_pipe_cl(n, a, cfg->fine_scheme, 0, &ccap, st) == cudaSuccess &&
+          (int)ccap >= rsw::pipeline_cluster_size() * std::min(K + 1, 6)) {
+        use_cl = true;
+        cap = ccap;
+        a.GC = rsw::pipeline_cluster_size();
+      } else {
+        cudaGetLastError();  // a failed capacity query must not poison the next launch
+      }
+    }
+  }
+  if (!use_cl) CUDA_TRY(rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, 0, &cap, st));
   const char* egr = getenv("RSW_PIPE_GRID");
   const int grid = egr ? atoi(egr) : (int)cap;
   if (a.GC > grid) return fail(RSW_ERR_CONFIG, "pipelined schedule: not enough co-resident CTAs");
@@ -671,7 +690,8 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   CUDA_TRY(cudaMemcpyAsync(a.stopk, &stop_init, sizeof(int), cudaMemcpyHostToDevice, st));
   for (int k = 0; k <= K; ++k)  // U^k_0 = u0 for every iteration
     CUDA_TRY(cudaMemcpyAsync(a.Uall + (size_t)k * (S + 1) * L, u0, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
-  CUDA_TRY(rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, grid, nullptr, st));
+  if (use_cl) CUDA_TRY(rsw::launch_parareal_pipe_cl(n, a, cfg->fine_scheme, grid, nullptr, st));
+  else CUDA_TRY(rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, grid, nullptr, st));
   int stopk = 0;
   unsigned wd = 0;
   std::vector<double> res(K + 1, 0.0);
@@ -684,7 +704,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     CUDA_TRY(cudaMemcpy(tr.data(), a.trace, sizeof(unsigned long long) * ntr, cudaMemcpyDeviceToHost));
     const double t0 = (double)tr[0];
     auto ms = [&](unsigned long long t) { return t ? (t - t0) * 1e-6 : -1.0; };
-    fprintf(stderr, "[rsw pipe] grid %d NG %d GC %d npairs %d\n", grid, a.NG, a.GC, a.npairs);
+    fprintf(stderr, "[rsw pipe] grid %d NG %d GC %d npairs %d cluster %d\n", grid, a.NG, a.GC, a.npairs, (int)use_cl);
     for (int k = 0; k <= K; ++k) {
       const unsigned long long* sl = tr.data() + 2 * (K + 1) + (size_t)k * S;
       fprintf(stderr, "[rsw pipe] sweep %d: start %.3f end %.3f | slice 0 %.3f, S/4 %.3f, S/2 %.3f, S-1 %.3f\n", k,

@@ -54,6 +54,11 @@ struct CoarseArgs {
   double* rparts;       // [S][K+1][2] residual partials or null
   int n_end;            // number of chain steps (S)
   unsigned long long* prof;  // optional phase timestamps (CTA 0; RSW_PROFILE_COARSE=1), else null
+  // cluster mode (pipelined sweep on one thread-block cluster, rsw_pipeline.cu): partials and stage
+  // inputs stay in the cluster's shared memory (DSMEM) instead of global memory; cls = 0: off
+  int cls;              // cluster size (CTAs per sweep)
+  double2* plocal;      // this CTA's partial slots [NPC][3][Kc] (shared memory; read remotely by owners)
+  double2* yown;        // this CTA's owned stage-input entries [3][Kc] (shared memory; gathered remotely)
 };
 
 // Pipelined parareal (rsw_pipeline.cu): every iteration's buffers stay resident
@@ -81,6 +86,9 @@ struct PipeArgs {
 };
 bool pipeline_supported(int n);
 cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);
+bool pipeline_cluster_supported(int n, int M);
+int pipeline_cluster_size();
+cudaError_t launch_parareal_pipe_cl(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);
 
 cudaError_t launch_fine(int n, int scheme, bool lin, const double* in, double* out, int S, int m, double h,
                         const FineTab& tab, cudaStream_t st);

@@ -358,6 +358,22 @@ def test_pipelined_group_layouts_bitwise(rsw_gpu, gc, ng, monkeypatch):
     assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
 
 
+@pytest.mark.parametrize("max_iters,tol", [(2, 0.0), (5, 0.3)])
+def test_pipelined_cluster_mode_bitwise(rsw_gpu, max_iters, tol, monkeypatch):
+    """The opt-in cluster mode (one thread-block cluster per sweep, partials and stage inputs over
+    DSMEM, RSW_PIPE_CLUSTER=1) reduces in the same fixed order: bitwise equal to the bulk schedule on
+    C3, also when the tolerance stops it early (abort raised through the cluster's stage barrier)."""
+    w = inputs.C3
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=max_iters, tol=tol)
+    a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    monkeypatch.setenv("RSW_PIPE_CLUSTER", "1")
+    b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
+    assert b["stats"]["pipelined"]
+    assert a["iters"] == b["iters"] and a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
+
+
 def test_pipelined_rejects_unsupported(rsw_gpu):
     w = inputs.C1
     p = P(rsw_gpu, w.eps, w.F, w.mu, 512)
