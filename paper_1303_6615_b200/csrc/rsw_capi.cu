@@ -3,6 +3,7 @@
 // communicator.  Implements include/rsw.h.
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; inert unless a profiler (nsys, ncu) injects its library
 
 #include <cmath>
 #include <complex>
@@ -21,6 +22,15 @@
 using cd = std::complex<double>;
 
 namespace {
+
+// NVTX range for the host-side phases (entry points; per iteration: fine sweep, all-gather, coarse
+// sweep) so a timeline tool shows where a solve spends its time
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 thread_local std::string g_err;
 rsw_status fail(rsw_status s, const std::string& msg) {
@@ -479,6 +489,7 @@ double rsw_flops_per_unit(int32_t n, int32_t which) {
 }
 
 rsw_status rsw_nonlinear(const rsw_params* p, int32_t n_states, const double* u_in, double* out, void* stream) {
+  Nvtx nvtx_("rsw_nonlinear");
   rsw_status s = check_params(p);
   if (s != RSW_OK) return s;
   if (n_states < 0) return fail(RSW_ERR_CONFIG, "n_states < 0");
@@ -495,6 +506,7 @@ rsw_status rsw_nonlinear(const rsw_params* p, int32_t n_states, const double* u_
 
 rsw_status rsw_fine_propagate(const rsw_params* p, int32_t scheme, uint32_t flags, double dT, double dt,
                               int32_t n_slices, const double* u_in, double* u_out, void* stream) {
+  Nvtx nvtx_("rsw_fine_propagate");
   rsw_status s = check_params(p);
   if (s != RSW_OK) return s;
   if (scheme != RSW_FINE_ETDRK4 && scheme != RSW_FINE_STRANG && scheme != RSW_FINE_IFRK4)
@@ -519,6 +531,7 @@ rsw_status rsw_fine_propagate(const rsw_params* p, int32_t scheme, uint32_t flag
 
 rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n_states, const double* u_in,
                             double* rhs_out, void* stream) {
+  Nvtx nvtx_("rsw_averaged_rhs");
   rsw_status s = check_params(p);
   if (s != RSW_OK) return s;
   if (!finite_pos(T0)) return fail(RSW_ERR_CONFIG, "T0 must be finite and > 0");
@@ -539,6 +552,7 @@ rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n
 
 rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, double dT, double T0, int32_t M,
                                 int32_t n_states, const double* u_in, double* u_out, void* stream) {
+  Nvtx nvtx_("rsw_coarse_propagate");
   rsw_status s = check_params(p);
   if (s != RSW_OK) return s;
   if (coarse_scheme != RSW_COARSE_RK4 && coarse_scheme != RSW_COARSE_MIDPOINT &&
@@ -775,6 +789,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
 rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
                                double* resid_hist, int32_t* iters_done, rsw_comm* comm, void* stream,
                                double* F_out, double* G_out, rsw_parareal_stats* stats) {
+  Nvtx nvtx_("parareal_iterate");
   rsw_status s = check_params(p);
   if (s != RSW_OK) return s;
   if (!cfg) return fail(RSW_ERR_CONFIG, "cfg is NULL");
@@ -866,6 +881,7 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   int64_t fine_steps = 0;
   for (int k = 1; k <= cfg->max_iters; ++k) {
     // parfor n: F_n = φ(U^{k-1}_n) on this rank's shard
+    Nvtx nvtx_it("parareal iteration (fine sweep, all-gather, coarse sweep)");
     CUDA_TRY(cudaEventRecord(ev[0], st));
     if (!comm && vworld > 1) {
       // test knob RSW_VIRTUAL_WORLD=P: run the P shards' fine sweeps as separate launches into their
