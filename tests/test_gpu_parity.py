@@ -374,6 +374,29 @@ def test_pipelined_cluster_mode_bitwise(rsw_gpu, max_iters, tol, monkeypatch):
     assert a["iters"] == b["iters"] and a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
 
 
+def test_repeatability_soak(rsw_gpu):
+    """Stand-in for racecheck (compute-sanitizer is unavailable on this pool): the lock-free protocols
+    (pipelined sentinel hand-offs, task claiming, in-place FFT passes with one barrier each, TMEM
+    slots) must give bitwise-identical results run after run under varying timing."""
+    w = inputs.C3
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=2)
+    ref = rsw_gpu.parareal_iterate(p, u0, **kw)
+    for _ in range(8):
+        r = rsw_gpu.parareal_iterate(p, u0, **kw)
+        assert r["resid"] == ref["resid"] and torch.equal(r["U"], ref["U"])
+    p5 = P(rsw_gpu, 1e-4, 1.0, 1e-6, 1024)
+    u5 = dev(inputs.random_states(1024, 600, seed=21, kmax=64))
+    f_ref = rsw_gpu.fine_propagate(p5, u5, 4e-5, 2e-5, 0)
+    p4 = P(rsw_gpu, 1e-3, 1.0, 0.0, 512)
+    u4 = dev(inputs.random_states(512, 600, seed=22))
+    a_ref = rsw_gpu.averaged_rhs(p4, u4, 0.01, 32)
+    for _ in range(4):
+        assert torch.equal(rsw_gpu.fine_propagate(p5, u5, 4e-5, 2e-5, 0), f_ref)
+        assert torch.equal(rsw_gpu.averaged_rhs(p4, u4, 0.01, 32), a_ref)
+
+
 def test_pipelined_rejects_unsupported(rsw_gpu):
     w = inputs.C1
     p = P(rsw_gpu, w.eps, w.F, w.mu, 512)
