@@ -10,7 +10,8 @@
 //  * Spectral state: compact signed wavenumbers j = 0..Kc-1, Kc = 2K+1, K = floor(N/3) (R10):
 //    κ(j) = j for j <= K, j - Kc otherwise.  Eigen coordinates c_α(κ), α = -1, 0, +1 stored
 //    [α+1][j], in the closed-form eigenbasis of L̂(κ).
-//  * Work buffer W: double2[3][N] (fields v1, v2, h) — full spectrum or physical grid.
+//  * Work buffer W: nl_core's padded buffer (fields v1, v2, h at stride N + N/R, then the v1 copy) —
+//    full spectrum or physical grid (digit-reversed order between the transforms).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h,
   constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
   constexpr double invN = 1.0 / N;
   extern __shared__ double2 smem[];
-  double2* W = smem;              // nl_core X (swizzled)
+  double2* W = smem;              // nl_core X (padded layout)
   double2* Yb = W + 3 * N;        // nl_core Y
   double2* TW = Yb + 3 * N;       // packed twiddles
   double2* S1 = TW + fft_tw_size<N, R>();
