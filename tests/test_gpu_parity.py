@@ -209,6 +209,27 @@ def test_parareal_c5_prefix(rsw_gpu, k):
     assert rel_l2(to_np(g["U"])[1:9], ref[1:9], w.n).max() < TOL
 
 
+def test_parareal_c5_full_size_identities(rsw_gpu):
+    """C5 at full size (4096 slices, n = 1024) through properties that hold at any size, on the GPU's
+    own arrays (no oracle input comes from the CUDA path): the k = 0 sweep is the coarse chain
+    U^0_{n+1} = G(U^0_n); the first iteration's update U^1_{n+1} = G(U^1_n) + (F(U^0_n) - G(U^0_n))
+    holds bitwise; U_0 is never modified; r_1 recomputed on the host (R12)."""
+    w = inputs.C5
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = inputs.initial_state(w)
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, want_FG=True, allow_diverged=True)
+    r0 = rsw_gpu.parareal_iterate(p, dev(u0), max_iters=0, **kw)
+    r1 = rsw_gpu.parareal_iterate(p, dev(u0), max_iters=1, **kw)
+    U0, G0 = to_np(r0["U"]), to_np(r0["G"])
+    U1, F0, G1 = to_np(r1["U"]), to_np(r1["F"]), to_np(r1["G"])
+    assert np.isfinite(U1).all()
+    assert np.array_equal(U0[1:], G0)
+    assert np.array_equal(U1[1:], G1 + (F0 - G0))
+    assert np.array_equal(U1[0], u0) and np.array_equal(U0[0], u0)
+    r_host = rel_l2(U0[1:], U1[1:], w.n).max()
+    assert r1["iters"] == 1 and abs(r1["resid"][0] - r_host) <= 1e-10 * r_host
+
+
 # ------------------------------------------------------------------------------ edge cases
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_virtual_world_bitwise(rsw_gpu, world, monkeypatch):
