@@ -209,6 +209,29 @@ def test_parareal_c5_prefix(rsw_gpu, k):
     assert rel_l2(to_np(g["U"])[1:9], ref[1:9], w.n).max() < TOL
 
 
+def test_averaged_rhs_c4_full_size_sampled(rsw_gpu, orc):
+    """C4 at full size (4096 states, n = 512, M = 256) in the bench's launch configuration; the oracle
+    evaluates sampled states one by one (first and last pair, a pair in the middle)."""
+    w = inputs.C4
+    u = inputs.initial_state(w)
+    assert u.shape[0] == 4096
+    got = to_np(rsw_gpu.averaged_rhs(P(rsw_gpu, w.eps, w.F, w.mu, w.n), dev(u), w.T0, w.M))
+    idx = np.array([0, 1, 2047, 2048, 4094, 4095])
+    ref = orc.averaged_rhs(u[idx], w.eps, w.F, w.mu, w.n, w.T0, w.M)
+    assert rel_l2(got[idx], ref, w.n).max() < TOL
+
+
+def test_fine_c5_full_size_sampled(rsw_gpu, orc):
+    """The bench's fine_c5 launch: the C5 fine sweep over 4096 slices (n = 1024, 391 ETDRK4 steps, two
+    pair-groups per CTA); the oracle propagates the first and the last slice one by one."""
+    w = inputs.C5
+    u = inputs.random_states(w.n, w.n_slices, seed=0, kmax=64)
+    got = to_np(rsw_gpu.fine_propagate(P(rsw_gpu, w.eps, w.F, w.mu, w.n), dev(u), w.dT, w.dt, 0))
+    idx = np.array([0, w.n_slices - 1])
+    ref = orc.fine_propagate(u[idx], w.eps, w.F, w.mu, w.n, w.dT, w.dt, 0)
+    assert rel_l2(got[idx], ref, w.n).max() < TOL
+
+
 def test_parareal_c5_full_size_identities(rsw_gpu):
     """C5 at full size (4096 slices, n = 1024) through properties that hold at any size, on the GPU's
     own arrays (no oracle input comes from the CUDA path): the k = 0 sweep is the coarse chain
