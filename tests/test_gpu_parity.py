@@ -99,8 +99,9 @@ def test_fine_in_place(rsw_gpu, orc):
     assert rel_l2(to_np(t), ref, w.n).max() < TOL
 
 
-@pytest.mark.parametrize("n,eps,T0,M", [(64, 1e-2, 0.05, 32), (128, 1e-2, 0.05, 64), (256, 1e-3, 0.01, 128),
-                                        (512, 1e-3, 0.01, 256)])
+@pytest.mark.parametrize("n,eps,T0,M", [(16, 1e-2, 0.05, 8), (32, 1e-2, 0.05, 16), (64, 1e-2, 0.05, 32),
+                                        (128, 1e-2, 0.05, 64), (256, 1e-3, 0.01, 128), (512, 1e-3, 0.01, 256),
+                                        (1024, 1e-4, 0.002, 16)])
 def test_averaged_rhs(rsw_gpu, orc, n, eps, T0, M):
     nb = 3 if n < 512 else 2
     u = inputs.random_states(n, nb, seed=11)
@@ -117,6 +118,16 @@ def test_coarse(rsw_gpu, orc, scheme, wname):
     got = to_np(rsw_gpu.coarse_propagate(P(rsw_gpu, w.eps, w.F, w.mu, w.n), dev(u), w.dT, w.T0, w.M, scheme))
     ref = orc.coarse_propagate(u, w.eps, w.F, w.mu, w.n, w.dT, w.T0, w.M, scheme)
     assert rel_l2(got, ref, w.n).max() < TOL
+
+
+@pytest.mark.parametrize("n", [512, 1024])
+def test_coarse_large_n(rsw_gpu, orc, n):
+    """Coarse step at the radix-16 sizes (512 = 2.16.16, 1024 = 4.16.16) with a small sample count."""
+    u = inputs.random_states(n, 2, seed=31, kmax=64)
+    eps, mu, dT, T0, M = 1e-4, 1e-6, 0.0078125, 0.002, 8
+    got = to_np(rsw_gpu.coarse_propagate(P(rsw_gpu, eps, 1.0, mu, n), dev(u), dT, T0, M, 0))
+    ref = orc.coarse_propagate(u, eps, 1.0, mu, n, dT, T0, M, 0)
+    assert rel_l2(got, ref, n).max() < TOL
 
 
 def _parareal_both(rsw, orc, w, seed=0, max_iters=None, tol=None):
