@@ -117,6 +117,16 @@ def cpu_baseline(w, steps_per_slice: int = 0, target_s: float = 15.0):
                       f"(n={w.n}), {dt:.1f} s wall"}
 
 
+def bench_config(w, args, world, iters=None):
+    """The workload description shared by both arms' JSON lines."""
+    return {"workload": w.name, "n": w.n, "slices": w.n_slices, "fine_steps_per_slice": w.m_fine,
+            "dt_eff": w.dt_eff, "iterations": w.max_iters if iters is None else iters, "M": w.M, "T0": w.T0,
+            "eps": w.eps, "fine_scheme": "ETDRK4" if args.fine_scheme == 0 else "Strang",
+            "parallelism": ("1 GPU, pipelined parareal megakernel" if world == 1 else
+                            f"slices sharded over {world} GPUs, NCCL all-gather, replicated coarse"),
+            "l2": "flushed (256 MB write) before every timed step"}
+
+
 def run_reference(args):
     """--impl reference: the oracle (this tier's reference arm) on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -133,7 +143,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "n": w.n, "slices": w.n_slices, "note": "oracle fine sweep sample"},
+            "config": dict(bench_config(w, args, 1), parallelism="CPU oracle, OpenMP over slices on the host cores",
+                           l2="n/a", note="oracle fine sweep sample"),
             "cpu_baseline": b, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                                        "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -362,12 +373,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "n": w.n, "slices": w.n_slices, "fine_steps_per_slice": w.m_fine,
-                       "dt_eff": w.dt_eff, "iterations": iters, "M": w.M, "T0": w.T0, "eps": w.eps,
-                       "fine_scheme": "ETDRK4" if args.fine_scheme == 0 else "Strang",
-                       "parallelism": (f"1 GPU, pipelined parareal megakernel" if world == 1 else
-                                       f"slices sharded over {world} GPUs, NCCL all-gather, replicated coarse"),
-                       "l2": "flushed (256 MB write) before every timed step"},
+            "config": bench_config(w, args, world, iters),
             "time_to_solution_ms": ms_max,
             "setup_ms": {"first_call_wall": first_ms, "steady_call": ms_max,
                          "one_time_setup_estimate": max(first_ms - ms_max, 0.0)},
