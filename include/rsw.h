@@ -131,7 +131,11 @@ typedef struct {
    max_iters iterations; tol > 0: stop at the first r_k < tol (RSW_NOT_CONVERGED if none).
    Requires 0 <= max_iters <= n_slices and n_slices divisible by the comm world size.
    Testing: with comm == NULL and the environment variable RSW_VIRTUAL_WORLD=P, the fine sweep runs
-   as P separate shard launches (the blocks P ranks would compute); results must be bitwise equal. */
+   as P separate shard launches (the blocks P ranks would compute); results must be bitwise equal.
+   Schedule knobs (results bitwise identical under all of them): RSW_PIPELINE=0 (auto → bulk),
+   RSW_PIPE_GC / RSW_PIPE_NG (coarse sub-CTAs per sweep / concurrent sweeps), RSW_PIPE_CLUSTER=1
+   (one thread-block cluster per sweep, n = 256; slower on B200), RSW_PIPE_TRACE=1
+   (timeline to stderr). */
 rsw_status parareal_iterate(const rsw_params* p, const parareal_config* cfg, const double* u0,
                             double* U, double* resid_hist, int32_t* iters_done, rsw_comm* comm,
                             void* stream);
