@@ -217,9 +217,10 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
         const int kf = full_index(kap, N);
         const uint32_t ts = tb + o * 36;
         double2 s1[3], s0[3], s2[3];
-        tmem_ld3(ts, s1);                                            // S1 (every stage)
-        if (RK && st == 1) tmem_ld3(ts + 12, s0);                    // S0 = E2 c
-        if (RK && st == 2) tmem_ld3(ts + 24, s2);                    // S2 = E2 a - Q Nu (IF: E c)
+        // S1 (every stage), with S0 = E2 c (stage 1) or S2 = E2 a - Q Nu (IF: E c; stage 2) under one wait
+        if (RK && st == 1) tmem_ld3x2(ts, s1, ts + 12, s0);
+        else if (RK && st == 2) tmem_ld3x2(ts, s1, ts + 24, s2);
+        else tmem_ld3(ts, s1);
         const double as = kap < 0 ? -sGA[ak] : sGA[ak];
         const double p = sGP[ak], q = sGQ[ak];
         double2 nn[3];

@@ -497,6 +497,34 @@ __device__ __forceinline__ void tmem_ld3(uint32_t taddr, double2 (&x)[3]) {
   for (int a = 0; a < 3; ++a)
     x[a] = make_double2(__hiloint2double(r[4 * a + 1], r[4 * a]), __hiloint2double(r[4 * a + 3], r[4 * a + 2]));
 }
+// two 3-complex slots with ONE wait (the second load's latency overlaps the first's)
+__device__ __forceinline__ void tmem_ld3x2(uint32_t ta, double2 (&x)[3], uint32_t tb, double2 (&y)[3]) {
+  uint32_t r[12], q[12];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+      : "r"(ta)
+      : "memory");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
+               : "r"(ta + 8)
+               : "memory");
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7])
+      : "r"(tb)
+      : "memory");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11])
+               : "r"(tb + 8)
+               : "memory");
+  tmem_wait_ld();
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    x[a] = make_double2(__hiloint2double(r[4 * a + 1], r[4 * a]), __hiloint2double(r[4 * a + 3], r[4 * a + 2]));
+    y[a] = make_double2(__hiloint2double(q[4 * a + 1], q[4 * a]), __hiloint2double(q[4 * a + 3], q[4 * a + 2]));
+  }
+}
 __device__ __forceinline__ void tmem_st3(uint32_t taddr, const double2 (&x)[3]) {
   uint32_t r[12];
 #pragma unroll
