@@ -450,3 +450,91 @@ def test_standard_parareal_exact_after_S(orc):
     assert rel_l2(r["U"][1:], np.stack(ser[1:]), w.n).max() < 1e-13
     g = orc.coarse_propagate(u0, w.eps, w.F, w.mu, w.n, w.dT, w.T0, w.M, scheme=2)
     assert rel_l2(g, orc.fine_propagate(u0, w.eps, w.F, w.mu, w.n, w.dT, w.dT, scheme=1), w.n) == 0.0
+
+
+# ---------------------------------------------------------------- residual norm and D half-steps
+def _grid(u, n):
+    """Physical grid values of a half-spectrum state (numpy.fft.irfft; û_k = (1/n) Σ u_j e^{-ikx_j})."""
+    c = cplx(np.asarray(u))
+    return np.fft.irfft(c * n, n=n, axis=-1)
+
+
+def test_residual_is_physical_relative_l2(orc):
+    """R12 (Alg.4): r_k = max_{n=1..S} ||U^k_n - U^{k-1}_n||_2 / ||U^k_n||_2 with the L2 norm
+    taken over the 3 fields ON THE GRID.  Recomputed here from the oracle's own iterates (runs with
+    max_iters = k-1 and k) through numpy.fft.irfft, with no Parseval weights: a residual with unit
+    weights, with the denominator U^{k-1}, or with the max taken without slice S fails."""
+    w = inputs.C1
+    n = w.n
+    u0 = inputs.initial_state(w)
+    run = lambda k: orc.parareal(u0, w.eps, w.F, w.mu, n, dT=w.dT, dt=w.dt, T0=w.T0, M=w.M,
+                                 n_slices=w.n_slices, max_iters=k)
+    runs = [run(k) for k in range(0, 5)]
+    argmax_at_S = 0
+    for k in range(1, 5):
+        new, old = _grid(runs[k]["U"][1:], n), _grid(runs[k - 1]["U"][1:], n)
+        num = np.sqrt(((new - old) ** 2).sum(axis=(-1, -2)))
+        den = np.sqrt((new ** 2).sum(axis=(-1, -2)))
+        rs = num / den
+        # the difference U^k - U^{k-1} cancels ~4 digits at k = 4 (r_4 ~ 1.5e-4), so the grid and the
+        # half-spectrum evaluations agree to ~1e-12 relative, not to the 1e-16 of the states
+        assert abs(runs[k]["resid"][k - 1] - rs.max()) <= 1e-11 * rs.max(), (k, runs[k]["resid"], rs)
+        # the history of the longer run agrees with the shorter ones (same iterates)
+        assert np.array_equal(runs[4]["resid"][:k], runs[k]["resid"])
+        argmax_at_S += int(np.argmax(rs) == w.n_slices - 1)
+        # the pin is sharp: the alternative readings differ from r_k by far more than 1e-13
+        den_old = np.sqrt((old ** 2).sum(axis=(-1, -2)))
+        assert abs((num / den_old).max() - rs.max()) > 1e-9 * rs.max()
+    # slice S attains the max in at least one iteration, so dropping it from the max is caught
+    assert argmax_at_S >= 1
+
+
+def test_residual_weights_are_parseval(orc):
+    """The half-spectrum norm the oracle uses equals the grid L2 (Parseval, P:571 / R12): checked on
+    its rel_l2 entry against irfft, for random states with a non-zero k = n/2-adjacent spectrum."""
+    n = 64
+    a = inputs.random_states(n, 2, seed=21)
+    ga, gb = _grid(a[0], n), _grid(a[1], n)
+    ref = np.sqrt(((ga - gb) ** 2).sum() / (gb ** 2).sum())
+    assert abs(orc.rel_l2(n, a[0], a[1]) - ref) < 1e-14 * ref
+    # unit weights would give a different value on these states
+    d = cplx(a[0] - a[1])
+    unit = np.sqrt((np.abs(d) ** 2).sum() / (np.abs(cplx(a[1])) ** 2).sum())
+    assert abs(unit - ref) > 1e-3 * ref
+
+
+def test_coarse_D_half_steps_without_nonlinearity(orc):
+    """Alg.2: G = e^{-(ΔT/ε)L̂} e^{(ΔT/2)D̂} RK4_N̄ e^{(ΔT/2)D̂}.  With ε -> ∞
+    (L̂/ε -> 0) and v1 ≡ 0 (N ≡ 0, so N̄ ≡ 0) the RK4 stage is the identity and G(u) = e^{-μk⁴ΔT} u
+    per mode: a dropped, doubled or un-halved D half-step fails."""
+    n, dT, mu = 32, 0.05, 0.3
+    rng = np.random.default_rng(5)
+    c = np.zeros((3, n // 2 + 1), complex)
+    K = n // 3
+    c[1:, 1:K + 1] = rng.standard_normal((2, K)) + 1j * rng.standard_normal((2, K))
+    c[1:, 0] = rng.standard_normal(2)
+    for scheme in (0, 1):
+        got = cplx(orc.coarse_propagate(pack(c), 1e30, 1.0, mu, n, dT, 0.05, 16, scheme=scheme))
+        k = np.arange(n // 2 + 1)
+        ref = c * np.exp(-mu * k ** 4 * dT)[None, :]
+        assert np.abs(got - ref).max() <= 1e-14 * np.abs(ref).max(), scheme
+
+
+def test_coarse_D_half_steps_around_rk4(orc):
+    """The same composition on a general state: D½ ∘ RK4_N ∘ D½ (ε -> ∞, μ > 0), built from
+    oracle.nonlinear and numpy.exp(-μk⁴ΔT/2).  Putting both half-steps before (or after) the RK4
+    step, or using a full step on one side, changes the result by O(μk⁴ΔT · ΔT N)."""
+    n, dT, mu = 32, 0.05, 0.02
+    u = inputs.random_states(n, 1, seed=14, scale=0.5)[0]
+    k = np.arange(n // 2 + 1)
+    dh = np.exp(-mu * k ** 4 * dT / 2)[None, :, None]
+    f = lambda x: orc.nonlinear(x, 1e30, 1.0, mu, n)
+    ref = dh * _rk4(f, dh * u, dT)
+    got = orc.coarse_propagate(u, 1e30, 1.0, mu, n, dT, 0.05, 16)
+    assert rel_l2(got, ref, n) < 1e-14
+    # the alternative placements differ measurably on this state
+    alt = _rk4(f, dh * dh * u, dT)
+    assert rel_l2(alt, ref, n) > 1e-6
+    refm = dh * ((dh * u) + dT * f(dh * u + 0.5 * dT * f(dh * u)))
+    gotm = orc.coarse_propagate(u, 1e30, 1.0, mu, n, dT, 0.05, 16, scheme=1)
+    assert rel_l2(gotm, refm, n) < 1e-14
