@@ -110,7 +110,7 @@ def cpu_baseline(w, steps_per_slice: int = 0, target_s: float = 15.0):
     steps = steps_per_slice
     dT = steps * w.dt_eff
     t0 = time.perf_counter()
-    oracle.fine_propagate(u, w.eps, w.F, w.mu, w.n, dT, w.dt_eff * (1 + 1e-12), 0)
+    oracle.fine_propagate(u, w.eps, w.F, w.mu, w.n, dT, min(w.dt_eff * (1 + 1e-12), dT), 0)
     dt = time.perf_counter() - t0
     return {"value": cores * steps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"oracle ETDRK4 fine sweep, {cores} slices x {steps} steps of {w.name} "
@@ -150,9 +150,31 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def relaunch_cmd(argv: list[str], gpus: int, port: int) -> list[str] | None:
+    """`bench.py --gpus N` started as a plain process (no WORLD_SIZE in the environment) re-executes
+    itself under torch.distributed.run with N ranks on this node (one per GPU, rendezvous on
+    127.0.0.1); None when no relaunch is needed (N = 1, or already a torchrun rank)."""
+    if gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
 # ---------------------------------------------------------------------------------------------
 def main():
     args = parse()
+    cmd = relaunch_cmd(sys.argv[1:], args.gpus, _free_port())
+    if cmd is not None:
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         return run_reference(args)
     import torch

@@ -13,7 +13,10 @@
  *   double[batch][3][n/2+1][2]  — field-major (v1, v2, h), wavenumber k = 0..n/2, (re, im).
  *   û_k = (1/n) Σ_j u_j e^{-ikx_j}, x_j = 2πj/n (so k = 0 is the mean).  Real fields (R16):
  *   Im(û_0) must be 0.  Dealiasing (R10): modes k > n/3 must be 0 on input and are 0 on output.
- *   Violations return RSW_ERR_CONFIG only where checking is free; otherwise they are undefined.
+ *   parareal_iterate checks u0 on the device (it synchronises anyway) and returns RSW_ERR_CONFIG on a
+ *   violation; rsw_check_states performs the same check for any batch (synchronous).  The purely
+ *   asynchronous entry points (fine / averaged / coarse / nonlinear) do not check: the Python
+ *   binding calls rsw_check_states before them unless told not to.
  *
  * MEMORY: all state pointers are DEVICE pointers (caller-owned, e.g. torch CUDA tensors),
  *   8-byte aligned, on the current device, unless a parameter says "host".
@@ -37,7 +40,10 @@ extern "C" {
 #endif
 
 /* Physical parameters: ε Rossby number, F (Froude = F^{1/2} ε), μ hyperviscosity
-   (D̂(k) = -μk^4, sign R2), n = grid points = FFT length (power of two, 16..1024). */
+   (D̂(k) = -μk^4, sign R2), n = grid points = FFT length (power of two, 16..1024; the cap is
+   reading R18 of DESIGN.md: the largest BASELINE configuration is n = 1024 and the on-chip layout of
+   a state pair — three packed fields plus the product buffer, 4(n + n/16) complex — fits one CTA's
+   shared memory only up to n = 1024 next to the coefficient tables). */
 typedef struct {
   double eps, F, mu;
   int32_t n;
@@ -60,6 +66,10 @@ enum { RSW_COARSE_RK4 = 0, RSW_COARSE_MIDPOINT = 1, RSW_COARSE_STRANG = 2 };
 /* RSW_COARSE_STRANG: standard parareal — the coarse solver is one Strang step of
    size dT on the full equation (Alg.3 with m = 1); T0 and M are then ignored. */
 enum { RSW_FLAG_LINEAR_ONLY = 1u }; /* N ≡ 0: exact-linear test mode only */
+
+/* Layout check (STATE LAYOUT above; R10, R16) of n_states device states u: RSW_ERR_CONFIG if any
+   mode k > n/3 is non-zero or any Im(û_0) != 0, RSW_OK otherwise.  Synchronises `stream`. */
+rsw_status rsw_check_states(const rsw_params* p, int32_t n_states, const double* u, void* stream);
 
 /* N(u) = -(v1 ∂x v1, v1 ∂x v2, ∂x(h v1)) for n_states independent states, evaluated
    pseudo-spectrally (inverse FFT -> pointwise products -> FFT, 2/3 rule).
@@ -97,7 +107,7 @@ rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, doub
 /* Schedule of the parareal iteration (results are bitwise identical; only the order of the work
    differs):
      RSW_SCHEDULE_AUTO      pipelined when supported (single GPU, n in {64, 128, 256}, coarse RK4 or
-                            midpoint), bulk otherwise;
+                            midpoint, enough co-resident CTAs for its coarse groups), bulk otherwise;
      RSW_SCHEDULE_BULK      per iteration: the fine sweep over all slices, then the serial coarse sweep;
      RSW_SCHEDULE_PIPELINED one persistent kernel in which sweep k trails sweep k-1 slice by slice and
                             each fine solve F(U^k_n) starts as soon as U^k_n exists (SURVEY
@@ -130,12 +140,18 @@ typedef struct {
    rank).  resid_hist: HOST double[max_iters].  iters_done: HOST.  tol <= 0: run exactly
    max_iters iterations; tol > 0: stop at the first r_k < tol (RSW_NOT_CONVERGED if none).
    Requires 0 <= max_iters <= n_slices and n_slices divisible by the comm world size.
-   Testing: with comm == NULL and the environment variable RSW_VIRTUAL_WORLD=P, the fine sweep runs
-   as P separate shard launches (the blocks P ranks would compute); results must be bitwise equal.
+   u0 is layout-checked on the device first (RSW_ERR_CONFIG on a violation).  With a communicator
+   (any world size, 1 included) the fine endpoints are exchanged with an in-place ncclAllGather: rank
+   r's block [lo_r, hi_r) lands at offset lo_r of the F array (rsw_shard_range).
+   Testing: with comm == NULL and the environment variable RSW_VIRTUAL_WORLD=P (P <= 16), the fine
+   sweep runs as P separate shard launches into P separate shard buffers, and F is assembled from them
+   with one copy per shard at offset lo_r; results must be bitwise equal to P = 1.
    Schedule knobs (results bitwise identical under all of them): RSW_PIPELINE=0 (auto → bulk),
-   RSW_PIPE_GC / RSW_PIPE_NG (coarse sub-CTAs per sweep / concurrent sweeps), RSW_PIPE_CLUSTER=1
-   (one thread-block cluster per sweep, n = 256; slower on B200), RSW_PIPE_TRACE=1
-   (timeline to stderr). */
+   RSW_PIPE_GC / RSW_PIPE_NG (coarse sub-CTAs per sweep / concurrent sweeps), RSW_PIPE_TRACE=1
+   (timeline to stderr).  The pipelined schedule's dependency waits give up (RSW_ERR_CUDA) only after
+   ~4 s without ANY progress in the kernel (a heartbeat bumped by fine steps and coarse slices).
+   Workspace: calls on different streams are ordered by an event the library records at the end of
+   each call, so they never overlap on the shared per-device workspace. */
 rsw_status parareal_iterate(const rsw_params* p, const parareal_config* cfg, const double* u0,
                             double* U, double* resid_hist, int32_t* iters_done, rsw_comm* comm,
                             void* stream);

@@ -29,7 +29,7 @@ EXPORTS = [
     "rsw_nonlinear", "rsw_fine_propagate", "rsw_averaged_rhs", "rsw_coarse_propagate",
     "parareal_iterate", "parareal_iterate_ex", "rsw_shard_range", "rsw_nccl_unique_id",
     "rsw_comm_init", "rsw_comm_destroy", "rsw_fp64_peak", "rsw_flops_per_unit", "rsw_last_error",
-    "rsw_shutdown",
+    "rsw_shutdown", "rsw_check_states",
 ]
 
 
@@ -82,6 +82,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L = ctypes.CDLL(path)
     vp, dp, i32, u32, dbl = ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_double
     P = ctypes.POINTER(_Params)
+    L.rsw_check_states.argtypes = [P, i32, dp, vp]
     L.rsw_nonlinear.argtypes = [P, i32, dp, dp, vp]
     L.rsw_fine_propagate.argtypes = [P, i32, u32, dbl, dbl, i32, dp, dp, vp]
     L.rsw_averaged_rhs.argtypes = [P, dbl, i32, i32, dp, dp, vp]
@@ -125,37 +126,58 @@ def _state_arg(t, n: int):
     return ctypes.c_void_p(t.data_ptr()), t.numel() // (3 * (n // 2 + 1) * 2)
 
 
-def nonlinear(p: Params, u):
+def check_states(p: Params, u):
+    """Layout check on the device (R10: modes k > n/3 zero; R16: Im û_0 zero); raises RSWError
+    (RSW_ERR_CONFIG) on a violation.  Synchronises the current stream."""
+    a, nb = _state_arg(u, p.n)
+    _check(load().rsw_check_states(ctypes.byref(p._c()), nb, a, _stream()))
+
+
+def nonlinear(p: Params, u, validate: bool = True):
     """N(u) for a batch of states (paper operator table, sign R1)."""
     import torch
     a, nb = _state_arg(u, p.n)
+    if validate:
+        check_states(p, u)
     out = torch.empty_like(u)
     _check(load().rsw_nonlinear(ctypes.byref(p._c()), nb, a, ctypes.c_void_p(out.data_ptr()), _stream()))
     return out
 
 
-def fine_propagate(p: Params, u, dT: float, dt: float, scheme: int = FINE_ETDRK4, flags: int = 0, out=None):
+def fine_propagate(p: Params, u, dT: float, dt: float, scheme: int = FINE_ETDRK4, flags: int = 0, out=None,
+                   validate: bool = True):
+    """F: each state advanced by dT with ceil(dT/dt - 1e-9) ETDRK4 / Strang / IF-RK4 steps (R9)."""
     import torch
     a, nb = _state_arg(u, p.n)
     out = torch.empty_like(u) if out is None else out
-    _state_arg(out, p.n)
+    _, nbo = _state_arg(out, p.n)
+    if nbo != nb or out.device != u.device:
+        raise RSWError(RSW_ERR_CONFIG, "out must hold as many states as u, on the same device")
+    if validate:
+        check_states(p, u)
     _check(load().rsw_fine_propagate(ctypes.byref(p._c()), scheme, flags, dT, dt, nb, a,
                                      ctypes.c_void_p(out.data_ptr()), _stream()))
     return out
 
 
-def averaged_rhs(p: Params, u, T0: float, M: int):
+def averaged_rhs(p: Params, u, T0: float, M: int, validate: bool = True):
+    """N̄ for a batch of states (Alg.1; R4, R5)."""
     import torch
     a, nb = _state_arg(u, p.n)
+    if validate:
+        check_states(p, u)
     out = torch.empty_like(u)
     _check(load().rsw_averaged_rhs(ctypes.byref(p._c()), T0, M, nb, a, ctypes.c_void_p(out.data_ptr()),
                                    _stream()))
     return out
 
 
-def coarse_propagate(p: Params, u, dT: float, T0: float, M: int, scheme: int = COARSE_RK4):
+def coarse_propagate(p: Params, u, dT: float, T0: float, M: int, scheme: int = COARSE_RK4, validate: bool = True):
+    """G for a batch of states (Alg.2; R3, R6)."""
     import torch
     a, nb = _state_arg(u, p.n)
+    if validate:
+        check_states(p, u)
     out = torch.empty_like(u)
     _check(load().rsw_coarse_propagate(ctypes.byref(p._c()), scheme, dT, T0, M, nb, a,
                                        ctypes.c_void_p(out.data_ptr()), _stream()))
@@ -208,9 +230,16 @@ def parareal_iterate(p: Params, u0, *, dT, dt, T0, M, n_slices, max_iters, tol=0
     """Asymptotic parareal (Eq. HMM parareal iteration P:428-430, Alg.4).
     Returns dict(U, resid, iters, status, stats[, F, G])."""
     import torch
-    a, _ = _state_arg(u0, p.n)
+    a, nb = _state_arg(u0, p.n)
+    if u0.dim() != 3 or nb != 1:
+        raise RSWError(RSW_ERR_CONFIG, f"u0 must be one state of shape (3, {p.n // 2 + 1}, 2)")
     shape = (n_slices + 1, 3, p.n // 2 + 1, 2)
-    U = torch.empty(shape, dtype=torch.float64, device=u0.device) if U is None else U
+    if U is None:
+        U = torch.empty(shape, dtype=torch.float64, device=u0.device)
+    else:
+        _state_arg(U, p.n)
+        if tuple(U.shape) != shape or U.device != u0.device:
+            raise RSWError(RSW_ERR_CONFIG, f"U must be a contiguous float64 tensor of shape {shape} on {u0.device}")
     F = torch.empty((n_slices,) + shape[1:], dtype=torch.float64, device=u0.device) if want_FG else None
     G = torch.empty_like(F) if want_FG else None
     resid = (ctypes.c_double * max(max_iters, 1))()

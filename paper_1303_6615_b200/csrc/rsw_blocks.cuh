@@ -100,8 +100,6 @@ __device__ __forceinline__ void store_pair_prim(const double2* C, const ModeGeom
   }
 }
 
-// write prim(x) of every retained entry as the next N-eval input and zero the tail
-
 // ---------------------------------------------------------------------------------------------
 // K1/K2: fine propagator.  One CTA = one pair of slices, state resident in shared memory for all
 // m steps; the only global traffic is one load and one store per slice.
@@ -158,7 +156,8 @@ struct FineTmem {  // TMEM columns of one fine pair-group: per mode slot o, S1 /
 template <int N, int R, int TG, int SCHEME, bool LIN, class GRP, bool TBLK = false>
 __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double2* Y, const FineSmemTab& st_,
                                               uint32_t tcol, const ModeGeom& gg, const double* uA,
-                                              const double* uB, double* oA, double* oB, int m_steps, double h) {
+                                              const double* uB, double* oA, double* oB, int m_steps, double h,
+                                              unsigned* hb = nullptr) {
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, OMAX = FineTmem<N, TG>::OMAX;
   constexpr double invN = 1.0 / N;
   const double2* sCP = st_.CP;
@@ -204,6 +203,7 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
   const int nst = RK ? 4 : 2;
   for (int step = 0; step < m_steps; ++step) {
     const bool last_step = (step == m_steps - 1);
+    if (hb && t == 0 && (step & 7) == 7) atomicAdd(hb, 1u);  // pipelined: heartbeat of the watchdog
     for (int st = 0; st < nst; ++st) {
       if (!LIN) nl_core<N, R, TG>(W, Y, st_.TW, grp);
       // epilogue (this stage's update) fused with the prologue of the next N-eval (rolled when a
@@ -370,11 +370,28 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// bounded spins (pipelined parareal): acquire loads, back off, give up after ~4 s or when another
-// CTA raised the watchdog flag wd (a dependency that never completes is a bug: the kernel then
-// reports an error instead of hanging the GPU)
-__device__ __forceinline__ bool watchdog_expired(unsigned long long t0, unsigned* wd) {
-  if (gtimer() - t0 > 4000000000ull) {
+// bounded spins (pipelined parareal): acquire loads, back off, give up once NOTHING in the kernel has
+// progressed for ~4 s — the heartbeat `hb` (bumped by the fine workers every 8 steps and by every
+// finished coarse slice) did not move — or when another CTA raised the watchdog flag wd.  A
+// dependency that never completes is a bug: the kernel then reports an error instead of hanging the
+// GPU, while a legitimately long wait (one fine solve of many steps) keeps the heartbeat moving.
+struct Watch {
+  unsigned long long t0;
+  unsigned hb;
+};
+__device__ __forceinline__ Watch watch_start(const unsigned* hb) {
+  return Watch{gtimer(), hb ? *(volatile const unsigned*)hb : 0u};
+}
+__device__ __forceinline__ bool watchdog_expired(Watch& w, unsigned* wd, const unsigned* hb) {
+  const unsigned long long now = gtimer();
+  if (hb) {
+    const unsigned h = *(volatile const unsigned*)hb;
+    if (h != w.hb) {
+      w.hb = h;
+      w.t0 = now;
+    }
+  }
+  if (now - w.t0 > 4000000000ull) {
     if (wd) atomicExch(wd, 1u);
     return true;
   }
@@ -382,14 +399,14 @@ __device__ __forceinline__ bool watchdog_expired(unsigned long long t0, unsigned
 }
 // stopk / kself: give up as well once the run stopped before iteration kself (the waiting sweep is
 // discarded: its remaining work only has to reach the next group barrier, where it aborts)
-__device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target, unsigned* wd,
+__device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target, unsigned* wd, const unsigned* hb,
                                                const int* stopk = nullptr, int kself = 0) {
   if (ld_acquire_gpu(p) >= target) return;
-  const unsigned long long t0 = gtimer();
+  Watch w = watch_start(hb);
   for (unsigned it = 0;; ++it) {
     if (ld_acquire_gpu(p) >= target) return;
     if (stopk && *(volatile const int*)stopk < kself) return;
-    if ((it & 63) == 63 && watchdog_expired(t0, wd)) return;
+    if ((it & 63) == 63 && watchdog_expired(w, wd, hb)) return;
     __nanosleep(64);
   }
 }
@@ -416,57 +433,12 @@ __device__ __forceinline__ double2 yin_sentinel() {
   return make_double2(s, s);
 }
 
-// ---------------------------------------------------------------------------------------------
-// thread-block cluster helpers (cluster-mode pipelined sweep): DSMEM mapping and a CTA-level stage
-// barrier built from remote mbarrier arrivals (each CTA's barrier expects one arrival per CTA of the
-// cluster; release / acquire at cluster scope)
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_idx() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-  return r;
-}
-template <class T>
-__device__ __forceinline__ T* cluster_map(T* p, uint32_t rank) {  // generic address of *p in CTA `rank`
-  uint64_t r;
-  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"((uint64_t)p), "r"(rank));
-  return reinterpret_cast<T*>(r);
-}
-__device__ __forceinline__ void cluster_sync_all() {  // every thread of every CTA of the cluster
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(mb)), "r"(count)
-               : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint64_t* mb, uint32_t rank) {
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"((uint32_t)__cvta_generic_to_shared(mb)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* mb, unsigned parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"((uint32_t)__cvta_generic_to_shared(mb)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
 // Samples phase of one RK stage (Alg.1): poll the stage input y into C, then evaluate this
 // CTA's sample pairs (m_A, m_B) = (2p+1, 2p+2), p = rank, rank + P, ..., SPLIT pairs at a time on
 // SPLIT thread parts (each with its own X/Y at X + h*6N and named barrier 8 + h), writing one
 // partial Σ_{m in pair} w_m P+_m N(P-_m y) per pair to part[p] (per-pair partials: the owners'
 // reduction order is then independent of the CTA count, so every schedule agrees bitwise).
-template <int N, int R, int T, class GRP = CtaGroup, int NPC = 1, int SPLIT = 1, bool LOCALP = false>
+template <int N, int R, int T, class GRP = CtaGroup, int NPC = 1, int SPLIT = 1>
 __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* part, int M, const AvgTab& tab,
                                                      double2* X, double2* /*Y (= X + 3N)*/, const double2* TW,
                                                      double2* C, double2* /*A (unused)*/, const double2* PH,
@@ -489,12 +461,10 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
   constexpr double invN = 1.0 / N;
   // stage input (triple-buffered, sentinel = not yet written): poll, keep
-  if (y) {  // (cluster mode: the caller gathered y into C)
-    for (int i = tid_; i < 3 * Kc; i += T) {
-      double2 v = ld_relaxed_v2(y + i);
-      while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(y + i);
-      C[i] = v;
-    }
+  for (int i = tid_; i < 3 * Kc; i += T) {
+    double2 v = ld_relaxed_v2(y + i);
+    while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(y + i);
+    C[i] = v;
   }
   grp.sync();
   const int h = SPLIT > 1 ? tid_ / TH : 0, th = tid_ - h * TH;
@@ -531,7 +501,7 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
     if (SPLIT > 1) nl_core<N, R, TH>(Xh, Yh, TW, hg); else nl_core<N, R, T>(Xh, Yh, TW, grp);
     STAMP(2)
     const double wA = cached ? SWq[0] : __ldg(tab.w + mA), wB = hasB ? (cached ? SWq[1] : __ldg(tab.w + mB)) : 0.0;
-    double2* Pp = part + (size_t)(LOCALP ? q : pr) * 3 * Kc;  // LOCALP: this CTA's slot q (read over DSMEM)
+    double2* Pp = part + (size_t)pr * 3 * Kc;
     for (int j = th; j < Kc; j += TH) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
       const double as = kap < 0 ? -GA[ak] : GA[ak];
@@ -581,12 +551,8 @@ __device__ __forceinline__ void push_stage_input(const CoarseArgs& ca, const dou
   constexpr int Kc3 = 3 * (2 * (N / 3) + 1);
   grp.sync();
   if (tid_ < NOWN * 6 && yidx[tid_] >= 0) {
-    if (ca.yown) {  // cluster mode: gathered over DSMEM after the stage barrier
-      ca.yown[yidx[tid_]] = yv[tid_];
-    } else {
-      st_relaxed_v2(ca.yin + (size_t)(u % 3) * Kc3 + yidx[tid_], yv[tid_]);
-      st_relaxed_v2(ca.yin + (size_t)((u + 2) % 3) * Kc3 + yidx[tid_], yin_sentinel());
-    }
+    st_relaxed_v2(ca.yin + (size_t)(u % 3) * Kc3 + yidx[tid_], yv[tid_]);
+    st_relaxed_v2(ca.yin + (size_t)((u + 2) % 3) * Kc3 + yidx[tid_], yin_sentinel());
   }
 }
 
@@ -615,8 +581,8 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
     const int o = tid_ / 3, f = tid_ % 3, ak = rank + o * P;
     if (ak <= K) {
       // pipelined parareal: F(U^{k-1}_n) and the previous sweep's slice n must be complete
-      if (ca.wF) spin_until_geq(ca.wF + n / 2, 1u, ca.wd, ca.stopk, ca.kself);
-      if (ca.wprog) spin_until_geq(ca.wprog, ca.wunit * (unsigned)(n + 1), ca.wd, ca.stopk, ca.kself);
+      if (ca.wF) spin_until_geq(ca.wF + n / 2, 1u, ca.wd, ca.hb, ca.stopk, ca.kself);
+      if (ca.wprog) spin_until_geq(ca.wprog, ca.wunit * (unsigned)(n + 1), ca.wd, ca.hb, ca.stopk, ca.kself);
       if (ca.F) pf_F = __ldcg(reinterpret_cast<const double2*>(ca.F) + (size_t)n * Ls + f * NH + ak);
       pf_G = __ldcg(reinterpret_cast<const double2*>(ca.Gprev) + (size_t)n * Ls + f * NH + ak);
       pf_U = __ldcg(reinterpret_cast<const double2*>(ca.Uprev) + (size_t)(n + 1) * Ls + f * NH + ak);
@@ -640,12 +606,7 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int b = b0 + u * RQ;
-            if (ca.cls > 0)  // cluster mode: pair b's partial is slot b / cls of CTA b % cls (DSMEM)
-              buf[u] = b < ca.nparts ? *cluster_map(ca.plocal + (size_t)(b / ca.cls) * 3 * Kc + al * Kc + j,
-                                                    (uint32_t)(b % ca.cls))
-                                     : make_double2(0.0, 0.0);
-            else
-              buf[u] = b < ca.nparts ? __ldcg(src + (size_t)b * 3 * Kc) : make_double2(0.0, 0.0);
+            buf[u] = b < ca.nparts ? __ldcg(src + (size_t)b * 3 * Kc) : make_double2(0.0, 0.0);
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) sacc = cadd(sacc, buf[u]);

@@ -54,7 +54,7 @@ rsw_status check_params(const rsw_params* p) {
   if (!(std::isfinite(p->mu) && p->mu >= 0.0)) return fail(RSW_ERR_CONFIG, "mu must be finite and >= 0");
   const int n = p->n;
   if (n < 16 || n > 1024 || (n & (n - 1)))
-    return fail(RSW_ERR_CONFIG, "n must be a power of two in 16..1024");
+    return fail(RSW_ERR_CONFIG, "n must be a power of two in 16..1024 (DESIGN.md reading R18)");
   return RSW_OK;
 }
 
@@ -266,14 +266,21 @@ cudaError_t get_coarse(const rsw_params* p, double dT, CoarseTables** out) {
 // ---------------------------------------------------------------------------------------------
 // Workspace (per device), grown on demand
 // ---------------------------------------------------------------------------------------------
+constexpr int kMaxVirtualWorld = 16;
 struct Workspace {
-  DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof, Gnew, yin;
+  DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof, Gnew, yin, chk;
   DevBuf pU, pG, pF, prp, pres, pctl, pyb, ppart;  // pipelined schedule
+  DevBuf vshard[kMaxVirtualWorld];                 // RSW_VIRTUAL_WORLD: one fine-endpoint buffer per virtual rank
   double* rhost = nullptr;
+  unsigned* chost = nullptr;
   std::vector<cudaEvent_t> ev;
+  cudaEvent_t last = nullptr;  // recorded at the end of every call that used the workspace
+  bool last_rec = false;
   ~Workspace() {
     if (rhost) cudaFreeHost(rhost);
+    if (chost) cudaFreeHost(chost);
     for (auto e : ev) cudaEventDestroy(e);
+    if (last) cudaEventDestroy(last);
   }
 };
 std::map<int, std::unique_ptr<Workspace>> g_ws;
@@ -293,10 +300,43 @@ Workspace* workspace() {
   if (!w) {
     w = std::make_unique<Workspace>();
     cudaMallocHost(&w->rhost, sizeof(double) * 8);
+    cudaMallocHost(&w->chost, sizeof(unsigned) * 2);
     w->ev.resize(8);
     for (auto& e : w->ev) cudaEventCreate(&e);
+    cudaEventCreateWithFlags(&w->last, cudaEventDisableTiming);
   }
   return w.get();
+}
+
+// The workspace is shared by every call on the device, whatever its stream: a call first makes its
+// stream wait for the previous call's end event, and records that event again when it returns, so
+// two calls on different streams never overlap on the shared buffers.
+struct WsGuard {
+  Workspace* ws;
+  cudaStream_t st;
+  bool ok = true;
+  WsGuard(Workspace* w, cudaStream_t s) : ws(w), st(s) {
+    if (ws->last_rec) ok = cudaStreamWaitEvent(st, ws->last, 0) == cudaSuccess;
+  }
+  ~WsGuard() {
+    if (cudaEventRecord(ws->last, st) == cudaSuccess) ws->last_rec = true;
+  }
+  WsGuard(const WsGuard&) = delete;
+  WsGuard& operator=(const WsGuard&) = delete;
+};
+
+// Layout check of n_states input states (R10: modes k > n/3 zero; R16: Im û_0 zero) on the device;
+// synchronises the stream to read the verdict.
+rsw_status check_states_sync(const rsw_params* p, int n_states, const double* u, cudaStream_t st, Workspace* ws) {
+  CUDA_TRY(ensure(ws->chk, sizeof(unsigned) * 2));
+  CUDA_TRY(cudaMemsetAsync(ws->chk.p, 0, sizeof(unsigned) * 2, st));
+  CUDA_TRY(rsw::launch_check_states(p->n, u, n_states, (unsigned*)ws->chk.p, st));
+  CUDA_TRY(cudaMemcpyAsync(ws->chost, ws->chk.p, sizeof(unsigned) * 2, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (ws->chost[0])
+    return fail(RSW_ERR_CONFIG, "input state violates the layout: a non-zero mode k > n/3 (2/3 rule, R10)");
+  if (ws->chost[1]) return fail(RSW_ERR_CONFIG, "input state violates the layout: Im(u_hat_0) != 0 (real fields, R16)");
+  return RSW_OK;
 }
 
 size_t state_doubles(int n) { return (size_t)3 * (n / 2 + 1) * 2; }
@@ -357,6 +397,7 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   ca.wunit = 0;
   ca.wF = nullptr;
   ca.wd = nullptr;
+  ca.hb = nullptr;
   ca.stopk = nullptr;
   ca.kself = 0;
   ca.rparts = rparts;
@@ -504,6 +545,21 @@ rsw_status rsw_nonlinear(const rsw_params* p, int32_t n_states, const double* u_
   return RSW_OK;
 }
 
+rsw_status rsw_check_states(const rsw_params* p, int32_t n_states, const double* u, void* stream) {
+  Nvtx nvtx_("rsw_check_states");
+  rsw_status s = check_params(p);
+  if (s != RSW_OK) return s;
+  if (n_states < 0) return fail(RSW_ERR_CONFIG, "n_states < 0");
+  if (n_states == 0) return RSW_OK;
+  if (!u) return fail(RSW_ERR_CONFIG, "NULL state pointer");
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace* ws = workspace();
+  WsGuard wsg(ws, st);
+  if (!wsg.ok) return fail(RSW_ERR_CUDA, "cudaStreamWaitEvent on the workspace event failed");
+  return check_states_sync(p, n_states, u, st, ws);
+}
+
 rsw_status rsw_fine_propagate(const rsw_params* p, int32_t scheme, uint32_t flags, double dT, double dt,
                               int32_t n_slices, const double* u_in, double* u_out, void* stream) {
   Nvtx nvtx_("rsw_fine_propagate");
@@ -566,6 +622,8 @@ rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, doub
   std::lock_guard<std::mutex> lk(g_mu);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace* ws = workspace();
+  WsGuard wsg(ws, st);
+  if (!wsg.ok) return fail(RSW_ERR_CUDA, "cudaStreamWaitEvent on the workspace event failed");
   const size_t L = state_doubles(p->n);
   CUDA_TRY(ensure(ws->Ubuf, sizeof(double) * 2 * L));
   CUDA_TRY(ensure(ws->Gbuf, sizeof(double) * L));
@@ -592,7 +650,8 @@ rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, doub
 // residual history and the iteration count are bitwise identical (tests/test_gpu_parity.py).
 rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
                          double* resid_hist, int32_t* iters_done, cudaStream_t st, double* F_out, double* G_out,
-                         rsw_parareal_stats* stats, Workspace* ws) {
+                         rsw_parareal_stats* stats, Workspace* ws, bool* unsupported) {
+  *unsupported = false;
   const int n = p->n, Km = n / 3, Kc = 2 * Km + 1, S = cfg->n_slices, K = cfg->max_iters, M = cfg->M;
   const size_t L = state_doubles(n);
   const int m = n_fine_steps(cfg->dT, cfg->dt);
@@ -635,29 +694,23 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   const char* eg = getenv("RSW_PIPE_GC");
   if (eg) a.GC = std::max(1, atoi(eg));
   while ((Km + 1 + a.GC - 1) / a.GC > 8 || (M / 2 + a.GC - 1) / a.GC > 8) a.GC *= 2;  // <= 8 modes / pairs per CTA
-  // cluster mode (one thread-block cluster per sweep, stage communication over DSMEM; opt-in with
-  // RSW_PIPE_CLUSTER=1): bitwise identical, but slower on B200 — at most 7 clusters of 16 one-CTA-per-SM
-  // CTAs are co-resident (112 of 148 SMs) and 16 CTAs per sweep means 4 sample pairs per SM and stage
-  // (C3: 12.9 us per stage, 50.9 ms per solve, vs 10 us / 38.6 ms with 24-CTA global-memory groups)
-  bool use_cl = false;
   {
-    const char* ec = getenv("RSW_PIPE_CLUSTER");
-    if ((ec && ec[0] == '1') && !eg && rsw::pipeline_cluster_supported(n, M)) {
-      size_t ccap = 0;
-      if (rsw::launch_parareal_pipe_cl(n, a, cfg->fine_scheme, 0, &ccap, st) == cudaSuccess &&
-          (int)ccap >= rsw::pipeline_cluster_size() * std::min(K + 1, 6)) {
-        use_cl = true;
-        cap = ccap;
-        a.GC = rsw::pipeline_cluster_size();
-      } else {
-        cudaGetLastError();  // a failed capacity query must not poison the next launch
-      }
+    const cudaError_t qe = rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, 0, &cap, st);
+    if (qe != cudaSuccess) {  // capacity query failed: not runnable here (AUTO falls back to bulk)
+      cudaGetLastError();
+      *unsupported = true;
+      return fail(RSW_ERR_CONFIG, std::string("pipelined schedule: capacity query failed: ") + cudaGetErrorString(qe));
     }
   }
-  if (!use_cl) CUDA_TRY(rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, 0, &cap, st));
   const char* egr = getenv("RSW_PIPE_GRID");
   const int grid = egr ? atoi(egr) : (int)cap;
-  if (a.GC > grid) return fail(RSW_ERR_CONFIG, "pipelined schedule: not enough co-resident CTAs");
+  if (a.GC > grid && !eg) {  // many sample pairs: up to 8 pairs / 8 owned modes per coarse CTA (PIPE_CFG)
+    a.GC = std::max(std::max((std::max(M / 2, 1) + 7) / 8, (Km + 1 + 7) / 8), 1);
+  }
+  if (a.GC > grid) {
+    *unsupported = true;
+    return fail(RSW_ERR_CONFIG, "pipelined schedule: not enough co-resident CTAs");
+  }
   int ng = grid / a.GC;
   const char* en = getenv("RSW_PIPE_NG");
   if (en) ng = atoi(en);
@@ -669,7 +722,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   CUDA_TRY(ensure(ws->pF, sizeof(double) * nF));
   CUDA_TRY(ensure(ws->prp, sizeof(double) * 2 * (size_t)(K + 1) * S * (Km + 1)));
   CUDA_TRY(ensure(ws->pres, sizeof(double) * (K + 1)));
-  const size_t nctl = (size_t)(K + 1) + (size_t)std::max(K, 1) * a.npairs + std::max(K, 1) + 4 + (size_t)a.NG * 32;
+  const size_t nctl = (size_t)(K + 1) + (size_t)std::max(K, 1) * a.npairs + std::max(K, 1) + 5 + (size_t)a.NG * 32;
   CUDA_TRY(ensure(ws->pctl, sizeof(unsigned) * nctl));
   CUDA_TRY(ensure(ws->pyb, sizeof(double2) * (size_t)a.NG * 3 * 3 * Kc));
   CUDA_TRY(ensure(ws->ppart, sizeof(double2) * (size_t)a.NG * std::max(M / 2, 1) * 3 * Kc));
@@ -684,7 +737,8 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   a.next = a.doneF + (size_t)std::max(K, 1) * a.npairs;
   a.stopk = (int*)(a.next + std::max(K, 1));
   a.wd = (unsigned*)(a.stopk + 1);
-  a.ticket = a.wd + 1;
+  a.hb = a.wd + 1;
+  a.ticket = a.hb + 1;
   a.gbar = a.ticket + 2;
   a.ybuf = (double2*)ws->pyb.p;
   a.part = (double2*)ws->ppart.p;
@@ -704,8 +758,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   CUDA_TRY(cudaMemcpyAsync(a.stopk, &stop_init, sizeof(int), cudaMemcpyHostToDevice, st));
   for (int k = 0; k <= K; ++k)  // U^k_0 = u0 for every iteration
     CUDA_TRY(cudaMemcpyAsync(a.Uall + (size_t)k * (S + 1) * L, u0, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
-  if (use_cl) CUDA_TRY(rsw::launch_parareal_pipe_cl(n, a, cfg->fine_scheme, grid, nullptr, st));
-  else CUDA_TRY(rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, grid, nullptr, st));
+  CUDA_TRY(rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, grid, nullptr, st));
   int stopk = 0;
   unsigned wd = 0;
   std::vector<double> res(K + 1, 0.0);
@@ -718,7 +771,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     CUDA_TRY(cudaMemcpy(tr.data(), a.trace, sizeof(unsigned long long) * ntr, cudaMemcpyDeviceToHost));
     const double t0 = (double)tr[0];
     auto ms = [&](unsigned long long t) { return t ? (t - t0) * 1e-6 : -1.0; };
-    fprintf(stderr, "[rsw pipe] grid %d NG %d GC %d npairs %d cluster %d\n", grid, a.NG, a.GC, a.npairs, (int)use_cl);
+    fprintf(stderr, "[rsw pipe] grid %d NG %d GC %d npairs %d\n", grid, a.NG, a.GC, a.npairs);
     for (int k = 0; k <= K; ++k) {
       const unsigned long long* sl = tr.data() + 2 * (K + 1) + (size_t)k * S;
       fprintf(stderr, "[rsw pipe] sweep %d: start %.3f end %.3f | slice 0 %.3f, S/4 %.3f, S/2 %.3f, S-1 %.3f\n", k,
@@ -814,7 +867,11 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   std::lock_guard<std::mutex> lk(g_mu);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace* ws = workspace();
+  WsGuard wsg(ws, st);  // orders this call after the previous user of the workspace (any stream)
+  if (!wsg.ok) return fail(RSW_ERR_CUDA, "cudaStreamWaitEvent on the workspace event failed");
   if (stats) stats->pipelined = 0;
+  // the initial state must satisfy the layout (R10, R16): checked on the device before the solve
+  if ((s = check_states_sync(p, 1, u0, st, ws)) != RSW_OK) return s;
   {
     const char* vwe = getenv("RSW_VIRTUAL_WORLD");
     const bool can_pipe = !comm && rsw::pipeline_supported(p->n) && cfg->coarse_scheme != RSW_COARSE_STRANG &&
@@ -826,8 +883,14 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     if (cfg->schedule != RSW_SCHEDULE_AUTO && cfg->schedule != RSW_SCHEDULE_BULK &&
         cfg->schedule != RSW_SCHEDULE_PIPELINED)
       return fail(RSW_ERR_CONFIG, "unknown schedule");
-    if (can_pipe && (auto_pipe || cfg->schedule == RSW_SCHEDULE_PIPELINED))
-      return run_pipelined(p, cfg, u0, U, resid_hist, iters_done, st, F_out, G_out, stats, ws);
+    if (can_pipe && (auto_pipe || cfg->schedule == RSW_SCHEDULE_PIPELINED)) {
+      bool unsupported = false;
+      s = run_pipelined(p, cfg, u0, U, resid_hist, iters_done, st, F_out, G_out, stats, ws, &unsupported);
+      // AUTO: a configuration the pipelined kernel cannot hold (too few co-resident CTAs for its coarse
+      // groups, failed capacity query) runs the bulk schedule instead; an explicit request fails
+      if (!(unsupported && cfg->schedule == RSW_SCHEDULE_AUTO)) return s;
+      if (stats) stats->pipelined = 0;
+    }
   }
   const int n = p->n, K = n / 3;
   const size_t L = state_doubles(n);
@@ -878,20 +941,31 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   const char* vw = getenv("RSW_VIRTUAL_WORLD");
   const int vworld = vw ? atoi(vw) : 1;
   if (!comm && vworld > 1 && S % vworld != 0) return fail(RSW_ERR_CONFIG, "RSW_VIRTUAL_WORLD must divide n_slices");
+  if (!comm && vworld > kMaxVirtualWorld) return fail(RSW_ERR_CONFIG, "RSW_VIRTUAL_WORLD must be <= 16");
+  if (!comm && vworld > 1) {
+    for (int r = 0; r < vworld; ++r) CUDA_TRY(ensure(ws->vshard[r], sizeof(double) * L * (S / vworld)));
+  }
   int64_t fine_steps = 0;
   for (int k = 1; k <= cfg->max_iters; ++k) {
     // parfor n: F_n = φ(U^{k-1}_n) on this rank's shard
     Nvtx nvtx_it("parareal iteration (fine sweep, all-gather, coarse sweep)");
     CUDA_TRY(cudaEventRecord(ev[0], st));
     if (!comm && vworld > 1) {
-      // test knob RSW_VIRTUAL_WORLD=P: run the P shards' fine sweeps as separate launches into their
-      // blocks of F (what P ranks would compute before the all-gather) on this one GPU
+      // test knob RSW_VIRTUAL_WORLD=P: the P shards' fine sweeps run as separate launches into P separate
+      // shard buffers (what P ranks hold before the exchange); F is then assembled with one copy per
+      // shard at offset lo_r — the layout the in-place all-gather below produces
       for (int r = 0; r < vworld; ++r) {
         int32_t vlo, vhi;
         if ((s = rsw_shard_range(S, r, vworld, &vlo, &vhi)) != RSW_OK) return s;
-        CUDA_TRY(rsw::launch_fine(n, cfg->fine_scheme, false, U + (size_t)vlo * L, F + (size_t)vlo * L, vhi - vlo,
+        CUDA_TRY(rsw::launch_fine(n, cfg->fine_scheme, false, U + (size_t)vlo * L, (double*)ws->vshard[r].p, vhi - vlo,
                                   m, h, ftab, st));
         ++launches;
+      }
+      for (int r = 0; r < vworld; ++r) {
+        int32_t vlo, vhi;
+        rsw_shard_range(S, r, vworld, &vlo, &vhi);
+        CUDA_TRY(cudaMemcpyAsync(F + (size_t)vlo * L, ws->vshard[r].p, sizeof(double) * L * (vhi - vlo),
+                                 cudaMemcpyDeviceToDevice, st));
       }
     } else {
       CUDA_TRY(rsw::launch_fine(n, cfg->fine_scheme, false, U + (size_t)lo * L, F + (size_t)lo * L, hi - lo, m, h,
@@ -900,7 +974,7 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     }
     fine_steps += (int64_t)(hi - lo) * m;
     CUDA_TRY(cudaEventRecord(ev[1], st));
-    if (comm && world > 1) {
+    if (comm) {  // a6: every rank's block lands at its offset lo_r (in place; world 1 is a plain NCCL no-op copy)
       ncclResult_t r = g_nccl.allGather(F + (size_t)lo * L, F, (size_t)(hi - lo) * L, ncclDouble,
                                         (ncclComm_t)comm->comm, st);
       if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");

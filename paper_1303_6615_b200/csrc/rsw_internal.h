@@ -1,4 +1,4 @@
-// rsw_internal.h — internal structs shared by the kernels (rsw_kernels.cu) and the host library
+// rsw_internal.h — internal structs shared by the kernels (rsw_k_*.cu, rsw_pipeline.cu) and the host library
 // (rsw_capi.cu).  Not part of the C-ABI.
 #pragma once
 #include <cuda_runtime.h>
@@ -49,16 +49,12 @@ struct CoarseArgs {
   unsigned wunit;
   const unsigned* wF;     // pipelined: done flags of the previous iteration's fine pairs, or null
   unsigned* wd;           // pipelined: watchdog flag (set when a wait times out), or null
+  const unsigned* hb;     // pipelined: progress heartbeat read by the watchdog, or null
   const int* stopk;       // pipelined: first stopped iteration (waits of sweep kself > *stopk give up), or null
   int kself;
   double* rparts;       // [S][K+1][2] residual partials or null
   int n_end;            // number of chain steps (S)
   unsigned long long* prof;  // optional phase timestamps (CTA 0; RSW_PROFILE_COARSE=1), else null
-  // cluster mode (pipelined sweep on one thread-block cluster, rsw_pipeline.cu): partials and stage
-  // inputs stay in the cluster's shared memory (DSMEM) instead of global memory; cls = 0: off
-  int cls;              // cluster size (CTAs per sweep)
-  double2* plocal;      // this CTA's partial slots [NPC][3][Kc] (shared memory; read remotely by owners)
-  double2* yown;        // this CTA's owned stage-input entries [3][Kc] (shared memory; gathered remotely)
 };
 
 // Pipelined parareal (rsw_pipeline.cu): every iteration's buffers stay resident
@@ -78,6 +74,7 @@ struct PipeArgs {
   unsigned* next;       // [K]     next unclaimed fine pair per iteration
   int* stopk;           // first iteration that stopped the run (K+1: none)
   unsigned* wd;         // watchdog flag
+  unsigned* hb;         // progress heartbeat (fine steps, coarse slices): waits time out only without progress
   unsigned* ticket;     // role tickets
   unsigned* gbar;       // [NG][32] group barrier counters
   double2* ybuf;        // [NG][3][3Kc] stage inputs
@@ -86,9 +83,6 @@ struct PipeArgs {
 };
 bool pipeline_supported(int n);
 cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);
-bool pipeline_cluster_supported(int n, int M);
-int pipeline_cluster_size();
-cudaError_t launch_parareal_pipe_cl(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);
 
 cudaError_t launch_fine(int n, int scheme, bool lin, const double* in, double* out, int S, int m, double h,
                         const FineTab& tab, cudaStream_t st);
@@ -100,5 +94,7 @@ cudaError_t launch_coarse_sweep(int n, const CoarseArgs& ca, const AvgTab& tab, 
 cudaError_t launch_strang_sweep(int n, const FineTab& tab, double h, double* U, double* G, const double* F,
                                 double* Gnew, int S, double* r_out, cudaStream_t st);
 cudaError_t launch_dfma_peak(double* out, int blocks, int iters, cudaStream_t st);
+// bad[0] |= any non-zero mode k > n/3, bad[1] |= any Im û_0 != 0, over n_states states
+cudaError_t launch_check_states(int n, const double* u, int n_states, unsigned* bad, cudaStream_t st);
 
 }  // namespace rsw

@@ -1,6 +1,8 @@
 // rsw_k_misc.cu — standalone N(u) (a1), batched averaged nonlinearity (a3) and the DFMA peak probe.
 #include "rsw_blocks.cuh"
 
+#include <algorithm>
+
 namespace rsw {
 
 template <typename KernelT>
@@ -279,6 +281,28 @@ cudaError_t launch_avg_states(int n, const double* in, double* out, int S, int M
 #define C(NN) launch_avg_n<NN>(in, out, S, M, tab, st)
   RSW_DISPATCH(n, C)
 #undef C
+}
+
+// Layout check of input states (include/rsw.h STATE LAYOUT; R10, R16): one thread per half-spectrum
+// entry, grid-stride; any violation raises a flag (bad[0]: mode k > n/3 non-zero, bad[1]: Im û_0 != 0).
+__global__ void k_check_states(const double2* __restrict__ u, long long entries, int nh, int K, unsigned* bad) {
+  unsigned hi = 0, im0 = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < entries; i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i % nh);
+    const double2 v = __ldg(u + i);
+    if (k > K && (v.x != 0.0 || v.y != 0.0)) hi = 1;
+    if (k == 0 && v.y != 0.0) im0 = 1;
+  }
+  if (__any_sync(0xffffffffu, hi) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+  if (__any_sync(0xffffffffu, im0) && (threadIdx.x & 31) == 0) atomicOr(bad + 1, 1u);
+}
+
+cudaError_t launch_check_states(int n, const double* u, int n_states, unsigned* bad, cudaStream_t st) {
+  const int nh = n / 2 + 1;
+  const long long entries = (long long)n_states * 3 * nh;
+  const int blocks = (int)std::min<long long>((entries + 255) / 256, 148 * 8);
+  k_check_states<<<blocks, 256, 0, st>>>(reinterpret_cast<const double2*>(u), entries, nh, n / 3, bad);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_dfma_peak(double* out, int blocks, int iters, cudaStream_t st) {

@@ -22,7 +22,8 @@
 // Stop rule (tol > 0): the group that finishes sweep k computes r_k; the first r_k < tol (or a
 // divergence) lowers stopk; later sweeps abort at their next group barrier (the abort travels in
 // the barrier counter, so every CTA of a group takes the same decision) and no more fine tasks of
-// iterations >= stopk are claimed.  Every wait is bounded (watchdog flag, ~4 s).
+// iterations >= stopk are claimed.  Every wait is bounded: it gives up after ~4 s without any progress
+// anywhere in the kernel (heartbeat counter; watchdog flag).
 #include "rsw_blocks.cuh"
 
 #include <cstdio>
@@ -52,16 +53,16 @@ constexpr unsigned ABORT_BIT = 1u << 28;
 // nothing else is left to do)
 template <class GRP>
 __device__ __forceinline__ bool group_barrier(unsigned* bar, unsigned P, unsigned& epoch, bool raise, unsigned* wd,
-                                              unsigned* s_flag, const GRP& grp) {
+                                              const unsigned* hb, unsigned* s_flag, const GRP& grp) {
   grp.sync();
   if (grp.tid() == 0) {
     ++epoch;
     red_release_add(bar, raise ? ABORT_BIT + 1 : 1);
     const unsigned target = epoch * P;
     unsigned v = ld_acquire_gpu(bar);
-    const unsigned long long t0 = gtimer();
+    Watch w = watch_start(hb);
     for (unsigned it = 0; v < target && !(v & ABORT_BIT); ++it) {
-      if ((it & 63) == 63 && watchdog_expired(t0, wd)) {
+      if ((it & 63) == 63 && watchdog_expired(w, wd, hb)) {
         v = ABORT_BIT;
         break;
       }
@@ -120,7 +121,7 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
   for (;;) {
     if (grp.tid() == 0) {
       int tk = -1, tp = -1;
-      const unsigned long long t0 = gtimer();
+      Watch w = watch_start(a.hb);
       for (unsigned it = 0;; ++it) {
         const int lim = min(Kit, *(volatile int*)a.stopk) - 1;  // F^k is needed by sweep k+1 <= stop
         bool all_claimed = true;
@@ -135,7 +136,7 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
           }
         }
         if (tk >= 0 || all_claimed) break;
-        if ((it & 63) == 63 && watchdog_expired(t0, a.wd)) break;
+        if ((it & 63) == 63 && watchdog_expired(w, a.wd, a.hb)) break;
         __nanosleep(128);
       }
       task[0] = tk;
@@ -151,7 +152,7 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
     const double* Uk = a.Uall + (size_t)tk * (S + 1) * L;
     double* Fk = a.Fall + (size_t)tk * S * L;
     fine_pair_run<N, RF, TG, FSCHEME, false>(grp, W, Yb, ft, tcol, a.ft.g, Uk + nA * L, nB < S ? Uk + nB * L : nullptr,
-                                             Fk + nA * L, nB < S ? Fk + nB * L : nullptr, a.m_fine, a.h);
+                                             Fk + nA * L, nB < S ? Fk + nB * L : nullptr, a.m_fine, a.h, a.hb);
     grp.sync();  // the whole pair's F is written
     if (grp.tid() == 0) {
       st_release_u32(a.doneF + (size_t)tk * npairs + tp, 1u);
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         // sweep start: the three stage-input buffers of the group start empty
         for (int i = c * TC + ct; i < 3 * Kc3; i += P * TC) st_relaxed_v2(yb + i, yin_sentinel());
         const bool stop_now = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
-        if (group_barrier(bar, P, epoch, stop_now, a.wd, &s_flag, cg)) break;
+        if (group_barrier(bar, P, epoch, stop_now, a.wd, a.hb, &s_flag, cg)) break;
         if (a.trace && c == 0 && ct == 0) a.trace[2 * k] = gtimer();
         CoarseArgs ca = a.base;
         ca.U = a.Uall + (size_t)k * (S + 1) * L;
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         ca.wunit = (unsigned)P;
         ca.wF = k ? a.doneF + (size_t)(k - 1) * a.npairs : nullptr;
         ca.wd = a.wd;
+        ca.hb = a.hb;
         ca.stopk = a.stopk;
         ca.kself = k;
         ca.prof = nullptr;
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
                                                              C, A, PH, SW, GA, GP, GQ, nullptr, c, P, cg);
             if (stp) stp[1] = gtimer();
             const bool raise = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
-            if (group_barrier(bar, P, epoch, raise, a.wd, &s_flag, cg)) {
+            if (group_barrier(bar, P, epoch, raise, a.wd, a.hb, &s_flag, cg)) {
               aborted = true;
               break;
             }
@@ -297,12 +299,15 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
           }
           if (!aborted) {
             cg.sync();  // this CTA's part of U^k_{n+1}, G^k_n is written
-            if (ct == 0) red_release_add(a.prog + k, 1u);
+            if (ct == 0) {
+              red_release_add(a.prog + k, 1u);
+              if (c == 0) atomicAdd(a.hb, 1u);  // watchdog heartbeat: a slice of sweep k is done
+            }
             if (a.trace && c == 0 && ct == 0) a.trace[2 * (Kit + 1) + (size_t)k * S + n] = gtimer();
           }
         }
         if (aborted) break;
-        if (group_barrier(bar, P, epoch, false, a.wd, &s_flag, cg)) break;  // every slice's residual partials written
+        if (group_barrier(bar, P, epoch, false, a.wd, a.hb, &s_flag, cg)) break;  // every slice's residual partials written
         if (a.trace && c == 0 && ct == 0) a.trace[2 * k + 1] = gtimer();
         if (c == 0 && k > 0) {  // r_k = max_n sqrt(Σ num / Σ den) (fixed order, as the bulk sweep)
           double mx = 0.0;
@@ -341,237 +346,6 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
   }
   tmem_fence_before();
   __syncthreads();
-  if (warp == 0) {
-    tmem_fence_after();
-    tmem_dealloc<512>(tslot);
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Cluster-mode pipelined parareal: the same roles and dependencies as k_parareal_pipe, but each
-// sweep group is ONE thread-block cluster of CS CTAs (its coarse sub-CTAs), so the per-stage
-// communication stays on the cluster's shared memory: every CTA keeps its sample pairs' partials
-// and its owned stage-input entries in its own smem; the owners reduce the partials of their modes
-// over DSMEM (same fixed order as the global-memory sweep: bitwise identical results) and every CTA
-// gathers the next stage input over DSMEM; the two stage barriers are remote mbarrier arrivals
-// (release / acquire at cluster scope) instead of a global counter polled through L2.  Clusters with
-// index >= NG (no sweep) run extra fine groups in their coarse threads.
-// ---------------------------------------------------------------------------------------------
-template <int N, int RC, int TC, int NOWN, int NPC, int RF, int TG, int NPG, int FSCHEME, int CS>
-__global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe_cl(const PipeArgs a) {
-  using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG>;
-  using CL = typename LY::CL;
-  static_assert(NPG * LY::CPG <= 512, "fine groups must fit in TMEM");
-  static_assert(LY::SPLIT * CS >= 1 && NPC <= LY::SPLIT, "one round of sample pairs per stage");
-  constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NH = N / 2 + 1, Kc3 = 3 * Kc;
-  constexpr size_t L = (size_t)3 * NH * 2;
-  // cluster-mode buffers after the fine groups' region
-  constexpr int PLOC = (int)(LY::bytes / sizeof(double2)), YOWN = PLOC + NPC * Kc3;
-  extern __shared__ double2 smem[];
-  __shared__ uint32_t tslot;
-  __shared__ unsigned s_flag;
-  __shared__ unsigned s_abort;  // written remotely by rank 0: k + 1 = abort sweep k
-  __shared__ alignas(8) uint64_t s_mb[2];  // stage barriers, used alternately (see stage_barrier)
-  __shared__ int s_task[NPG + TC / TG][2];
-  const int warp = threadIdx.x >> 5;
-  const uint32_t rank = cluster_ctarank();
-  const int cid = (int)cluster_idx();
-  if (warp == 0) tmem_alloc<512>(&tslot);
-  if (threadIdx.x == 0) {
-    mbar_init(&s_mb[0], CS);
-    mbar_init(&s_mb[1], CS);
-    s_abort = 0;
-  }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  cluster_sync_all();  // every CTA's mbarrier is initialised before anyone arrives remotely
-  const int S = a.S, Kit = a.K;
-  const FineSmemTab ft = stage_fine_tables<N, RF, TC + NPG * TG>(
-      smem + LY::F_TW, smem + LY::F_CP, reinterpret_cast<double*>(smem + LY::F_D), a.ft, threadIdx.x, TC + NPG * TG);
-  __syncthreads();
-
-  constexpr int FT = NPG * TG;
-  if ((int)threadIdx.x >= FT) {
-    const NamedGroup cg{FT, 15, TC};
-    const int ct = (int)threadIdx.x - FT;
-    if (cid >= a.NG) {
-      constexpr int XG = TC / TG;
-      const int xi = ct / TG;
-      if (xi < XG && (NPG + XG) * LY::CPG <= 512)
-        fine_worker_loop<N, RF, TG, FSCHEME>(a, NamedGroup{FT + xi * TG, 1 + NPG + xi, TG},
-                                            smem + LY::C0 + (size_t)xi * 6 * N, ft,
-                                            tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi]);
-    } else {
-      const int g = cid, c = (int)rank, P = CS;
-      double2* cs = smem + LY::C0;
-      double2* X = cs + CL::X;
-      double2* Y = cs + CL::Y;
-      double2* TW = cs + CL::TW;
-      double2* C = cs + CL::C;
-      double2* A = cs + CL::A;
-      double2* Vs = cs + CL::VS;
-      double2* KSs = cs + CL::KS;
-      double2* kk = cs + CL::KK;
-      double2* un_s = cs + CL::UN;
-      double2* rdb = cs + CL::RDB;
-      double2* PH = cs + CL::PH;
-      double2* yv = cs + CL::YV;
-      double2* plocal = smem + PLOC;
-      double2* yown = smem + YOWN;
-      double* sd = reinterpret_cast<double*>(cs + CL::D);
-      double* red = sd + CL::RED;
-      double* GA = sd + CL::GA;
-      double* GP = sd + CL::GP;
-      double* GQ = sd + CL::GQ;
-      double* SW = sd + CL::SW;
-      int* yidx = reinterpret_cast<int*>(sd + CL::YI);
-      const AvgTab& tab = a.at;
-      const int M = a.M;
-      fill_packed_twiddles<N, LY::RC, TC>(TW, tab.tw, ct);
-      for (int k = ct; k <= K; k += TC) {
-        GA[k] = __ldg(tab.g.a + k);
-        GP[k] = __ldg(tab.g.p + k);
-        GQ[k] = __ldg(tab.g.q + k);
-      }
-      for (int q = 0; q < NPC; ++q) {
-        const int pr = c + q * P;
-        if (pr >= M / 2) break;
-        const int mA = 2 * pr + 1, mB = 2 * pr + 2;
-        for (int k = ct; k <= K; k += TC) {
-          PH[(size_t)q * 2 * KP + k] = __ldg(tab.phase + (size_t)mA * KP + k);
-          PH[(size_t)q * 2 * KP + KP + k] = __ldg(tab.phase + (size_t)mB * KP + k);
-        }
-        if (ct == 0) {
-          SW[2 * q] = __ldg(tab.w + mA);
-          SW[2 * q + 1] = mB <= M - 1 ? __ldg(tab.w + mB) : 0.0;
-        }
-      }
-      cg.sync();
-      unsigned nbar = 0;
-      // stage barrier of the cluster's coarse sub-CTAs: thread ct < CS arrives on CTA ct's mbarrier
-      // (after the sub-CTA's writes, ordered by cg.sync(); release at cluster scope), thread 0 waits
-      // on its own (acquire, bounded).  Two mbarriers alternate: a CTA's arrival for use u+1 can then
-      // never be counted in use u of a slower CTA's barrier (it targets the other object, and its
-      // arrival for use u+2 happens after every arrival of use u through the use-(u+1) barrier).
-      // Rank 0 may raise the abort for sweep k by writing k + 1 into every CTA's s_abort before its
-      // arrivals.
-      auto stage_barrier = [&](bool raise, int k) -> bool {
-        const unsigned b = nbar & 1u, parity = (nbar >> 1) & 1u;
-        ++nbar;
-        cg.sync();
-        if (ct < CS) {
-          if (raise) *cluster_map(&s_abort, (uint32_t)ct) = (unsigned)(k + 1);
-          mbar_arrive_remote(&s_mb[b], (uint32_t)ct);
-        }
-        if (ct == 0) {
-          const unsigned long long t0 = gtimer();
-          bool to = false;
-          for (unsigned it = 0; !mbar_try_wait(&s_mb[b], parity); ++it)
-            if ((it & 63) == 63 && watchdog_expired(t0, a.wd)) {
-              to = true;
-              break;
-            }
-          s_flag = (to || *(volatile unsigned*)&s_abort == (unsigned)(k + 1)) ? 1u : 0u;
-        }
-        cg.sync();
-        return s_flag != 0;
-      };
-      const int nst = a.base.scheme == 0 ? 4 : 2;
-      for (int k = g; k <= Kit; k += a.NG) {
-        const bool stop_now = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
-        if (stage_barrier(stop_now, k)) break;
-        if (a.trace && c == 0 && ct == 0) a.trace[2 * k] = gtimer();
-        CoarseArgs ca = a.base;
-        ca.U = a.Uall + (size_t)k * (S + 1) * L;
-        ca.G = a.Gall + (size_t)k * S * L;
-        ca.Uprev = k ? a.Uall + (size_t)(k - 1) * (S + 1) * L : ca.U;
-        ca.Gprev = k ? a.Gall + (size_t)(k - 1) * S * L : ca.G;
-        ca.F = k ? a.Fall + (size_t)(k - 1) * S * L : nullptr;
-        ca.rparts = k ? a.rparts + (size_t)k * S * KP * 2 : nullptr;
-        ca.part = nullptr;
-        ca.nparts = M / 2 > 0 ? M / 2 : 1;
-        ca.yin = nullptr;
-        ca.n_end = S;
-        ca.wprog = k ? a.prog + (k - 1) : nullptr;
-        ca.wunit = (unsigned)P;
-        ca.wF = k ? a.doneF + (size_t)(k - 1) * a.npairs : nullptr;
-        ca.wd = a.wd;
-        ca.stopk = a.stopk;
-        ca.kself = k;
-        ca.prof = nullptr;
-        ca.cls = CS;
-        ca.plocal = plocal;
-        ca.yown = yown;
-        unsigned ucount = 0;
-        coarse_update_phase<N, TC, NOWN>(ca, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, c, P, cg);
-        bool aborted = stage_barrier(false, k);
-        for (int n = 0; n < S && !aborted; ++n) {
-          for (int st = 1; st <= nst; ++st) {
-            // gather the stage input: entry (α, j) is owned by CTA |κ(j)| mod CS
-            for (int i = ct; i < Kc3; i += TC) {
-              const int j = i % Kc, kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
-              C[i] = *cluster_map(yown + i, (uint32_t)(ak % CS));
-            }
-            coarse_samples_phase<N, LY::RC, TC, NamedGroup, NPC, LY::SPLIT, true>(nullptr, plocal, M, tab, X, Y, TW, C,
-                                                                                 A, PH, SW, GA, GP, GQ, nullptr, c, P, cg);
-            const bool raise = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
-            if (stage_barrier(raise, k)) {  // partials complete
-              aborted = true;
-              break;
-            }
-            ++ucount;
-            coarse_update_phase<N, TC, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, c, P, cg);
-            if (stage_barrier(false, k)) {  // owned inputs complete, partial slots free
-              aborted = true;
-              break;
-            }
-          }
-          if (!aborted) {
-            if (ct == 0) red_release_add(a.prog + k, 1u);  // (the stage barrier ordered this CTA's writes)
-            if (a.trace && c == 0 && ct == 0) a.trace[2 * (Kit + 1) + (size_t)k * S + n] = gtimer();
-          }
-        }
-        if (aborted) break;
-        if (a.trace && c == 0 && ct == 0) a.trace[2 * k + 1] = gtimer();
-        if (c == 0 && k > 0) {  // r_k = max_n sqrt(Σ num / Σ den) (fixed order, as the bulk sweep)
-          double mx = 0.0;
-          bool bad = false;
-          for (int s2 = ct; s2 < S; s2 += TC) {
-            double num = 0.0, den = 0.0;
-            for (int q = 0; q <= K; ++q) {
-              num += __ldcg(ca.rparts + ((size_t)s2 * KP + q) * 2);
-              den += __ldcg(ca.rparts + ((size_t)s2 * KP + q) * 2 + 1);
-            }
-            const double r = sqrt(num / den);
-            if (!(r == r) || isinf(r)) bad = true;
-            mx = fmax(mx, r);
-          }
-          red[ct] = bad ? __longlong_as_double(0x7ff8000000000000LL) : mx;
-          cg.sync();
-          if (ct == 0) {
-            double m = 0.0;
-            bool nan = false;
-            for (int t = 0; t < TC; ++t) {
-              if (red[t] != red[t]) nan = true;
-              m = fmax(m, red[t]);
-            }
-            const double r = nan ? __longlong_as_double(0x7ff8000000000000LL) : m;
-            a.resid[k] = r;
-            if (!(r == r) || r > 1e6 || (a.tol > 0 && r < a.tol)) atomicMin(a.stopk, k);
-          }
-          cg.sync();
-        }
-      }
-    }
-  } else {
-    const int gi = threadIdx.x / TG;
-    fine_worker_loop<N, RF, TG, FSCHEME>(a, NamedGroup{gi * TG, 1 + gi, TG}, smem + LY::F_G + (size_t)gi * 6 * N,
-                                        ft, tslot + (uint32_t)(gi * LY::CPG), s_task[gi]);
-  }
-  tmem_fence_before();
-  __syncthreads();
-  cluster_sync_all();  // no CTA leaves while another may still read its shared memory
   if (warp == 0) {
     tmem_fence_after();
     tmem_dealloc<512>(tslot);
@@ -627,63 +401,6 @@ static cudaError_t launch_pipe_n(const PipeArgs& a, int fine_scheme, int grid, s
 }
 
 bool pipeline_supported(int n) { return n == 64 || n == 128 || n == 256; }
-
-// cluster-mode launcher (n = 256: clusters of 16 CTAs, each coarse sub-CTA evaluates its four sample
-// pairs at once on four 96-thread parts next to one 96-thread fine group).  grid <= 0: capacity query
-// (co-resident CTAs of whole clusters) into *out.
-#ifndef RSW_PIPE_CLUSTER_SIZE
-#define RSW_PIPE_CLUSTER_SIZE 16
-#endif
-template <int N, int FSCHEME>
-static cudaError_t launch_pipe_cl_nf(const PipeArgs& a, int grid, size_t* out, cudaStream_t st) {
-  constexpr int CS = RSW_PIPE_CLUSTER_SIZE;
-  constexpr int RC = coarse_radix<N>(), RF = fine_radix<N>(), TG = core_threads<N, RF>();
-  constexpr int TC = 4 * core_threads<N, RC>(), NOWN = 8, NPC = 4, NPG = 1;
-  using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG>;
-  static_assert(LY::SPLIT == 4, "four sample-pair parts per coarse sub-CTA");
-  constexpr int Kc3 = 3 * (2 * (N / 3) + 1);
-  const size_t sm = LY::bytes + sizeof(double2) * (size_t)(NPC + 1) * Kc3;
-  auto kfn = k_parareal_pipe_cl<N, RC, TC, NOWN, NPC, RF, TG, NPG, FSCHEME, CS>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CS;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeCooperative;
-  at[1].val.cooperative = 1;
-  cfg.blockDim = dim3(LY::T);
-  cfg.dynamicSmemBytes = sm;
-  cfg.stream = st;
-  cfg.attrs = at;
-  cfg.numAttrs = 2;
-  if (grid <= 0) {
-    int nc = 0;
-    cfg.gridDim = dim3(CS);
-    if ((e = cudaOccupancyMaxActiveClusters(&nc, kfn, &cfg)) != cudaSuccess) return e;
-    if (out) *out = (size_t)nc * CS;
-    if (getenv("RSW_PIPE_TRACE"))
-      fprintf(stderr, "[rsw pipe cl] n=%d: %d threads (coarse %d + fine %d), %zu B smem, %d clusters of %d\n", N,
-              LY::T, TC, TG, sm, nc, CS);
-    return cudaSuccess;
-  }
-  cfg.gridDim = dim3(grid);
-  return cudaLaunchKernelEx(&cfg, kfn, a);
-}
-
-bool pipeline_cluster_supported(int n, int M) { return n == 256 && M / 2 <= 4 * RSW_PIPE_CLUSTER_SIZE && M >= 2; }
-
-cudaError_t launch_parareal_pipe_cl(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out,
-                                    cudaStream_t st) {
-  if (n != 256) return cudaErrorInvalidValue;
-  return fine_scheme == 0 ? launch_pipe_cl_nf<256, 0>(a, grid, out, st)
-       : fine_scheme == 1 ? launch_pipe_cl_nf<256, 1>(a, grid, out, st)
-                          : launch_pipe_cl_nf<256, 2>(a, grid, out, st);
-}
-int pipeline_cluster_size() { return RSW_PIPE_CLUSTER_SIZE; }
 
 // grid <= 0: return the number of co-resident CTAs in *out (capacity query)
 cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out,

@@ -1,0 +1,45 @@
+"""Worker of tests/test_multigpu.py (one rank per GPU, launched by torch.distributed.run).
+
+Runs the C3 solve (BASELINE configs[2], 5 iterations) through the library with a real NCCL
+communicator: each rank advances its shard of slices, the in-place ncclAllGather exchanges the fine
+endpoints (a6), every rank runs the replicated coarse sweep.  Writes, per rank, a digest of U and the
+residual history; rank 0 also writes the single-GPU (comm = None) bulk result and the sampled slices
+the oracle fixture holds, for the test to compare."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_1303_6615_b200 as rsw  # noqa: E402
+from paper_1303_6615_b200 import inputs  # noqa: E402
+
+
+def main(out_dir):
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank = dist.get_rank()
+    rsw.load()
+    comm = rsw.Comm.from_torch_distributed()
+    w = inputs.C3
+    p = rsw.Params(w.eps, w.F, w.mu, w.n)
+    u0 = torch.from_numpy(inputs.initial_state(w)).cuda()
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=w.max_iters)
+    g = rsw.parareal_iterate(p, u0, comm=comm, **kw)
+    U = g["U"].cpu().numpy()
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=U, resid=np.array(g["resid"]), iters=g["iters"],
+             comm_ms=g["stats"]["comm_ms"], fine_steps=g["stats"]["fine_slice_steps"])
+    if rank == 0:
+        s = rsw.parareal_iterate(p, u0, schedule=rsw.SCHEDULE_BULK, **kw)
+        np.savez(os.path.join(out_dir, "single.npz"), U=s["U"].cpu().numpy(), resid=np.array(s["resid"]))
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])

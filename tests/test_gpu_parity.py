@@ -413,20 +413,114 @@ def test_pipelined_group_layouts_bitwise(rsw_gpu, gc, ng, monkeypatch):
     assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
 
 
-@pytest.mark.parametrize("max_iters,tol", [(2, 0.0), (5, 0.3)])
-def test_pipelined_cluster_mode_bitwise(rsw_gpu, max_iters, tol, monkeypatch):
-    """The opt-in cluster mode (one thread-block cluster per sweep, partials and stage inputs over
-    DSMEM, RSW_PIPE_CLUSTER=1) reduces in the same fixed order: bitwise equal to the bulk schedule on
-    C3, also when the tolerance stops it early (abort raised through the cluster's stage barrier)."""
+def test_check_states_layout(rsw_gpu):
+    """§8(b): an input with a non-zero mode k > n/3 (R10) or Im û_0 != 0 (R16) is RSW_ERR_CONFIG —
+    through rsw_check_states, through parareal_iterate's own device check of u0, and through the
+    binding's default check before the asynchronous entry points."""
+    w = inputs.C1
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u = inputs.random_states(w.n, 3, seed=1)
+    rsw_gpu.check_states(p, dev(u))
+    hi = u.copy()
+    hi[1, 2, w.n // 3 + 1, 0] = 1e-3
+    im0 = u.copy()
+    im0[2, 0, 0, 1] = 0.5
+    for bad in (hi, im0):
+        with pytest.raises(rsw_gpu.RSWError) as e:
+            rsw_gpu.check_states(p, dev(bad))
+        assert e.value.status == rsw_gpu.RSW_ERR_CONFIG
+        with pytest.raises(rsw_gpu.RSWError) as e:
+            rsw_gpu.fine_propagate(p, dev(bad), w.dT, w.dt)
+        assert e.value.status == rsw_gpu.RSW_ERR_CONFIG
+    for k in (1, 2):
+        bad0 = hi[1] if k == 1 else im0[2]
+        for sched in (rsw_gpu.SCHEDULE_BULK, rsw_gpu.SCHEDULE_AUTO):
+            with pytest.raises(rsw_gpu.RSWError) as e:
+                rsw_gpu.parareal_iterate(p, dev(bad0), dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices,
+                                         max_iters=1, schedule=sched)
+            assert e.value.status == rsw_gpu.RSW_ERR_CONFIG
+    # the library stays usable
+    g = rsw_gpu.parareal_iterate(p, dev(u[0]), dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=1)
+    assert g["status"] == rsw_gpu.RSW_OK
+
+
+def test_auto_schedule_falls_back_to_bulk(rsw_gpu):
+    """AUTO must run the bulk schedule when the pipelined kernel cannot hold the
+    configuration (M/2 = 1250 sample pairs > 8 per coarse CTA x 148 co-resident CTAs); an explicit
+    PIPELINED request fails with RSW_ERR_CONFIG.  With M/2 = 500 pairs the coarse groups are re-sized
+    (8 pairs per CTA) and the pipelined schedule runs, bitwise equal to bulk."""
+    w = inputs.C1
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    for M, pipelined in ((2500, False), (1000, True)):
+        kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=M, n_slices=w.n_slices, max_iters=2)
+        a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_AUTO, **kw)
+        b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+        assert a["stats"]["pipelined"] == pipelined
+        assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
+        if not pipelined:
+            with pytest.raises(rsw_gpu.RSWError) as e:
+                rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
+            assert e.value.status == rsw_gpu.RSW_ERR_CONFIG
+
+
+@pytest.mark.parametrize("schedule", ["bulk", "pipelined"])
+def test_two_streams_share_the_workspace_safely(rsw_gpu, schedule):
+    """two parareal_iterate calls issued back to back on different streams (no stats, so the
+    first returns with its copies out of the workspace still queued) must not corrupt each other:
+    the library orders every call after the previous user of the workspace."""
+    import ctypes
+    w = inputs.C3
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    sch = rsw_gpu.SCHEDULE_BULK if schedule == "bulk" else rsw_gpu.SCHEDULE_PIPELINED
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=2, schedule=sch)
+    u0 = [dev(inputs.initial_state(w, seed=s)) for s in (0, 1)]
+    ref = [rsw_gpu.parareal_iterate(p, u, **kw)["U"].clone() for u in u0]
+    L = rsw_gpu.load()
+    cfg = rsw_gpu._PararealConfig(w.dT, w.dt, w.T0, 0.0, w.M, w.n_slices, 2, 0, 0, sch)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    out = [torch.full_like(ref[0], float("nan")) for _ in range(2)]
+    res = [(ctypes.c_double * 2)() for _ in range(2)]
+    its = [ctypes.c_int32() for _ in range(2)]
+    torch.cuda.synchronize()
+    for i in range(2):
+        rc = L.parareal_iterate(ctypes.byref(p._c()), ctypes.byref(cfg), ctypes.c_void_p(u0[i].data_ptr()),
+                                ctypes.c_void_p(out[i].data_ptr()), res[i], ctypes.byref(its[i]), None,
+                                ctypes.c_void_p(streams[i].cuda_stream))
+        assert rc == rsw_gpu.RSW_OK
+    torch.cuda.synchronize()
+    for i in range(2):
+        assert torch.equal(out[i], ref[i])
+
+
+def test_comm_world1_runs_the_nccl_exchange(rsw_gpu):
+    """a6 through the library on one GPU: a real NCCL communicator of world size 1 (rsw_nccl_unique_id,
+    rsw_comm_init, the in-place ncclAllGather of parareal_iterate) gives the bulk schedule's iterates
+    bitwise."""
+    import os
+    import socket
+    import torch.distributed as dist
     w = inputs.C3
     p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
     u0 = dev(inputs.initial_state(w))
-    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=max_iters, tol=tol)
-    a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
-    monkeypatch.setenv("RSW_PIPE_CLUSTER", "1")
-    b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
-    assert b["stats"]["pipelined"]
-    assert a["iters"] == b["iters"] and a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=2)
+    ref = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", torch.cuda.current_device()))
+    comm = None
+    try:
+        comm = rsw_gpu.Comm.from_torch_distributed()
+        g = rsw_gpu.parareal_iterate(p, u0, comm=comm, **kw)
+        assert not g["stats"]["pipelined"]
+        assert g["resid"] == ref["resid"] and torch.equal(g["U"], ref["U"])
+    finally:
+        if comm:
+            comm.close()
+        dist.destroy_process_group()
 
 
 def test_repeatability_soak(rsw_gpu):
