@@ -9,8 +9,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "librsw.so")
-SOURCES = ["rsw_k_fine.cu", "rsw_k_coarse.cu", "rsw_k_misc.cu", "rsw_pipeline.cu", "rsw_capi.cu"]
-HEADERS = ["rsw_device.cuh", "rsw_internal.h", "rsw_blocks.cuh"]
+SOURCES = ["rsw_pipe_256.cu", "rsw_pipe_128.cu", "rsw_pipe_64.cu", "rsw_k_coarse.cu", "rsw_k_fine.cu", "rsw_k_misc.cu",
+           "rsw_pipeline.cu", "rsw_capi.cu"]
+HEADERS = ["rsw_device.cuh", "rsw_internal.h", "rsw_blocks.cuh", "rsw_pipeline.cuh"]
 
 
 def _host_cxx() -> str:

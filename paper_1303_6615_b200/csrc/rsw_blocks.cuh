@@ -153,13 +153,14 @@ struct FineTmem {  // TMEM columns of one fine pair-group: per mode slot o, S1 /
 // TMEM layout of the group's thread-private slots: lane quarter = (CTA warp) mod 4; column block =
 // (group warp) / 4 (TBLK = false: groups own disjoint column ranges starting at tcol) or (CTA warp) / 4
 // (TBLK = true: tcol is the CTA's base and the groups of a CTA interleave, 3 blocks for 12 warps).
-template <int N, int R, int TG, int SCHEME, bool LIN, class GRP, bool TBLK = false>
+// TWT / twcol: twiddle policy of the FFT core (fft_tw_src) and, for TWT = 2, the TMEM column address of
+// the CTA's twiddle region (filled by the caller with tw_tmem_fill).
+template <int N, int R, int TG, int SCHEME, bool LIN, class GRP, bool TBLK = false, int TWT = 0>
 __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double2* Y, const FineSmemTab& st_,
                                               uint32_t tcol, const ModeGeom& gg, const double* uA,
                                               const double* uB, double* oA, double* oB, int m_steps, double h,
-                                              unsigned* hb = nullptr) {
+                                              unsigned* hb = nullptr, uint32_t twcol = 0) {
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, OMAX = FineTmem<N, TG>::OMAX;
-  constexpr double invN = 1.0 / N;
   const double2* sCP = st_.CP;
   const double* sC0 = st_.C0;
   const double* sGA = st_.GA;
@@ -171,6 +172,7 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
   grp.sync();
   // thread-private TMEM slot of mode slot o: columns o*36 + {S1: 0, S0: 12, S2: 24} + 4α
   const uint32_t tb = tcol + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(((TBLK ? warp : gwarp) >> 2) * OMAX * 36);
+  const uint32_t twt = twcol + ((uint32_t)(32 * (warp & 3)) << 16);
   double2 c0v[OMAX][3];
 #pragma unroll
   for (int o = 0; o < OMAX; ++o) {
@@ -191,9 +193,7 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
     tmem_st3(tb + o * 36, c0v[o]);
     if (!LIN && j < Kc) {
       const double as = kap < 0 ? -sGA[ak] : sGA[ak];
-      double2 u[3];
-      to_prim(as, sGP[ak], sGQ[ak], c0v[o], u);
-      put_input_z<N, R>(W, full_index(kap, N), (double)kap, u);
+      put_input_eigen<N, R>(W, full_index(kap, N), (double)kap, as, sGP[ak], sGQ[ak], c0v[o]);
     }
   }
   tmem_wait_st();
@@ -205,7 +205,7 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
     const bool last_step = (step == m_steps - 1);
     if (hb && t == 0 && (step & 7) == 7) atomicAdd(hb, 1u);  // pipelined: heartbeat of the watchdog
     for (int st = 0; st < nst; ++st) {
-      if (!LIN) nl_core<N, R, TG>(W, Y, st_.TW, grp);
+      if (!LIN) nl_core<N, R, TG, GRP, TWT>(W, Y, st_.TW, grp, twt);
       // epilogue (this stage's update) fused with the prologue of the next N-eval (rolled when a
       // thread owns many modes: an unrolled body of 4 modes spills at 168 registers)
 #pragma unroll (OMAX > 2 ? 1 : OMAX)
@@ -225,9 +225,7 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
         const double p = sGP[ak], q = sGQ[ak];
         double2 nn[3];
         if (!LIN && valid) {
-          double2 nh[3];
-          get_output_z<N, R>(W, kf, (double)kap, invN, nh);
-          to_eigen(as, p, q, nh, nn);
+          get_output_eigen<N, R>(W, kf, (double)kap, as, p, q, nn);
         } else {
 #pragma unroll
           for (int al = 0; al < 3; ++al) nn[al] = make_double2(0.0, 0.0);
@@ -301,11 +299,7 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
           tmem_st3(ts + 12, s0);
           tmem_st3(ts + 24, s2);
         }
-        if (!LIN && valid) {
-          double2 u[3];
-          to_prim(as, p, q, x, u);
-          put_input_z<N, R>(W, kf, (double)kap, u);
-        }
+        if (!LIN && valid) put_input_eigen<N, R>(W, kf, (double)kap, as, p, q, x);
       }
       tmem_wait_st();
       grp.sync();

@@ -68,6 +68,28 @@ __device__ __forceinline__ void dft4(double2& v0, double2& v1, double2& v2, doub
   v3 = csub(t1, t3);
 }
 
+// e ± o·w for a compile-time twiddle w = (c, σ) in FMA form (6 DP instructions instead of a complex
+// multiply plus two complex adds): o·w = f·u with u = o + i (σ/c) o, f = c when |c| >= |σ|, or
+// u = (c/σ) o + i o, f = σ otherwise (the ratio is <= 1 in magnitude), then e ± f u by FMAs.
+template <int SIGN>
+__device__ __forceinline__ void tw_butterfly(double2& lo, double2& hi, const double2 e, const double2 o, const double c,
+                                             const double sg) {
+  const bool cf = (c >= 0 ? c : -c) >= (sg >= 0 ? sg : -sg);
+  double2 u;
+  double f;
+  if (cf) {
+    const double r = sg / c;
+    u = make_double2(fma(-r, o.y, o.x), fma(r, o.x, o.y));
+    f = c;
+  } else {
+    const double r = c / sg;
+    u = make_double2(fma(r, o.x, -o.y), fma(r, o.y, o.x));
+    f = sg;
+  }
+  lo = make_double2(fma(f, u.x, e.x), fma(f, u.y, e.y));
+  hi = make_double2(fma(-f, u.x, e.x), fma(-f, u.y, e.y));
+}
+
 template <int SIGN>
 __device__ __forceinline__ void dft8(double2* v) {
   const double s = 0.70710678118654752440084436210485;  // 1/sqrt(2)
@@ -75,18 +97,19 @@ __device__ __forceinline__ void dft8(double2* v) {
   double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
   dft4<SIGN>(e0, e1, e2, e3);
   dft4<SIGN>(o0, o1, o2, o3);
-  // w8^q = e^{SIGN 2πi q/8}: q=1: s(1 + SIGN i), q=2: SIGN i, q=3: s(-1 + SIGN i)
-  double2 t1 = make_double2(s * (o1.x - SIGN * o1.y), s * (o1.y + SIGN * o1.x));
-  double2 t2 = rot90<SIGN>(o2);
-  double2 t3 = make_double2(s * (-o3.x - SIGN * o3.y), s * (-o3.y + SIGN * o3.x));
+  // w8^q = e^{SIGN 2πi q/8}: q=1: s(1 + SIGN i), q=2: SIGN i, q=3: s(-1 + SIGN i); the factor s is
+  // applied by the FMAs of the output pair
+  const double2 u1 = make_double2(o1.x - SIGN * o1.y, o1.y + SIGN * o1.x);
+  const double2 u3 = make_double2(-o3.x - SIGN * o3.y, -o3.y + SIGN * o3.x);
+  const double2 t2 = rot90<SIGN>(o2);
   v[0] = cadd(e0, o0);
   v[4] = csub(e0, o0);
-  v[1] = cadd(e1, t1);
-  v[5] = csub(e1, t1);
+  v[1] = make_double2(fma(s, u1.x, e1.x), fma(s, u1.y, e1.y));
+  v[5] = make_double2(fma(-s, u1.x, e1.x), fma(-s, u1.y, e1.y));
   v[2] = cadd(e2, t2);
   v[6] = csub(e2, t2);
-  v[3] = cadd(e3, t3);
-  v[7] = csub(e3, t3);
+  v[3] = make_double2(fma(s, u3.x, e3.x), fma(s, u3.y, e3.y));
+  v[7] = make_double2(fma(-s, u3.x, e3.x), fma(-s, u3.y, e3.y));
 }
 
 template <int SIGN>
@@ -102,18 +125,19 @@ __device__ __forceinline__ void dft16(double2* v) {
   }
   dft8<SIGN>(e);
   dft8<SIGN>(o);
-  const double2 w[8] = {make_double2(1.0, 0.0),      make_double2(c1, SIGN * s1),  make_double2(h, SIGN * h),
-                        make_double2(s1, SIGN * c1), make_double2(0.0, SIGN * 1.0), make_double2(-s1, SIGN * c1),
-                        make_double2(-h, SIGN * h),  make_double2(-c1, SIGN * s1)};
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    double2 t;
-    if (q == 0) t = o[0];
-    else if (q == 4) t = rot90<SIGN>(o[4]);
-    else t = cmul(o[q], w[q]);
-    v[q] = cadd(e[q], t);
-    v[q + 8] = csub(e[q], t);
+  // w16^q = (cos, SIGN sin)(2π q/16)
+  const double cs[8] = {1.0, c1, h, s1, 0.0, -s1, -h, -c1};
+  const double sn[8] = {0.0, s1, h, c1, 1.0, c1, h, s1};
+  v[0] = cadd(e[0], o[0]);
+  v[8] = csub(e[0], o[0]);
+  {
+    const double2 t = rot90<SIGN>(o[4]);
+    v[4] = cadd(e[4], t);
+    v[12] = csub(e[4], t);
   }
+#pragma unroll
+  for (int q = 1; q < 8; ++q)
+    if (q != 4) tw_butterfly<SIGN>(v[q], v[q + 8], e[q], o[q], cs[q], SIGN * sn[q]);
 }
 
 template <int SIGN>
@@ -261,30 +285,67 @@ __host__ __device__ constexpr int fft_len(int p) {  // block length L_p
   for (int q = 0; q < p; ++q) L /= fft_rad<N, R>(q);
   return L;
 }
+// Twiddles of pass p: radix >= 8 passes of the large transforms (N >= 512) read every power from a
+// full table TW[off_p + (s-1) d_p + k1] = e^{-2πi s k1 / L_p}, s = 1..r-1 (exact table values, one
+// shared-memory load per twiddle instead of forming the 15 powers of a radix-16 butterfly in
+// registers: ~60 DP instructions per butterfly, ~20% of the transform); the other passes store the
+// bases e^{-2πi k1 / L_p} only and form the powers in registers (small radices, or the latency-bound
+// small transforms, where the product chain was measured faster than the loads).
 template <int N, int R>
-__host__ __device__ constexpr int fft_tw_off(int p) {  // offset of pass p's twiddle bases
+__host__ __device__ constexpr bool fft_tw_full(int p) { return N >= 512 && fft_rad<N, R>(p) >= 8; }
+template <int N, int R>
+__host__ __device__ constexpr int fft_tw_len(int p) {  // table entries of pass p (last pass: none)
+  return (p >= fft_npass<N, R>() - 1) ? 0
+         : (fft_tw_full<N, R>(p) ? (fft_rad<N, R>(p) - 1) : 1) * (fft_len<N, R>(p) / fft_rad<N, R>(p));
+}
+template <int N, int R>
+__host__ __device__ constexpr int fft_tw_off(int p) {  // offset of pass p's twiddles
   int o = 0;
-  for (int q = 0; q < p; ++q) o += fft_len<N, R>(q) / fft_rad<N, R>(q);
+  for (int q = 0; q < p; ++q) o += fft_tw_len<N, R>(q);
   return o;
 }
-// twiddle bases TW[off_p + k1] = e^{-2πi k1 / L_p}, k1 < d_p, for the passes p < m-1 (the last pass
-// has d = 1 and no twiddles)
+// size of the twiddle table for the passes p < m-1 (the last pass has d = 1 and no twiddles)
 template <int N, int R>
 __host__ __device__ constexpr int fft_tw_size() { return fft_tw_off<N, R>(fft_npass<N, R>() - 1) > 0 ? fft_tw_off<N, R>(fft_npass<N, R>() - 1) : 1; }
 
-// fill the twiddle bases from the plain table tw[m] = e^{-2πi m/N} (threads t0, t0 + T, ...)
+// Twiddle source of pass p for a kernel's policy TWT (only passes with a full table differ):
+//   0 = powers formed in registers from the base (the s = 1 row of the full table),
+//   1 = the full shared-memory table,
+//   2 = the full table copied once into the thread's own TMEM lane (passes of radix R: each thread has
+//       ONE butterfly there, so its r-1 twiddles are fixed for the whole kernel) — loaded with
+//       tcgen05.ld, which takes those reads off the shared-memory pipe (the binding resource of the
+//       n = 1024 fine kernel: 81% of peak wavefronts with the smem table, 72% with register powers).
+template <int N, int R, int TWT>
+__host__ __device__ constexpr int fft_tw_src(int p) {
+  return (p >= fft_npass<N, R>() - 1 || !fft_tw_full<N, R>(p)) ? 0
+         : (TWT == 2 && fft_rad<N, R>(p) == R) ? 2 : (TWT == 0 ? 0 : 1);
+}
+// TMEM columns of pass p's twiddles (chunks of 3 complex = 12 columns) and their total
+template <int N, int R>
+__host__ __device__ constexpr int fft_tw_tcol(int p) {
+  int o = 0;
+  for (int q = 0; q < p; ++q)
+    if (fft_tw_src<N, R, 2>(q) == 2) o += (fft_rad<N, R>(q) + 1) / 3 * 12;
+  return o;
+}
+template <int N, int R>
+__host__ __device__ constexpr int fft_tw_tcols() { return fft_tw_tcol<N, R>(fft_npass<N, R>()); }
+
+// fill the twiddle table from the plain table tw[m] = e^{-2πi m/N} (threads t0, t0 + T, ...)
 template <int N, int R, int T>
 __device__ __forceinline__ void fill_packed_twiddles(double2* TW, const double2* __restrict__ tw, int t0 = -1, int nthr = T) {
   constexpr int m = fft_npass<N, R>();
   for (int i = (t0 < 0 ? (int)threadIdx.x : t0); i < fft_tw_off<N, R>(m - 1); i += nthr) {
     int p = 0;
     while (p < m - 2 && i >= fft_tw_off<N, R>(p + 1)) ++p;
-    TW[i] = __ldg(tw + (i - fft_tw_off<N, R>(p)) * (N / fft_len<N, R>(p)));
+    const int li = i - fft_tw_off<N, R>(p), L = fft_len<N, R>(p), d = L / fft_rad<N, R>(p);
+    const int sk = fft_tw_full<N, R>(p) ? (li / d + 1) * (li % d) : li;  // s k1 (< L)
+    TW[i] = __ldg(tw + sk * (N / L));
   }
 }
 
 __device__ __forceinline__ double2 csqr(double2 a) {  // a^2
-  return make_double2((a.x + a.y) * (a.x - a.y), (a.x + a.x) * a.y);
+  return make_double2(fma(a.x, a.x, -a.y * a.y), (a.x + a.x) * a.y);
 }
 
 // v[s] *= w^s (CONJ: conj(w)^s), s = 1..r-1, for a twiddle base w read from the shared table; the
@@ -292,6 +353,57 @@ __device__ __forceinline__ double2 csqr(double2 a) {  // a^2
 // w^{8+s} = w^8·w^s: at most 5 roundings deep, error ≲ 5 ulp): the shared-memory pipe is the binding
 // resource of the FFT core (ncu, n = 1024: 80% of peak wavefronts, twiddle loads ~23% of them),
 // while the FP64 pipe has room.
+// v[s] *= TWs[(s-1) d] (CONJ: its conjugate), s = 1..r-1: full-table twiddles of one butterfly
+template <int r, bool CONJ>
+__device__ __forceinline__ void apply_twiddles_tab(double2* v, const double2* TWs, int d) {
+#pragma unroll
+  for (int s = 1; s < r; ++s) v[s] = CONJ ? cmulc(v[s], TWs[(s - 1) * d]) : cmul(v[s], TWs[(s - 1) * d]);
+}
+
+// TMEM twiddles: chunk c of a pass's slot holds s = 3c+1 .. 3c+3 (12 columns); loads are issued one
+// chunk ahead of their use.  The wait names the chunk's registers as in/out operands, so no use of
+// them can be scheduled before the asynchronous load completed.
+__device__ __forceinline__ void tmem_ld12_issue(uint32_t ta, uint32_t (&r)[12]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+      : "r"(ta)
+      : "memory");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
+               : "r"(ta + 8)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait12(uint32_t (&r)[12]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11])
+               :
+               : "memory");
+}
+template <int r, bool CONJ>
+__device__ __forceinline__ void apply_twiddles_tmem(double2* v, uint32_t ta) {
+  constexpr int NCH = (r + 1) / 3;  // chunks covering s = 1..r-1
+  uint32_t ca[12], cb[12];
+  tmem_ld12_issue(ta, ca);
+  tmem_wait12(ca);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    uint32_t(&cur)[12] = (c & 1) ? cb : ca;
+    uint32_t(&nxt)[12] = (c & 1) ? ca : cb;
+    if (c + 1 < NCH) tmem_ld12_issue(ta + 12 * (c + 1), nxt);
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int sidx = 3 * c + 1 + u;
+      if (sidx < r) {
+        const double2 w = make_double2(__hiloint2double(cur[4 * u + 1], cur[4 * u]), __hiloint2double(cur[4 * u + 3], cur[4 * u + 2]));
+        v[sidx] = CONJ ? cmulc(v[sidx], w) : cmul(v[sidx], w);
+      }
+    }
+    if (c + 1 < NCH) tmem_wait12(nxt);
+  }
+}
+
 template <int r, bool CONJ>
 __device__ __forceinline__ void apply_twiddles(double2* v, const double2 w1) {
 #define TWM(s, w) v[s] = CONJ ? cmulc(v[s], w) : cmul(v[s], w)
@@ -326,9 +438,9 @@ __device__ __forceinline__ int fft_elem0(int b) {  // first element of butterfly
 }
 
 // synthesis passes p..m-1 of field buffer Xf (sign +); the last pass leaves its outputs in v
-template <int N, int R, int p, class GRP>
+template <int N, int R, int p, int TWT, class GRP>
 __device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* Xf, int j, bool act, const double2* TW,
-                                             const GRP& grp) {
+                                             uint32_t twt, const GRP& grp) {
   constexpr int m = fft_npass<N, R>(), r = fft_rad<N, R>(p), L = fft_len<N, R>(p), d = L / r, NJ = N / R;
   constexpr int K = N / 3;
   if (act) {
@@ -344,7 +456,10 @@ __device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* Xf, int j
       }
       dftR<r, +1>(&v[i * r]);
       if constexpr (p < m - 1) {
-        apply_twiddles<r, true>(&v[i * r], TW[fft_tw_off<N, R>(p) + (b % d)]);  // ω_L^{+s k1}
+        if constexpr (fft_tw_src<N, R, TWT>(p) == 2) apply_twiddles_tmem<r, true>(&v[i * r], twt + fft_tw_tcol<N, R>(p));
+        else if constexpr (fft_tw_src<N, R, TWT>(p) == 1)
+          apply_twiddles_tab<r, true>(&v[i * r], TW + fft_tw_off<N, R>(p) + (b % d), d);
+        else apply_twiddles<r, true>(&v[i * r], TW[fft_tw_off<N, R>(p) + (b % d)]);  // ω_L^{+s k1}
 #pragma unroll
         for (int s = 0; s < r; ++s) Xf[fpad<R>(e0) + fpad<R>(d * s)] = v[i * r + s];
       }
@@ -352,14 +467,14 @@ __device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* Xf, int j
   }
   if constexpr (p < m - 1) {
     grp.sync();
-    core_inverse<N, R, p + 1>(v, Xf, j, act, TW, grp);
+    core_inverse<N, R, p + 1, TWT>(v, Xf, j, act, TW, twt, grp);
   }
 }
 
 // analysis passes p, p-1, ..., 0 (sign -); pass 0 stores the retained modes only
-template <int N, int R, int p, class GRP>
+template <int N, int R, int p, int TWT, class GRP>
 __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j, bool act, const double2* TW,
-                                             const GRP& grp) {
+                                             uint32_t twt, const GRP& grp) {
   if constexpr (p >= 0) {
     constexpr int r = fft_rad<N, R>(p), L = fft_len<N, R>(p), d = L / r, NJ = N / R;
     constexpr int K = N / 3;
@@ -370,7 +485,10 @@ __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j
         double2* xb = Xf + fpad<R>(e0);
 #pragma unroll
         for (int s = 0; s < r; ++s) v[i * r + s] = xb[fpad<R>(d * s)];
-        apply_twiddles<r, false>(&v[i * r], TW[fft_tw_off<N, R>(p) + (b % d)]);  // e^{-2πi s k1/L}
+        if constexpr (fft_tw_src<N, R, TWT>(p) == 2) apply_twiddles_tmem<r, false>(&v[i * r], twt + fft_tw_tcol<N, R>(p));
+        else if constexpr (fft_tw_src<N, R, TWT>(p) == 1)
+          apply_twiddles_tab<r, false>(&v[i * r], TW + fft_tw_off<N, R>(p) + (b % d), d);
+        else apply_twiddles<r, false>(&v[i * r], TW[fft_tw_off<N, R>(p) + (b % d)]);  // e^{-2πi s k1/L}
         dftR<r, -1>(&v[i * r]);
 #pragma unroll
         for (int s = 0; s < r; ++s) {
@@ -380,7 +498,7 @@ __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j
       }
     }
     grp.sync();
-    core_forward<N, R, p - 1>(v, Xf, j, act, TW, grp);
+    core_forward<N, R, p - 1, TWT>(v, Xf, j, act, TW, twt, grp);
   }
 }
 
@@ -388,9 +506,11 @@ __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j
 // padded layout, then V (the v1 copy) at 3 FS — holds the retained spectra of (v1, iκ v2, h) on entry
 // and the retained spectra of (v1²/2, v1 v2x, h v1) (unnormalised) on exit.  The second argument is
 // unused (kept for the callers' layouts, which reserve >= nl_buf entries from X).  2m barriers
-// (m = passes), the last one on exit.
-template <int N, int R, int T, class GRP = CtaGroup>
-__device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const double2* TW, const GRP& grp = GRP()) {
+// (m = passes), the last one on exit.  TWT: twiddle policy (fft_tw_src); with TWT = 2, twt is the
+// thread's TMEM address of its twiddle slots (lane quarter + column base, filled by tw_tmem_fill).
+template <int N, int R, int T, class GRP = CtaGroup, int TWT = 1>
+__device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const double2* TW, const GRP& grp = GRP(),
+                                        uint32_t twt = 0) {
   static_assert(T >= 3 * (N / R), "nl_core: T must cover 3 N/R field-columns");
   constexpr int m = fft_npass<N, R>(), NJ = N / R, K = N / 3;
   constexpr int rl = fft_rad<N, R>(m - 1), Ll = fft_len<N, R>(m - 1), dl = Ll / rl;
@@ -402,7 +522,7 @@ __device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const d
   double2* Xf = X + (act ? f : 0) * FS;
   double2* V = X + 3 * FS + fpad<R>(j * R);
   double2 v[R];
-  core_inverse<N, R, 0>(v, Xf, j, act, TW, grp);
+  core_inverse<N, R, 0, TWT>(v, Xf, j, act, TW, twt, grp);
   // grid products (R1, R10): the last synthesis pass left the grid values of positions j R + s in
   // registers; v1 is shared with the v2x / h threads through V
   if (act && f == 0) {
@@ -431,7 +551,7 @@ __device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const d
     }
   }
   grp.sync();
-  core_forward<N, R, m - 2>(v, Xf, j, act, TW, grp);
+  core_forward<N, R, m - 2, TWT>(v, Xf, j, act, TW, twt, grp);
 }
 
 // N-eval input / output of one retained entry in the padded layout of nl_core
@@ -451,6 +571,40 @@ __device__ __forceinline__ void get_output_z(const double2* X, int k_full, doubl
   nh[0] = cmulmi(cscale(Q0, kap));  // -iκ Q0
   nh[1] = make_double2(-Q1.x, -Q1.y);
   nh[2] = cmulmi(cscale(Q2, kap));  // -iκ Q2
+}
+
+// The same two maps fused with the eigenbasis change (per mode: 14 DP instructions plus 4-5
+// scalar products instead of ~32 / ~20): the FFT output of a retained entry straight into eigen
+// coordinates, nn = R^H diag(-iκ, -1, -iκ) Z / N, i.e. (with as = κ/√F, s = 1/√2)
+//   c∓ = -(p/N)(Z1 + as κ Z2) ± (s κ/N) Z0,   c0 = -i (q/N)(κ Z2 - as Z1);
+// and an eigen state into the FFT input, (u0, iκ u1, u2) with u = R c, i.e. with d = c+ - c-,
+// e = c+ + c-:  X0 = i s d,  X1 = iκ p e - κ as q c0,  X2 = q c0 + i as p e.
+template <int N, int R>
+__device__ __forceinline__ void get_output_eigen(const double2* X, int k_full, double kap, double as, double p,
+                                                 double q, double2* nn) {
+  constexpr int FS = fft_fs<N, R>();
+  constexpr double invN = 1.0 / N, sN = 0.70710678118654752440084436210485 / N;
+  const int i = fpad<R>(k_full);
+  const double2 X0 = X[i], X1 = X[FS + i], X2 = X[2 * FS + i];
+  const double ak = as * kap, sk = sN * kap, pn = p * invN, qn = q * invN;
+  const double2 T = make_double2(fma(ak, X2.x, X1.x), fma(ak, X2.y, X1.y));
+  const double2 A = make_double2(sk * X0.x, sk * X0.y);
+  nn[0] = make_double2(fma(-pn, T.x, A.x), fma(-pn, T.y, A.y));
+  nn[2] = make_double2(fma(-pn, T.x, -A.x), fma(-pn, T.y, -A.y));
+  const double2 W = make_double2(fma(kap, X2.x, -as * X1.x), fma(kap, X2.y, -as * X1.y));
+  nn[1] = make_double2(qn * W.y, -qn * W.x);
+}
+template <int N, int R>
+__device__ __forceinline__ void put_input_eigen(double2* X, int k_full, double kap, double as, double p, double q,
+                                                const double2* c) {
+  constexpr int FS = fft_fs<N, R>();
+  constexpr double s = 0.70710678118654752440084436210485;
+  const int i = fpad<R>(k_full);
+  const double2 d = csub(c[2], c[0]), e = cadd(c[2], c[0]);
+  const double kp = kap * p, kaq = kap * as * q, ap = as * p;
+  X[i] = make_double2(-s * d.y, s * d.x);
+  X[FS + i] = make_double2(fma(-kp, e.y, -kaq * c[1].x), fma(kp, e.x, -kaq * c[1].y));
+  X[2 * FS + i] = make_double2(fma(q, c[1].x, -ap * e.y), fma(q, c[1].y, ap * e.x));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -540,6 +694,33 @@ __device__ __forceinline__ void tmem_st3(uint32_t taddr, const double2 (&x)[3]) 
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr + 8), "r"(r[8]),
                "r"(r[9]), "r"(r[10]), "r"(r[11])
                : "memory");
+}
+
+// Copy this thread's TMEM-sourced twiddles (fft_tw_src == 2: radix-R passes, one butterfly b = j per
+// thread) from the staged shared-memory table into its own TMEM lane at twt.  Warp-collective: every
+// thread of the warp calls it.  Warps sharing a lane quarter write their lanes with the same values
+// in the layouts used (k1 = j mod d depends on the lane only, or on a column half the quarter fixes).
+template <int N, int R, int TWT>
+__device__ __forceinline__ void tw_tmem_fill(const double2* TW, uint32_t twt, int t) {
+  if constexpr (TWT == 2) {
+    constexpr int m = fft_npass<N, R>(), NJ = N / R;
+    const int j = t % NJ;
+#pragma unroll
+    for (int p = 0; p < m - 1; ++p) {
+      if (fft_tw_src<N, R, 2>(p) == 2) {
+        const int r = fft_rad<N, R>(p), d = fft_len<N, R>(p) / r, k1 = j % d;
+        for (int c = 0; c < (r + 1) / 3; ++c) {
+          double2 w[3];
+#pragma unroll
+          for (int u = 0; u < 3; ++u) {
+            const int sidx = 3 * c + 1 + u;
+            w[u] = sidx < r ? TW[fft_tw_off<N, R>(p) + (sidx - 1) * d + k1] : make_double2(0.0, 0.0);
+          }
+          tmem_st3(twt + fft_tw_tcol<N, R>(p) + 12 * c, w);
+        }
+      }
+    }
+  }
 }
 
 __device__ __forceinline__ int full_index(int kap, int N) { return kap >= 0 ? kap : kap + N; }

@@ -29,6 +29,10 @@ static cudaError_t set_smem(KernelT k, size_t bytes) {
 // NPG = 1); group g advances slices 2(NPG b + g), +1.  Shared memory: per group the N-eval buffer W
 // (3N) and the v1 copy V (N), then the tables shared by the groups (twiddle bases, ETDRK4 / Strang
 // coefficients, geometry).  TMEM: the groups' thread-private state slots interleave (TBLK layout).
+#ifndef RSW_FINE_TWT
+#define RSW_FINE_TWT 2  // twiddle policy of the n >= 512 transforms (fft_tw_src): TMEM copies of the radix-R passes
+#endif
+
 template <int N, int R, int TG, int NPG>
 struct FineLayout {  // dynamic shared memory of k_fine (double2 units first, then doubles)
   static constexpr int K = N / 3, KP = K + 1, Kc = 2 * K + 1;
@@ -37,7 +41,9 @@ struct FineLayout {  // dynamic shared memory of k_fine (double2 units first, th
   static constexpr int ND = 9 * KP;  // C0 [6][KP], GA, GP, GQ
   static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
   static constexpr int T = NPG * TG, OMAX = (Kc + TG - 1) / TG, BLKS = (T / 32 + 3) / 4;
-  static constexpr int NCOL = tmem_cols_pow2<BLKS * OMAX * 36>();
+  static constexpr int TWC = BLKS * OMAX * 36;  // TMEM: state slots, then the twiddle copies (TWT = 2)
+  static constexpr int TWT = (TWC + fft_tw_tcols<N, R>() <= 512) ? RSW_FINE_TWT : (RSW_FINE_TWT == 2 ? 1 : RSW_FINE_TWT);
+  static constexpr int NCOL = tmem_cols_pow2<TWC + (TWT == 2 ? fft_tw_tcols<N, R>() : 0)>();
   static_assert(BLKS * OMAX * 36 <= 512, "k_fine: TMEM state does not fit");
 };
 
@@ -55,6 +61,13 @@ __global__ void __launch_bounds__(NPG * TG) k_fine(const double* u_in, double* u
   __syncthreads();
   tmem_fence_after();
   const int g = (NPG == 1) ? 0 : (int)threadIdx.x / TG;
+  if constexpr (LY::TWT == 2) {  // each thread's radix-R twiddles into its TMEM lane
+    tw_tmem_fill<N, R, 2>(st_.TW, tslot + LY::TWC + ((uint32_t)(32 * ((threadIdx.x >> 5) & 3)) << 16), (int)threadIdx.x - g * TG);
+    tmem_wait_st();
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+  }
   const int sA = 2 * (NPG * blockIdx.x + g), sB = sA + 1;
   const size_t L = (size_t)3 * NH * 2;
   if (sA < n_slices) {
@@ -64,11 +77,12 @@ __global__ void __launch_bounds__(NPG * TG) k_fine(const double* u_in, double* u
     double* oA = u_out + sA * L;
     double* oB = (sB < n_slices) ? u_out + sB * L : nullptr;
     if constexpr (NPG == 1)
-      fine_pair_run<N, R, TG, SCHEME, LIN, CtaGroup, true>(CtaGroup(), W, nullptr, st_, tslot, tab.g, uA, uB, oA, oB,
-                                                           m_steps, h);
+      fine_pair_run<N, R, TG, SCHEME, LIN, CtaGroup, true, LY::TWT>(CtaGroup(), W, nullptr, st_, tslot, tab.g, uA, uB, oA,
+                                                                    oB, m_steps, h, nullptr, tslot + LY::TWC);
     else
-      fine_pair_run<N, R, TG, SCHEME, LIN, NamedGroup, true>(NamedGroup{g * TG, 1 + g, TG}, W, nullptr, st_, tslot,
-                                                             tab.g, uA, uB, oA, oB, m_steps, h);
+      fine_pair_run<N, R, TG, SCHEME, LIN, NamedGroup, true, LY::TWT>(NamedGroup{g * TG, 1 + g, TG}, W, nullptr, st_, tslot,
+                                                                      tab.g, uA, uB, oA, oB, m_steps, h, nullptr,
+                                                                      tslot + LY::TWC);
   }
   tmem_fence_before();
   __syncthreads();

@@ -99,10 +99,15 @@ __global__ void __launch_bounds__(T) k_nonlinear(const double* u_in, double* out
 #ifndef RSW_AVG_MINB
 #define RSW_AVG_MINB 1
 #endif
-template <int N, int T>
+#ifndef RSW_AVG_TWT
+#define RSW_AVG_TWT 2  // twiddle policy of the n >= 512 transforms (fft_tw_src): TMEM copies of the radix-R passes
+#endif
+template <int N, int T, int R>
 struct AvgTmem {
   static constexpr int Kc = 2 * (N / 3) + 1, OMAX = (Kc + T - 1) / T, BLKS = (T / 32 + 3) / 4;
-  static constexpr int NCOL = tmem_cols_pow2<BLKS * OMAX * 24>();
+  static constexpr int TWC = BLKS * OMAX * 24;  // state / accumulator slots, then the twiddle copies
+  static constexpr int TWT = (TWC + fft_tw_tcols<N, R>() <= 512) ? RSW_AVG_TWT : (RSW_AVG_TWT == 2 ? 1 : RSW_AVG_TWT);
+  static constexpr int NCOL = tmem_cols_pow2<TWC + (TWT == 2 ? fft_tw_tcols<N, R>() : 0)>();
   static_assert(BLKS * OMAX * 24 <= 512, "k_avg_states: TMEM slots do not fit");
 };
 
@@ -118,9 +123,8 @@ template <int N, int R, int T>
 __global__ void __launch_bounds__(T, RSW_AVG_MINB) k_avg_states(const double* u_in, double* out, int n_states, int M,
                                                   const AvgTab tab) {
   using LY = AvgLayout<N, R, T>;
-  using TM = AvgTmem<N, T>;
+  using TM = AvgTmem<N, T, R>;
   constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1, KP = K + 1, OMAX = TM::OMAX;
-  constexpr double invN = 1.0 / N;
   extern __shared__ double2 smem[];
   __shared__ uint32_t tslot;
   double2* X = smem + LY::X;
@@ -137,6 +141,11 @@ __global__ void __launch_bounds__(T, RSW_AVG_MINB) k_avg_states(const double* u_
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
+  const uint32_t twt = tslot + TM::TWC + ((uint32_t)(32 * (warp & 3)) << 16);
+  if constexpr (TM::TWT == 2) {  // each thread's radix-R twiddles into its TMEM lane (the table is staged above)
+    tw_tmem_fill<N, R, 2>(smem + LY::TW, twt, (int)threadIdx.x);
+    tmem_wait_st();
+  }
   const uint32_t tb = tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * OMAX * 24);
   double2 ph[OMAX];
   {
@@ -157,12 +166,11 @@ __global__ void __launch_bounds__(T, RSW_AVG_MINB) k_avg_states(const double* u_
       if (j < Kc) {
         const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
         ph[o] = __ldg(tab.phase + (size_t)1 * KP + ak);  // e^{iωτ_1}
-        double2 c[3], u[3];
+        double2 c[3];
         c[0] = cmul(cc[o][0], ph[o]);   // α=-1: e^{+iωτ}
         c[1] = cc[o][1];                // α=0
         c[2] = cmulc(cc[o][2], ph[o]);  // α=+1: e^{-iωτ}
-        to_prim(kap < 0 ? -GA[ak] : GA[ak], GP[ak], GQ[ak], c, u);
-        put_input_z<N, R>(X, full_index(kap, N), (double)kap, u);
+        put_input_eigen<N, R>(X, full_index(kap, N), (double)kap, kap < 0 ? -GA[ak] : GA[ak], GP[ak], GQ[ak], c);
       }
     }
     tmem_wait_st();
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(T, RSW_AVG_MINB) k_avg_states(const double* u_
       const int kap = kappa_of(j < Kc ? j : 0, K), ak = kap < 0 ? -kap : kap;
       phn[o] = (j < Kc && m + 1 <= M - 1) ? __ldg(tab.phase + (size_t)(m + 1) * KP + ak) : make_double2(1.0, 0.0);
     }
-    nl_core<N, R, T>(X, nullptr, smem + LY::TW);
+    nl_core<N, R, T, CtaGroup, TM::TWT>(X, nullptr, smem + LY::TW, CtaGroup(), twt);
     const double wm = __ldg(tab.w + m);
 #pragma unroll
     for (int o = 0; o < OMAX; ++o) {
@@ -189,19 +197,17 @@ __global__ void __launch_bounds__(T, RSW_AVG_MINB) k_avg_states(const double* u_
         const int kf = full_index(kap, N);
         const double as = kap < 0 ? -GA[ak] : GA[ak];
         const double p = GP[ak], q = GQ[ak];
-        double2 nh[3], nn[3];
-        get_output_z<N, R>(X, kf, (double)kap, invN, nh);
-        to_eigen(as, p, q, nh, nn);
+        double2 nn[3];
+        get_output_eigen<N, R>(X, kf, (double)kap, as, p, q, nn);
         acc[0] = caxpy(wm, cmulc(nn[0], ph[o]), acc[0]);  // α=-1: e^{-iωτ}
         acc[1] = caxpy(wm, nn[1], acc[1]);                // α=0
         acc[2] = caxpy(wm, cmul(nn[2], ph[o]), acc[2]);   // α=+1: e^{+iωτ}
         if (m + 1 <= M - 1) {
-          double2 c[3], u[3];
+          double2 c[3];
           c[0] = cmul(cc[0], phn[o]);
           c[1] = cc[1];
           c[2] = cmulc(cc[2], phn[o]);
-          to_prim(as, p, q, c, u);
-          put_input_z<N, R>(X, kf, (double)kap, u);
+          put_input_eigen<N, R>(X, kf, (double)kap, as, p, q, c);
         }
       }
       tmem_st3(tb + o * 24 + 12, acc);

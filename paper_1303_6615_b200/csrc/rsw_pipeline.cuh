@@ -1,0 +1,404 @@
+// rsw_pipeline.cuh — pipelined parareal as ONE persistent cooperative kernel.
+//
+// The bulk-synchronous schedule (rsw_capi.cu) runs, per iteration, the fine sweep over every slice
+// and then the serial coarse sweep; the GPU is almost idle during the sweep (one sample pair per
+// SM, a latency-bound chain of 4S stages).  The data dependencies of the iteration (Eq. "HMM parareal
+// iteration" P:428-430, Alg.4) are finer than that:
+//     F(U^k_n)        needs U^k_n only                       (sweep k, slice n-1)
+//     U^k_{n+1}      = G(U^k_n) + F(U^{k-1}_n) - G(U^{k-1}_n)  needs sweep k at slice n, the fine
+//                     solve of U^{k-1}_n and sweep k-1 at slice n
+// so sweep k can trail sweep k-1 by one fine-slice latency, and the fine solves fill the SMs the
+// sweeps leave idle (P:433-438 notes the slices "can be computed as soon as" their input exists).
+// The values computed are exactly those of the bulk schedule (same kernels' arithmetic, same fixed
+// reduction orders), so the iterates, residuals and iteration counts are bitwise identical.
+//
+// Roles (by arrival ticket; 2 CTAs per SM, all co-resident):
+//   * NG coarse groups of GC CTAs: group g runs sweeps k = g, g+NG, ... (rsw_blocks.cuh phases with a
+//     group-local barrier counter and stage-input buffers); after every slice each CTA bumps
+//     prog[k] (release); the finalize of slice n waits for doneF[k-1][n/2] and prog[k-1] (acquire).
+//   * fine workers: NPG thread groups per CTA (named barriers), each claims the lowest-iteration
+//     ready pair task (k, p) (slices 2p, 2p+1 of U^k; ready when prog[k] covers them), runs the
+//     fine pair integrator (state in TMEM), writes F^k and sets doneF[k][p] (release).
+// Stop rule (tol > 0): the group that finishes sweep k computes r_k; the first r_k < tol (or a
+// divergence) lowers stopk; later sweeps abort at their next group barrier (the abort travels in
+// the barrier counter, so every CTA of a group takes the same decision) and no more fine tasks of
+// iterations >= stopk are claimed.  Every wait is bounded: it gives up after ~4 s without any progress
+// anywhere in the kernel (heartbeat counter; watchdog flag).
+#pragma once
+#include "rsw_blocks.cuh"
+
+#include <cstdio>
+
+#ifndef RSW_PIPE_COARSE_THREADS
+#define RSW_PIPE_COARSE_THREADS 288  // coarse sub-CTA: three 96-thread parts evaluate three sample pairs at once
+#endif
+#ifndef RSW_PIPE_FINE_TMUL
+#define RSW_PIPE_FINE_TMUL 2  // threads per fine group = TMUL x 3N/R
+#endif
+#ifndef RSW_PIPE_FINE_GROUPS
+#define RSW_PIPE_FINE_GROUPS 1  // fine worker groups per CTA (two slowed the sweeps on C3)
+#endif
+
+namespace rsw {
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+constexpr unsigned ABORT_BIT = 1u << 28;
+
+// group barrier over P CTAs (their coarse sub-CTAs `grp`) on counter `bar`; rank 0 may raise the abort
+// bit, which every CTA of the group observes on the same barrier (or the one before it, where
+// nothing else is left to do)
+template <class GRP>
+__device__ __forceinline__ bool group_barrier(unsigned* bar, unsigned P, unsigned& epoch, bool raise, unsigned* wd,
+                                              const unsigned* hb, unsigned* s_flag, const GRP& grp) {
+  grp.sync();
+  if (grp.tid() == 0) {
+    ++epoch;
+    red_release_add(bar, raise ? ABORT_BIT + 1 : 1);
+    const unsigned target = epoch * P;
+    unsigned v = ld_acquire_gpu(bar);
+    Watch w = watch_start(hb);
+    for (unsigned it = 0; v < target && !(v & ABORT_BIT); ++it) {
+      if ((it & 63) == 63 && watchdog_expired(w, wd, hb)) {
+        v = ABORT_BIT;
+        break;
+      }
+      v = ld_acquire_gpu(bar);
+    }
+    *s_flag = (v & ABORT_BIT) ? 1u : 0u;
+  }
+  grp.sync();
+  return *s_flag != 0;
+}
+
+// CTA = NPG fine groups of TG threads (threads [0, NPG TG), named barriers 1..NPG) + one coarse
+// sub-CTA (the TC highest threads, named barrier 15; the warp arbiter prefers high warp ids, so the
+// latency-critical sweep wins issue slots over the throughput-bound fine solves).  The tcgen05
+// allocation limits a cooperative launch to one CTA per SM, so the roles are warp-specialized inside
+// the CTA rather than spread over CTAs.
+// smallest radix whose FFT core fits in `threads` threads
+template <int N>
+__host__ __device__ constexpr int radix_for_threads(int threads) {
+  return (3 * (N / 4) <= threads) ? 4 : (3 * (N / 8) <= threads) ? 8 : (3 * (N / 16) <= threads) ? 16 : 32;
+}
+template <int N, int TC, int NPC, int RC0>
+__host__ __device__ constexpr int pipe_split() {  // sample pairs a coarse sub-CTA evaluates concurrently
+  // parts must be whole warps (named-barrier thread counts) and must run the bulk sweep's radix RC0
+  // (another radix rounds differently: the schedules would no longer agree bitwise)
+  return (NPC >= 4 && (TC / 4) % 32 == 0 && 3 * (N / RC0) <= TC / 4 && TC / 4 < TC / 3 - 31) ? 4
+       : (NPC >= 3 && (TC / 3) % 32 == 0 && 3 * (N / RC0) <= TC / 3) ? 3
+       : (NPC >= 2 && (TC / 2) % 32 == 0 && 3 * (N / RC0) <= TC / 2) ? 2 : 1;
+}
+
+template <int N, int RC0, int TC, int NOWN, int NPC, int RF, int TG, int NPG>
+struct PipeLayout {
+  static constexpr int SPLIT = pipe_split<N, TC, NPC, RC0>();
+  static constexpr int RC = RC0;
+  using CL = CoarseLayout<N, RC, TC, NOWN, NPC, SPLIT>;
+  static constexpr int K = N / 3, KP = K + 1;
+  // coarse region: the coarse sub-CTA's layout, or (CTAs without a coarse role) TC/TG extra fine groups' X/Y
+  static constexpr int XG = TC / TG;
+  static constexpr size_t CREG = CL::bytes > sizeof(double2) * XG * 6 * N ? CL::bytes : sizeof(double2) * XG * 6 * N;
+  static constexpr int C0 = 0, F0 = (int)((CREG + 15) / 16);  // double2 offsets of the coarse / fine regions
+  static constexpr int F_TW = F0, F_CP = F_TW + fft_tw_size<N, RF>(), F_D = F_CP + 6 * KP, F_ND = 9 * KP,
+                       F_G = F_D + (F_ND + 1) / 2;  // first fine group's X
+  static constexpr size_t bytes = sizeof(double2) * (F_G + NPG * 6 * N);
+  static constexpr int CPG = (FineTmem<N, TG>::COLS + 31) / 32 * 32;  // TMEM columns per fine group
+  static constexpr int T = TC + NPG * TG;
+};
+
+// fine worker group: claim the lowest-iteration ready pair task (k, p) — slices 2p, 2p+1 of U^k, ready
+// when prog[k] covers them — run the fine pair integrator, write F^k, set doneF[k][p] (release)
+template <int N, int RF, int TG, int FSCHEME>
+__device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedGroup grp, double2* W,
+                                                 const FineSmemTab& ft, uint32_t tcol, int* task) {
+  constexpr size_t L = (size_t)3 * (N / 2 + 1) * 2;
+  const int S = a.S, Kit = a.K, npairs = a.npairs;
+  double2* Yb = W + 3 * N;
+  for (;;) {
+    if (grp.tid() == 0) {
+      int tk = -1, tp = -1;
+      Watch w = watch_start(a.hb);
+      for (unsigned it = 0;; ++it) {
+        const int lim = min(Kit, *(volatile int*)a.stopk) - 1;  // F^k is needed by sweep k+1 <= stop
+        bool all_claimed = true;
+        for (int k = 0; k <= lim && tk < 0; ++k) {
+          const unsigned t = *(volatile unsigned*)(a.next + k);
+          if ((int)t >= npairs) continue;
+          all_claimed = false;
+          const int need = (2 * (int)t + 1 < S) ? 2 * (int)t + 1 : 2 * (int)t;  // U^k_{2t}, U^k_{2t+1}
+          if (ld_acquire_gpu(a.prog + k) >= (unsigned)(a.GC * need) && atomicCAS(a.next + k, t, t + 1) == t) {
+            tk = k;
+            tp = (int)t;
+          }
+        }
+        if (tk >= 0 || all_claimed) break;
+        if ((it & 63) == 63 && watchdog_expired(w, a.wd, a.hb)) break;
+        __nanosleep(128);
+      }
+      task[0] = tk;
+      task[1] = tp;
+    }
+    grp.sync();
+    const int tk = task[0], tp = task[1];
+    if (tk < 0) break;
+    const int nA = 2 * tp, nB = nA + 1;
+    unsigned long long* tf =
+        a.trace ? a.trace + 2 * (Kit + 1) + (size_t)(Kit + 1) * S + ((size_t)tk * npairs + tp) * 2 : nullptr;
+    if (tf && grp.tid() == 0) tf[0] = gtimer();
+    const double* Uk = a.Uall + (size_t)tk * (S + 1) * L;
+    double* Fk = a.Fall + (size_t)tk * S * L;
+    fine_pair_run<N, RF, TG, FSCHEME, false>(grp, W, Yb, ft, tcol, a.ft.g, Uk + nA * L, nB < S ? Uk + nB * L : nullptr,
+                                             Fk + nA * L, nB < S ? Fk + nB * L : nullptr, a.m_fine, a.h, a.hb);
+    grp.sync();  // the whole pair's F is written
+    if (grp.tid() == 0) {
+      st_release_u32(a.doneF + (size_t)tk * npairs + tp, 1u);
+      if (tf) tf[1] = gtimer();
+    }
+  }
+}
+
+template <int N, int RC, int TC, int NOWN, int NPC, int RF, int TG, int NPG, int FSCHEME>
+__global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeArgs a) {
+  using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG>;
+  using CL = typename LY::CL;
+  static_assert(NPG * LY::CPG <= 512, "fine groups must fit in TMEM");
+  static_assert(NPG <= 7, "named barrier ids (fine 1..7, split parts 8..11, staging 14, coarse 15)");
+  constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NH = N / 2 + 1, Kc3 = 3 * Kc;
+  constexpr size_t L = (size_t)3 * NH * 2;  // doubles per state
+  extern __shared__ double2 smem[];
+  __shared__ uint32_t tslot;
+  __shared__ unsigned s_ticket, s_flag;
+  __shared__ int s_task[NPG + TC / TG][2];
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1u);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const int ticket = (int)s_ticket;
+  const int S = a.S, Kit = a.K;
+  // fine tables (shared by every fine group of the CTA), staged by all threads
+  const FineSmemTab ft = stage_fine_tables<N, RF, TC + NPG * TG>(
+      smem + LY::F_TW, smem + LY::F_CP, reinterpret_cast<double*>(smem + LY::F_D), a.ft, threadIdx.x, TC + NPG * TG);
+  __syncthreads();
+
+  constexpr int FT = NPG * TG;  // fine groups take the low warps, the coarse sub-CTA the high ones
+  if ((int)threadIdx.x >= FT) {
+    // ===================================== coarse sub-CTA =====================================
+    const NamedGroup cg{FT, 15, TC};
+    const int ct = (int)threadIdx.x - FT;
+    if (ticket >= a.NG * a.GC) {
+      // no coarse role: the coarse threads run XG more fine groups (in the coarse region of smem)
+      constexpr int XG = TC / TG;
+      const int xi = ct / TG;
+      if (xi < XG && (NPG + XG) * LY::CPG <= 512)
+        fine_worker_loop<N, RF, TG, FSCHEME>(a, NamedGroup{FT + xi * TG, 1 + NPG + xi, TG},
+                                            smem + LY::C0 + (size_t)xi * 6 * N, ft,
+                                            tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi]);
+    } else {
+      const int g = ticket / a.GC, c = ticket % a.GC, P = a.GC;
+      double2* cs = smem + LY::C0;
+      double2* X = cs + CL::X;
+      double2* Y = cs + CL::Y;
+      double2* TW = cs + CL::TW;
+      double2* C = cs + CL::C;
+      double2* A = cs + CL::A;
+      double2* Vs = cs + CL::VS;
+      double2* KSs = cs + CL::KS;
+      double2* kk = cs + CL::KK;
+      double2* un_s = cs + CL::UN;
+      double2* rdb = cs + CL::RDB;
+      double2* PH = cs + CL::PH;
+      double2* yv = cs + CL::YV;
+      double* sd = reinterpret_cast<double*>(cs + CL::D);
+      double* red = sd + CL::RED;
+      double* GA = sd + CL::GA;
+      double* GP = sd + CL::GP;
+      double* GQ = sd + CL::GQ;
+      double* SW = sd + CL::SW;
+      int* yidx = reinterpret_cast<int*>(sd + CL::YI);
+      const AvgTab& tab = a.at;
+      const int M = a.M;
+      fill_packed_twiddles<N, LY::RC, TC>(TW, tab.tw, ct);
+      for (int k = ct; k <= K; k += TC) {
+        GA[k] = __ldg(tab.g.a + k);
+        GP[k] = __ldg(tab.g.p + k);
+        GQ[k] = __ldg(tab.g.q + k);
+      }
+      for (int q = 0; q < NPC; ++q) {  // phases / weights of this CTA's pairs c, c + P, ...
+        const int pr = c + q * P;
+        if (pr >= M / 2) break;
+        const int mA = 2 * pr + 1, mB = 2 * pr + 2;
+        for (int k = ct; k <= K; k += TC) {
+          PH[(size_t)q * 2 * KP + k] = __ldg(tab.phase + (size_t)mA * KP + k);
+          PH[(size_t)q * 2 * KP + KP + k] = __ldg(tab.phase + (size_t)mB * KP + k);
+        }
+        if (ct == 0) {
+          SW[2 * q] = __ldg(tab.w + mA);
+          SW[2 * q + 1] = mB <= M - 1 ? __ldg(tab.w + mB) : 0.0;
+        }
+      }
+      cg.sync();
+      unsigned* bar = a.gbar + g * 32;
+      double2* yb = a.ybuf + (size_t)g * 3 * Kc3;
+      double2* part = a.part + (size_t)g * (M / 2 > 0 ? M / 2 : 1) * Kc3;
+      const int nst = a.base.scheme == 0 ? 4 : 2;
+      unsigned epoch = 0;
+      for (int k = g; k <= Kit; k += a.NG) {
+        // sweep start: the three stage-input buffers of the group start empty
+        for (int i = c * TC + ct; i < 3 * Kc3; i += P * TC) st_relaxed_v2(yb + i, yin_sentinel());
+        const bool stop_now = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
+        if (group_barrier(bar, P, epoch, stop_now, a.wd, a.hb, &s_flag, cg)) break;
+        if (a.trace && c == 0 && ct == 0) a.trace[2 * k] = gtimer();
+        CoarseArgs ca = a.base;
+        ca.U = a.Uall + (size_t)k * (S + 1) * L;
+        ca.G = a.Gall + (size_t)k * S * L;
+        ca.Uprev = k ? a.Uall + (size_t)(k - 1) * (S + 1) * L : ca.U;
+        ca.Gprev = k ? a.Gall + (size_t)(k - 1) * S * L : ca.G;
+        ca.F = k ? a.Fall + (size_t)(k - 1) * S * L : nullptr;
+        ca.rparts = k ? a.rparts + (size_t)k * S * KP * 2 : nullptr;
+        ca.part = part;
+        ca.nparts = M / 2 > 0 ? M / 2 : 1;
+        ca.yin = yb;
+        ca.n_end = S;
+        ca.wprog = k ? a.prog + (k - 1) : nullptr;
+        ca.wunit = (unsigned)P;
+        ca.wF = k ? a.doneF + (size_t)(k - 1) * a.npairs : nullptr;
+        ca.wd = a.wd;
+        ca.hb = a.hb;
+        ca.stopk = a.stopk;
+        ca.kself = k;
+        ca.prof = nullptr;
+        unsigned ucount = 0;
+        coarse_update_phase<N, TC, NOWN>(ca, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, c, P, cg);
+        bool aborted = false;
+        for (int n = 0; n < S && !aborted; ++n) {
+          for (int st = 1; st <= nst; ++st) {
+            // optional stage-phase stamps (trace, group 0 rank 0, slices 8..23 of sweep g): samples / barrier / update
+            unsigned long long* stp = (a.trace && g == 0 && c == 0 && ct == 0 && n >= 8 && n < 24 && k == g)
+                                          ? a.trace + 2 * (Kit + 1) + (size_t)(Kit + 1) * S + 2 * (size_t)(Kit > 0 ? Kit : 1) * a.npairs +
+                                                ((n - 8) * nst + st - 1) * 4
+                                          : nullptr;
+            if (stp) stp[0] = gtimer();
+            coarse_samples_phase<N, LY::RC, TC, NamedGroup, NPC, LY::SPLIT>(yb + (size_t)(ucount % 3) * Kc3, part, M, tab, X, Y, TW,
+                                                             C, A, PH, SW, GA, GP, GQ, nullptr, c, P, cg);
+            if (stp) stp[1] = gtimer();
+            const bool raise = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
+            if (group_barrier(bar, P, epoch, raise, a.wd, a.hb, &s_flag, cg)) {
+              aborted = true;
+              break;
+            }
+            if (stp) stp[2] = gtimer();
+            ++ucount;
+            coarse_update_phase<N, TC, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, c, P, cg);
+            if (stp) stp[3] = gtimer();
+          }
+          if (!aborted) {
+            cg.sync();  // this CTA's part of U^k_{n+1}, G^k_n is written
+            if (ct == 0) {
+              red_release_add(a.prog + k, 1u);
+              if (c == 0) atomicAdd(a.hb, 1u);  // watchdog heartbeat: a slice of sweep k is done
+            }
+            if (a.trace && c == 0 && ct == 0) a.trace[2 * (Kit + 1) + (size_t)k * S + n] = gtimer();
+          }
+        }
+        if (aborted) break;
+        if (group_barrier(bar, P, epoch, false, a.wd, a.hb, &s_flag, cg)) break;  // every slice's residual partials written
+        if (a.trace && c == 0 && ct == 0) a.trace[2 * k + 1] = gtimer();
+        if (c == 0 && k > 0) {  // r_k = max_n sqrt(Σ num / Σ den) (fixed order, as the bulk sweep)
+          double mx = 0.0;
+          bool bad = false;
+          for (int s = ct; s < S; s += TC) {
+            double num = 0.0, den = 0.0;
+            for (int q = 0; q <= K; ++q) {
+              num += __ldcg(ca.rparts + ((size_t)s * KP + q) * 2);
+              den += __ldcg(ca.rparts + ((size_t)s * KP + q) * 2 + 1);
+            }
+            const double r = sqrt(num / den);
+            if (!(r == r) || isinf(r)) bad = true;
+            mx = fmax(mx, r);
+          }
+          red[ct] = bad ? __longlong_as_double(0x7ff8000000000000LL) : mx;
+          cg.sync();
+          if (ct == 0) {
+            double m = 0.0;
+            bool nan = false;
+            for (int t = 0; t < TC; ++t) {
+              if (red[t] != red[t]) nan = true;
+              m = fmax(m, red[t]);
+            }
+            const double r = nan ? __longlong_as_double(0x7ff8000000000000LL) : m;
+            a.resid[k] = r;
+            if (!(r == r) || r > 1e6 || (a.tol > 0 && r < a.tol)) atomicMin(a.stopk, k);
+          }
+        }
+      }
+    }
+  } else {
+    // ======================================= fine worker group 0 =======================================
+    const int gi = threadIdx.x / TG;
+    fine_worker_loop<N, RF, TG, FSCHEME>(a, NamedGroup{gi * TG, 1 + gi, TG}, smem + LY::F_G + (size_t)gi * 6 * N,
+                                        ft, tslot + (uint32_t)(gi * LY::CPG), s_task[gi]);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc<512>(tslot);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// launcher: picks the configuration for n, checks co-residency (2 CTAs per SM), launches
+// ---------------------------------------------------------------------------------------------
+template <int N, int NOWN, int NPC, int FSCHEME>
+static inline cudaError_t launch_pipe_nf(const PipeArgs& a, int grid, size_t* out, cudaStream_t st) {
+  constexpr int RC = coarse_radix<N>();
+  constexpr int TC = RSW_PIPE_COARSE_THREADS > coarse_threads<N>() ? RSW_PIPE_COARSE_THREADS : coarse_threads<N>();
+  constexpr int RF = fine_radix<N>(), TG = RSW_PIPE_FINE_TMUL * core_threads<N, RF>();
+  constexpr int CPG = (FineTmem<N, TG>::COLS + 31) / 32 * 32;
+  constexpr int NPG = RSW_PIPE_FINE_GROUPS * CPG <= 512 ? RSW_PIPE_FINE_GROUPS : 512 / CPG;
+  using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG>;
+  auto kfn = k_parareal_pipe<N, RC, TC, NOWN, NPC, RF, TG, NPG, FSCHEME>;
+  const size_t sm = LY::bytes;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  if (grid <= 0) {  // query: co-resident CTAs (tensor-memory kernels: one per SM)
+    int per_sm = 0, dev = 0, sms = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, LY::T, sm)) != cudaSuccess) return e;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if (out) *out = (size_t)(per_sm > 1 ? 1 : per_sm) * sms;
+    if (getenv("RSW_PIPE_TRACE"))
+      fprintf(stderr, "[rsw pipe] n=%d: %d threads (coarse %d + %d fine groups of %d), %zu B smem, %d CTA/SM\n", N,
+              LY::T, TC, NPG, TG, sm, per_sm);
+    return cudaSuccess;
+  }
+  void* args[] = {(void*)&a};
+  return cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(LY::T), args, sm, st);
+}
+
+template <int N>
+static inline cudaError_t launch_pipe_n(const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st) {
+  constexpr int K = N / 3;
+  const int nown = (K + 1 + a.GC - 1) / a.GC;
+  const int npc = (a.M / 2 + a.GC - 1) / a.GC;  // sample pairs per coarse CTA
+#define PIPE_CFG(NW, NP)                                                                            \
+  if (nown <= NW && npc <= NP) return fine_scheme == 0 ? launch_pipe_nf<N, NW, NP, 0>(a, grid, out, st) \
+                                    : fine_scheme == 1 ? launch_pipe_nf<N, NW, NP, 1>(a, grid, out, st) \
+                                                       : launch_pipe_nf<N, NW, NP, 2>(a, grid, out, st);
+  PIPE_CFG(2, 1)
+  PIPE_CFG(2, 2)
+  PIPE_CFG(4, 2)
+  PIPE_CFG(8, 4)
+  PIPE_CFG(8, 8)
+#undef PIPE_CFG
+  return cudaErrorInvalidConfiguration;
+}
+
+}  // namespace rsw
