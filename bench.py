@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--impl", default="rsw", choices=["rsw", "reference"])
     ap.add_argument("--fine-scheme", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5-iteration", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=0, help="oracle sample: steps per slice")
     return ap.parse_args()
 
@@ -372,6 +373,30 @@ def main():
               "kernel": "k_avg_states<512,8,192> (state and accumulator in TMEM)"}
     del u4
 
+    # ---- C5 (BASELINE configs[4]) time per parareal iteration at this rank count (bulk schedule: the
+    # pipelined megakernel supports n <= 256): the k = 0 coarse sweep (16384 serial stages at n = 1024),
+    # then one iteration = fine sweep of this rank's slices + all-gather + coarse sweep.  One iteration
+    # only: the C5 iterate blows up at k = 2 (docs/c5_stability.json).
+    c5_iteration = None
+    if not args.no_c5_iteration:
+        U5 = torch.empty((w5.n_slices + 1,) + w5.state_shape, dtype=torch.float64, device="cuda")
+        u50 = torch.from_numpy(inputs.initial_state(w5)).cuda()
+        barrier()
+        r5 = rsw.parareal_iterate(p5, u50, dT=w5.dT, dt=w5.dt, T0=w5.T0, M=w5.M, n_slices=w5.n_slices, max_iters=1,
+                                  comm=comm, U=U5, allow_diverged=True, schedule=rsw.SCHEDULE_BULK)
+        s5 = r5["stats"]
+        tt = torch.tensor([s5["total_ms"], s5["sweep0_ms"], s5["fine_ms"], s5["comm_ms"], s5["coarse_ms"] - s5["sweep0_ms"]],
+                          dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tt = tt.tolist()
+        c5_iteration = {"workload": "C5 parareal, k = 0 sweep + 1 iteration (bulk schedule)", "slices": w5.n_slices,
+                        "total_ms": tt[0], "sweep0_ms": tt[1], "fine_sweep_ms": tt[2], "allgather_ms": tt[3],
+                        "coarse_sweep_ms": tt[4], "coarse_stages_per_sweep": 4 * w5.n_slices,
+                        "us_per_coarse_stage": tt[4] * 1e3 / (4 * w5.n_slices), "r_1": r5["resid"],
+                        "status": r5["status"]}
+        del U5
+
     # ---- e2e: same solve through the C-ABI from pinned host buffers, H2D + D2H inside the region
     U_host = torch.empty(U.shape, dtype=torch.float64).pin_memory()
     e2e = []
@@ -400,14 +425,26 @@ def main():
             "setup_ms": {"first_call_wall": first_ms, "steady_call": ms_max,
                          "one_time_setup_estimate": max(first_ms - ms_max, 0.0)},
             "schedule": "pipelined (one persistent launch per solve)" if pipelined else "bulk (fine sweep + coarse sweep per iteration)",
-            "phases_ms": ({"pipelined_total": statistics.median(s["total_ms"] for s in stats)} if pipelined else
+            "phases_ms": ({"pipelined_total": statistics.median(s["total_ms"] for s in stats),
+                           "sweep0": statistics.median(s["sweep0_ms"] for s in stats),
+                           "per_further_iteration": statistics.median(s["lag_ms"] for s in stats),
+                           "fine_task_latency": statistics.median(s["fine_task_ms"] for s in stats),
+                           "note": "k = 0 coarse sweep (2048 serial stages) + iterations x the lag each adds "
+                                   "(one fine pair task + hand-off); in-kernel globaltimer stamps"} if pipelined else
                           {"fine": statistics.median(s["fine_ms"] for s in stats), "allgather": comm_ms,
-                           "coarse": coarse_ms, "total_library": statistics.median(s["total_ms"] for s in stats)}),
+                           "coarse": coarse_ms, "sweep0": statistics.median(s["sweep0_ms"] for s in stats),
+                           "per_iteration": statistics.median(s["lag_ms"] for s in stats),
+                           "total_library": statistics.median(s["total_ms"] for s in stats)}),
+            "convergence": {"iterations": iters, "rule": "fixed count (BASELINE configs[2]: 5 iterations)",
+                            "resid": res["resid"],
+                            "converged": bool(res["resid"] and res["resid"][-1] < 1e-6),
+                            "note": "time to 5 fixed iterations; the C3 iteration has not converged by k = 5"},
             "fine_kernel_slice_steps_per_s": local_slices * w.m_fine / (fine_ms * 1e-3) * world,
             "roofline": roof,
             "roofline_fine": roof_fine,
             "fine_c5": fine_c5,
             "avg_c4": avg_c4,
+            "c5_iteration": c5_iteration,
             "clocks": clk.summary(),
             "e2e": {"value": total_slice_steps / (e2e_ms * 1e-3), "unit": UNIT, "ms": e2e_ms,
                     "h2d_bytes_per_step": u0_host.numel() * 8, "d2h_bytes_per_step": U_host.numel() * 8},

@@ -129,6 +129,12 @@ typedef struct {
   int64_t kernel_launches;  /* kernels this library launched during the call */
   int32_t pipelined;        /* 1: the pipelined schedule ran (fine / coarse times overlap: only
                                total_ms is meaningful, fine_ms = coarse_ms = total_ms) */
+  /* phase split of the time to solution (P:718-725 cost terms).  Pipelined: sweep0_ms = the k = 0
+     coarse sweep, lag_ms = mean time each further iteration adds (sweep k end - sweep k-1 end),
+     fine_task_ms = mean latency of one fine pair task (in-kernel globaltimer stamps).  Bulk:
+     sweep0_ms = the k = 0 sweep, lag_ms = one iteration (fine sweep + exchange + coarse sweep),
+     fine_task_ms = one fine sweep of this rank's shard. */
+  double sweep0_ms, lag_ms, fine_task_ms;
 } rsw_parareal_stats;
 
 /* The asymptotic parareal iteration (Eq. HMM parareal iteration P:428-430; Alg.4):

@@ -55,7 +55,8 @@ class _Stats(ctypes.Structure):
     _fields_ = [("fine_ms", ctypes.c_double), ("comm_ms", ctypes.c_double),
                 ("coarse_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
                 ("fine_slice_steps", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
-                ("pipelined", ctypes.c_int32)]
+                ("pipelined", ctypes.c_int32), ("sweep0_ms", ctypes.c_double), ("lag_ms", ctypes.c_double),
+                ("fine_task_ms", ctypes.c_double)]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -256,7 +257,8 @@ def parareal_iterate(p: Params, u0, *, dT, dt, T0, M, n_slices, max_iters, tol=0
     out = dict(U=U, resid=[resid[i] for i in range(it.value)], iters=it.value, status=rc,
                stats=dict(fine_ms=st.fine_ms, comm_ms=st.comm_ms, coarse_ms=st.coarse_ms,
                           total_ms=st.total_ms, fine_slice_steps=st.fine_slice_steps,
-                          kernel_launches=st.kernel_launches, pipelined=bool(st.pipelined)))
+                          kernel_launches=st.kernel_launches, pipelined=bool(st.pipelined),
+                          sweep0_ms=st.sweep0_ms, lag_ms=st.lag_ms, fine_task_ms=st.fine_task_ms))
     if want_FG:
         out["F"], out["G"] = F, G
     return out

@@ -269,7 +269,7 @@ cudaError_t get_coarse(const rsw_params* p, double dT, CoarseTables** out) {
 constexpr int kMaxVirtualWorld = 16;
 struct Workspace {
   DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof, Gnew, yin, chk;
-  DevBuf pU, pG, pF, prp, pres, pctl, pyb, ppart;  // pipelined schedule
+  DevBuf pU, pG, pF, prp, pres, pctl, pyb, ppart, pst;  // pipelined schedule
   DevBuf vshard[kMaxVirtualWorld];                 // RSW_VIRTUAL_WORLD: one fine-endpoint buffer per virtual rank
   double* rhost = nullptr;
   unsigned* chost = nullptr;
@@ -743,6 +743,9 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   a.ybuf = (double2*)ws->pyb.p;
   a.part = (double2*)ws->ppart.p;
   a.trace = nullptr;
+  const size_t nst = 2 * (size_t)(K + 1) + 2;
+  CUDA_TRY(ensure(ws->pst, sizeof(unsigned long long) * nst));
+  a.stamps = (unsigned long long*)ws->pst.p;
   static const bool trace = getenv("RSW_PIPE_TRACE") != nullptr;
   const size_t ntr0 = 2 * (size_t)(K + 1) + (size_t)(K + 1) * S + 2 * (size_t)std::max(K, 1) * a.npairs;
   const size_t ntr = ntr0 + 16 * 4 * 4;  // + stage-phase stamps (16 slices x 4 stages x 4)
@@ -754,6 +757,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   cudaEvent_t* ev = ws->ev.data();
   CUDA_TRY(cudaEventRecord(ev[6], st));
   CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(unsigned) * nctl, st));
+  CUDA_TRY(cudaMemsetAsync(a.stamps, 0, sizeof(unsigned long long) * nst, st));
   const int stop_init = K + 1;
   CUDA_TRY(cudaMemcpyAsync(a.stopk, &stop_init, sizeof(int), cudaMemcpyHostToDevice, st));
   for (int k = 0; k <= K; ++k)  // U^k_0 = u0 for every iteration
@@ -765,6 +769,8 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   CUDA_TRY(cudaMemcpyAsync(&stopk, a.stopk, sizeof(int), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(&wd, a.wd, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(res.data(), a.resid, sizeof(double) * (K + 1), cudaMemcpyDeviceToHost, st));
+  std::vector<unsigned long long> stamps(nst, 0ull);
+  CUDA_TRY(cudaMemcpyAsync(stamps.data(), a.stamps, sizeof(unsigned long long) * nst, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (trace) {  // debug timeline to stderr (ms since the first sweep start)
     std::vector<unsigned long long> tr(ntr);
@@ -829,6 +835,12 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     stats->fine_slice_steps = (int64_t)kout * S * m;
     stats->kernel_launches = 1;
     stats->pipelined = 1;
+    // phase split from the in-kernel globaltimer stamps: the k = 0 sweep (first sweep start to its
+    // end), the mean time each further iteration adds (sweep k end - sweep k-1 end), the mean fine task
+    const unsigned long long t0 = stamps[0];
+    stats->sweep0_ms = (stamps[1] > t0) ? (stamps[1] - t0) * 1e-6 : 0.0;
+    stats->lag_ms = (kout >= 1 && stamps[2 * kout + 1] > stamps[1]) ? (stamps[2 * kout + 1] - stamps[1]) * 1e-6 / kout : 0.0;
+    stats->fine_task_ms = stamps[2 * (K + 1) + 1] ? stamps[2 * (K + 1)] * 1e-6 / (double)stamps[2 * (K + 1) + 1] : 0.0;
   }
   if (kout >= 1 && (!std::isfinite(res[kout]) || res[kout] > 1e6))
     return fail(RSW_ERR_DIVERGED, "parareal residual non-finite or > 1e6");
@@ -926,11 +938,13 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     return s;
   }
   CUDA_TRY(cudaEventRecord(ev[1], st));
+  double sweep0_ms = 0;
   {
     float ms;
     CUDA_TRY(cudaEventSynchronize(ev[1]));
     CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[1]));
     coarse_ms += ms;
+    sweep0_ms = ms;
   }
   Chain ch;
   if (!strang_coarse && (s = setup_chain(ch, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, F,
@@ -1022,6 +1036,9 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     stats->total_ms = tot;
     stats->fine_slice_steps = fine_steps;
     stats->kernel_launches = launches;
+    stats->sweep0_ms = sweep0_ms;                                    // the k = 0 coarse sweep
+    stats->lag_ms = done ? (tot - sweep0_ms) / done : 0.0;           // one iteration (fine + exchange + sweep)
+    stats->fine_task_ms = done ? fine_ms / done : 0.0;               // one fine sweep (this rank's shard)
   }
   if (status == RSW_NOT_CONVERGED) g_err = "parareal: tolerance not reached within max_iters";
   return status;

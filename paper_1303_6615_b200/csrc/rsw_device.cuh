@@ -437,6 +437,16 @@ __device__ __forceinline__ int fft_elem0(int b) {  // first element of butterfly
   return (b / d) * L + (b % d);
 }
 
+// Synchronisation between two passes of the SAME field: every pass touches only its own field's
+// buffer, so when a field's N/R threads lie inside one warp (N/R divides 32) a warp barrier orders the
+// passes; otherwise the group barrier.  Called by every thread of the group (also the inactive ones,
+// which may share a warp with active ones), so __syncwarp always sees the full warp.
+template <int N, int R, class GRP>
+__device__ __forceinline__ void pass_sync(const GRP& grp) {
+  if constexpr ((N / R) <= 32 && 32 % (N / R) == 0) __syncwarp();
+  else grp.sync();
+}
+
 // synthesis passes p..m-1 of field buffer Xf (sign +); the last pass leaves its outputs in v
 template <int N, int R, int p, int TWT, class GRP>
 __device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* Xf, int j, bool act, const double2* TW,
@@ -466,7 +476,7 @@ __device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* Xf, int j
     }
   }
   if constexpr (p < m - 1) {
-    grp.sync();
+    pass_sync<N, R>(grp);
     core_inverse<N, R, p + 1, TWT>(v, Xf, j, act, TW, twt, grp);
   }
 }
@@ -497,7 +507,8 @@ __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j
         }
       }
     }
-    grp.sync();
+    if constexpr (p > 0) pass_sync<N, R>(grp);  // the next pass reads this field only
+    else grp.sync();                              // exit: the caller reads every field
     core_forward<N, R, p - 1, TWT>(v, Xf, j, act, TW, twt, grp);
   }
 }
@@ -505,8 +516,9 @@ __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j
 // N(u) core on the packed pair: X = double2[nl_buf<N, R>()] — fields (v1, i κ v2, h) at f FS in the
 // padded layout, then V (the v1 copy) at 3 FS — holds the retained spectra of (v1, iκ v2, h) on entry
 // and the retained spectra of (v1²/2, v1 v2x, h v1) (unnormalised) on exit.  The second argument is
-// unused (kept for the callers' layouts, which reserve >= nl_buf entries from X).  2m barriers
-// (m = passes), the last one on exit.  TWT: twiddle policy (fft_tw_src); with TWT = 2, twt is the
+// unused (kept for the callers' layouts, which reserve >= nl_buf entries from X).  Group barriers: the
+// v1 copy before the products and the exit; between passes of a field a warp barrier when the field
+// lies in one warp (N/R <= 32: n <= 256), else a group barrier (2m in all).  TWT: twiddle policy (fft_tw_src); with TWT = 2, twt is the
 // thread's TMEM address of its twiddle slots (lane quarter + column base, filled by tw_tmem_fill).
 template <int N, int R, int T, class GRP = CtaGroup, int TWT = 1>
 __device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const double2* TW, const GRP& grp = GRP(),
@@ -550,7 +562,8 @@ __device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const d
       if (m > 1 || e <= K || e >= N - K) xb[fpad<R>(s)] = v[s];
     }
   }
-  grp.sync();
+  if constexpr (m > 1) pass_sync<N, R>(grp);  // analysis pass m-1 wrote its own field only
+  else grp.sync();
   core_forward<N, R, m - 2, TWT>(v, Xf, j, act, TW, twt, grp);
 }
 

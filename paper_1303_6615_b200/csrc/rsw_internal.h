@@ -80,6 +80,7 @@ struct PipeArgs {
   double2* ybuf;        // [NG][3][3Kc] stage inputs
   double2* part;        // [NG][GC][3Kc] partial sums
   unsigned long long* trace;  // optional timeline (RSW_PIPE_TRACE): sweep [K+1][2], slice [K+1][S], fine [K][npairs][2]
+  unsigned long long* stamps; // always: sweep start / end [K+1][2] (globaltimer ns), fine-task latency sum, count
 };
 bool pipeline_supported(int n);
 cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);

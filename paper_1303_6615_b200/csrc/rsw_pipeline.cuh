@@ -149,7 +149,8 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
     const int nA = 2 * tp, nB = nA + 1;
     unsigned long long* tf =
         a.trace ? a.trace + 2 * (Kit + 1) + (size_t)(Kit + 1) * S + ((size_t)tk * npairs + tp) * 2 : nullptr;
-    if (tf && grp.tid() == 0) tf[0] = gtimer();
+    const unsigned long long t_start = (grp.tid() == 0) ? gtimer() : 0ull;
+    if (tf && grp.tid() == 0) tf[0] = t_start;
     const double* Uk = a.Uall + (size_t)tk * (S + 1) * L;
     double* Fk = a.Fall + (size_t)tk * S * L;
     fine_pair_run<N, RF, TG, FSCHEME, false>(grp, W, Yb, ft, tcol, a.ft.g, Uk + nA * L, nB < S ? Uk + nB * L : nullptr,
@@ -157,7 +158,10 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
     grp.sync();  // the whole pair's F is written
     if (grp.tid() == 0) {
       st_release_u32(a.doneF + (size_t)tk * npairs + tp, 1u);
-      if (tf) tf[1] = gtimer();
+      const unsigned long long t_end = gtimer();
+      if (tf) tf[1] = t_end;
+      atomicAdd(a.stamps + 2 * (Kit + 1), t_end - t_start);  // fine-task latency sum / count (stats)
+      atomicAdd(a.stamps + 2 * (Kit + 1) + 1, 1ull);
     }
   }
 }
@@ -254,7 +258,11 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         for (int i = c * TC + ct; i < 3 * Kc3; i += P * TC) st_relaxed_v2(yb + i, yin_sentinel());
         const bool stop_now = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
         if (group_barrier(bar, P, epoch, stop_now, a.wd, a.hb, &s_flag, cg)) break;
-        if (a.trace && c == 0 && ct == 0) a.trace[2 * k] = gtimer();
+        if (c == 0 && ct == 0) {
+          const unsigned long long t = gtimer();
+          a.stamps[2 * k] = t;  // sweep k start (stats)
+          if (a.trace) a.trace[2 * k] = t;
+        }
         CoarseArgs ca = a.base;
         ca.U = a.Uall + (size_t)k * (S + 1) * L;
         ca.G = a.Gall + (size_t)k * S * L;
@@ -309,7 +317,11 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         }
         if (aborted) break;
         if (group_barrier(bar, P, epoch, false, a.wd, a.hb, &s_flag, cg)) break;  // every slice's residual partials written
-        if (a.trace && c == 0 && ct == 0) a.trace[2 * k + 1] = gtimer();
+        if (c == 0 && ct == 0) {
+          const unsigned long long t = gtimer();
+          a.stamps[2 * k + 1] = t;  // sweep k end (stats)
+          if (a.trace) a.trace[2 * k + 1] = t;
+        }
         if (c == 0 && k > 0) {  // r_k = max_n sqrt(Σ num / Σ den) (fixed order, as the bulk sweep)
           double mx = 0.0;
           bool bad = false;
