@@ -478,7 +478,7 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       const double as = kap < 0 ? -GA[ak] : GA[ak];
       const double2 pA = cached ? PHq[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
       const double2 pB = !hasB ? make_double2(1.0, 0.0) : (cached ? PHq[KP + ak] : __ldg(tab.phase + (size_t)mB * KP + ak));
-      double2 c[3], u[3];
+      double2 c[3];
       // packed eigen input: P-_{mA} y + i P-_{mB} y   (P-: α=-1 -> e^{+iωτ}, α=+1 -> e^{-iωτ})
       const double2 ym = C[j], y0 = C[Kc + j], yp = C[2 * Kc + j];
       const double2 bm = hasB ? cmul(ym, pB) : make_double2(0.0, 0.0);
@@ -487,8 +487,7 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       c[0] = cadd(cmul(ym, pA), cmuli(bm));
       c[1] = cadd(y0, cmuli(b0));
       c[2] = cadd(cmulc(yp, pA), cmuli(bp));
-      to_prim(as, GP[ak], GQ[ak], c, u);
-      put_input_z<N, R>(Xh, full_index(kap, N), (double)kap, u);
+      put_input_eigen<N, R>(Xh, full_index(kap, N), (double)kap, as, GP[ak], GQ[ak], c);
     }
     if (SPLIT > 1) hg.sync(); else grp.sync();
     STAMP(1)
@@ -500,17 +499,20 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
       const double as = kap < 0 ? -GA[ak] : GA[ak];
       const double p = GP[ak], q = GQ[ak];
-      double2 zp[3], zm[3], na[3], nb[3], ea[3], eb[3];
-      get_output_z<N, R>(Xh, full_index(kap, N), (double)kap, invN, zp);
-      get_output_z<N, R>(Xh, full_index(-kap, N), (double)(-kap), invN, zm);
+      // unpack the two samples from the raw outputs Z(±κ): with D = diag(-iκ, -1, -iκ)/N the map of the
+      // packed pair, conj(D(-κ) Z(-κ)) = D(κ) conj Z(-κ), so N_A(κ) = D(κ) (Z(κ) + conj Z(-κ))/2 and
+      // N_B(κ) = D(κ) (-i)(Z(κ) - conj Z(-κ))/2: the half-sums go through the fused eigen map (scale 1/2N)
+      constexpr int FS = fft_fs<N, R>();
+      const int ip = fpad<R>(full_index(kap, N)), im = fpad<R>(full_index(-kap, N));
+      double2 ra[3], rb[3], ea[3], eb[3];
 #pragma unroll
-      for (int f = 0; f < 3; ++f) {  // unpack: N_A(κ) = (Z(κ) + conj Z(-κ))/2, N_B = (Z - conj Z(-κ))/(2i)
-        const double2 zc = cconj(zm[f]);
-        na[f] = cscale(cadd(zp[f], zc), 0.5);
-        nb[f] = cscale(cmulmi(csub(zp[f], zc)), 0.5);
+      for (int f = 0; f < 3; ++f) {
+        const double2 zp = Xh[f * FS + ip], zc = cconj(Xh[f * FS + im]);
+        ra[f] = cadd(zp, zc);
+        rb[f] = cmulmi(csub(zp, zc));
       }
-      to_eigen(as, p, q, na, ea);
-      to_eigen(as, p, q, nb, eb);
+      eigen_from_raw(ra[0], ra[1], ra[2], (double)kap, as, p, q, 0.5 * invN, ea);
+      eigen_from_raw(rb[0], rb[1], rb[2], (double)kap, as, p, q, 0.5 * invN, eb);
       const double2 pA = cached ? PHq[ak] : __ldg(tab.phase + (size_t)mA * KP + ak);
       const double2 z0 = make_double2(0.0, 0.0);
       double2 am = caxpy(wA, cmulc(ea[0], pA), z0);  // P+: α=-1 -> e^{-iωτ}, α=+1 -> e^{+iωτ}

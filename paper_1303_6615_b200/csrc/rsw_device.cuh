@@ -291,8 +291,11 @@ __host__ __device__ constexpr int fft_len(int p) {  // block length L_p
 // registers: ~60 DP instructions per butterfly, ~20% of the transform); the other passes store the
 // bases e^{-2πi k1 / L_p} only and form the powers in registers (small radices, or the latency-bound
 // small transforms, where the product chain was measured faster than the loads).
+#ifndef RSW_TW_FULL_MIN_N
+#define RSW_TW_FULL_MIN_N 512  // smallest transform whose radix >= 8 passes keep a full twiddle table
+#endif
 template <int N, int R>
-__host__ __device__ constexpr bool fft_tw_full(int p) { return N >= 512 && fft_rad<N, R>(p) >= 8; }
+__host__ __device__ constexpr bool fft_tw_full(int p) { return N >= RSW_TW_FULL_MIN_N && fft_rad<N, R>(p) >= 8; }
 template <int N, int R>
 __host__ __device__ constexpr int fft_tw_len(int p) {  // table entries of pass p (last pass: none)
   return (p >= fft_npass<N, R>() - 1) ? 0
@@ -520,7 +523,7 @@ __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j
 // v1 copy before the products and the exit; between passes of a field a warp barrier when the field
 // lies in one warp (N/R <= 32: n <= 256), else a group barrier (2m in all).  TWT: twiddle policy (fft_tw_src); with TWT = 2, twt is the
 // thread's TMEM address of its twiddle slots (lane quarter + column base, filled by tw_tmem_fill).
-template <int N, int R, int T, class GRP = CtaGroup, int TWT = 1>
+template <int N, int R, int T, class GRP = CtaGroup, int TWT = 0>
 __device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const double2* TW, const GRP& grp = GRP(),
                                         uint32_t twt = 0) {
   static_assert(T >= 3 * (N / R), "nl_core: T must cover 3 N/R field-columns");
@@ -592,20 +595,24 @@ __device__ __forceinline__ void get_output_z(const double2* X, int k_full, doubl
 //   c∓ = -(p/N)(Z1 + as κ Z2) ± (s κ/N) Z0,   c0 = -i (q/N)(κ Z2 - as Z1);
 // and an eigen state into the FFT input, (u0, iκ u1, u2) with u = R c, i.e. with d = c+ - c-,
 // e = c+ + c-:  X0 = i s d,  X1 = iκ p e - κ as q c0,  X2 = q c0 + i as p e.
-template <int N, int R>
-__device__ __forceinline__ void get_output_eigen(const double2* X, int k_full, double kap, double as, double p,
-                                                 double q, double2* nn) {
-  constexpr int FS = fft_fs<N, R>();
-  constexpr double invN = 1.0 / N, sN = 0.70710678118654752440084436210485 / N;
-  const int i = fpad<R>(k_full);
-  const double2 X0 = X[i], X1 = X[FS + i], X2 = X[2 * FS + i];
-  const double ak = as * kap, sk = sN * kap, pn = p * invN, qn = q * invN;
+// the map on raw (unnormalised) FFT outputs X0..X2 of one entry, with the normalisation `scale` (1/N,
+// or 1/(2N) for the unpacked half-sums of the coarse sample pairs)
+__device__ __forceinline__ void eigen_from_raw(const double2 X0, const double2 X1, const double2 X2, double kap,
+                                               double as, double p, double q, double scale, double2* nn) {
+  const double ak = as * kap, sk = 0.70710678118654752440084436210485 * scale * kap, pn = p * scale, qn = q * scale;
   const double2 T = make_double2(fma(ak, X2.x, X1.x), fma(ak, X2.y, X1.y));
   const double2 A = make_double2(sk * X0.x, sk * X0.y);
   nn[0] = make_double2(fma(-pn, T.x, A.x), fma(-pn, T.y, A.y));
   nn[2] = make_double2(fma(-pn, T.x, -A.x), fma(-pn, T.y, -A.y));
   const double2 W = make_double2(fma(kap, X2.x, -as * X1.x), fma(kap, X2.y, -as * X1.y));
   nn[1] = make_double2(qn * W.y, -qn * W.x);
+}
+template <int N, int R>
+__device__ __forceinline__ void get_output_eigen(const double2* X, int k_full, double kap, double as, double p,
+                                                 double q, double2* nn) {
+  constexpr int FS = fft_fs<N, R>();
+  const int i = fpad<R>(k_full);
+  eigen_from_raw(X[i], X[FS + i], X[2 * FS + i], kap, as, p, q, 1.0 / N, nn);
 }
 template <int N, int R>
 __device__ __forceinline__ void put_input_eigen(double2* X, int k_full, double kap, double as, double p, double q,

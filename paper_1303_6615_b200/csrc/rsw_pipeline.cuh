@@ -107,18 +107,29 @@ struct PipeLayout {
   static constexpr int F_TW = F0, F_CP = F_TW + fft_tw_size<N, RF>(), F_D = F_CP + 6 * KP, F_ND = 9 * KP,
                        F_G = F_D + (F_ND + 1) / 2;  // first fine group's X
   static constexpr size_t bytes = sizeof(double2) * (F_G + NPG * 6 * N);
-  static constexpr int CPG = (FineTmem<N, TG>::COLS + 31) / 32 * 32;  // TMEM columns per fine group
+  // fine groups read their radix-R twiddles from TMEM whenever the transform keeps full tables (as k_fine
+  // does: the two schedules must round alike)
+  static constexpr int TWT = fft_tw_tcols<N, RF>() > 0 ? 2 : 0;
+  static constexpr int CPG = (FineTmem<N, TG>::COLS + (TWT == 2 ? fft_tw_tcols<N, RF>() : 0) + 31) / 32 * 32;  // TMEM columns per fine group
   static constexpr int T = TC + NPG * TG;
 };
 
 // fine worker group: claim the lowest-iteration ready pair task (k, p) — slices 2p, 2p+1 of U^k, ready
 // when prog[k] covers them — run the fine pair integrator, write F^k, set doneF[k][p] (release)
-template <int N, int RF, int TG, int FSCHEME>
+template <int N, int RF, int TG, int FSCHEME, int TWT>
 __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedGroup grp, double2* W,
                                                  const FineSmemTab& ft, uint32_t tcol, int* task) {
   constexpr size_t L = (size_t)3 * (N / 2 + 1) * 2;
   const int S = a.S, Kit = a.K, npairs = a.npairs;
   double2* Yb = W + 3 * N;
+  const uint32_t twcol = tcol + FineTmem<N, TG>::COLS;  // this group's twiddle copies (TWT = 2)
+  if constexpr (TWT == 2) {
+    tw_tmem_fill<N, RF, 2>(ft.TW, twcol + ((uint32_t)(32 * ((threadIdx.x >> 5) & 3)) << 16), grp.tid());
+    tmem_wait_st();
+    tmem_fence_before();
+    grp.sync();
+    tmem_fence_after();
+  }
   for (;;) {
     if (grp.tid() == 0) {
       int tk = -1, tp = -1;
@@ -153,8 +164,10 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
     if (tf && grp.tid() == 0) tf[0] = t_start;
     const double* Uk = a.Uall + (size_t)tk * (S + 1) * L;
     double* Fk = a.Fall + (size_t)tk * S * L;
-    fine_pair_run<N, RF, TG, FSCHEME, false>(grp, W, Yb, ft, tcol, a.ft.g, Uk + nA * L, nB < S ? Uk + nB * L : nullptr,
-                                             Fk + nA * L, nB < S ? Fk + nB * L : nullptr, a.m_fine, a.h, a.hb);
+    fine_pair_run<N, RF, TG, FSCHEME, false, NamedGroup, false, TWT>(grp, W, Yb, ft, tcol, a.ft.g, Uk + nA * L,
+                                                                   nB < S ? Uk + nB * L : nullptr, Fk + nA * L,
+                                                                   nB < S ? Fk + nB * L : nullptr, a.m_fine, a.h, a.hb,
+                                                                   twcol);
     grp.sync();  // the whole pair's F is written
     if (grp.tid() == 0) {
       st_release_u32(a.doneF + (size_t)tk * npairs + tp, 1u);
@@ -201,7 +214,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
       constexpr int XG = TC / TG;
       const int xi = ct / TG;
       if (xi < XG && (NPG + XG) * LY::CPG <= 512)
-        fine_worker_loop<N, RF, TG, FSCHEME>(a, NamedGroup{FT + xi * TG, 1 + NPG + xi, TG},
+        fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{FT + xi * TG, 1 + NPG + xi, TG},
                                             smem + LY::C0 + (size_t)xi * 6 * N, ft,
                                             tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi]);
     } else {
@@ -354,7 +367,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
   } else {
     // ======================================= fine worker group 0 =======================================
     const int gi = threadIdx.x / TG;
-    fine_worker_loop<N, RF, TG, FSCHEME>(a, NamedGroup{gi * TG, 1 + gi, TG}, smem + LY::F_G + (size_t)gi * 6 * N,
+    fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{gi * TG, 1 + gi, TG}, smem + LY::F_G + (size_t)gi * 6 * N,
                                         ft, tslot + (uint32_t)(gi * LY::CPG), s_task[gi]);
   }
   tmem_fence_before();
