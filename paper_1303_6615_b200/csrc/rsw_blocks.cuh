@@ -341,6 +341,11 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // grid barrier: monotone arrival counter, arrive with a gpu-scope release RMW, spin with
 // gpu-scope acquire loads (1.2 us at 128-148 CTAs on B200, vs 2.2 us for a volatile-flag barrier;
@@ -393,12 +398,14 @@ __device__ __forceinline__ bool watchdog_expired(Watch& w, unsigned* wd, const u
 }
 // stopk / kself: give up as well once the run stopped before iteration kself (the waiting sweep is
 // discarded: its remaining work only has to reach the next group barrier, where it aborts)
+// sys: the flag is released by another GPU (multi-GPU pipelined schedule): system-scope acquire
 __device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target, unsigned* wd, const unsigned* hb,
-                                               const int* stopk = nullptr, int kself = 0) {
-  if (ld_acquire_gpu(p) >= target) return;
+                                               const int* stopk = nullptr, int kself = 0, bool sys = false) {
+  auto ld = [&] { return sys ? ld_acquire_sys(p) : ld_acquire_gpu(p); };
+  if (ld() >= target) return;
   Watch w = watch_start(hb);
   for (unsigned it = 0;; ++it) {
-    if (ld_acquire_gpu(p) >= target) return;
+    if (ld() >= target) return;
     if (stopk && *(volatile const int*)stopk < kself) return;
     if ((it & 63) == 63 && watchdog_expired(w, wd, hb)) return;
     __nanosleep(64);
@@ -577,7 +584,7 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
     const int o = tid_ / 3, f = tid_ % 3, ak = rank + o * P;
     if (ak <= K) {
       // pipelined parareal: F(U^{k-1}_n) and the previous sweep's slice n must be complete
-      if (ca.wF) spin_until_geq(ca.wF + n / 2, 1u, ca.wd, ca.hb, ca.stopk, ca.kself);
+      if (ca.wF) spin_until_geq(ca.wF + n / 2, 1u, ca.wd, ca.hb, ca.stopk, ca.kself, ca.wsys != 0);
       if (ca.wprog) spin_until_geq(ca.wprog, ca.wunit * (unsigned)(n + 1), ca.wd, ca.hb, ca.stopk, ca.kself);
       if (ca.F) pf_F = __ldcg(reinterpret_cast<const double2*>(ca.F) + (size_t)n * Ls + f * NH + ak);
       pf_G = __ldcg(reinterpret_cast<const double2*>(ca.Gprev) + (size_t)n * Ls + f * NH + ak);

@@ -270,6 +270,7 @@ constexpr int kMaxVirtualWorld = 16;
 struct Workspace {
   DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof, Gnew, yin, chk;
   DevBuf pU, pG, pF, prp, pres, pctl, pyb, ppart, pst;  // pipelined schedule
+  DevBuf mirF, mirC;                                     // RSW_PIPE_MIRROR test: a same-GPU "peer"
   DevBuf vshard[kMaxVirtualWorld];                 // RSW_VIRTUAL_WORLD: one fine-endpoint buffer per virtual rank
   double* rhost = nullptr;
   unsigned* chost = nullptr;
@@ -468,6 +469,11 @@ rsw_status run_strang_chain(const rsw_params* p, double dT, Workspace* ws, doubl
 struct rsw_comm {
   void* comm = nullptr;  // ncclComm_t
   int rank = 0, world = 1;
+  // multi-GPU pipelined schedule: the peers' fine-endpoint buffers and control words, IPC-mapped once
+  // per (peer, allocation) and re-mapped only when a peer's allocation changed
+  std::vector<cudaIpcMemHandle_t> hF, hC;
+  std::vector<void*> mF, mC;
+  void* scratch = nullptr;  // device bytes for the handle all-gather and the stream barriers
 };
 
 namespace {
@@ -477,6 +483,7 @@ struct NcclApi {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
 };
 NcclApi g_nccl;
@@ -490,8 +497,9 @@ rsw_status load_nccl() {
   g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
   g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
+  g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
   g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
-  if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.commDestroy || !g_nccl.allGather)
+  if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.commDestroy || !g_nccl.allGather || !g_nccl.allReduce)
     return fail(RSW_ERR_NCCL, "libnccl is missing symbols");
   g_nccl.h = h;
   return RSW_OK;
@@ -499,6 +507,51 @@ rsw_status load_nccl() {
 
 rsw_status nccl_fail(ncclResult_t r, const char* what) {
   return fail(RSW_ERR_NCCL, std::string(what) + ": " + (g_nccl.errStr ? g_nccl.errStr(r) : "nccl error"));
+}
+
+// stream-ordered barrier of all ranks (a one-int all-reduce): orders this rank's preceding work (the
+// memsets of the buffers the peers write into) before every rank's following work, and the peers'
+// preceding kernels (their pushes into this rank's buffers) before this rank's following work
+rsw_status comm_barrier(rsw_comm* c, cudaStream_t st) {
+  ncclResult_t r = g_nccl.allReduce((int*)c->scratch, (int*)c->scratch + 1, 1, ncclInt32, ncclSum,
+                                    (ncclComm_t)c->comm, st);
+  return r == ncclSuccess ? RSW_OK : nccl_fail(r, "ncclAllReduce (barrier)");
+}
+
+// all-gather of every rank's IPC handles of (F buffer, control words); open the peers' (cached)
+rsw_status exchange_peer_buffers(rsw_comm* c, void* myF, void* myC, cudaStream_t st) {
+  const int W = c->world;
+  cudaIpcMemHandle_t h[2];
+  CUDA_TRY(cudaIpcGetMemHandle(&h[0], myF));
+  CUDA_TRY(cudaIpcGetMemHandle(&h[1], myC));
+  const size_t HB = sizeof(h);
+  char* dev = (char*)c->scratch + 64;
+  CUDA_TRY(cudaMemcpyAsync(dev + c->rank * HB, h, HB, cudaMemcpyHostToDevice, st));
+  ncclResult_t r = g_nccl.allGather(dev + c->rank * HB, dev, HB, ncclChar, (ncclComm_t)c->comm, st);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather (IPC handles)");
+  std::vector<cudaIpcMemHandle_t> all(2 * W);
+  CUDA_TRY(cudaMemcpyAsync(all.data(), dev, HB * W, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if ((int)c->mF.size() != W) {
+    c->hF.assign(W, cudaIpcMemHandle_t{});
+    c->hC.assign(W, cudaIpcMemHandle_t{});
+    c->mF.assign(W, nullptr);
+    c->mC.assign(W, nullptr);
+  }
+  for (int q = 0; q < W; ++q) {
+    if (q == c->rank) continue;
+    for (int b = 0; b < 2; ++b) {
+      cudaIpcMemHandle_t& hold = b ? c->hC[q] : c->hF[q];
+      void*& mp = b ? c->mC[q] : c->mF[q];
+      const cudaIpcMemHandle_t& hn = all[2 * q + b];
+      if (mp && std::memcmp(&hold, &hn, sizeof(hn)) == 0) continue;
+      if (mp) cudaIpcCloseMemHandle(mp);
+      mp = nullptr;
+      CUDA_TRY(cudaIpcOpenMemHandle(&mp, hn, cudaIpcMemLazyEnablePeerAccess));
+      hold = hn;
+    }
+  }
+  return RSW_OK;
 }
 }  // namespace
 
@@ -650,8 +703,12 @@ rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, doub
 // residual history and the iteration count are bitwise identical (tests/test_gpu_parity.py).
 rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
                          double* resid_hist, int32_t* iters_done, cudaStream_t st, double* F_out, double* G_out,
-                         rsw_parareal_stats* stats, Workspace* ws, bool* unsupported) {
+                         rsw_parareal_stats* stats, Workspace* ws, bool* unsupported, rsw_comm* comm) {
   *unsupported = false;
+  const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
+  const char* emir = getenv("RSW_PIPE_MIRROR");
+  const bool mirror = emir && emir[0] == '1';
+  const bool use_mirror = mirror && world == 1;  // test: push every pair to a same-GPU "peer" buffer too
   const int n = p->n, Km = n / 3, Kc = 2 * Km + 1, S = cfg->n_slices, K = cfg->max_iters, M = cfg->M;
   const size_t L = state_doubles(n);
   const int m = n_fine_steps(cfg->dT, cfg->dt);
@@ -703,7 +760,16 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     }
   }
   const char* egr = getenv("RSW_PIPE_GRID");
-  const int grid = egr ? atoi(egr) : (int)cap;
+  int grid = egr ? atoi(egr) : (int)cap;
+  if (world > 1) {  // every rank must run the same sweeps with the same groups: agree on the smallest grid
+    if (!comm->scratch) CUDA_TRY(cudaMalloc(&comm->scratch, 64 + 2 * sizeof(cudaIpcMemHandle_t) * (rsw::kMaxPeers + 1)));
+    CUDA_TRY(cudaMemcpyAsync((int*)comm->scratch + 2, &grid, sizeof(int), cudaMemcpyHostToDevice, st));
+    ncclResult_t r = g_nccl.allReduce((int*)comm->scratch + 2, (int*)comm->scratch + 3, 1, ncclInt32, ncclMin,
+                                      (ncclComm_t)comm->comm, st);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce (grid)");
+    CUDA_TRY(cudaMemcpyAsync(&grid, (int*)comm->scratch + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
   if (a.GC > grid && !eg) {  // many sample pairs: up to 8 pairs / 8 owned modes per coarse CTA (PIPE_CFG)
     a.GC = std::max(std::max((std::max(M / 2, 1) + 7) / 8, (Km + 1 + 7) / 8), 1);
   }
@@ -742,6 +808,35 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   a.gbar = a.ticket + 2;
   a.ybuf = (double2*)ws->pyb.p;
   a.part = (double2*)ws->ppart.p;
+  // fine tasks of this rank: the pairs of its slice shard (rsw_shard_range; S divisible by 2 x world)
+  {
+    int32_t lo = 0, hi = S;
+    if (world > 1) {
+      rsw_status sr = rsw_shard_range(S, rank, world, &lo, &hi);
+      if (sr != RSW_OK) return sr;
+    }
+    a.pair_lo = lo / 2;
+    a.pair_hi = (world > 1) ? hi / 2 : a.npairs;
+  }
+  a.npeers = 0;
+  if (world > 1) {
+    rsw_status xs = exchange_peer_buffers(comm, ws->pF.p, ws->pctl.p, st);
+    if (xs != RSW_OK) return xs;
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) continue;
+      a.peerF[a.npeers] = (double*)comm->mF[q];
+      a.peerDoneF[a.npeers] = (unsigned*)comm->mC[q] + (a.doneF - ctl);
+      ++a.npeers;
+    }
+  }
+  if (use_mirror) {
+    CUDA_TRY(ensure(ws->mirF, sizeof(double) * nF));
+    CUDA_TRY(ensure(ws->mirC, sizeof(unsigned) * nctl));
+    CUDA_TRY(cudaMemsetAsync(ws->mirC.p, 0, sizeof(unsigned) * nctl, st));
+    a.peerF[0] = (double*)ws->mirF.p;
+    a.peerDoneF[0] = (unsigned*)ws->mirC.p + (a.doneF - ctl);
+    a.npeers = 1;
+  }
   a.trace = nullptr;
   const size_t nst = 2 * (size_t)(K + 1) + 2;
   CUDA_TRY(ensure(ws->pst, sizeof(unsigned long long) * nst));
@@ -762,7 +857,15 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   CUDA_TRY(cudaMemcpyAsync(a.stopk, &stop_init, sizeof(int), cudaMemcpyHostToDevice, st));
   for (int k = 0; k <= K; ++k)  // U^k_0 = u0 for every iteration
     CUDA_TRY(cudaMemcpyAsync(a.Uall + (size_t)k * (S + 1) * L, u0, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
+  if (world > 1) {  // every rank's flags are zeroed before any peer may push into them
+    rsw_status bs = comm_barrier(comm, st);
+    if (bs != RSW_OK) return bs;
+  }
   CUDA_TRY(rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, grid, nullptr, st));
+  if (world > 1) {  // no peer kernel is still pushing into this rank's buffers after this point
+    rsw_status bs = comm_barrier(comm, st);
+    if (bs != RSW_OK) return bs;
+  }
   int stopk = 0;
   unsigned wd = 0;
   std::vector<double> res(K + 1, 0.0);
@@ -814,13 +917,20 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   }
   if (wd) return fail(RSW_ERR_CUDA, "pipelined parareal: a dependency wait timed out (watchdog)");
   const int kout = stopk <= K ? stopk : K;
+  if (use_mirror && kout >= 1) {  // every pair of the iterations used was pushed and released
+    std::vector<unsigned> mc((size_t)kout * a.npairs);
+    CUDA_TRY(cudaMemcpy(mc.data(), (unsigned*)ws->mirC.p + (a.doneF - ctl), sizeof(unsigned) * mc.size(),
+                        cudaMemcpyDeviceToHost));
+    for (unsigned v : mc)
+      if (v != 1u) return fail(RSW_ERR_CUDA, "pipelined parareal (mirror test): a pushed pair was not released");
+  }
   for (int k = 1; k <= kout; ++k) resid_hist[k - 1] = res[k];
   *iters_done = kout;
   CUDA_TRY(cudaMemcpyAsync(U, a.Uall + (size_t)kout * (S + 1) * L, sizeof(double) * L * (S + 1),
                            cudaMemcpyDeviceToDevice, st));
-  if (F_out && kout >= 1)
-    CUDA_TRY(cudaMemcpyAsync(F_out, a.Fall + (size_t)(kout - 1) * S * L, sizeof(double) * L * S,
-                             cudaMemcpyDeviceToDevice, st));
+  if (F_out && kout >= 1)  // (mirror test: the pushed copy)
+    CUDA_TRY(cudaMemcpyAsync(F_out, (use_mirror ? (double*)ws->mirF.p : a.Fall) + (size_t)(kout - 1) * S * L,
+                             sizeof(double) * L * S, cudaMemcpyDeviceToDevice, st));
   if (G_out)
     CUDA_TRY(cudaMemcpyAsync(G_out, a.Gall + (size_t)kout * S * L, sizeof(double) * L * S, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(cudaEventRecord(ev[7], st));
@@ -832,7 +942,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     stats->comm_ms = 0;
     stats->coarse_ms = tot;
     stats->total_ms = tot;
-    stats->fine_slice_steps = (int64_t)kout * S * m;
+    stats->fine_slice_steps = (int64_t)kout * std::min(S, 2 * (a.pair_hi - a.pair_lo)) * m;  // this rank's tasks
     stats->kernel_launches = 1;
     stats->pipelined = 1;
     // phase split from the in-kernel globaltimer stamps: the k = 0 sweep (first sweep start to its
@@ -886,7 +996,10 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   if ((s = check_states_sync(p, 1, u0, st, ws)) != RSW_OK) return s;
   {
     const char* vwe = getenv("RSW_VIRTUAL_WORLD");
-    const bool can_pipe = !comm && rsw::pipeline_supported(p->n) && cfg->coarse_scheme != RSW_COARSE_STRANG &&
+    // multi-GPU: every rank runs the replicated sweeps and its shard's fine tasks, pushing F to the peers
+    // (S divisible by 2 x world so shards are whole pairs); a world-1 communicator keeps the bulk path
+    const bool comm_ok = !comm || (comm->world > 1 && comm->world <= rsw::kMaxPeers + 1 && S % (2 * comm->world) == 0);
+    const bool can_pipe = comm_ok && rsw::pipeline_supported(p->n) && cfg->coarse_scheme != RSW_COARSE_STRANG &&
                           !(vwe && atoi(vwe) > 1);
     const char* pe = getenv("RSW_PIPELINE");
     const bool auto_pipe = cfg->schedule == RSW_SCHEDULE_AUTO && !(pe && pe[0] == '0');
@@ -897,7 +1010,7 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
       return fail(RSW_ERR_CONFIG, "unknown schedule");
     if (can_pipe && (auto_pipe || cfg->schedule == RSW_SCHEDULE_PIPELINED)) {
       bool unsupported = false;
-      s = run_pipelined(p, cfg, u0, U, resid_hist, iters_done, st, F_out, G_out, stats, ws, &unsupported);
+      s = run_pipelined(p, cfg, u0, U, resid_hist, iters_done, st, F_out, G_out, stats, ws, &unsupported, comm);
       // AUTO: a configuration the pipelined kernel cannot hold (too few co-resident CTAs for its coarse
       // groups, failed capacity query) runs the bulk schedule instead; an explicit request fails
       if (!(unsupported && cfg->schedule == RSW_SCHEDULE_AUTO)) return s;
@@ -1079,6 +1192,11 @@ rsw_status rsw_comm_init(const void* id128, int32_t rank, int32_t world, rsw_com
 
 rsw_status rsw_comm_destroy(rsw_comm* comm) {
   if (!comm) return RSW_OK;
+  for (void* m : comm->mF)
+    if (m) cudaIpcCloseMemHandle(m);
+  for (void* m : comm->mC)
+    if (m) cudaIpcCloseMemHandle(m);
+  if (comm->scratch) cudaFree(comm->scratch);
   if (comm->comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)comm->comm);
   delete comm;
   return RSW_OK;

@@ -50,12 +50,15 @@ struct CoarseArgs {
   const unsigned* wF;     // pipelined: done flags of the previous iteration's fine pairs, or null
   unsigned* wd;           // pipelined: watchdog flag (set when a wait times out), or null
   const unsigned* hb;     // pipelined: progress heartbeat read by the watchdog, or null
+  int wsys;               // pipelined multi-GPU: wF flags are released by other GPUs (system-scope acquire)
   const int* stopk;       // pipelined: first stopped iteration (waits of sweep kself > *stopk give up), or null
   int kself;
   double* rparts;       // [S][K+1][2] residual partials or null
   int n_end;            // number of chain steps (S)
   unsigned long long* prof;  // optional phase timestamps (CTA 0; RSW_PROFILE_COARSE=1), else null
 };
+
+constexpr int kMaxPeers = 8;  // ranks of one NVSwitch node
 
 // Pipelined parareal (rsw_pipeline.cu): every iteration's buffers stay resident
 struct PipeArgs {
@@ -81,6 +84,12 @@ struct PipeArgs {
   double2* part;        // [NG][GC][3Kc] partial sums
   unsigned long long* trace;  // optional timeline (RSW_PIPE_TRACE): sweep [K+1][2], slice [K+1][S], fine [K][npairs][2]
   unsigned long long* stamps; // always: sweep start / end [K+1][2] (globaltimer ns), fine-task latency sum, count
+  // multi-GPU pipelined schedule: this rank runs every sweep (replicated) but only the fine tasks of its
+  // slice shard, pairs [pair_lo, pair_hi), and pushes each finished pair to the peers' Fall over NVLink
+  // (IPC-mapped), releasing the peer's doneF flag at system scope; one GPU: [0, npairs), no peers
+  int pair_lo, pair_hi, npeers;
+  double* peerF[kMaxPeers];
+  unsigned* peerDoneF[kMaxPeers];
 };
 bool pipeline_supported(int n);
 cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);

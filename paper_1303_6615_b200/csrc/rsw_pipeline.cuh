@@ -47,6 +47,9 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_sys_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 constexpr unsigned ABORT_BIT = 1u << 28;
 
 // group barrier over P CTAs (their coarse sub-CTAs `grp`) on counter `bar`; rank 0 may raise the abort
@@ -138,13 +141,14 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
         const int lim = min(Kit, *(volatile int*)a.stopk) - 1;  // F^k is needed by sweep k+1 <= stop
         bool all_claimed = true;
         for (int k = 0; k <= lim && tk < 0; ++k) {
-          const unsigned t = *(volatile unsigned*)(a.next + k);
-          if ((int)t >= npairs) continue;
+          const unsigned t = *(volatile unsigned*)(a.next + k);  // local task index: pair pair_lo + t
+          if ((int)t >= a.pair_hi - a.pair_lo) continue;
           all_claimed = false;
-          const int need = (2 * (int)t + 1 < S) ? 2 * (int)t + 1 : 2 * (int)t;  // U^k_{2t}, U^k_{2t+1}
+          const int pp = a.pair_lo + (int)t;
+          const int need = (2 * pp + 1 < S) ? 2 * pp + 1 : 2 * pp;  // U^k_{2p}, U^k_{2p+1}
           if (ld_acquire_gpu(a.prog + k) >= (unsigned)(a.GC * need) && atomicCAS(a.next + k, t, t + 1) == t) {
             tk = k;
-            tp = (int)t;
+            tp = pp;
           }
         }
         if (tk >= 0 || all_claimed) break;
@@ -169,6 +173,20 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
                                                                    nB < S ? Fk + nB * L : nullptr, a.m_fine, a.h, a.hb,
                                                                    twcol);
     grp.sync();  // the whole pair's F is written
+    if (a.npeers > 0) {
+      // multi-GPU: push the pair's endpoints into every peer's F^k at the same offset (NVLink stores to
+      // IPC-mapped memory), make them visible at system scope, then release the peers' done flags
+      const size_t cnt = (size_t)(nB < S ? 2 : 1) * L / 2;  // double2 entries
+      const double2* src = reinterpret_cast<const double2*>(Fk + nA * L);
+      for (int r = 0; r < a.npeers; ++r) {
+        double2* dst = reinterpret_cast<double2*>(a.peerF[r] + (size_t)tk * S * L + nA * L);
+        for (size_t i = grp.tid(); i < cnt; i += TG) dst[i] = __ldcg(src + i);
+      }
+      __threadfence_system();
+      grp.sync();
+      if (grp.tid() == 0)
+        for (int r = 0; r < a.npeers; ++r) st_release_sys_u32(a.peerDoneF[r] + (size_t)tk * npairs + tp, 1u);
+    }
     if (grp.tid() == 0) {
       st_release_u32(a.doneF + (size_t)tk * npairs + tp, 1u);
       const unsigned long long t_end = gtimer();
@@ -292,6 +310,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         ca.wF = k ? a.doneF + (size_t)(k - 1) * a.npairs : nullptr;
         ca.wd = a.wd;
         ca.hb = a.hb;
+        ca.wsys = a.npeers > 0 || a.pair_hi - a.pair_lo < a.npairs;  // flags of other ranks' tasks
         ca.stopk = a.stopk;
         ca.kself = k;
         ca.prof = nullptr;

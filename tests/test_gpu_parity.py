@@ -523,6 +523,24 @@ def test_comm_world1_runs_the_nccl_exchange(rsw_gpu):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("wname,max_iters,tol", [("C3", 2, 0.0), ("C2", 64, 1e-6)])
+def test_pipelined_push_to_peer_mirror(rsw_gpu, wname, max_iters, tol, monkeypatch):
+    """Multi-GPU pipelined schedule on one GPU (RSW_PIPE_MIRROR=1): every finished fine pair is ALSO
+    pushed into a same-GPU "peer" copy of F (NVLink-store code path: copy, system fence, system-scope
+    release of the peer's done flag).  The pushed copy must equal F bitwise and every pair of the
+    iterations used must be released; the solve itself is unchanged (bitwise equal to bulk)."""
+    w = getattr(inputs, wname)
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=max_iters, tol=tol, want_FG=True)
+    a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    monkeypatch.setenv("RSW_PIPE_MIRROR", "1")
+    b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
+    assert b["stats"]["pipelined"]
+    assert a["iters"] == b["iters"] and a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
+    assert torch.equal(a["F"], b["F"])  # b["F"] is the pushed (mirror) copy
+
+
 def test_repeatability_soak(rsw_gpu):
     """Stand-in for racecheck (compute-sanitizer is unavailable on this pool): the lock-free protocols
     (pipelined sentinel hand-offs, task claiming, in-place FFT passes with one barrier each, TMEM
