@@ -229,11 +229,6 @@ __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h,
   if (r_out && threadIdx.x == 0) *r_out = rmax;
 }
 
-// M0: DFMA peak probe — independent FMA chains, every SM
-
-
-
-
 template <int N, int NOWN, int R = coarse_radix<N>(), int T = coarse_threads<N>()>
 static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar,
                                             double* r_out, int grid, cudaStream_t st) {
