@@ -220,16 +220,20 @@ __device__ __forceinline__ void to_prim(double as, double p, double q, const dou
 }
 
 // thread-group policies: the whole CTA, or a warp-aligned group of a CTA with its own named barrier
+// fbar(): first of three named barriers the FFT core may use per field (0: none, use the group barrier)
 struct CtaGroup {
   __device__ __forceinline__ int base() const { return 0; }
   __device__ __forceinline__ int tid() const { return threadIdx.x; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ int fbar() const { return 1; }  // ids 1..3 (kernels whose whole CTA is one group)
 };
 struct NamedGroup {
   int b0, id, nthr;  // first thread, barrier id (1..15), thread count (multiple of 32)
+  int fb = 0;        // per-field barrier ids fb..fb+2, or 0
   __device__ __forceinline__ int base() const { return b0; }
   __device__ __forceinline__ int tid() const { return threadIdx.x - b0; }
   __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory"); }
+  __device__ __forceinline__ int fbar() const { return fb; }
 };
 
 // Padded storage of the FFT buffers: element e of a field lives at fpad(e) = e + e / R (one pad slot
@@ -444,16 +448,29 @@ __device__ __forceinline__ int fft_elem0(int b) {  // first element of butterfly
 // buffer, so when a field's N/R threads lie inside one warp (N/R divides 32) a warp barrier orders the
 // passes; otherwise the group barrier.  Called by every thread of the group (also the inactive ones,
 // which may share a warp with active ones), so __syncwarp always sees the full warp.
+// Fields spanning several whole warps (N/R = 64, 128) synchronise on a named barrier of their own
+// N/R threads when the group provides per-field barrier ids (the three fields then run their passes
+// independently); the threads outside the three fields (act = false) skip it.
 template <int N, int R, class GRP>
-__device__ __forceinline__ void pass_sync(const GRP& grp) {
-  if constexpr ((N / R) <= 32 && 32 % (N / R) == 0) __syncwarp();
-  else grp.sync();
+__device__ __forceinline__ void pass_sync(const GRP& grp, int f = 0, bool act = true) {
+  constexpr int NJ = N / R;
+  if constexpr (NJ <= 32 && 32 % NJ == 0) {
+    __syncwarp();
+  } else if constexpr (NJ % 32 == 0) {
+    if (grp.fbar() > 0) {
+      if (act) asm volatile("bar.sync %0, %1;" ::"r"(grp.fbar() + f), "r"(NJ) : "memory");
+    } else {
+      grp.sync();
+    }
+  } else {
+    grp.sync();
+  }
 }
 
 // synthesis passes p..m-1 of field buffer Xf (sign +); the last pass leaves its outputs in v
 template <int N, int R, int p, int TWT, class GRP>
 __device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* Xf, int j, bool act, const double2* TW,
-                                             uint32_t twt, const GRP& grp) {
+                                             uint32_t twt, const GRP& grp, int f) {
   constexpr int m = fft_npass<N, R>(), r = fft_rad<N, R>(p), L = fft_len<N, R>(p), d = L / r, NJ = N / R;
   constexpr int K = N / 3;
   if (act) {
@@ -479,15 +496,15 @@ __device__ __forceinline__ void core_inverse(double2 (&v)[R], double2* Xf, int j
     }
   }
   if constexpr (p < m - 1) {
-    pass_sync<N, R>(grp);
-    core_inverse<N, R, p + 1, TWT>(v, Xf, j, act, TW, twt, grp);
+    pass_sync<N, R>(grp, f, act);
+    core_inverse<N, R, p + 1, TWT>(v, Xf, j, act, TW, twt, grp, f);
   }
 }
 
 // analysis passes p, p-1, ..., 0 (sign -); pass 0 stores the retained modes only
 template <int N, int R, int p, int TWT, class GRP>
 __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j, bool act, const double2* TW,
-                                             uint32_t twt, const GRP& grp) {
+                                             uint32_t twt, const GRP& grp, int f) {
   if constexpr (p >= 0) {
     constexpr int r = fft_rad<N, R>(p), L = fft_len<N, R>(p), d = L / r, NJ = N / R;
     constexpr int K = N / 3;
@@ -510,9 +527,9 @@ __device__ __forceinline__ void core_forward(double2 (&v)[R], double2* Xf, int j
         }
       }
     }
-    if constexpr (p > 0) pass_sync<N, R>(grp);  // the next pass reads this field only
-    else grp.sync();                              // exit: the caller reads every field
-    core_forward<N, R, p - 1, TWT>(v, Xf, j, act, TW, twt, grp);
+    if constexpr (p > 0) pass_sync<N, R>(grp, f, act);  // the next pass reads this field only
+    else grp.sync();                                     // exit: the caller reads every field
+    core_forward<N, R, p - 1, TWT>(v, Xf, j, act, TW, twt, grp, f);
   }
 }
 
@@ -537,7 +554,7 @@ __device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const d
   double2* Xf = X + (act ? f : 0) * FS;
   double2* V = X + 3 * FS + fpad<R>(j * R);
   double2 v[R];
-  core_inverse<N, R, 0, TWT>(v, Xf, j, act, TW, twt, grp);
+  core_inverse<N, R, 0, TWT>(v, Xf, j, act, TW, twt, grp, f);
   // grid products (R1, R10): the last synthesis pass left the grid values of positions j R + s in
   // registers; v1 is shared with the v2x / h threads through V
   if (act && f == 0) {
@@ -565,9 +582,9 @@ __device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const d
       if (m > 1 || e <= K || e >= N - K) xb[fpad<R>(s)] = v[s];
     }
   }
-  if constexpr (m > 1) pass_sync<N, R>(grp);  // analysis pass m-1 wrote its own field only
+  if constexpr (m > 1) pass_sync<N, R>(grp, f, act);  // analysis pass m-1 wrote its own field only
   else grp.sync();
-  core_forward<N, R, m - 2, TWT>(v, Xf, j, act, TW, twt, grp);
+  core_forward<N, R, m - 2, TWT>(v, Xf, j, act, TW, twt, grp, f);
 }
 
 // N-eval input / output of one retained entry in the padded layout of nl_core

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(NPG * TG) k_fine(const double* u_in, double* u
       fine_pair_run<N, R, TG, SCHEME, LIN, CtaGroup, true, LY::TWT>(CtaGroup(), W, nullptr, st_, tslot, tab.g, uA, uB, oA,
                                                                     oB, m_steps, h, nullptr, tslot + LY::TWC);
     else
-      fine_pair_run<N, R, TG, SCHEME, LIN, NamedGroup, true, LY::TWT>(NamedGroup{g * TG, 1 + g, TG}, W, nullptr, st_, tslot,
+      fine_pair_run<N, R, TG, SCHEME, LIN, NamedGroup, true, LY::TWT>(NamedGroup{g * TG, 1 + g, TG, 3 + 3 * g}, W, nullptr, st_, tslot,
                                                                       tab.g, uA, uB, oA, oB, m_steps, h, nullptr,
                                                                       tslot + LY::TWC);
   }
