@@ -18,6 +18,25 @@
 
 namespace rsw {
 
+// Debug build only (-DRSW_PHASE_PROF, e.g. tools/build_variant.py): cycles of the N-eval phases seen by
+// thread 0 of CTA 0 (0 = between N-evals, i.e. the epilogue, 1 = inverse FFT, 2 = products and the
+// first analysis pass, 3 = the other analysis passes), printed per launch by k_fine.
+#ifdef RSW_PHASE_PROF
+static __device__ unsigned long long g_phase[8];
+#define RSW_PHASE(i)                                                 \
+  do {                                                               \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                       \
+      const unsigned long long c_ = clock64();                       \
+      if (g_phase[7]) g_phase[i] += c_ - g_phase[7];                 \
+      g_phase[7] = c_;                                               \
+    }                                                                \
+  } while (0)
+#else
+#define RSW_PHASE(i) \
+  do {               \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------------------------------------
 // complex arithmetic on double2
 // ---------------------------------------------------------------------------------------------
@@ -554,7 +573,9 @@ __device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const d
   double2* Xf = X + (act ? f : 0) * FS;
   double2* V = X + 3 * FS + fpad<R>(j * R);
   double2 v[R];
+  RSW_PHASE(0);
   core_inverse<N, R, 0, TWT>(v, Xf, j, act, TW, twt, grp, f);
+  RSW_PHASE(1);
   // grid products (R1, R10): the last synthesis pass left the grid values of positions j R + s in
   // registers; v1 is shared with the v2x / h threads through V
   if (act && f == 0) {
@@ -584,7 +605,9 @@ __device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const d
   }
   if constexpr (m > 1) pass_sync<N, R>(grp, f, act);  // analysis pass m-1 wrote its own field only
   else grp.sync();
+  RSW_PHASE(2);
   core_forward<N, R, m - 2, TWT>(v, Xf, j, act, TW, twt, grp, f);
+  RSW_PHASE(3);
 }
 
 // N-eval input / output of one retained entry in the padded layout of nl_core

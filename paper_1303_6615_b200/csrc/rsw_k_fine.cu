@@ -90,6 +90,12 @@ __global__ void __launch_bounds__(NPG * TG) k_fine(const double* u_in, double* u
     tmem_fence_after();
     tmem_dealloc<LY::NCOL>(tslot);
   }
+#ifdef RSW_PHASE_PROF
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    printf("[k_fine n=%d R=%d TG=%d] cycles per N-eval: epilogue+gaps %.0f inverse %.0f products %.0f forward %.0f\n", N, R,
+           TG, (double)g_phase[0] / (4.0 * m_steps), (double)g_phase[1] / (4.0 * m_steps), (double)g_phase[2] / (4.0 * m_steps),
+           (double)g_phase[3] / (4.0 * m_steps));
+#endif
 }
 
 
