@@ -10,5 +10,4 @@ python tools/ncu_summary.py gpurun_out/r2_pipe_c3.ncu-rep > gpurun_out/r2_pipe_c
 python tools/ncu_dpflops.py gpurun_out/r2_pipe_c3.ncu-rep > gpurun_out/r2_pipe_c3_dp.json 2>&1
 python tools/ncu_lines.py gpurun_out/r2_pipe_c3.ncu-rep 40 > gpurun_out/r2_pipe_c3_lines.txt 2>&1
 rm -f gpurun_out/r2_pipe_c3.ncu-rep
-RSW_LIB=variants/librsw_avgminb3.so timeout 300 python tools/run_kernel.py --what avg --reps 3 2>&1 | tail -1
 timeout 300 python tools/run_kernel.py --what avg --reps 3 2>&1 | tail -1
