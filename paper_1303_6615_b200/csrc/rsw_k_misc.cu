@@ -265,9 +265,12 @@ static cudaError_t launch_nl_n(const double* in, double* out, int S, const FineT
   return cudaGetLastError();
 }
 
+#ifndef RSW_AVG_R512
+#define RSW_AVG_R512 8  // radix of the batched N-bar at n = 512 (measurement knob)
+#endif
 template <int N>
 static cudaError_t launch_avg_n(const double* in, double* out, int S, int M, const AvgTab& tab, cudaStream_t st) {
-  constexpr int R = fine_radix<N>(), T = core_threads<N, R>();
+  constexpr int R = (N == 512) ? RSW_AVG_R512 : fine_radix<N>(), T = core_threads<N, R>();
   auto kfn = k_avg_states<N, R, T>;
   constexpr size_t sm = AvgLayout<N, R, T>::bytes;
   cudaError_t e = set_smem(kfn, sm);
