@@ -390,7 +390,9 @@ __device__ __forceinline__ bool watchdog_expired(Watch& w, unsigned* wd, const u
       w.t0 = now;
     }
   }
-  if (now - w.t0 > 4000000000ull) {
+  // limit: hb[1] ms without progress (the host writes it next to the heartbeat; RSW_WATCHDOG_MS, 4 s)
+  const unsigned long long lim = hb ? 1000000ull * *(volatile const unsigned*)(hb + 1) : 4000000000ull;
+  if (now - w.t0 > lim) {
     if (wd) atomicExch(wd, 1u);
     return true;
   }

@@ -788,7 +788,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   CUDA_TRY(ensure(ws->pF, sizeof(double) * nF));
   CUDA_TRY(ensure(ws->prp, sizeof(double) * 2 * (size_t)(K + 1) * S * (Km + 1)));
   CUDA_TRY(ensure(ws->pres, sizeof(double) * (K + 1)));
-  const size_t nctl = (size_t)(K + 1) + (size_t)std::max(K, 1) * a.npairs + std::max(K, 1) + 5 + (size_t)a.NG * 32;
+  const size_t nctl = (size_t)(K + 1) + (size_t)std::max(K, 1) * a.npairs + std::max(K, 1) + 6 + (size_t)a.NG * 32;
   CUDA_TRY(ensure(ws->pctl, sizeof(unsigned) * nctl));
   CUDA_TRY(ensure(ws->pyb, sizeof(double2) * (size_t)a.NG * 3 * 3 * Kc));
   CUDA_TRY(ensure(ws->ppart, sizeof(double2) * (size_t)a.NG * std::max(M / 2, 1) * 3 * Kc));
@@ -803,8 +803,8 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   a.next = a.doneF + (size_t)std::max(K, 1) * a.npairs;
   a.stopk = (int*)(a.next + std::max(K, 1));
   a.wd = (unsigned*)(a.stopk + 1);
-  a.hb = a.wd + 1;
-  a.ticket = a.hb + 1;
+  a.hb = a.wd + 1;  // a.hb[1]: the watchdog limit in ms
+  a.ticket = a.hb + 2;
   a.gbar = a.ticket + 2;
   a.ybuf = (double2*)ws->pyb.p;
   a.part = (double2*)ws->ppart.p;
@@ -855,6 +855,9 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   CUDA_TRY(cudaMemsetAsync(a.stamps, 0, sizeof(unsigned long long) * nst, st));
   const int stop_init = K + 1;
   CUDA_TRY(cudaMemcpyAsync(a.stopk, &stop_init, sizeof(int), cudaMemcpyHostToDevice, st));
+  const char* ewd = getenv("RSW_WATCHDOG_MS");  // dependency waits give up after this long without ANY progress
+  const unsigned wd_ms = (unsigned)((ewd && atol(ewd) > 0) ? atol(ewd) : 4000);
+  CUDA_TRY(cudaMemcpyAsync(a.hb + 1, &wd_ms, sizeof(unsigned), cudaMemcpyHostToDevice, st));
   for (int k = 0; k <= K; ++k)  // U^k_0 = u0 for every iteration
     CUDA_TRY(cudaMemcpyAsync(a.Uall + (size_t)k * (S + 1) * L, u0, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
   if (world > 1) {  // every rank's flags are zeroed before any peer may push into them

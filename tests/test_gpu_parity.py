@@ -541,6 +541,22 @@ def test_pipelined_push_to_peer_mirror(rsw_gpu, wname, max_iters, tol, monkeypat
     assert torch.equal(a["F"], b["F"])  # b["F"] is the pushed (mirror) copy
 
 
+def test_pipelined_long_fine_task_outlives_the_watchdog_limit(rsw_gpu, monkeypatch):
+    """a dependency wait may legitimately last one whole fine solve.  With the watchdog limit
+    lowered to 100 ms (RSW_WATCHDOG_MS) and fine tasks of ~150k steps (several times the limit), the
+    pipelined solve must still complete — the waits time out only without progress anywhere (the fine
+    workers' heartbeat) — and equal the bulk schedule bitwise."""
+    w = inputs.C1
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dT / 150000, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=1)
+    a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    monkeypatch.setenv("RSW_WATCHDOG_MS", "100")
+    b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
+    assert b["stats"]["fine_task_ms"] > 300.0, b["stats"]  # each task lasted several watchdog limits
+    assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
+
+
 def test_repeatability_soak(rsw_gpu):
     """Stand-in for racecheck (compute-sanitizer is unavailable on this pool): the lock-free protocols
     (pipelined sentinel hand-offs, task claiming, in-place FFT passes with one barrier each, TMEM
