@@ -106,8 +106,8 @@ rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, doub
 
 /* Schedule of the parareal iteration (results are bitwise identical; only the order of the work
    differs):
-     RSW_SCHEDULE_AUTO      pipelined when supported (single GPU, n in {64, 128, 256}, coarse RK4 or
-                            midpoint, enough co-resident CTAs for its coarse groups), bulk otherwise;
+     RSW_SCHEDULE_AUTO      pipelined when supported (n in {64, 128, 256}, coarse RK4 or midpoint, enough
+                            co-resident CTAs for its coarse groups; multi-GPU: see below), bulk otherwise;
      RSW_SCHEDULE_BULK      per iteration: the fine sweep over all slices, then the serial coarse sweep;
      RSW_SCHEDULE_PIPELINED one persistent kernel in which sweep k trails sweep k-1 slice by slice and
                             each fine solve F(U^k_n) starts as soon as U^k_n exists (SURVEY
@@ -154,8 +154,14 @@ typedef struct {
    with one copy per shard at offset lo_r; results must be bitwise equal to P = 1.
    Schedule knobs (results bitwise identical under all of them): RSW_PIPELINE=0 (auto → bulk),
    RSW_PIPE_GC / RSW_PIPE_NG (coarse sub-CTAs per sweep / concurrent sweeps), RSW_PIPE_TRACE=1
-   (timeline to stderr).  The pipelined schedule's dependency waits give up (RSW_ERR_CUDA) only after
-   ~4 s without ANY progress in the kernel (a heartbeat bumped by fine steps and coarse slices).
+   (timeline to stderr), RSW_PIPE_MIRROR=1 (one GPU: also push every fine pair into a same-GPU copy of
+   F, the multi-GPU store path, checked against F).  The pipelined schedule's dependency waits give up
+   (RSW_ERR_CUDA) only after RSW_WATCHDOG_MS (default 4000) ms without ANY progress in the kernel (a
+   heartbeat bumped by fine steps and coarse slices).
+   Multi-GPU (comm with world > 1): AUTO / PIPELINED run the pipelined schedule when n <= 256 and
+   n_slices is divisible by 2 x world (every rank runs the replicated sweeps and its shard's fine
+   tasks, pushing each finished pair into the peers' F over NVLink: IPC-mapped buffers, system-scope
+   release / acquire); otherwise the bulk schedule with the in-place all-gather.
    Workspace: calls on different streams are ordered by an event the library records at the end of
    each call, so they never overlap on the shared per-device workspace. */
 rsw_status parareal_iterate(const rsw_params* p, const parareal_config* cfg, const double* u0,
