@@ -176,6 +176,18 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
                                void* stream, double* F_out, double* G_out,
                                rsw_parareal_stats* stats);
 
+/* Checkpoint / resume: the state {U^k, G(U^k_n), k} determines the continuation of the
+   iteration.  A checkpoint is the U and G_out of a parareal_iterate_ex call that ran k iterations;
+   parareal_resume continues from it with iterations k_done+1 .. cfg->max_iters (bulk schedule): U
+   (device [S+1][3][n/2+1][2]) is read as U^{k_done} and overwritten with the result, G_in (device
+   [S][3][n/2+1][2]) holds G(U^{k_done}_n).  resid_hist (host) receives the residuals of the
+   iterations run here (cfg->max_iters - k_done entries), *iters_done the total count.  The result is
+   bitwise that of one uninterrupted bulk run of max_iters iterations.  RSW_ERR_CONFIG for
+   k_done < 0, k_done > max_iters, a NULL G_in or schedule = RSW_SCHEDULE_PIPELINED. */
+rsw_status parareal_resume(const rsw_params* p, const parareal_config* cfg, double* U, const double* G_in,
+                           int32_t k_done, double* resid_hist, int32_t* iters_done, rsw_comm* comm,
+                           void* stream, double* F_out, double* G_out, rsw_parareal_stats* stats);
+
 /* Slices owned by `rank` of `world` in the fine sweep: [*lo, *hi) (contiguous blocks, §8(e)). */
 rsw_status rsw_shard_range(int32_t n_slices, int32_t rank, int32_t world, int32_t* lo,
                            int32_t* hi);

@@ -29,7 +29,7 @@ EXPORTS = [
     "rsw_nonlinear", "rsw_fine_propagate", "rsw_averaged_rhs", "rsw_coarse_propagate",
     "parareal_iterate", "parareal_iterate_ex", "rsw_shard_range", "rsw_nccl_unique_id",
     "rsw_comm_init", "rsw_comm_destroy", "rsw_fp64_peak", "rsw_flops_per_unit", "rsw_last_error",
-    "rsw_shutdown", "rsw_check_states",
+    "rsw_shutdown", "rsw_check_states", "parareal_resume",
 ]
 
 
@@ -91,6 +91,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.parareal_iterate.argtypes = [P, ctypes.POINTER(_PararealConfig), dp, dp,
                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32), vp, vp]
     L.parareal_iterate_ex.argtypes = L.parareal_iterate.argtypes + [dp, dp, ctypes.POINTER(_Stats)]
+    L.parareal_resume.argtypes = [P, ctypes.POINTER(_PararealConfig), dp, dp, i32, ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(i32), vp, vp, dp, dp, ctypes.POINTER(_Stats)]
     L.rsw_shard_range.argtypes = [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.rsw_nccl_unique_id.argtypes = [vp]
     L.rsw_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
@@ -261,6 +263,39 @@ def parareal_iterate(p: Params, u0, *, dT, dt, T0, M, n_slices, max_iters, tol=0
                           sweep0_ms=st.sweep0_ms, lag_ms=st.lag_ms, fine_task_ms=st.fine_task_ms))
     if want_FG:
         out["F"], out["G"] = F, G
+    return out
+
+
+def parareal_resume(p: Params, U, G, k_done: int, *, dT, dt, T0, M, n_slices, max_iters, tol=0.0,
+                    fine_scheme=FINE_ETDRK4, coarse_scheme=COARSE_RK4, comm: Comm | None = None, want_FG=False,
+                    allow_diverged=False):
+    """Continue a parareal iteration from the checkpoint {U = U^k_done, G = G(U^k_done_n)} (the U and G of
+    a parareal_iterate(..., want_FG=True) call) up to max_iters (bulk schedule).  U is updated in place.
+    Returns dict(U, resid (of the iterations run here), iters (total), status, stats[, F, G])."""
+    import torch
+    shape = (n_slices + 1, 3, p.n // 2 + 1, 2)
+    _state_arg(U, p.n)
+    _state_arg(G, p.n)
+    if tuple(U.shape) != shape or tuple(G.shape) != (n_slices,) + shape[1:] or U.device != G.device:
+        raise RSWError(RSW_ERR_CONFIG, f"U must be {shape} and G {(n_slices,) + shape[1:]} on one device")
+    F_o = torch.empty_like(G) if want_FG else None
+    G_o = torch.empty_like(G) if want_FG else None
+    nres = max(max_iters - k_done, 1)
+    resid = (ctypes.c_double * nres)()
+    it = ctypes.c_int32(0)
+    st = _Stats()
+    cfg = _PararealConfig(dT, dt, T0, tol, M, n_slices, max_iters, fine_scheme, coarse_scheme, SCHEDULE_BULK)
+    rc = load().parareal_resume(ctypes.byref(p._c()), ctypes.byref(cfg), ctypes.c_void_p(U.data_ptr()),
+                                ctypes.c_void_p(G.data_ptr()), int(k_done), resid, ctypes.byref(it),
+                                comm.handle if comm else None, _stream(),
+                                ctypes.c_void_p(F_o.data_ptr()) if want_FG else None,
+                                ctypes.c_void_p(G_o.data_ptr()) if want_FG else None, ctypes.byref(st))
+    _check(rc, ok=(RSW_OK, RSW_NOT_CONVERGED) + ((RSW_ERR_DIVERGED,) if allow_diverged else ()))
+    out = dict(U=U, resid=[resid[i] for i in range(it.value - k_done)], iters=it.value, status=rc,
+               stats=dict(fine_ms=st.fine_ms, comm_ms=st.comm_ms, coarse_ms=st.coarse_ms, total_ms=st.total_ms,
+                          fine_slice_steps=st.fine_slice_steps, kernel_launches=st.kernel_launches))
+    if want_FG:
+        out["F"], out["G"] = F_o, G_o
     return out
 
 

@@ -964,10 +964,14 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   return RSW_OK;
 }
 
-rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
-                               double* resid_hist, int32_t* iters_done, rsw_comm* comm, void* stream,
-                               double* F_out, double* G_out, rsw_parareal_stats* stats) {
-  Nvtx nvtx_("parareal_iterate");
+// The parareal driver.  Resume (G_resume != NULL): U holds U^{k_done} and G_resume the coarse values
+// G(U^{k_done}_n) of that iterate's sweep (a checkpoint: the U and G_out of an earlier call); the k = 0
+// sweep is skipped and iterations k_done+1 .. max_iters run on the bulk schedule (resid_hist receives
+// their residuals, *iters_done the total count).
+static rsw_status parareal_impl(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
+                                double* resid_hist, int32_t* iters_done, rsw_comm* comm, void* stream,
+                                double* F_out, double* G_out, rsw_parareal_stats* stats, const double* G_resume,
+                                int k_done) {
   rsw_status s = check_params(p);
   if (s != RSW_OK) return s;
   if (!cfg) return fail(RSW_ERR_CONFIG, "cfg is NULL");
@@ -983,8 +987,9 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   if (cfg->coarse_scheme != RSW_COARSE_RK4 && cfg->coarse_scheme != RSW_COARSE_MIDPOINT &&
       cfg->coarse_scheme != RSW_COARSE_STRANG)
     return fail(RSW_ERR_CONFIG, "unknown coarse scheme");
-  if (!u0 || !U || !iters_done || (cfg->max_iters > 0 && !resid_hist))
+  if (!u0 || !U || !iters_done || (cfg->max_iters > k_done && !resid_hist))
     return fail(RSW_ERR_CONFIG, "NULL pointer argument");
+  if (k_done < 0 || k_done > cfg->max_iters) return fail(RSW_ERR_CONFIG, "need 0 <= k_done <= max_iters");
   const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
   int32_t lo, hi;
   if ((s = rsw_shard_range(S, rank, world, &lo, &hi)) != RSW_OK) return s;
@@ -1011,7 +1016,9 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     if (cfg->schedule != RSW_SCHEDULE_AUTO && cfg->schedule != RSW_SCHEDULE_BULK &&
         cfg->schedule != RSW_SCHEDULE_PIPELINED)
       return fail(RSW_ERR_CONFIG, "unknown schedule");
-    if (can_pipe && (auto_pipe || cfg->schedule == RSW_SCHEDULE_PIPELINED)) {
+    if (G_resume && cfg->schedule == RSW_SCHEDULE_PIPELINED)
+      return fail(RSW_ERR_CONFIG, "resume runs the bulk schedule");
+    if (!G_resume && can_pipe && (auto_pipe || cfg->schedule == RSW_SCHEDULE_PIPELINED)) {
       bool unsupported = false;
       s = run_pipelined(p, cfg, u0, U, resid_hist, iters_done, st, F_out, G_out, stats, ws, &unsupported, comm);
       // AUTO: a configuration the pipelined kernel cannot hold (too few co-resident CTAs for its coarse
@@ -1040,18 +1047,22 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   cudaEvent_t* ev = ws->ev.data();
   CUDA_TRY(cudaEventRecord(ev[6], st));
 
-  // k = 0: U_0 = u0, U_{n+1} = G(U_n)   (Alg.4)
-  if (U != u0) CUDA_TRY(cudaMemcpyAsync(U, u0, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
   const bool strang_coarse = cfg->coarse_scheme == RSW_COARSE_STRANG;
-  Chain ch0;
-  if (!strang_coarse &&
-      (s = setup_chain(ch0, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, nullptr, nullptr, S)))
-    return s;
   CUDA_TRY(cudaEventRecord(ev[0], st));
-  if (strang_coarse) {
-    if ((s = run_strang_chain(p, cfg->dT, ws, U, G, nullptr, S, nullptr, st, &launches))) return s;
-  } else if ((s = run_chain(ch0, ws, nullptr, st, &launches))) {
-    return s;
+  if (G_resume) {  // resume from the checkpoint {U^{k_done}, G(U^{k_done}_n)}
+    CUDA_TRY(cudaMemcpyAsync(G, G_resume, sizeof(double) * L * S, cudaMemcpyDeviceToDevice, st));
+  } else {
+    // k = 0: U_0 = u0, U_{n+1} = G(U_n)   (Alg.4)
+    if (U != u0) CUDA_TRY(cudaMemcpyAsync(U, u0, sizeof(double) * L, cudaMemcpyDeviceToDevice, st));
+    Chain ch0;
+    if (!strang_coarse &&
+        (s = setup_chain(ch0, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, nullptr, nullptr, S)))
+      return s;
+    if (strang_coarse) {
+      if ((s = run_strang_chain(p, cfg->dT, ws, U, G, nullptr, S, nullptr, st, &launches))) return s;
+    } else if ((s = run_chain(ch0, ws, nullptr, st, &launches))) {
+      return s;
+    }
   }
   CUDA_TRY(cudaEventRecord(ev[1], st));
   double sweep0_ms = 0;
@@ -1066,8 +1077,8 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
   if (!strang_coarse && (s = setup_chain(ch, p, cfg->coarse_scheme, cfg->dT, cfg->T0, cfg->M, ws, U, G, F,
                                          (double*)ws->rparts.p, S)))
     return s;
-  rsw_status status = (cfg->tol > 0 && cfg->max_iters > 0) ? RSW_NOT_CONVERGED : RSW_OK;
-  int done = 0;
+  rsw_status status = (cfg->tol > 0 && cfg->max_iters > k_done) ? RSW_NOT_CONVERGED : RSW_OK;
+  int done = k_done;
   const char* vw = getenv("RSW_VIRTUAL_WORLD");
   const int vworld = vw ? atoi(vw) : 1;
   if (!comm && vworld > 1 && S % vworld != 0) return fail(RSW_ERR_CONFIG, "RSW_VIRTUAL_WORLD must divide n_slices");
@@ -1076,7 +1087,7 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     for (int r = 0; r < vworld; ++r) CUDA_TRY(ensure(ws->vshard[r], sizeof(double) * L * (S / vworld)));
   }
   int64_t fine_steps = 0;
-  for (int k = 1; k <= cfg->max_iters; ++k) {
+  for (int k = k_done + 1; k <= cfg->max_iters; ++k) {
     // parfor n: F_n = φ(U^{k-1}_n) on this rank's shard
     Nvtx nvtx_it("parareal iteration (fine sweep, all-gather, coarse sweep)");
     CUDA_TRY(cudaEventRecord(ev[0], st));
@@ -1127,7 +1138,7 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     comm_ms += b;
     coarse_ms += c;
     const double r = ws->rhost[0];
-    resid_hist[k - 1] = r;
+    resid_hist[k - 1 - k_done] = r;
     done = k;
     if (!std::isfinite(r) || r > 1e6) {
       status = fail(RSW_ERR_DIVERGED, "parareal residual non-finite or > 1e6");
@@ -1153,16 +1164,32 @@ rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, 
     stats->fine_slice_steps = fine_steps;
     stats->kernel_launches = launches;
     stats->sweep0_ms = sweep0_ms;                                    // the k = 0 coarse sweep
-    stats->lag_ms = done ? (tot - sweep0_ms) / done : 0.0;           // one iteration (fine + exchange + sweep)
-    stats->fine_task_ms = done ? fine_ms / done : 0.0;               // one fine sweep (this rank's shard)
+    const int ran = done - k_done;
+    stats->lag_ms = ran ? (tot - sweep0_ms) / ran : 0.0;             // one iteration (fine + exchange + sweep)
+    stats->fine_task_ms = ran ? fine_ms / ran : 0.0;                 // one fine sweep (this rank's shard)
   }
   if (status == RSW_NOT_CONVERGED) g_err = "parareal: tolerance not reached within max_iters";
   return status;
 }
 
+rsw_status parareal_iterate_ex(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
+                               double* resid_hist, int32_t* iters_done, rsw_comm* comm, void* stream,
+                               double* F_out, double* G_out, rsw_parareal_stats* stats) {
+  Nvtx nvtx_("parareal_iterate");
+  return parareal_impl(p, cfg, u0, U, resid_hist, iters_done, comm, stream, F_out, G_out, stats, nullptr, 0);
+}
+
 rsw_status parareal_iterate(const rsw_params* p, const parareal_config* cfg, const double* u0, double* U,
                             double* resid_hist, int32_t* iters_done, rsw_comm* comm, void* stream) {
   return parareal_iterate_ex(p, cfg, u0, U, resid_hist, iters_done, comm, stream, nullptr, nullptr, nullptr);
+}
+
+rsw_status parareal_resume(const rsw_params* p, const parareal_config* cfg, double* U, const double* G_in,
+                           int32_t k_done, double* resid_hist, int32_t* iters_done, rsw_comm* comm, void* stream,
+                           double* F_out, double* G_out, rsw_parareal_stats* stats) {
+  Nvtx nvtx_("parareal_resume");
+  if (!G_in) return fail(RSW_ERR_CONFIG, "G_in is NULL");
+  return parareal_impl(p, cfg, U, U, resid_hist, iters_done, comm, stream, F_out, G_out, stats, G_in, k_done);
 }
 
 rsw_status rsw_nccl_unique_id(void* out128) {

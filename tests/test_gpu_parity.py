@@ -557,6 +557,25 @@ def test_pipelined_long_fine_task_outlives_the_watchdog_limit(rsw_gpu, monkeypat
     assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
 
 
+@pytest.mark.parametrize("wname,k_ckpt", [("C3", 2), ("C2", 6)])
+def test_checkpoint_resume_bitwise(rsw_gpu, wname, k_ckpt):
+    """Checkpoint / resume: the {U^k, G(U^k_n), k} of a run stopped after k iterations (any
+    schedule) continued with parareal_resume gives the uninterrupted run bitwise — iterates, residual
+    history, and (C2) the tolerance stop at the same iteration."""
+    w = getattr(inputs, wname)
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, tol=w.tol)
+    full = rsw_gpu.parareal_iterate(p, u0, max_iters=w.max_iters, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    part = rsw_gpu.parareal_iterate(p, u0, max_iters=k_ckpt, want_FG=True, **kw)  # AUTO: pipelined
+    assert part["iters"] == k_ckpt
+    U, G = part["U"].clone(), part["G"].clone()
+    res = rsw_gpu.parareal_resume(p, U, G, k_ckpt, max_iters=w.max_iters, **kw)
+    assert res["iters"] == full["iters"]
+    assert part["resid"] + res["resid"] == full["resid"]
+    assert torch.equal(res["U"], full["U"])
+
+
 def test_repeatability_soak(rsw_gpu):
     """Stand-in for racecheck (compute-sanitizer is unavailable on this pool): the lock-free protocols
     (pipelined sentinel hand-offs, task claiming, in-place FFT passes with one barrier each, TMEM
