@@ -38,3 +38,18 @@ def test_gpus_2_relaunches_two_ranks_one_line():
     assert len(lines) == 1, r.stdout
     line = json.loads(lines[0])
     assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+
+
+def test_runner_flags_override_the_preset():
+    """`python -m paper_1303_6615_b200` (SURVEY §5 flags): a preset supplies every parameter, flags
+    override single ones, and the initial state is projected onto the retained modes (CPU only)."""
+    import numpy as np
+    from paper_1303_6615_b200 import __main__ as cli
+    from paper_1303_6615_b200 import inputs
+    a = cli.parse_args(["--preset", "C3", "--modes", "64", "--slices", "16", "--T", "0.5", "--mbar", "16",
+                        "--fine", "strang", "--coarse", "midpoint", "--max-iter", "2"])
+    w = cli.workload_from_args(a)
+    assert (w.n, w.n_slices, w.T, w.M, w.max_iters, w.fine_scheme, w.coarse_scheme) == (64, 16, 0.5, 16, 2, 1, 1)
+    assert (w.eps, w.mu, w.T0) == (inputs.C3.eps, inputs.C3.mu, inputs.C3.T0)
+    u0 = cli.initial_state(w, 0)
+    assert u0.shape == (3, 33, 2) and not np.any(u0[:, 64 // 3 + 1:]) and not np.any(u0[:, 0, 1])

@@ -576,6 +576,30 @@ def test_checkpoint_resume_bitwise(rsw_gpu, wname, k_ckpt):
     assert torch.equal(res["U"], full["U"])
 
 
+def test_runner_cli_and_checkpoint(rsw_gpu, tmp_path):
+    """The command-line runner (python -m paper_1303_6615_b200): a 2-iteration C1 run writing a checkpoint,
+    then a resumed run to 4 iterations — JSON reports and the final U equal the direct 4-iteration solve."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    run = lambda *a: subprocess.run([sys.executable, "-m", "paper_1303_6615_b200", "--preset", "C1", *a],
+                                    capture_output=True, text=True, timeout=300, cwd=root)
+    r1 = run("--max-iter", "2", "--checkpoint", str(tmp_path / "ck.npz"), "--output", str(tmp_path / "r1.json"))
+    assert r1.returncode == 0, r1.stderr[-2000:]
+    r2 = run("--max-iter", "4", "--resume", str(tmp_path / "ck.npz"), "--save-U", str(tmp_path / "U.npy"),
+             "--output", str(tmp_path / "r2.json"))
+    assert r2.returncode == 0, r2.stderr[-2000:]
+    j1, j2 = (json.load(open(tmp_path / f)) for f in ("r1.json", "r2.json"))
+    w = inputs.C1
+    ref = rsw_gpu.parareal_iterate(P(rsw_gpu, w.eps, w.F, w.mu, w.n), dev(inputs.initial_state(w)), dT=w.dT, dt=w.dt,
+                                   T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=4)
+    assert j1["iterations"] == 2 and j2["iterations"] == 4 and j2["status"] == "ok"
+    assert j1["residuals"] + j2["residuals"] == ref["resid"]
+    assert np.array_equal(np.load(tmp_path / "U.npy"), to_np(ref["U"]))
+
+
 def test_repeatability_soak(rsw_gpu):
     """Stand-in for racecheck (compute-sanitizer is unavailable on this pool): the lock-free protocols
     (pipelined sentinel hand-offs, task claiming, in-place FFT passes with one barrier each, TMEM
