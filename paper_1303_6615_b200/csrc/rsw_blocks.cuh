@@ -155,11 +155,14 @@ struct FineTmem {  // TMEM columns of one fine pair-group: per mode slot o, S1 /
 // (TBLK = true: tcol is the CTA's base and the groups of a CTA interleave, 3 blocks for 12 warps).
 // TWT / twcol: twiddle policy of the FFT core (fft_tw_src) and, for TWT = 2, the TMEM column address of
 // the CTA's twiddle region (filled by the caller with tw_tmem_fill).
+// po / poff: optional peer outputs (multi-GPU bulk schedule): the pair's endpoints are also stored at
+// po->out[r] + poff (A) and + poff + L (B, when present), then made visible at system scope.
 template <int N, int R, int TG, int SCHEME, bool LIN, class GRP, bool TBLK = false, int TWT = 0>
 __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double2* Y, const FineSmemTab& st_,
                                               uint32_t tcol, const ModeGeom& gg, const double* uA,
                                               const double* uB, double* oA, double* oB, int m_steps, double h,
-                                              unsigned* hb = nullptr, uint32_t twcol = 0) {
+                                              unsigned* hb = nullptr, uint32_t twcol = 0,
+                                              const PeerOut* po = nullptr, size_t poff = 0) {
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, OMAX = FineTmem<N, TG>::OMAX;
   const double2* sCP = st_.CP;
   const double* sC0 = st_.C0;
@@ -319,6 +322,12 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
   }
   grp.sync();
   store_pair_prim<N, TG>(W, gg, oA, oB, t);
+  if (po && po->n > 0) {
+    constexpr size_t L = (size_t)3 * (N / 2 + 1) * 2;
+    for (int r = 0; r < po->n; ++r)
+      store_pair_prim<N, TG>(W, gg, po->out[r] + poff, oB ? po->out[r] + poff + L : nullptr, t);
+    __threadfence_system();
+  }
 }
 
 

@@ -471,8 +471,8 @@ struct rsw_comm {
   int rank = 0, world = 1;
   // multi-GPU pipelined schedule: the peers' fine-endpoint buffers and control words, IPC-mapped once
   // per (peer, allocation) and re-mapped only when a peer's allocation changed
-  std::vector<cudaIpcMemHandle_t> hF, hC;
-  std::vector<void*> mF, mC;
+  std::vector<cudaIpcMemHandle_t> hF, hC, hB;
+  std::vector<void*> mF, mC, mB;  // pipelined F, pipelined control words, bulk F
   void* scratch = nullptr;  // device bytes for the handle all-gather and the stream barriers
 };
 
@@ -518,8 +518,9 @@ rsw_status comm_barrier(rsw_comm* c, cudaStream_t st) {
   return r == ncclSuccess ? RSW_OK : nccl_fail(r, "ncclAllReduce (barrier)");
 }
 
-// all-gather of every rank's IPC handles of (F buffer, control words); open the peers' (cached)
-rsw_status exchange_peer_buffers(rsw_comm* c, void* myF, void* myC, cudaStream_t st) {
+// all-gather of every rank's IPC handles of two buffers (pipelined: F and the control words; bulk: F
+// twice); open the peers' mappings into (mF, mC) or, for the bulk F, into mB (cached per allocation)
+rsw_status exchange_peer_buffers(rsw_comm* c, void* myF, void* myC, cudaStream_t st, bool bulk = false) {
   const int W = c->world;
   cudaIpcMemHandle_t h[2];
   CUDA_TRY(cudaIpcGetMemHandle(&h[0], myF));
@@ -535,14 +536,16 @@ rsw_status exchange_peer_buffers(rsw_comm* c, void* myF, void* myC, cudaStream_t
   if ((int)c->mF.size() != W) {
     c->hF.assign(W, cudaIpcMemHandle_t{});
     c->hC.assign(W, cudaIpcMemHandle_t{});
+    c->hB.assign(W, cudaIpcMemHandle_t{});
     c->mF.assign(W, nullptr);
     c->mC.assign(W, nullptr);
+    c->mB.assign(W, nullptr);
   }
   for (int q = 0; q < W; ++q) {
     if (q == c->rank) continue;
-    for (int b = 0; b < 2; ++b) {
-      cudaIpcMemHandle_t& hold = b ? c->hC[q] : c->hF[q];
-      void*& mp = b ? c->mC[q] : c->mF[q];
+    for (int b = 0; b < (bulk ? 1 : 2); ++b) {
+      cudaIpcMemHandle_t& hold = bulk ? c->hB[q] : (b ? c->hC[q] : c->hF[q]);
+      void*& mp = bulk ? c->mB[q] : (b ? c->mC[q] : c->mF[q]);
       const cudaIpcMemHandle_t& hn = all[2 * q + b];
       if (mp && std::memcmp(&hold, &hn, sizeof(hn)) == 0) continue;
       if (mp) cudaIpcCloseMemHandle(mp);
@@ -1086,6 +1089,28 @@ static rsw_status parareal_impl(const rsw_params* p, const parareal_config* cfg,
   if (!comm && vworld > 1) {
     for (int r = 0; r < vworld; ++r) CUDA_TRY(ensure(ws->vshard[r], sizeof(double) * L * (S / vworld)));
   }
+  // multi-GPU bulk exchange: the fine kernel stores its endpoints straight into every peer's F (NVLink,
+  // IPC-mapped), bracketed by two stream barriers (no peer writes into F while this rank's previous
+  // sweep may still read it; every peer's stores have landed before the sweep); RSW_ALLGATHER=1 keeps
+  // the in-place ncclAllGather instead.  RSW_BULK_MIRROR=1 (one GPU): the stores also go to a
+  // same-GPU mirror of F, whose copy is returned as F_out (tests).
+  const char* eag = getenv("RSW_ALLGATHER");
+  const char* ebm = getenv("RSW_BULK_MIRROR");
+  const bool peer_store = comm && world > 1 && !(eag && eag[0] == '1');
+  const bool bulk_mirror = !comm && ebm && ebm[0] == '1' && vworld <= 1;
+  rsw::PeerOut po{};
+  if (peer_store) {
+    if (!comm->scratch) CUDA_TRY(cudaMalloc(&comm->scratch, 64 + 2 * sizeof(cudaIpcMemHandle_t) * (rsw::kMaxPeers + 1)));
+    if (world - 1 > rsw::kMaxPeers) return fail(RSW_ERR_CONFIG, "too many ranks for the peer-store exchange");
+    rsw_status xs = exchange_peer_buffers(comm, ws->F.p, ws->F.p, st, true);
+    if (xs != RSW_OK) return xs;
+    for (int q = 0; q < world; ++q)
+      if (q != rank) po.out[po.n++] = (double*)comm->mB[q];
+  } else if (bulk_mirror) {
+    CUDA_TRY(ensure(ws->mirF, sizeof(double) * L * S));
+    po.out[po.n++] = (double*)ws->mirF.p;
+  }
+  for (int q = 0; q < po.n; ++q) po.out[q] += (size_t)lo * L;  // this rank's block, same offsets
   int64_t fine_steps = 0;
   for (int k = k_done + 1; k <= cfg->max_iters; ++k) {
     // parfor n: F_n = φ(U^{k-1}_n) on this rank's shard
@@ -1109,13 +1134,20 @@ static rsw_status parareal_impl(const rsw_params* p, const parareal_config* cfg,
                                  cudaMemcpyDeviceToDevice, st));
       }
     } else {
+      if (peer_store) {
+        rsw_status bs = comm_barrier(comm, st);
+        if (bs != RSW_OK) return bs;
+      }
       CUDA_TRY(rsw::launch_fine(n, cfg->fine_scheme, false, U + (size_t)lo * L, F + (size_t)lo * L, hi - lo, m, h,
-                                ftab, st));
+                                ftab, st, po.n ? &po : nullptr));
       ++launches;
     }
     fine_steps += (int64_t)(hi - lo) * m;
     CUDA_TRY(cudaEventRecord(ev[1], st));
-    if (comm) {  // a6: every rank's block lands at its offset lo_r (in place; world 1 is a plain NCCL no-op copy)
+    if (peer_store) {  // a6 fused into the fine kernel: wait until every rank's stores have landed
+      rsw_status bs = comm_barrier(comm, st);
+      if (bs != RSW_OK) return bs;
+    } else if (comm) {  // a6: every rank's block lands at its offset lo_r (in place; world 1 is a plain NCCL no-op copy)
       ncclResult_t r = g_nccl.allGather(F + (size_t)lo * L, F, (size_t)(hi - lo) * L, ncclDouble,
                                         (ncclComm_t)comm->comm, st);
       if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
@@ -1150,7 +1182,9 @@ static rsw_status parareal_impl(const rsw_params* p, const parareal_config* cfg,
     }
   }
   *iters_done = done;
-  if (F_out) CUDA_TRY(cudaMemcpyAsync(F_out, F, sizeof(double) * L * S, cudaMemcpyDeviceToDevice, st));
+  if (F_out)  // (mirror test: the stored copy)
+    CUDA_TRY(cudaMemcpyAsync(F_out, bulk_mirror ? (double*)ws->mirF.p : F, sizeof(double) * L * S,
+                             cudaMemcpyDeviceToDevice, st));
   if (G_out) CUDA_TRY(cudaMemcpyAsync(G_out, G, sizeof(double) * L * S, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(cudaEventRecord(ev[7], st));
   if (stats) {
@@ -1225,6 +1259,8 @@ rsw_status rsw_comm_destroy(rsw_comm* comm) {
   for (void* m : comm->mF)
     if (m) cudaIpcCloseMemHandle(m);
   for (void* m : comm->mC)
+    if (m) cudaIpcCloseMemHandle(m);
+  for (void* m : comm->mB)
     if (m) cudaIpcCloseMemHandle(m);
   if (comm->scratch) cudaFree(comm->scratch);
   if (comm->comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)comm->comm);

@@ -94,8 +94,15 @@ struct PipeArgs {
 bool pipeline_supported(int n);
 cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);
 
+// Fine-sweep outputs also stored straight into other GPUs' buffers (multi-GPU bulk schedule: the
+// exchange of the fine endpoints fused into the fine kernel's epilogue; NVLink stores to IPC-mapped
+// memory).  out[r] receives the same slices at the same offsets as the local output.
+struct PeerOut {
+  int n;
+  double* out[kMaxPeers];
+};
 cudaError_t launch_fine(int n, int scheme, bool lin, const double* in, double* out, int S, int m, double h,
-                        const FineTab& tab, cudaStream_t st);
+                        const FineTab& tab, cudaStream_t st, const PeerOut* po = nullptr);
 cudaError_t launch_nonlinear(int n, const double* in, double* out, int S, const FineTab& tab, cudaStream_t st);
 cudaError_t launch_avg_states(int n, const double* in, double* out, int S, int M, const AvgTab& tab,
                               cudaStream_t st);

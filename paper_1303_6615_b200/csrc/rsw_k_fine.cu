@@ -49,7 +49,7 @@ struct FineLayout {  // dynamic shared memory of k_fine (double2 units first, th
 
 template <int N, int R, int TG, int NPG, int SCHEME, bool LIN>
 __global__ void __launch_bounds__(NPG * TG) k_fine(const double* u_in, double* u_out, int n_slices, int m_steps,
-                                                   double h, const FineTab tab) {
+                                                   double h, const FineTab tab, const PeerOut po) {
   using LY = FineLayout<N, R, TG, NPG>;
   constexpr int NH = N / 2 + 1;
   extern __shared__ double2 smem[];
@@ -78,11 +78,12 @@ __global__ void __launch_bounds__(NPG * TG) k_fine(const double* u_in, double* u
     double* oB = (sB < n_slices) ? u_out + sB * L : nullptr;
     if constexpr (NPG == 1)
       fine_pair_run<N, R, TG, SCHEME, LIN, CtaGroup, true, LY::TWT>(CtaGroup(), W, nullptr, st_, tslot, tab.g, uA, uB, oA,
-                                                                    oB, m_steps, h, nullptr, tslot + LY::TWC);
+                                                                    oB, m_steps, h, nullptr, tslot + LY::TWC, &po,
+                                                                    (size_t)sA * L);
     else
       fine_pair_run<N, R, TG, SCHEME, LIN, NamedGroup, true, LY::TWT>(NamedGroup{g * TG, 1 + g, TG, 3 + 3 * g}, W, nullptr, st_, tslot,
                                                                       tab.g, uA, uB, oA, oB, m_steps, h, nullptr,
-                                                                      tslot + LY::TWC);
+                                                                      tslot + LY::TWC, &po, (size_t)sA * L);
   }
   tmem_fence_before();
   __syncthreads();
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(NPG * TG) k_fine(const double* u_in, double* u
 
 template <int N, int R, int NPG, int TMUL = 1>
 static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
-                                  const FineTab& tab, cudaStream_t st) {
+                                  const FineTab& tab, cudaStream_t st, const PeerOut& po) {
   constexpr int TG = TMUL * core_threads<N, R>();
   const int grid = ((S + 1) / 2 + NPG - 1) / NPG;
   const size_t sm = FineLayout<N, R, TG, NPG>::bytes;
@@ -110,7 +111,7 @@ static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double
   {                                                                           \
     auto kfn = k_fine<N, R, TG, NPG, SC, LN>;                                 \
     if ((e = set_smem(kfn, sm)) != cudaSuccess) return e;                     \
-    kfn<<<grid, NPG * TG, sm, st>>>(in, out, S, m, h, tab);                   \
+    kfn<<<grid, NPG * TG, sm, st>>>(in, out, S, m, h, tab, po);               \
   }
   if (scheme == 0 && !lin) LAUNCH_FINE(0, false)
   else if (scheme == 0 && lin) LAUNCH_FINE(0, true)
@@ -124,12 +125,12 @@ static cudaError_t launch_fine_nr(int scheme, bool lin, const double* in, double
 
 template <int N>
 static cudaError_t launch_fine_n(int scheme, bool lin, const double* in, double* out, int S, int m, double h,
-                                 const FineTab& tab, cudaStream_t st) {
+                                 const FineTab& tab, cudaStream_t st, const PeerOut& po) {
   if constexpr (N == 256 || N == 512) {  // measurement knob: RSW_FINE_R = 4 or 16
     static const char* e = getenv("RSW_FINE_R");
-    if (e && atoi(e) == 16) return launch_fine_nr<N, 16, 1>(scheme, lin, in, out, S, m, h, tab, st);
-    if (e && atoi(e) == 4) return launch_fine_nr<N, 4, 1>(scheme, lin, in, out, S, m, h, tab, st);
-    if (e && atoi(e) == 82) return launch_fine_nr<N, 8, 1, 2>(scheme, lin, in, out, S, m, h, tab, st);  // 2x threads
+    if (e && atoi(e) == 16) return launch_fine_nr<N, 16, 1>(scheme, lin, in, out, S, m, h, tab, st, po);
+    if (e && atoi(e) == 4) return launch_fine_nr<N, 4, 1>(scheme, lin, in, out, S, m, h, tab, st, po);
+    if (e && atoi(e) == 82) return launch_fine_nr<N, 8, 1, 2>(scheme, lin, in, out, S, m, h, tab, st, po);  // 2x threads
   }
   if constexpr (N >= 64 && N <= 256) {
     // latency regime (at most ~2 pairs per SM, e.g. C3's 256 pairs): twice the threads per pair (the
@@ -141,15 +142,17 @@ static cudaError_t launch_fine_n(int scheme, bool lin, const double* in, double*
       if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
         sms = 148;
     }
-    if ((S + 1) / 2 <= 2 * sms) return launch_fine_nr<N, fine_radix<N>(), 1, 2>(scheme, lin, in, out, S, m, h, tab, st);
+    if ((S + 1) / 2 <= 2 * sms) return launch_fine_nr<N, fine_radix<N>(), 1, 2>(scheme, lin, in, out, S, m, h, tab, st, po);
   }
-  return launch_fine_nr<N, fine_radix<N>(), fine_groups<N>()>(scheme, lin, in, out, S, m, h, tab, st);
+  return launch_fine_nr<N, fine_radix<N>(), fine_groups<N>()>(scheme, lin, in, out, S, m, h, tab, st, po);
 }
 
 
 cudaError_t launch_fine(int n, int scheme, bool lin, const double* in, double* out, int S, int m, double h,
-                        const FineTab& tab, cudaStream_t st) {
-#define C(NN) launch_fine_n<NN>(scheme, lin, in, out, S, m, h, tab, st)
+                        const FineTab& tab, cudaStream_t st, const PeerOut* po) {
+  PeerOut none{};
+  const PeerOut& pv = po ? *po : none;
+#define C(NN) launch_fine_n<NN>(scheme, lin, in, out, S, m, h, tab, st, pv)
   RSW_DISPATCH(n, C)
 #undef C
 }

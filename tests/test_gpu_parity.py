@@ -541,6 +541,24 @@ def test_pipelined_push_to_peer_mirror(rsw_gpu, wname, max_iters, tol, monkeypat
     assert torch.equal(a["F"], b["F"])  # b["F"] is the pushed (mirror) copy
 
 
+@pytest.mark.parametrize("wname", ["C3", "C1"])
+def test_bulk_fine_kernel_stores_to_peer_mirror(rsw_gpu, wname, monkeypatch):
+    """Multi-GPU bulk schedule on one GPU (RSW_BULK_MIRROR=1): the fine kernel also stores every slice's
+    endpoint into a same-GPU "peer" copy of F (the fused compute + exchange path that replaces the
+    all-gather: NVLink stores from the fine epilogue, system fence).  The stored copy equals F bitwise
+    and the solve is unchanged."""
+    w = getattr(inputs, wname)
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=2, want_FG=True,
+              schedule=rsw_gpu.SCHEDULE_BULK)
+    a = rsw_gpu.parareal_iterate(p, u0, **kw)
+    monkeypatch.setenv("RSW_BULK_MIRROR", "1")
+    b = rsw_gpu.parareal_iterate(p, u0, **kw)
+    assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
+    assert torch.equal(a["F"], b["F"])  # b["F"] is the stored (mirror) copy
+
+
 def test_pipelined_long_fine_task_outlives_the_watchdog_limit(rsw_gpu, monkeypatch):
     """a dependency wait may legitimately last one whole fine solve.  With the watchdog limit
     lowered to 100 ms (RSW_WATCHDOG_MS) and fine tasks of ~150k steps (several times the limit), the

@@ -36,6 +36,7 @@ def test_two_rank_nccl_c3_bitwise(rsw_gpu, tmp_path):
     r0, r1, single = (np.load(tmp_path / f) for f in ("rank0.npz", "rank1.npz", "single.npz"))
     assert np.array_equal(r0["U"], r1["U"]) and np.array_equal(r0["resid"], r1["resid"])
     assert np.array_equal(r0["U"], single["U"]) and np.array_equal(r0["resid"], single["resid"])
+    assert np.array_equal(r0["Uag"], single["U"]) and np.array_equal(r1["Uag"], single["U"])  # all-gather path
     for r in (r0, r1):  # multi-GPU pipelined schedule: bitwise the single-GPU result on every rank
         assert bool(r["pipelined"])
         assert np.array_equal(r["Upipe"], single["U"]) and np.array_equal(r["resid_pipe"], single["resid"])
