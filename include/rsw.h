@@ -146,9 +146,12 @@ typedef struct {
    rank).  resid_hist: HOST double[max_iters].  iters_done: HOST.  tol <= 0: run exactly
    max_iters iterations; tol > 0: stop at the first r_k < tol (RSW_NOT_CONVERGED if none).
    Requires 0 <= max_iters <= n_slices and n_slices divisible by the comm world size.
-   u0 is layout-checked on the device first (RSW_ERR_CONFIG on a violation).  With a communicator
-   (any world size, 1 included) the fine endpoints are exchanged with an in-place ncclAllGather: rank
-   r's block [lo_r, hi_r) lands at offset lo_r of the F array (rsw_shard_range).
+   u0 is layout-checked on the device first (RSW_ERR_CONFIG on a violation).  Bulk schedule with a
+   communicator of world > 1: the fine kernel stores rank r's block [lo_r, hi_r) (rsw_shard_range)
+   straight into every peer's F at offset lo_r (NVLink stores to IPC-mapped memory, between two
+   stream barriers); RSW_ALLGATHER=1, or a world-1 communicator, uses an in-place ncclAllGather.
+   RSW_BULK_MIRROR=1 (one GPU, tests): the fine kernel also stores into a same-GPU copy of F, which
+   is returned as F_out.
    Testing: with comm == NULL and the environment variable RSW_VIRTUAL_WORLD=P (P <= 16), the fine
    sweep runs as P separate shard launches into P separate shard buffers, and F is assembled from them
    with one copy per shard at offset lo_r; results must be bitwise equal to P = 1.
