@@ -324,8 +324,9 @@ __device__ __forceinline__ void fine_pair_run(const GRP& grp, double2* W, double
   store_pair_prim<N, TG>(W, gg, oA, oB, t);
   if (po && po->n > 0) {
     constexpr size_t L = (size_t)3 * (N / 2 + 1) * 2;
-    for (int r = 0; r < po->n; ++r)
-      store_pair_prim<N, TG>(W, gg, po->out[r] + poff, oB ? po->out[r] + poff + L : nullptr, t);
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r)  // constant indices: the parameter array stays in parameter space
+      if (r < po->n) store_pair_prim<N, TG>(W, gg, po->out[r] + poff, oB ? po->out[r] + poff + L : nullptr, t);
     __threadfence_system();
   }
 }

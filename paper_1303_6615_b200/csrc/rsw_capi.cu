@@ -271,6 +271,7 @@ struct Workspace {
   DevBuf F, G, part, vky, rparts, rdev, Ubuf, Gbuf, bar, prof, Gnew, yin, chk;
   DevBuf pU, pG, pF, prp, pres, pctl, pyb, ppart, pst;  // pipelined schedule
   DevBuf mirF, mirC;                                     // RSW_PIPE_MIRROR test: a same-GPU "peer"
+  DevBuf ppeer;                                          // the pipelined kernel's peer pointer tables
   DevBuf vshard[kMaxVirtualWorld];                 // RSW_VIRTUAL_WORLD: one fine-endpoint buffer per virtual rank
   double* rhost = nullptr;
   unsigned* chost = nullptr;
@@ -822,13 +823,14 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     a.pair_hi = (world > 1) ? hi / 2 : a.npairs;
   }
   a.npeers = 0;
+  void* hpeer[2 * rsw::kMaxPeers] = {};  // [peerF..., peerDoneF...], copied to the device
   if (world > 1) {
     rsw_status xs = exchange_peer_buffers(comm, ws->pF.p, ws->pctl.p, st);
     if (xs != RSW_OK) return xs;
     for (int q = 0; q < world; ++q) {
       if (q == rank) continue;
-      a.peerF[a.npeers] = (double*)comm->mF[q];
-      a.peerDoneF[a.npeers] = (unsigned*)comm->mC[q] + (a.doneF - ctl);
+      hpeer[a.npeers] = comm->mF[q];
+      hpeer[rsw::kMaxPeers + a.npeers] = (unsigned*)comm->mC[q] + (a.doneF - ctl);
       ++a.npeers;
     }
   }
@@ -836,10 +838,14 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     CUDA_TRY(ensure(ws->mirF, sizeof(double) * nF));
     CUDA_TRY(ensure(ws->mirC, sizeof(unsigned) * nctl));
     CUDA_TRY(cudaMemsetAsync(ws->mirC.p, 0, sizeof(unsigned) * nctl, st));
-    a.peerF[0] = (double*)ws->mirF.p;
-    a.peerDoneF[0] = (unsigned*)ws->mirC.p + (a.doneF - ctl);
+    hpeer[0] = ws->mirF.p;
+    hpeer[rsw::kMaxPeers] = (unsigned*)ws->mirC.p + (a.doneF - ctl);
     a.npeers = 1;
   }
+  CUDA_TRY(ensure(ws->ppeer, sizeof(hpeer)));
+  CUDA_TRY(cudaMemcpyAsync(ws->ppeer.p, hpeer, sizeof(hpeer), cudaMemcpyHostToDevice, st));
+  a.peerF = (double* const*)ws->ppeer.p;
+  a.peerDoneF = (unsigned* const*)((void**)ws->ppeer.p + rsw::kMaxPeers);
   a.trace = nullptr;
   const size_t nst = 2 * (size_t)(K + 1) + 2;
   CUDA_TRY(ensure(ws->pst, sizeof(unsigned long long) * nst));

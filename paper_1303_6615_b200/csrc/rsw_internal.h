@@ -88,8 +88,8 @@ struct PipeArgs {
   // slice shard, pairs [pair_lo, pair_hi), and pushes each finished pair to the peers' Fall over NVLink
   // (IPC-mapped), releasing the peer's doneF flag at system scope; one GPU: [0, npairs), no peers
   int pair_lo, pair_hi, npeers;
-  double* peerF[kMaxPeers];
-  unsigned* peerDoneF[kMaxPeers];
+  double* const* peerF;         // device array [npeers]: the peers' Fall
+  unsigned* const* peerDoneF;   // device array [npeers]: the peers' doneF
 };
 bool pipeline_supported(int n);
 cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);

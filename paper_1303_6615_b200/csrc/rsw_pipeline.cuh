@@ -178,7 +178,7 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
       // IPC-mapped memory), make them visible at system scope, then release the peers' done flags
       const size_t cnt = (size_t)(nB < S ? 2 : 1) * L / 2;  // double2 entries
       const double2* src = reinterpret_cast<const double2*>(Fk + nA * L);
-      for (int r = 0; r < a.npeers; ++r) {
+      for (int r = 0; r < a.npeers; ++r) {  // (peer pointer tables in device memory: dynamic indexing)
         double2* dst = reinterpret_cast<double2*>(a.peerF[r] + (size_t)tk * S * L + nA * L);
         for (size_t i = grp.tid(); i < cnt; i += TG) dst[i] = __ldcg(src + i);
       }
