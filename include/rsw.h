@@ -126,7 +126,7 @@ typedef struct rsw_comm rsw_comm; /* opaque; NULL = single GPU */
 typedef struct {
   double fine_ms, comm_ms, coarse_ms, total_ms;
   int64_t fine_slice_steps; /* slice-steps advanced by THIS rank's fine sweeps */
-  int64_t kernel_launches;  /* kernels this library launched during the call */
+  int64_t kernel_launches;  /* kernels this library launched during the call (the u0 layout check included) */
   int32_t pipelined;        /* 1: the pipelined schedule ran (fine / coarse times overlap: only
                                total_ms is meaningful, fine_ms = coarse_ms = total_ms) */
   /* phase split of the time to solution (P:718-725 cost terms).  Pipelined: sweep0_ms = the k = 0

@@ -955,7 +955,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     stats->coarse_ms = tot;
     stats->total_ms = tot;
     stats->fine_slice_steps = (int64_t)kout * std::min(S, 2 * (a.pair_hi - a.pair_lo)) * m;  // this rank's tasks
-    stats->kernel_launches = 1;
+    stats->kernel_launches = 2;  // the layout check of u0 and the megakernel
     stats->pipelined = 1;
     // phase split from the in-kernel globaltimer stamps: the k = 0 sweep (first sweep start to its
     // end), the mean time each further iteration adds (sweep k end - sweep k-1 end), the mean fine task
@@ -1202,7 +1202,7 @@ static rsw_status parareal_impl(const rsw_params* p, const parareal_config* cfg,
     stats->coarse_ms = coarse_ms;
     stats->total_ms = tot;
     stats->fine_slice_steps = fine_steps;
-    stats->kernel_launches = launches;
+    stats->kernel_launches = launches + 1;  // + the layout check of u0 (resume: of U_0)
     stats->sweep0_ms = sweep0_ms;                                    // the k = 0 coarse sweep
     const int ran = done - k_done;
     stats->lag_ms = ran ? (tot - sweep0_ms) / ran : 0.0;             // one iteration (fine + exchange + sweep)
