@@ -457,7 +457,8 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
                                                      double2* C, double2* /*A (unused)*/, const double2* PH,
                                                      const double* SW, const double* GA, const double* GP,
                                                      const double* GQ, unsigned long long* cyc = nullptr,
-                                                     int rank = -1, int P = -1, const GRP& grp = GRP()) {
+                                                     int rank = -1, int P = -1, const GRP& grp = GRP(),
+                                                     unsigned long long* ystamp = nullptr) {
   static_assert(T % SPLIT == 0 && (T / SPLIT) % 32 == 0, "parts must be whole warps (bar.sync counts)");
   static_assert(3 * (N / R) <= T / SPLIT, "each part must cover 3N/R FFT threads");
   constexpr int TH = T / SPLIT;
@@ -480,6 +481,7 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
     C[i] = v;
   }
   grp.sync();
+  if (ystamp && tid_ == 0) *ystamp = gtimer();  // trace: the whole stage input has arrived
   const int h = SPLIT > 1 ? tid_ / TH : 0, th = tid_ - h * TH;
   const NamedGroup hg{grp.base() + h * TH, 8 + h, TH};  // named barriers 8..11
   double2* Xh = X + (size_t)h * 6 * N;

@@ -852,7 +852,8 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   a.stamps = (unsigned long long*)ws->pst.p;
   static const bool trace = getenv("RSW_PIPE_TRACE") != nullptr;
   const size_t ntr0 = 2 * (size_t)(K + 1) + (size_t)(K + 1) * S + 2 * (size_t)std::max(K, 1) * a.npairs;
-  const size_t ntr = ntr0 + 16 * 4 * 4;  // + stage-phase stamps (16 slices x 4 stages x 4)
+  const size_t ntr = ntr0 + 16 * 4 * 4 + 64 * 64 + 64;  // + stage-phase stamps (16 slices x 4 stages x 4), hand-off
+                                                          //   stamps (64 stages x 64 CTAs, 64 input arrivals)
   if (trace) {
     CUDA_TRY(ensure(ws->prof, sizeof(unsigned long long) * ntr));
     CUDA_TRY(cudaMemsetAsync(ws->prof.p, 0, sizeof(unsigned long long) * ntr, st));
@@ -926,6 +927,23 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     if (cs)
       fprintf(stderr, "[rsw pipe] sweep 0 stage (us): samples+poll %.2f  barrier %.2f  update %.2f  total %.2f\n",
               ph[0] / cs, ph[1] / cs, ph[2] / cs, cyc / cs);
+    // stage-input hand-off: the last owner's publication vs CTA 0's own, and the arrival at CTA 0
+    const unsigned long long* hd = sp + 256;
+    double skew = 0, vis = 0, wait = 0;
+    int hs = 0;
+    for (int i = 0; i + 1 < 64; ++i) {
+      unsigned long long last = 0;
+      for (int c = 0; c < std::min(a.GC, 64); ++c) last = std::max(last, hd[i * 64 + c]);
+      const unsigned long long own = hd[i * 64], yr = hd[4096 + i + 1], st0 = sp[(i + 1) * 4];
+      if (!own || !yr || !st0 || !last) continue;
+      skew += (double)(last - own) * 1e-3;
+      vis += ((double)yr - (double)last) * 1e-3;
+      wait += ((double)yr - (double)st0) * 1e-3;
+      ++hs;
+    }
+    if (hs)
+      fprintf(stderr, "[rsw pipe] stage input (us): last owner publishes %.2f after CTA 0, reaches CTA 0 %.2f later; "
+              "CTA 0 waits %.2f from its samples-phase start\n", skew / hs, vis / hs, wait / hs);
   }
   if (wd) return fail(RSW_ERR_CUDA, "pipelined parareal: a dependency wait timed out (watchdog)");
   const int kout = stopk <= K ? stopk : K;

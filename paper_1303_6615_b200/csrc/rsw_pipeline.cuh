@@ -324,9 +324,17 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
                                           ? a.trace + 2 * (Kit + 1) + (size_t)(Kit + 1) * S + 2 * (size_t)(Kit > 0 ? Kit : 1) * a.npairs +
                                                 ((n - 8) * nst + st - 1) * 4
                                           : nullptr;
+            // trace of the stage-input hand-off (same slices): every CTA's update-phase end, CTA 0's
+            // arrival of the complete stage input
+            const int sidx = (n - 8) * nst + st - 1;
+            unsigned long long* hand = (a.trace && g == 0 && ct == 0 && n >= 8 && n < 24 && k == g && c < 64)
+                                           ? a.trace + 2 * (Kit + 1) + (size_t)(Kit + 1) * S +
+                                                 2 * (size_t)(Kit > 0 ? Kit : 1) * a.npairs + 256
+                                           : nullptr;
             if (stp) stp[0] = gtimer();
             coarse_samples_phase<N, LY::RC, TC, NamedGroup, NPC, LY::SPLIT>(yb + (size_t)(ucount % 3) * Kc3, part, M, tab, X, Y, TW,
-                                                             C, A, PH, SW, GA, GP, GQ, nullptr, c, P, cg);
+                                                             C, A, PH, SW, GA, GP, GQ, nullptr, c, P, cg,
+                                                             (hand && c == 0) ? hand + 4096 + sidx : nullptr);
             if (stp) stp[1] = gtimer();
             const bool raise = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
             if (group_barrier(bar, P, epoch, raise, a.wd, a.hb, &s_flag, cg)) {
@@ -337,6 +345,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
             ++ucount;
             coarse_update_phase<N, TC, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, c, P, cg);
             if (stp) stp[3] = gtimer();
+            if (hand) hand[sidx * 64 + c] = gtimer();
           }
           if (!aborted) {
             cg.sync();  // this CTA's part of U^k_{n+1}, G^k_n is written
