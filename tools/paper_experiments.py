@@ -13,6 +13,7 @@ and the largest Δt whose error is at most the asymptotic parareal's error after
 
   python tools/paper_experiments.py [--out docs/paper_experiments.json]
   python tools/paper_experiments.py --serial [--out docs/paper_serial_accuracy.json]
+  python tools/paper_experiments.py --speedup            (measured B200 times -> docs/paper_speedup.json)
 """
 import argparse
 import json
@@ -85,6 +86,52 @@ def run(name, cfg, kmax=5):
     return out
 
 
+def timed_ms(fn, reps=2):
+    fn()  # warm-up (tables, workspace)
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+def speedup(name, cfg, errors, kmax=5):
+    """Measured B200 speedups of the paper's experiment (NEXT-1 / NEXT-2 on the GPU): the serial fine
+    ETDRK4 solve of the whole interval (one launch, T/Δt steps) against each parareal variant after
+    k = 1..kmax iterations (default schedule: pipelined for the averaged coarse solvers, bulk for the
+    Strang coarse solver), with the accuracies of docs/paper_experiments.json beside them."""
+    p = rsw.Params(cfg["eps"], F, MU, N_GRID)
+    u0 = torch.from_numpy(inputs.paper_initial_state(N_GRID)).cuda()
+    T = cfg["n_slices"] * cfg["dT"]
+    x = u0[None].contiguous()
+    t_serial = timed_ms(lambda: rsw.fine_propagate(p, x, T, cfg["dt"], 0, validate=False), reps=1)
+    out = {"eps": cfg["eps"], "T": T, "serial_fine_ms": t_serial,
+           "serial_fine_steps": int(np.ceil(T / cfg["dt"] - 1e-9)), "variants": {}}
+    runs = ([("asymptotic_midpoint(paper Alg.2)", cfg["dT"], 1), ("asymptotic_rk4", cfg["dT"], 0)]
+            + [(f"standard_strang_dT={d:g}", d, 2) for d in cfg["standard_dT"]])
+    for label, dT, coarse in runs:
+        S = int(round(T / dT))
+        rows = []
+        for k in range(1, kmax + 1):
+            res = {}
+
+            def solve():
+                res["r"] = rsw.parareal_iterate(p, u0, dT=dT, dt=cfg["dt"], T0=cfg["T0"], M=cfg["M"], n_slices=S,
+                                                max_iters=k, coarse_scheme=coarse, allow_diverged=True)
+            ms = timed_ms(solve)
+            err = errors.get(label, {}).get("max_rel_linf_error_k0..k5", [None] * (kmax + 1))[k]
+            rows.append({"k": k, "ms": ms, "speedup_vs_serial_fine": t_serial / ms, "max_rel_linf_error": err,
+                         "pipelined": bool(res["r"]["stats"]["pipelined"])})
+            print(name, label, k, f"{ms:.2f} ms", f"speedup {t_serial / ms:.1f}", err, flush=True)
+        out["variants"][label] = {"dT": dT, "slices": S, "iterations": rows}
+    return out
+
+
 SERIAL_SCHEMES = {"ETDRK4": 0, "IF-RK4": 2, "Strang": 1}
 
 
@@ -117,8 +164,19 @@ def main():
                                                   "docs", "paper_experiments.json"))
     ap.add_argument("--only", default="")
     ap.add_argument("--serial", action="store_true")
+    ap.add_argument("--speedup", action="store_true", help="measured B200 times -> docs/paper_speedup.json")
     a = ap.parse_args()
     res = {}
+    if a.speedup:
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        prev = json.load(open(os.path.join(root, "docs", "paper_experiments.json")))
+        for name, cfg in inputs.PAPER_EXPERIMENTS.items():
+            if a.only and name != a.only:
+                continue
+            res[name] = speedup(name, cfg, prev[name])
+        with open(os.path.join(root, "docs", "paper_speedup.json"), "w") as f:
+            json.dump(res, f, indent=1)
+        return
     if a.serial:
         root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
         prev = json.load(open(os.path.join(root, "docs", "paper_experiments.json")))
