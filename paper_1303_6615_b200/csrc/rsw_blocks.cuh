@@ -606,11 +606,15 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
     }
   }
   if (stage > 0) {
-    // deterministic reduction of the per-pair partials in a fixed order that does not depend on the
-    // CTA size or the owned-mode count: RQ = 8 lanes per item, lane q sums partials q, q+8, ...
-    // ascending, then a fixed xor tree over the 8 lanes (shuffles inside one warp)
-    constexpr int ITEMS = NOWN * 6, RQ = 8, IPR = T / RQ;  // items per round
-    static_assert(T % 32 == 0 && T >= RQ, "reduction layout");
+    // deterministic reduction of the per-pair partials in a fixed order that depends only on the number
+    // of partials (not on the CTA size or the owned-mode count, so every schedule agrees bitwise): RQ
+    // lanes per item, lane q sums partials q, q+RQ, ... ascending, then a fixed xor tree over the RQ
+    // lanes (shuffles inside one warp).  Above 128 partials (the paper's ε = 1e-2 case has 225) RQ = 32 keeps a lane's
+    // loads in one round of 8 (one L2 round trip instead of four); up to 128, RQ = 8 (16 lanes would
+    // halve the items per round and cost the round trip back: measured on C5's 128)
+    constexpr int ITEMS = NOWN * 6;
+    const int RQ = ca.nparts <= 128 ? 8 : 32, IPR = T / RQ;  // items per round
+    static_assert(T % 32 == 0, "reduction layout");
     for (int it0 = 0; it0 < ITEMS; it0 += IPR) {
       const int it = it0 + tid_ / RQ, qd = tid_ % RQ;
       double2 sacc = make_double2(0.0, 0.0);
@@ -629,7 +633,6 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
           for (int u = 0; u < 8; ++u) sacc = cadd(sacc, buf[u]);
         }
       }
-#pragma unroll
       for (int w = RQ / 2; w > 0; w >>= 1) {
         sacc.x += __shfl_xor_sync(0xffffffffu, sacc.x, w);
         sacc.y += __shfl_xor_sync(0xffffffffu, sacc.y, w);
