@@ -135,6 +135,10 @@ typedef struct {
      sweep0_ms = the k = 0 sweep, lag_ms = one iteration (fine sweep + exchange + coarse sweep),
      fine_task_ms = one fine sweep of this rank's shard. */
   double sweep0_ms, lag_ms, fine_task_ms;
+  /* pipelined: coarse groups (concurrent sweeps) and CTAs per group; die_aware = 1 when every group's
+     CTAs sit on one die of the GPU with the group's exchange arrays homed in that die's L2 (probed
+     once per workspace) */
+  int32_t coarse_groups, group_ctas, die_aware;
 } rsw_parareal_stats;
 
 /* The asymptotic parareal iteration (Eq. HMM parareal iteration P:428-430; Alg.4):

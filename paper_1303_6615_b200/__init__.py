@@ -56,7 +56,8 @@ class _Stats(ctypes.Structure):
                 ("coarse_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
                 ("fine_slice_steps", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
                 ("pipelined", ctypes.c_int32), ("sweep0_ms", ctypes.c_double), ("lag_ms", ctypes.c_double),
-                ("fine_task_ms", ctypes.c_double)]
+                ("fine_task_ms", ctypes.c_double), ("coarse_groups", ctypes.c_int32),
+                ("group_ctas", ctypes.c_int32), ("die_aware", ctypes.c_int32)]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -260,7 +261,8 @@ def parareal_iterate(p: Params, u0, *, dT, dt, T0, M, n_slices, max_iters, tol=0
                stats=dict(fine_ms=st.fine_ms, comm_ms=st.comm_ms, coarse_ms=st.coarse_ms,
                           total_ms=st.total_ms, fine_slice_steps=st.fine_slice_steps,
                           kernel_launches=st.kernel_launches, pipelined=bool(st.pipelined),
-                          sweep0_ms=st.sweep0_ms, lag_ms=st.lag_ms, fine_task_ms=st.fine_task_ms))
+                          sweep0_ms=st.sweep0_ms, lag_ms=st.lag_ms, fine_task_ms=st.fine_task_ms,
+                          coarse_groups=st.coarse_groups, group_ctas=st.group_ctas, die_aware=bool(st.die_aware)))
     if want_FG:
         out["F"], out["G"] = F, G
     return out

@@ -446,13 +446,37 @@ __device__ __forceinline__ double2 yin_sentinel() {
   return make_double2(s, s);
 }
 
+// Addressing of a coarse group's exchange arrays: element i of the stage-input triple buffer (y) and
+// of the per-pair partials (part).  FlatX: plain arrays (bulk sweep).  HomedX: 4 KB pages of a
+// HomedArena (rsw_internal.h) homed on the group's die, 256 double2 per page.
+struct FlatX {
+  double2* yb;
+  double2* pt;
+  __device__ __forceinline__ double2* y(size_t i) const { return yb + i; }
+  __device__ __forceinline__ double2* part(size_t i) const { return pt + i; }
+};
+__device__ __forceinline__ char* homed_page(const HomedArena& h, unsigned q) {
+  const unsigned c = q >> 8, r = q & 255u;
+  const unsigned pidx = 2u * r + ((__popc(r & 0xF7u) ^ (unsigned)(h.kmask >> c)) & 1u);  // parity of 2r & 0x1EF
+  return h.base + ((size_t)c << 21) + ((size_t)pidx << 12);
+}
+struct HomedX {
+  HomedArena h;
+  unsigned yp, pp;  // first logical pages of the stage inputs and of the partials
+  __device__ __forceinline__ double2* at(unsigned p0, size_t i) const {
+    return reinterpret_cast<double2*>(homed_page(h, p0 + (unsigned)(i >> 8))) + (i & 255);
+  }
+  __device__ __forceinline__ double2* y(size_t i) const { return at(yp, i); }
+  __device__ __forceinline__ double2* part(size_t i) const { return at(pp, i); }
+};
+
 // Samples phase of one RK stage (Alg.1): poll the stage input y into C, then evaluate this
 // CTA's sample pairs (m_A, m_B) = (2p+1, 2p+2), p = rank, rank + P, ..., SPLIT pairs at a time on
 // SPLIT thread parts (each with its own X/Y at X + h*6N and named barrier 8 + h), writing one
 // partial Σ_{m in pair} w_m P+_m N(P-_m y) per pair to part[p] (per-pair partials: the owners'
 // reduction order is then independent of the CTA count, so every schedule agrees bitwise).
-template <int N, int R, int T, class GRP = CtaGroup, int NPC = 1, int SPLIT = 1>
-__device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* part, int M, const AvgTab& tab,
+template <int N, int R, int T, class GRP = CtaGroup, int NPC = 1, int SPLIT = 1, class AX = FlatX>
+__device__ __forceinline__ void coarse_samples_phase(const AX& ax, size_t yoff, int M, const AvgTab& tab,
                                                      double2* X, double2* /*Y (= X + 3N)*/, const double2* TW,
                                                      double2* C, double2* /*A (unused)*/, const double2* PH,
                                                      const double* SW, const double* GA, const double* GP,
@@ -476,11 +500,13 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
   constexpr double invN = 1.0 / N;
   // stage input (triple-buffered, sentinel = not yet written): poll, keep
   for (int i = tid_; i < 3 * Kc; i += T) {
-    double2 v = ld_relaxed_v2(y + i);
-    while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(y + i);
+    const double2* yi = ax.y(yoff + i);
+    double2 v = ld_relaxed_v2(yi);
+    while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(yi);
     C[i] = v;
   }
   grp.sync();
+  STAMP(5)
   if (ystamp && tid_ == 0) *ystamp = gtimer();  // trace: the whole stage input has arrived
   const int h = SPLIT > 1 ? tid_ / TH : 0, th = tid_ - h * TH;
   const NamedGroup hg{grp.base() + h * TH, 8 + h, TH};  // named barriers 8..11
@@ -515,7 +541,7 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
     if (SPLIT > 1) nl_core<N, R, TH>(Xh, Yh, TW, hg); else nl_core<N, R, T>(Xh, Yh, TW, grp);
     STAMP(2)
     const double wA = cached ? SWq[0] : __ldg(tab.w + mA), wB = hasB ? (cached ? SWq[1] : __ldg(tab.w + mB)) : 0.0;
-    double2* Pp = part + (size_t)pr * 3 * Kc;
+    const size_t pb = (size_t)pr * 3 * Kc;
     for (int j = th; j < Kc; j += TH) {
       const int kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
       const double as = kap < 0 ? -GA[ak] : GA[ak];
@@ -545,9 +571,9 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
         a0 = caxpy(wB, eb[1], a0);
         ap = caxpy(wB, cmul(eb[2], pB), ap);
       }
-      Pp[j] = am;
-      Pp[Kc + j] = a0;
-      Pp[2 * Kc + j] = ap;
+      *ax.part(pb + j) = am;
+      *ax.part(pb + Kc + j) = a0;
+      *ax.part(pb + 2 * Kc + j) = ap;
     }
     if (SPLIT > 1) hg.sync(); else grp.sync();  // all mirror reads of X done before the next prologue
     STAMP(3)
@@ -561,24 +587,28 @@ __device__ __forceinline__ void coarse_samples_phase(const double2* y, double2* 
 // items i = o*6 + e, entries e = (α, +κ) for e < 3, (α, -κ) for e >= 3.  The stage base v and the RK
 // accumulator ks of owned modes live in this CTA's shared memory for the whole sweep; the stage
 // input y is published to global memory for the samples phase of every CTA.
-template <int N, int NOWN, int T, class GRP = CtaGroup>
-__device__ __forceinline__ void push_stage_input(const CoarseArgs& ca, const double2* yv, const int* yidx, unsigned u,
+template <int N, int NOWN, int T, class GRP = CtaGroup, class AX = FlatX>
+__device__ __forceinline__ void push_stage_input(const AX& ax, const double2* yv, const int* yidx, unsigned u,
                                                  const GRP& grp = GRP()) {
   const int tid_ = grp.tid();
   constexpr int Kc3 = 3 * (2 * (N / 3) + 1);
   grp.sync();
   if (tid_ < NOWN * 6 && yidx[tid_] >= 0) {
-    st_relaxed_v2(ca.yin + (size_t)(u % 3) * Kc3 + yidx[tid_], yv[tid_]);
-    st_relaxed_v2(ca.yin + (size_t)((u + 2) % 3) * Kc3 + yidx[tid_], yin_sentinel());
+    st_relaxed_v2(ax.y((size_t)(u % 3) * Kc3 + yidx[tid_]), yv[tid_]);
+    st_relaxed_v2(ax.y((size_t)((u + 2) % 3) * Kc3 + yidx[tid_]), yin_sentinel());
   }
 }
 
-template <int N, int T, int NOWN, class GRP = CtaGroup>
-__device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int stage, int n, double2* Vs,
+template <int N, int T, int NOWN, class GRP = CtaGroup, class AX = FlatX>
+__device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const AX& ax, int stage, int n, double2* Vs,
                                                     double2* KSs, double2* kk, double2* un_s, double* nd_s,
                                                     double2* red_buf, double2* yv, int* yidx, unsigned ucount,
-                                                    int rank = -1, int P = -1, const GRP& grp = GRP()) {
+                                                    int rank = -1, int P = -1, const GRP& grp = GRP(),
+                                                    unsigned long long* cyc = nullptr) {
   const int tid_ = grp.tid();
+#define USTAMP(i) \
+  if (cyc && tid_ == 0) cyc[i] = clock64();
+  USTAMP(0)
   constexpr int K = N / 3, Kc = 2 * K + 1, NH = N / 2 + 1;
   if (rank < 0) {
     rank = blockIdx.x;
@@ -605,6 +635,7 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
       pf_U = __ldcg(reinterpret_cast<const double2*>(ca.Uprev) + (size_t)(n + 1) * Ls + f * NH + ak);
     }
   }
+  USTAMP(1)
   if (stage > 0) {
     // deterministic reduction of the per-pair partials in a fixed order that depends only on the number
     // of partials (not on the CTA size or the owned-mode count, so every schedule agrees bitwise): RQ
@@ -621,13 +652,13 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
       int ak = 0, al = 0, j = 0;
       if (it < ITEMS) entry(it / 6, it % 6, ak, al, j);
       if (it < ITEMS && ak <= K) {
-        const double2* src = ca.part + al * Kc + j;
+        const size_t e0 = (size_t)al * Kc + j;
         for (int b0 = qd; b0 < ca.nparts; b0 += 8 * RQ) {  // 8 independent L2 loads in flight, summed in order
           double2 buf[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int b = b0 + u * RQ;
-            buf[u] = b < ca.nparts ? __ldcg(src + (size_t)b * 3 * Kc) : make_double2(0.0, 0.0);
+            buf[u] = b < ca.nparts ? __ldcg(ax.part(e0 + (size_t)b * 3 * Kc)) : make_double2(0.0, 0.0);
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) sacc = cadd(sacc, buf[u]);
@@ -639,7 +670,34 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
       }
       if (it < ITEMS && qd == 0) kk[it] = sacc;
     }
+    USTAMP(2)
+#ifdef RSW_REDUCE_PROBE
+    {  // debug: the same loads again (hot in L2, code hot in the i-cache): is the first round slow?
+      double sink = 0.0;
+      for (int it0 = 0; it0 < ITEMS; it0 += IPR) {
+        const int it = it0 + tid_ / RQ, qd = tid_ % RQ;
+        int ak = 0, al = 0, j = 0;
+        if (it < ITEMS) entry(it / 6, it % 6, ak, al, j);
+        if (it < ITEMS && ak <= K) {
+          const size_t e0 = (size_t)al * Kc + j;
+          for (int b0 = qd; b0 < ca.nparts; b0 += 8 * RQ) {
+            double2 buf[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int b = b0 + u * RQ;
+              buf[u] = b < ca.nparts ? __ldcg(ax.part(e0 + (size_t)b * 3 * Kc)) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sink += buf[u].x;
+          }
+        }
+      }
+      if (sink == 1.2345e300) kk[0].x = sink;
+    }
+    USTAMP(9)
+#endif
     grp.sync();
+    USTAMP(3)
     if (tid_ < NOWN * 6) {
       int ak, al, j;
       const int it = tid_;
@@ -672,11 +730,14 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
         yidx[it] = -1;
       }
     }
+    USTAMP(4)
     if (!last) {
-      push_stage_input<N, NOWN, T>(ca, yv, yidx, ucount, grp);
+      push_stage_input<N, NOWN, T>(ax, yv, yidx, ucount, grp);
+      USTAMP(5)
       return;
     }
     grp.sync();
+    USTAMP(5)
     // finalize: D half step, back-transform, primitive G, parareal update (thread per (o, f))
     if (tid_ < NOWN * 3) {
       const int o = tid_ / 3, f = tid_ % 3, ak = rank + o * P;
@@ -720,6 +781,7 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
         ca.rparts[((size_t)n * (K + 1) + ak) * 2 + 1] = t[1] + t[3] + t[5];
       }
     }
+    USTAMP(6)
     if (n + 1 >= ca.n_end) return;  // no next slice
   } else {
     // stage 0: load U_0 of owned modes
@@ -748,8 +810,11 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, int st
       yidx[it] = -1;
     }
   }
-  push_stage_input<N, NOWN, T>(ca, yv, yidx, ucount, grp);
+  USTAMP(7)
+  push_stage_input<N, NOWN, T>(ax, yv, yidx, ucount, grp);
   grp.sync();
+  USTAMP(8)
+#undef USTAMP
 }
 
 template <int N, int R, int T, int NOWN, int NPC = 1, int SPLIT = 1>

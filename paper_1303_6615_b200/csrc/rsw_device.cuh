@@ -245,12 +245,22 @@ struct CtaGroup {
   __device__ __forceinline__ int tid() const { return threadIdx.x; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
   __device__ __forceinline__ int fbar() const { return 1; }  // ids 1..3 (kernels whose whole CTA is one group)
+  __device__ __forceinline__ int ftid() const { return threadIdx.x; }
 };
 struct NamedGroup {
   int b0, id, nthr;  // first thread, barrier id (1..15), thread count (multiple of 32)
   int fb = 0;        // per-field barrier ids fb..fb+2, or 0
+  int wsw = 0;       // FFT roles with the group's warps 2 and 3 exchanged (ftid)
   __device__ __forceinline__ int base() const { return b0; }
   __device__ __forceinline__ int tid() const { return threadIdx.x - b0; }
+  // thread index of the FFT core's (field, column) roles: tid(), or with warps 2 and 3 exchanged, which
+  // moves the third field's warp to the SM sub-partition the group would otherwise leave without FFT work
+  // (warp w issues on sub-partition w mod 4; used by the pipelined schedule's fine group, whose CTA
+  // neighbours are the coarse parts)
+  __device__ __forceinline__ int ftid() const {
+    const int t = tid();
+    return (wsw && (t >> 6) == 1) ? (t ^ 32) : t;
+  }
   __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory"); }
   __device__ __forceinline__ int fbar() const { return fb; }
 };
@@ -566,7 +576,7 @@ __device__ __forceinline__ void nl_core(double2* X, double2* /*unused*/, const d
   constexpr int m = fft_npass<N, R>(), NJ = N / R, K = N / 3;
   constexpr int rl = fft_rad<N, R>(m - 1), Ll = fft_len<N, R>(m - 1), dl = Ll / rl;
   static_assert(dl == 1 && rl == R, "nl_core: the last pass must have radix R and stride 1");
-  const int t = grp.tid();
+  const int t = grp.ftid();
   const int f = t / NJ, j = t % NJ;
   const bool act = t < 3 * NJ;
   constexpr int FS = fft_fs<N, R>();

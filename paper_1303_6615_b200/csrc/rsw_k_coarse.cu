@@ -78,18 +78,19 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   // the three stage-input buffers start empty (sentinel) before anyone writes
   for (int i = blockIdx.x * T + threadIdx.x; i < 3 * Kc3; i += P * T) st_relaxed_v2(ca.yin + i, yin_sentinel());
   grid_barrier(bar, P, epoch);
-  coarse_update_phase<N, T, NOWN>(ca, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount);  // slice 0: v = e^{ΔT D̂/2} U_0
+  const FlatX ax{ca.yin, const_cast<double2*>(ca.part)};
+  coarse_update_phase<N, T, NOWN>(ca, ax, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount);  // slice 0: v = e^{ΔT D̂/2} U_0
   for (int n = 0; n < ca.n_end; ++n) {
     for (int st = 1; st <= nst; ++st) {
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 0] = gtimer();
-      const double2* inbox = ca.yin + (size_t)(ucount % 3) * Kc3;
-      coarse_samples_phase<N, R, T>(inbox, const_cast<double2*>(ca.part), M, tab, X, Y, TW, C, A, PHc, SW, GA, GP, GQ,
+      coarse_samples_phase<N, R, T>(ax, (size_t)(ucount % 3) * Kc3, M, tab, X, Y, TW, C, A, PHc, SW, GA, GP, GQ,
                                     (prof && ps == 8) ? ca.prof + 256 : nullptr);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 1] = gtimer();
       grid_barrier(bar, P, epoch);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 2] = gtimer();
       ++ucount;
-      coarse_update_phase<N, T, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount);
+      coarse_update_phase<N, T, NOWN>(ca, ax, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, -1, -1, CtaGroup(),
+                                      (prof && (ps == 9 || ps == 11)) ? ca.prof + (ps == 9 ? 300 : 320) : nullptr);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 3] = gtimer();
       ++ps;
     }

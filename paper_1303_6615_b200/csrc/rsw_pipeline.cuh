@@ -35,6 +35,12 @@
 #ifndef RSW_PIPE_FINE_TMUL
 #define RSW_PIPE_FINE_TMUL 2  // threads per fine group = TMUL x 3N/R
 #endif
+#ifndef RSW_PIPE_FINE_WSWAP
+#define RSW_PIPE_FINE_WSWAP 1  // fine FFT fields on warps 0, 1, 3 (NamedGroup::wsw)
+#endif
+#ifndef RSW_PIPE_CLAIM
+#define RSW_PIPE_CLAIM 1  // fine-task claim order: 0 lowest iteration first, 1 oldest ready task first
+#endif
 #ifndef RSW_PIPE_FINE_GROUPS
 #define RSW_PIPE_FINE_GROUPS 1  // fine worker groups per CTA (two slowed the sweeps on C3)
 #endif
@@ -140,6 +146,29 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
       for (unsigned it = 0;; ++it) {
         const int lim = min(Kit, *(volatile int*)a.stopk) - 1;  // F^k is needed by sweep k+1 <= stop
         bool all_claimed = true;
+#if RSW_PIPE_CLAIM == 1
+        // the oldest ready task first: sweeps advance at one pace, so the iteration whose next unclaimed
+        // pair became ready the most slices ago holds the earliest deadline (sweep k+1 needs it)
+        int bk = -1, bt = 0, bpp = 0, bage = -1;
+        for (int k = 0; k <= lim; ++k) {
+          const unsigned t = *(volatile unsigned*)(a.next + k);
+          if ((int)t >= a.pair_hi - a.pair_lo) continue;
+          all_claimed = false;
+          const int pp = a.pair_lo + (int)t;
+          const int need = (2 * pp + 1 < S) ? 2 * pp + 1 : 2 * pp;
+          const int age = (int)(ld_acquire_gpu(a.prog + k) / (unsigned)a.GC) - need;  // slices finalized past it
+          if (age >= 0 && age > bage) {
+            bage = age;
+            bk = k;
+            bt = (int)t;
+            bpp = pp;
+          }
+        }
+        if (bk >= 0 && atomicCAS(a.next + bk, (unsigned)bt, (unsigned)bt + 1) == (unsigned)bt) {
+          tk = bk;
+          tp = bpp;
+        }
+#else
         for (int k = 0; k <= lim && tk < 0; ++k) {
           const unsigned t = *(volatile unsigned*)(a.next + k);  // local task index: pair pair_lo + t
           if ((int)t >= a.pair_hi - a.pair_lo) continue;
@@ -151,6 +180,7 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
             tp = pp;
           }
         }
+#endif
         if (tk >= 0 || all_claimed) break;
         if ((it & 63) == 63 && watchdog_expired(w, a.wd, a.hb)) break;
         __nanosleep(128);
@@ -207,15 +237,39 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
   constexpr size_t L = (size_t)3 * NH * 2;  // doubles per state
   extern __shared__ double2 smem[];
   __shared__ uint32_t tslot;
-  __shared__ unsigned s_ticket, s_flag;
+  __shared__ unsigned s_flag;
+  __shared__ int s_role[3];  // coarse group (-1: none), rank in the group, die of the group's arrays
   __shared__ int s_task[NPG + TC / TG][2];
   const int warp = threadIdx.x >> 5;
   if (warp == 0) tmem_alloc<512>(&tslot);
-  if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1u);
+  if (threadIdx.x == 0) {  // role: coarse group g, rank c (or none); die-aware: from this SM's die ticket
+    int g = -1, c = 0, d = 0, slot = 0;
+    if (a.die_aware) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      d = smid < 192 ? (int)((a.diemask[smid >> 6] >> (smid & 63)) & 1ull) : 0;
+      const int t = (int)atomicAdd(a.dticket + d, 1u);
+      slot = t / a.GC;
+      if (slot < a.ndg[d]) {
+        g = a.dg[d][slot];
+        c = t % a.GC;
+      }
+    } else {
+      const int t = (int)atomicAdd(a.ticket, 1u);
+      if (t < a.NG * a.GC) {
+        g = t / a.GC;
+        c = t % a.GC;
+        d = g & 1;
+        slot = g >> 1;
+      }
+    }
+    s_role[0] = g;
+    s_role[1] = c;
+    s_role[2] = d | (slot << 1);
+  }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const int ticket = (int)s_ticket;
   const int S = a.S, Kit = a.K;
   // fine tables (shared by every fine group of the CTA), staged by all threads
   const FineSmemTab ft = stage_fine_tables<N, RF, TC + NPG * TG>(
@@ -227,7 +281,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
     // ===================================== coarse sub-CTA =====================================
     const NamedGroup cg{FT, 15, TC};
     const int ct = (int)threadIdx.x - FT;
-    if (ticket >= a.NG * a.GC) {
+    if (s_role[0] < 0) {
       // no coarse role: the coarse threads run XG more fine groups (in the coarse region of smem)
       constexpr int XG = TC / TG;
       const int xi = ct / TG;
@@ -236,7 +290,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
                                             smem + LY::C0 + (size_t)xi * 6 * N, ft,
                                             tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi]);
     } else {
-      const int g = ticket / a.GC, c = ticket % a.GC, P = a.GC;
+      const int g = s_role[0], c = s_role[1], P = a.GC, gd = s_role[2] & 1, gslot = s_role[2] >> 1;
       double2* cs = smem + LY::C0;
       double2* X = cs + CL::X;
       double2* Y = cs + CL::Y;
@@ -279,14 +333,16 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         }
       }
       cg.sync();
-      unsigned* bar = a.gbar + g * 32;
-      double2* yb = a.ybuf + (size_t)g * 3 * Kc3;
-      double2* part = a.part + (size_t)g * (M / 2 > 0 ? M / 2 : 1) * Kc3;
+      // the group's exchange arrays in pages homed on die gd: barrier counter, stage inputs, partials
+      constexpr unsigned YP = (3 * Kc3 + 255) / 256;
+      const unsigned PPG = ((unsigned)(M / 2 > 0 ? M / 2 : 1) * Kc3 + 255) / 256, GPG = 1 + YP + PPG;
+      unsigned* bar = reinterpret_cast<unsigned*>(homed_page(a.arena[gd], gslot * GPG));
+      const HomedX ax{a.arena[gd], gslot * GPG + 1, gslot * GPG + 1 + YP};
       const int nst = a.base.scheme == 0 ? 4 : 2;
       unsigned epoch = 0;
       for (int k = g; k <= Kit; k += a.NG) {
         // sweep start: the three stage-input buffers of the group start empty
-        for (int i = c * TC + ct; i < 3 * Kc3; i += P * TC) st_relaxed_v2(yb + i, yin_sentinel());
+        for (int i = c * TC + ct; i < 3 * Kc3; i += P * TC) st_relaxed_v2(ax.y(i), yin_sentinel());
         const bool stop_now = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
         if (group_barrier(bar, P, epoch, stop_now, a.wd, a.hb, &s_flag, cg)) break;
         if (c == 0 && ct == 0) {
@@ -301,9 +357,9 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         ca.Gprev = k ? a.Gall + (size_t)(k - 1) * S * L : ca.G;
         ca.F = k ? a.Fall + (size_t)(k - 1) * S * L : nullptr;
         ca.rparts = k ? a.rparts + (size_t)k * S * KP * 2 : nullptr;
-        ca.part = part;
+        ca.part = nullptr;  // (addressed through ax)
         ca.nparts = M / 2 > 0 ? M / 2 : 1;
-        ca.yin = yb;
+        ca.yin = nullptr;
         ca.n_end = S;
         ca.wprog = k ? a.prog + (k - 1) : nullptr;
         ca.wunit = (unsigned)P;
@@ -315,7 +371,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         ca.kself = k;
         ca.prof = nullptr;
         unsigned ucount = 0;
-        coarse_update_phase<N, TC, NOWN>(ca, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, c, P, cg);
+        coarse_update_phase<N, TC, NOWN>(ca, ax, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, c, P, cg);
         bool aborted = false;
         for (int n = 0; n < S && !aborted; ++n) {
           for (int st = 1; st <= nst; ++st) {
@@ -332,7 +388,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
                                                  2 * (size_t)(Kit > 0 ? Kit : 1) * a.npairs + 256
                                            : nullptr;
             if (stp) stp[0] = gtimer();
-            coarse_samples_phase<N, LY::RC, TC, NamedGroup, NPC, LY::SPLIT>(yb + (size_t)(ucount % 3) * Kc3, part, M, tab, X, Y, TW,
+            coarse_samples_phase<N, LY::RC, TC, NamedGroup, NPC, LY::SPLIT>(ax, (size_t)(ucount % 3) * Kc3, M, tab, X, Y, TW,
                                                              C, A, PH, SW, GA, GP, GQ, nullptr, c, P, cg,
                                                              (hand && c == 0) ? hand + 4096 + sidx : nullptr);
             if (stp) stp[1] = gtimer();
@@ -343,7 +399,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
             }
             if (stp) stp[2] = gtimer();
             ++ucount;
-            coarse_update_phase<N, TC, NOWN>(ca, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, c, P, cg);
+            coarse_update_phase<N, TC, NOWN>(ca, ax, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, c, P, cg);
             if (stp) stp[3] = gtimer();
             if (hand) hand[sidx * 64 + c] = gtimer();
           }
@@ -395,7 +451,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
   } else {
     // ======================================= fine worker group 0 =======================================
     const int gi = threadIdx.x / TG;
-    fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{gi * TG, 1 + gi, TG}, smem + LY::F_G + (size_t)gi * 6 * N,
+    fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{gi * TG, 1 + gi, TG, 0, RSW_PIPE_FINE_WSWAP}, smem + LY::F_G + (size_t)gi * 6 * N,
                                         ft, tslot + (uint32_t)(gi * LY::CPG), s_task[gi]);
   }
   tmem_fence_before();

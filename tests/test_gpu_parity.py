@@ -413,6 +413,27 @@ def test_pipelined_group_layouts_bitwise(rsw_gpu, gc, ng, monkeypatch):
     assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
 
 
+def test_pipelined_die_placement_bitwise(rsw_gpu, monkeypatch):
+    """C3 (2 iterations): the pipelined schedule with die-aware coarse groups (each group's CTAs on one
+    die, its exchange arrays in L2 pages homed there) and without the placement
+    (RSW_NO_DIE_AWARE=1: groups from the global ticket, same homed arena) give bitwise the bulk result;
+    the stats report the layout that ran."""
+    w = inputs.C3
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=2)
+    a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
+    monkeypatch.setenv("RSW_NO_DIE_AWARE", "1")
+    c = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
+    assert not c["stats"]["die_aware"]
+    assert b["stats"]["coarse_groups"] >= 1 and b["stats"]["group_ctas"] >= 1
+    for r in (b, c):
+        assert r["resid"] == a["resid"] and torch.equal(r["U"], a["U"])
+    print("die-aware placement:", b["stats"]["die_aware"], "groups", b["stats"]["coarse_groups"], "x",
+          b["stats"]["group_ctas"])
+
+
 def test_check_states_layout(rsw_gpu):
     """§8(b): an input with a non-zero mode k > n/3 (R10) or Im û_0 != 0 (R16) is RSW_ERR_CONFIG —
     through rsw_check_states, through parareal_iterate's own device check of u0, and through the
