@@ -38,6 +38,9 @@
 #ifndef RSW_PIPE_FINE_WSWAP
 #define RSW_PIPE_FINE_WSWAP 1  // fine FFT fields on warps 0, 1, 3 (NamedGroup::wsw)
 #endif
+#ifndef RSW_PIPE_REUSE_COARSE
+#define RSW_PIPE_REUSE_COARSE 0  // 1: a coarse CTA whose sweeps are done runs an extra fine group (C3: 34.2 -> 34.4 ms, not kept)
+#endif
 #ifndef RSW_PIPE_CLAIM
 #define RSW_PIPE_CLAIM 1  // fine-task claim order: 0 lowest iteration first, 1 oldest ready task first
 #endif
@@ -281,15 +284,18 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
     // ===================================== coarse sub-CTA =====================================
     const NamedGroup cg{FT, 15, TC};
     const int ct = (int)threadIdx.x - FT;
-    if (s_role[0] < 0) {
-      // no coarse role: the coarse threads run XG more fine groups (in the coarse region of smem)
+    // XG more fine groups on the coarse threads (in the coarse region of smem): in a CTA without a coarse
+    // role, and in a coarse CTA once its group's sweeps are done (the later iterations' fine tasks are
+    // then the bottleneck: each finished group adds GC fine groups)
+    auto extra_fine = [&]() {
       constexpr int XG = TC / TG;
       const int xi = ct / TG;
       if (xi < XG && (NPG + XG) * LY::CPG <= 512)
         fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{FT + xi * TG, 1 + NPG + xi, TG},
                                             smem + LY::C0 + (size_t)xi * 6 * N, ft,
                                             tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi]);
-    } else {
+    };
+    if (s_role[0] >= 0) {
       const int g = s_role[0], c = s_role[1], P = a.GC, gd = s_role[2] & 1, gslot = s_role[2] >> 1;
       double2* cs = smem + LY::C0;
       double2* X = cs + CL::X;
@@ -447,7 +453,9 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
           }
         }
       }
+      cg.sync();  // every coarse thread is past the sweeps: the coarse region of smem is free
     }
+    if (s_role[0] < 0 || RSW_PIPE_REUSE_COARSE) extra_fine();
   } else {
     // ======================================= fine worker group 0 =======================================
     const int gi = threadIdx.x / TG;
