@@ -455,11 +455,6 @@ struct FlatX {
   __device__ __forceinline__ double2* y(size_t i) const { return yb + i; }
   __device__ __forceinline__ double2* part(size_t i) const { return pt + i; }
 };
-__device__ __forceinline__ char* homed_page(const HomedArena& h, unsigned q) {
-  const unsigned c = q >> 8, r = q & 255u;
-  const unsigned pidx = 2u * r + ((__popc(r & 0xF7u) ^ (unsigned)(h.kmask >> c)) & 1u);  // parity of 2r & 0x1EF
-  return h.base + ((size_t)c << 21) + ((size_t)pidx << 12);
-}
 struct HomedX {
   HomedArena h;
   unsigned yp, pp;  // first logical pages of the stage inputs and of the partials

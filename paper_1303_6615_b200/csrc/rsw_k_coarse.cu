@@ -1,6 +1,9 @@
 // rsw_k_coarse.cu — the persistent cooperative coarse sweep (a3-a5) and the Strang-coarse serial sweep (NEXT-1).
 #include "rsw_blocks.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace rsw {
 
 template <typename KernelT>
@@ -22,12 +25,37 @@ static cudaError_t set_smem(KernelT k, size_t bytes) {
   }
 
 
+// Kernel argument of one sweep: the placement, the die the sweep runs on (-1: ranks = blocks) and the
+// participating CTA count P
+struct SweepRun {
+  SweepPlace pl;
+  int die, P;
+};
+
 template <int N, int R, int T, int NOWN>
-__global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const AvgTab tab, int M, unsigned* bar,
+__global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const AvgTab tab, int M, const SweepRun sr,
                                                     double* r_out) {
   using LY = CoarseLayout<N, R, T, NOWN>;
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
   extern __shared__ double2 smem[];
+  __shared__ int s_rank;
+  if (threadIdx.x == 0) {  // rank: the block index, or (die placement) a ticket among the die's CTAs
+    int r = (int)blockIdx.x;
+    if (sr.die >= 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      const int d = smid < 192 ? (int)((sr.pl.diemask[smid >> 6] >> (smid & 63)) & 1ull) : 0;
+      r = (d == sr.die) ? (int)atomicAdd(sr.pl.ticket, 1u) : -1;
+      if (r >= sr.P) r = -1;
+    }
+    s_rank = r;
+  }
+  __syncthreads();
+  const int rank = s_rank;
+  if (rank < 0) return;  // not part of this sweep (other die, or a surplus CTA)
+  const HomedArena& ha = sr.pl.arena[sr.die > 0 ? 1 : 0];
+  unsigned* bar = reinterpret_cast<unsigned*>(homed_page(ha, sr.pl.bpage));
+  const HomedX ax{ha, sr.pl.ypage, sr.pl.ppage};
   double2* X = smem + LY::X;
   double2* Y = smem + LY::Y;
   double2* TW = smem + LY::TW;
@@ -53,9 +81,10 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
     GP[k] = __ldg(tab.g.p + k);
     GQ[k] = __ldg(tab.g.q + k);
   }
-  const bool one_pair = (int)gridDim.x >= M / 2;
-  if (one_pair && (int)blockIdx.x < M / 2) {
-    const int mA = 2 * blockIdx.x + 1, mB = 2 * blockIdx.x + 2;
+  const unsigned P = (unsigned)sr.P;
+  const bool one_pair = (int)P >= M / 2;
+  if (one_pair && rank < M / 2) {
+    const int mA = 2 * rank + 1, mB = 2 * rank + 2;
     for (int k = threadIdx.x; k <= K; k += T) {
       PH[k] = __ldg(tab.phase + (size_t)mA * KP + k);
       PH[KP + k] = __ldg(tab.phase + (size_t)mB * KP + k);
@@ -69,34 +98,32 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   const double2* PHc = one_pair ? PH : nullptr;
   double2* yv = smem + LY::YV;
   int* yidx = reinterpret_cast<int*>(sd + LY::YI);
-  const unsigned P = gridDim.x;
   constexpr int Kc3 = 3 * Kc;
   const int nst = ca.scheme == 0 ? 4 : 2;
   unsigned epoch = 0, ucount = 0;
-  const bool prof = ca.prof && blockIdx.x == 0;
+  const bool prof = ca.prof && rank == 0;
   int ps = 0;
   // the three stage-input buffers start empty (sentinel) before anyone writes
-  for (int i = blockIdx.x * T + threadIdx.x; i < 3 * Kc3; i += P * T) st_relaxed_v2(ca.yin + i, yin_sentinel());
+  for (int i = rank * T + threadIdx.x; i < 3 * Kc3; i += P * T) st_relaxed_v2(ax.y(i), yin_sentinel());
   grid_barrier(bar, P, epoch);
-  const FlatX ax{ca.yin, const_cast<double2*>(ca.part)};
-  coarse_update_phase<N, T, NOWN>(ca, ax, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount);  // slice 0: v = e^{ΔT D̂/2} U_0
+  coarse_update_phase<N, T, NOWN>(ca, ax, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, rank, (int)P);  // slice 0: v = e^{ΔT D̂/2} U_0
   for (int n = 0; n < ca.n_end; ++n) {
     for (int st = 1; st <= nst; ++st) {
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 0] = gtimer();
       coarse_samples_phase<N, R, T>(ax, (size_t)(ucount % 3) * Kc3, M, tab, X, Y, TW, C, A, PHc, SW, GA, GP, GQ,
-                                    (prof && ps == 8) ? ca.prof + 256 : nullptr);
+                                    (prof && ps == 8) ? ca.prof + 256 : nullptr, rank, (int)P);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 1] = gtimer();
       grid_barrier(bar, P, epoch);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 2] = gtimer();
       ++ucount;
-      coarse_update_phase<N, T, NOWN>(ca, ax, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, -1, -1, CtaGroup(),
+      coarse_update_phase<N, T, NOWN>(ca, ax, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, rank, (int)P, CtaGroup(),
                                       (prof && (ps == 9 || ps == 11)) ? ca.prof + (ps == 9 ? 300 : 320) : nullptr);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 3] = gtimer();
       ++ps;
     }
   }
   grid_barrier(bar, P, epoch);  // every slice's U, G and residual partials are written
-  if (r_out && blockIdx.x == 0) {  // r_k = max_n sqrt(Σ num / Σ den) over slices (fixed order)
+  if (r_out && rank == 0) {  // r_k = max_n sqrt(Σ num / Σ den) over slices (fixed order)
     double mx = 0.0;
     bool bad = false;
     for (int s = threadIdx.x; s < ca.n_end; s += T) {
@@ -231,26 +258,38 @@ __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h,
 }
 
 template <int N, int NOWN, int R = coarse_radix<N>(), int T = coarse_threads<N>()>
-static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar,
-                                            double* r_out, int grid, cudaStream_t st) {
+static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& tab, int M, const SweepPlace& pl,
+                                            double* r_out, int grid, bool on_die, int* die_used, cudaStream_t st) {
   auto kfn = k_coarse_sweep<N, R, T, NOWN>;
-  const size_t sm = CoarseLayout<N, R, T, NOWN>::bytes;
-  cudaError_t e = set_smem(kfn, sm);
-  if (e != cudaSuccess) return e;
   int dev, sms, per_sm;
+  cudaError_t e;
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  SweepRun sr{pl, -1, grid};
+  size_t sm = CoarseLayout<N, R, T, NOWN>::bytes;
+  int launch = grid;
+  if (on_die) {  // on the die with more SMs; one CTA per SM on every SM (the others exit at once)
+    sr.die = pl.die_n[1] > pl.die_n[0] ? 1 : 0;
+    launch = sms;
+    if (sm < 120 * 1024) sm = 120 * 1024;  // > half an SM's shared memory: exactly one CTA per SM
+  }
+  if ((e = set_smem(kfn, sm)) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, T, sm)) != cudaSuccess) return e;
-  if (grid > per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
+  if (launch > per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
+  if (on_die && per_sm != 1) return cudaErrorInvalidConfiguration;
+  if (die_used) *die_used = sr.die;
   CoarseArgs c2 = ca;
-  if ((e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st)) != cudaSuccess) return e;
-  void* args[] = {(void*)&c2, (void*)&tab, (void*)&M, (void*)&bar, (void*)&r_out};
-  return cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(T), args, sm, st);
+  // the barrier counter (its arena page) and the die ticket start at zero
+  char* bpage = homed_page(pl.arena[sr.die > 0 ? 1 : 0], pl.bpage);
+  if ((e = cudaMemsetAsync(bpage, 0, 4096, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(pl.ticket, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+  void* args[] = {(void*)&c2, (void*)&tab, (void*)&M, (void*)&sr, (void*)&r_out};
+  return cudaLaunchCooperativeKernel((const void*)kfn, dim3(launch), dim3(T), args, sm, st);
 }
 
 template <int N>
-static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar,
-                                         double* r_out, int* grid_used, cudaStream_t st) {
+static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab, int M, const SweepPlace& pl,
+                                         double* r_out, int* grid_used, int* die_used, cudaStream_t st) {
   int dev, sms;
   cudaError_t e;
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
@@ -262,16 +301,25 @@ static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab
   if (grid < (K + 1 + 15) / 16) grid = (K + 1 + 15) / 16;
   if (grid > sms) grid = sms;
   if (grid < 1) grid = 1;
+  // die placement when the sweep fits on one die
+  const bool on_die = pl.die_ok && grid <= std::max(pl.die_n[0], pl.die_n[1]) && !getenv("RSW_NO_DIE_AWARE");
+  if (die_used) *die_used = -1;
   const int nown = (K + 1 + grid - 1) / grid;  // owned modes per CTA in the update phase
   if (grid_used) *grid_used = grid;
-  if (nown <= 1) return launch_coarse_sweep_nown<N, 1>(ca, tab, M, bar, r_out, grid, st);
-  if (nown <= 2) return launch_coarse_sweep_nown<N, 2>(ca, tab, M, bar, r_out, grid, st);
-  if (nown <= 4) return launch_coarse_sweep_nown<N, 4>(ca, tab, M, bar, r_out, grid, st);
-  if (nown <= 8) return launch_coarse_sweep_nown<N, 8>(ca, tab, M, bar, r_out, grid, st);
-  if (nown <= 16) return launch_coarse_sweep_nown<N, 16>(ca, tab, M, bar, r_out, grid, st);
+#define L_(NO) launch_coarse_sweep_nown<N, NO>(ca, tab, M, pl, r_out, grid, on_die, die_used, st)
+  if (nown <= 1) return L_(1);
+  if (nown <= 2) return L_(2);
+  if (nown <= 4) return L_(4);
+  if (nown <= 8) return L_(8);
+  if (nown <= 16) return L_(16);
+#undef L_
   return cudaErrorInvalidConfiguration;
 }
 
+unsigned sweep_pages(int n, int M) {
+  const unsigned Kc3 = 3u * (2u * (unsigned)(n / 3) + 1u), pairs = (unsigned)std::max(M / 2, 1);
+  return 1u + (3u * Kc3 + 255u) / 256u + (pairs * Kc3 + 255u) / 256u;
+}
 
 template <int N>
 static cudaError_t launch_strang_sweep_n(const FineTab& tab, double h, double* U, double* G, const double* F,
@@ -286,9 +334,9 @@ static cudaError_t launch_strang_sweep_n(const FineTab& tab, double h, double* U
 }
 
 
-cudaError_t launch_coarse_sweep(int n, const CoarseArgs& ca, const AvgTab& tab, int M, unsigned* bar, double* r_out,
-                                int* grid_used, cudaStream_t st) {
-#define C(NN) launch_coarse_sweep_n<NN>(ca, tab, M, bar, r_out, grid_used, st)
+cudaError_t launch_coarse_sweep(int n, const CoarseArgs& ca, const AvgTab& tab, int M, const SweepPlace& pl,
+                                double* r_out, int* grid_used, int* die_used, cudaStream_t st) {
+#define C(NN) launch_coarse_sweep_n<NN>(ca, tab, M, pl, r_out, grid_used, die_used, st)
   RSW_DISPATCH(n, C)
 #undef C
 }
