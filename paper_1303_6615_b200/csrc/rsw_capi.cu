@@ -504,8 +504,8 @@ rsw_status run_chain(const Chain& ch, Workspace* ws, double* r_out, cudaStream_t
     if (as != RSW_OK) return as;
   }
   rsw::SweepPlace pl{};
-  pl.arena[0] = rsw::HomedArena{ws->arena_base, ws->kmask0};
-  pl.arena[1] = rsw::HomedArena{ws->arena_base, ~ws->kmask0};
+  pl.arena[0] = rsw::HomedArena{ws->arena_base, ws->kmask0, 0};
+  pl.arena[1] = rsw::HomedArena{ws->arena_base, ~ws->kmask0, 0};
   pl.bpage = 0;
   pl.ypage = 1;
   pl.ppage = 1 + (3u * 3u * (2u * (unsigned)(ch.p->n / 3) + 1u) + 255u) / 256u;
@@ -972,8 +972,8 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
       a.ndg[1] = a.NG / 2;
     }
     for (int i = 0; i < 3; ++i) a.diemask[i] = ws->diemask[i];
-    a.arena[0] = rsw::HomedArena{ws->arena_base, ws->kmask0};
-    a.arena[1] = rsw::HomedArena{ws->arena_base, ~ws->kmask0};
+    a.arena[0] = rsw::HomedArena{ws->arena_base, ws->kmask0, 0};
+    a.arena[1] = rsw::HomedArena{ws->arena_base, ~ws->kmask0, 0};
   }
   a.Uall = (double*)ws->pU.p;
   a.Gall = (double*)ws->pG.p;

@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   __syncthreads();
   const int rank = s_rank;
   if (rank < 0) return;  // not part of this sweep (other die, or a surplus CTA)
-  const HomedArena& ha = sr.pl.arena[sr.die > 0 ? 1 : 0];
+  HomedArena ha = sr.pl.arena[sr.die > 0 ? 1 : 0];
+  ha.flat = sr.die < 0 ? 1 : 0;
   unsigned* bar = reinterpret_cast<unsigned*>(homed_page(ha, sr.pl.bpage));
   const HomedX ax{ha, sr.pl.ypage, sr.pl.ppage};
   double2* X = smem + LY::X;
@@ -280,7 +281,9 @@ static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& 
   if (die_used) *die_used = sr.die;
   CoarseArgs c2 = ca;
   // the barrier counter (its arena page) and the die ticket start at zero
-  char* bpage = homed_page(pl.arena[sr.die > 0 ? 1 : 0], pl.bpage);
+  HomedArena ha = pl.arena[sr.die > 0 ? 1 : 0];
+  ha.flat = sr.die < 0 ? 1 : 0;
+  char* bpage = homed_page(ha, pl.bpage);
   if ((e = cudaMemsetAsync(bpage, 0, 4096, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(pl.ticket, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
   void* args[] = {(void*)&c2, (void*)&tab, (void*)&M, (void*)&sr, (void*)&r_out};
