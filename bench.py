@@ -479,7 +479,7 @@ def main():
                            "per_further_iteration": statistics.median(s["lag_ms"] for s in stats),
                            "fine_task_latency": statistics.median(s["fine_task_ms"] for s in stats),
                            "layout": {"coarse_groups": stats[-1]["coarse_groups"], "ctas_per_group": stats[-1]["group_ctas"],
-                                      "die_aware": stats[-1]["die_aware"]},
+                                      "die_aware": stats[-1]["die_aware"], "die_sms": rsw.device_topology()["die_sms"]},
                            "note": "k = 0 coarse sweep (2048 serial stages) + iterations x the lag each adds "
                                    "(one fine pair task + hand-off); in-kernel globaltimer stamps"} if pipelined else
                           {"fine": statistics.median(s["fine_ms"] for s in stats), "allgather": comm_ms,

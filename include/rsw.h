@@ -71,6 +71,12 @@ enum { RSW_FLAG_LINEAR_ONLY = 1u }; /* N ≡ 0: exact-linear test mode only */
    mode k > n/3 is non-zero or any Im(û_0) != 0, RSW_OK otherwise.  Synchronises `stream`. */
 rsw_status rsw_check_states(const rsw_params* p, int32_t n_states, const double* u, void* stream);
 
+/* Device topology used by the coarse sweeps' placement: die_sms[d] = the SMs on die d
+   of the current device (die 0 = the probe master's die), *probed = 1 when the die-homing probe found
+   two dies and the page hash, 0 when placement is off (then die_sms = {SM count, 0}).  Runs the probe
+   (one cooperative launch, ~5 ms) on first use; synchronous; die_sms: HOST int32[2]. */
+rsw_status rsw_device_topology(int32_t* die_sms, int32_t* probed);
+
 /* N(u) = -(v1 ∂x v1, v1 ∂x v2, ∂x(h v1)) for n_states independent states, evaluated
    pseudo-spectrally (inverse FFT -> pointwise products -> FFT, 2/3 rule).
    Operator table, sign R1.  u_in and out must not alias.

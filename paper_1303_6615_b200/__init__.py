@@ -29,7 +29,7 @@ EXPORTS = [
     "rsw_nonlinear", "rsw_fine_propagate", "rsw_averaged_rhs", "rsw_coarse_propagate",
     "parareal_iterate", "parareal_iterate_ex", "rsw_shard_range", "rsw_nccl_unique_id",
     "rsw_comm_init", "rsw_comm_destroy", "rsw_fp64_peak", "rsw_flops_per_unit", "rsw_last_error",
-    "rsw_shutdown", "rsw_check_states", "parareal_resume",
+    "rsw_shutdown", "rsw_check_states", "parareal_resume", "rsw_device_topology",
 ]
 
 
@@ -99,6 +99,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.rsw_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.rsw_comm_destroy.argtypes = [vp]
     L.rsw_fp64_peak.argtypes = [ctypes.POINTER(ctypes.c_double), vp]
+    L.rsw_device_topology.argtypes = [ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.rsw_flops_per_unit.argtypes = [i32, i32]
     L.rsw_flops_per_unit.restype = ctypes.c_double
     L.rsw_last_error.restype = ctypes.c_char_p
@@ -135,6 +136,14 @@ def check_states(p: Params, u):
     (RSW_ERR_CONFIG) on a violation.  Synchronises the current stream."""
     a, nb = _state_arg(u, p.n)
     _check(load().rsw_check_states(ctypes.byref(p._c()), nb, a, _stream()))
+
+
+def device_topology() -> dict:
+    """SMs per die of the current device and whether the die-homing probe succeeded."""
+    d = (ctypes.c_int32 * 2)()
+    ok = ctypes.c_int32(0)
+    _check(load().rsw_device_topology(d, ctypes.byref(ok)))
+    return dict(die_sms=[d[0], d[1]], probed=bool(ok.value))
 
 
 def nonlinear(p: Params, u, validate: bool = True):

@@ -712,6 +712,25 @@ rsw_status rsw_nonlinear(const rsw_params* p, int32_t n_states, const double* u_
   return RSW_OK;
 }
 
+rsw_status rsw_device_topology(int32_t* die_sms, int32_t* probed) {
+  if (!die_sms || !probed) return fail(RSW_ERR_CONFIG, "NULL output pointer");
+  std::lock_guard<std::mutex> lk(g_mu);
+  Workspace* ws = workspace();
+  cudaStream_t st = nullptr;
+  WsGuard wsg(ws, st);
+  if (!wsg.ok) return fail(RSW_ERR_CUDA, "cudaStreamWaitEvent on the workspace event failed");
+  rsw_status s = ensure_arena(ws, std::max(ws->arena_nch, 1), st);
+  if (s != RSW_OK) return s;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  int dev = 0, smc = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&smc, cudaDevAttrMultiProcessorCount, dev));
+  *probed = ws->die_ok ? 1 : 0;
+  die_sms[0] = ws->die_ok ? ws->die_n[0] : smc;
+  die_sms[1] = ws->die_ok ? ws->die_n[1] : 0;
+  return RSW_OK;
+}
+
 rsw_status rsw_check_states(const rsw_params* p, int32_t n_states, const double* u, void* stream) {
   Nvtx nvtx_("rsw_check_states");
   rsw_status s = check_params(p);

@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
   } else {
     // ======================================= fine worker group 0 =======================================
     const int gi = threadIdx.x / TG;
-    fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{gi * TG, 1 + gi, TG, 0, RSW_PIPE_FINE_WSWAP}, smem + LY::F_G + (size_t)gi * 6 * N,
+    fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{gi * TG, 1 + gi, TG, 0, (RSW_PIPE_FINE_WSWAP && TG >= 128) ? 1 : 0}, smem + LY::F_G + (size_t)gi * 6 * N,
                                         ft, tslot + (uint32_t)(gi * LY::CPG), s_task[gi]);
   }
   tmem_fence_before();

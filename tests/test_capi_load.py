@@ -26,7 +26,7 @@ def header_functions():
 def test_exports_every_declared_symbol(lib):
     rsw, L = lib
     names = header_functions()
-    assert len(names) >= 16, names
+    assert len(names) >= 17, names
     for name in names:
         assert hasattr(L, name), name
     assert sorted(rsw.EXPORTS) == names

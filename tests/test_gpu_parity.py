@@ -434,6 +434,18 @@ def test_pipelined_die_placement_bitwise(rsw_gpu, monkeypatch):
           b["stats"]["group_ctas"])
 
 
+def test_device_topology(rsw_gpu):
+    """the die-homing probe splits the SMs into two dies (a B200 is two dies of 74 SMs
+    less the floorswept ones) and finds the page hash on every chunk; the split covers every SM."""
+    import torch
+    t = rsw_gpu.device_topology()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert sum(t["die_sms"]) == sms
+    assert t["probed"], t
+    assert min(t["die_sms"]) >= sms // 3
+    print("dies:", t)
+
+
 def test_check_states_layout(rsw_gpu):
     """§8(b): an input with a non-zero mode k > n/3 (R10) or Im û_0 != 0 (R16) is RSW_ERR_CONFIG —
     through rsw_check_states, through parareal_iterate's own device check of u0, and through the
