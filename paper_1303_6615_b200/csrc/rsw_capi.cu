@@ -1093,6 +1093,14 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     CUDA_TRY(cudaMemcpy(tr.data(), a.trace, sizeof(unsigned long long) * ntr, cudaMemcpyDeviceToHost));
     const double t0 = (double)tr[0];
     auto ms = [&](unsigned long long t) { return t ? (t - t0) * 1e-6 : -1.0; };
+    if (const char* dump = getenv("RSW_PIPE_TRACE_DUMP")) {  // raw timeline (globaltimer ns) for offline analysis
+      if (FILE* f = fopen(dump, "wb")) {
+        const int hdr[4] = {K, S, a.npairs, (int)ntr0};
+        fwrite(hdr, sizeof(int), 4, f);
+        fwrite(tr.data(), sizeof(unsigned long long), ntr0, f);
+        fclose(f);
+      }
+    }
     fprintf(stderr, "[rsw pipe] grid %d NG %d GC %d npairs %d die_aware %d (dies %d/%d, groups %d/%d, arena %d chunks, kmask0 %llx)\n",
             grid, a.NG, a.GC, a.npairs, a.die_aware, ws->die_n[0], ws->die_n[1], a.ndg[0], a.ndg[1], ws->arena_nch,
             ws->kmask0);
