@@ -431,6 +431,9 @@ __device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned targe
 // 8-byte half is single-copy atomic; the reset of ybuf[(u+2)%3] happens after every reader of it
 // (samples phase u-1) passed the release/acquire grid barrier before update u, and it is ordered
 // before any reader of ybuf[(u+2)%3] (samples phase u+2) by the grid barrier after samples u+1.
+#ifndef RSW_POLL_SLEEP_NS
+#define RSW_POLL_SLEEP_NS 0  // back-off of the stage-input poll and the group-barrier spin (0: none)
+#endif
 constexpr unsigned long long YIN_SENTINEL = 0x7FF4DEADBEEF0001ull;  // a signalling-NaN payload arithmetic never produces
 __device__ __forceinline__ double2 ld_relaxed_v2(const double2* p) {
   double2 v;
@@ -497,7 +500,10 @@ __device__ __forceinline__ void coarse_samples_phase(const AX& ax, size_t yoff, 
   for (int i = tid_; i < 3 * Kc; i += T) {
     const double2* yi = ax.y(yoff + i);
     double2 v = ld_relaxed_v2(yi);
-    while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(yi);
+    while (is_sentinel(v.x) || is_sentinel(v.y)) {
+      if (RSW_POLL_SLEEP_NS > 0) __nanosleep(RSW_POLL_SLEEP_NS);  // (spinning warps take issue slots from co-resident ones)
+      v = ld_relaxed_v2(yi);
+    }
     C[i] = v;
   }
   grp.sync();

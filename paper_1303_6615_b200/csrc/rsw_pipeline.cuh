@@ -79,6 +79,7 @@ __device__ __forceinline__ bool group_barrier(unsigned* bar, unsigned P, unsigne
         v = ABORT_BIT;
         break;
       }
+      if (RSW_POLL_SLEEP_NS > 0) __nanosleep(RSW_POLL_SLEEP_NS);
       v = ld_acquire_gpu(bar);
     }
     *s_flag = (v & ABORT_BIT) ? 1u : 0u;
