@@ -973,7 +973,9 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
         return std::min(ws->die_n[0] / gc, rsw::kMaxDieGroups) + std::min(ws->die_n[1] / gc, rsw::kMaxDieGroups) >= a.NG;
       };
       int gc = a.GC;
-      while (gc > 1 && !fits(gc) && rounds(gc - 1) == rounds(a.GC) && (Km + 1 + gc - 2) / (gc - 1) <= 8) --gc;
+      while (gc > 1 && !fits(gc) && rounds(gc - 1) == rounds(a.GC) && (Km + 1 + gc - 2) / (gc - 1) <= 8 &&
+             (pairs + gc - 2) / (gc - 1) <= 8)  // <= 8 owned modes and <= 8 pairs per CTA (PIPE_CFG)
+        --gc;
       if (fits(gc)) a.GC = gc;
     }
     if (aware) {

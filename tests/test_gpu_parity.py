@@ -434,6 +434,22 @@ def test_pipelined_die_placement_bitwise(rsw_gpu, monkeypatch):
           b["stats"]["group_ctas"])
 
 
+def test_pipelined_many_sample_pairs_layout(rsw_gpu):
+    """The paper's eps = 1e-2 experiment's coarse setting (n = 128, M = 450: 225 sample pairs per stage)
+    with 4 iterations on a truncated chain: the layout cost model picks up to 8 pairs per coarse CTA,
+    and the die placement must not shrink the groups past that (PIPE_CFG) — the regression was an
+    invalid launch configuration.  Bitwise equal to bulk."""
+    cfg = inputs.PAPER_EXPERIMENTS["eps1e-2"]
+    p = P(rsw_gpu, cfg["eps"], 1.0, 1e-4, 128)
+    u0 = dev(inputs.paper_initial_state(128))
+    kw = dict(dT=cfg["dT"], dt=cfg["dt"] * 10, T0=cfg["T0"], M=cfg["M"], n_slices=24, max_iters=4, allow_diverged=True)
+    a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
+    assert b["stats"]["pipelined"]
+    assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
+    print("layout:", b["stats"]["coarse_groups"], "x", b["stats"]["group_ctas"], "die_aware", b["stats"]["die_aware"])
+
+
 def test_device_topology(rsw_gpu):
     """the die-homing probe splits the SMs into two dies (a B200 is two dies of 74 SMs
     less the floorswept ones) and finds the page hash on every chunk; the split covers every SM."""
