@@ -988,6 +988,14 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
       }
     }
     a.die_aware = aware ? 1 : 0;
+    // the final layout's kernel (its template depends on the pairs / modes per CTA) must still fit
+    size_t cap2 = 0;
+    const cudaError_t qe2 = rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, 0, &cap2, st);
+    if (qe2 != cudaSuccess || (int)cap2 < grid) {
+      cudaGetLastError();
+      *unsupported = true;
+      return fail(RSW_ERR_CONFIG, "pipelined schedule: the chosen coarse layout does not fit the GPU");
+    }
     if (!aware) {
       a.ndg[0] = (a.NG + 1) / 2;
       a.ndg[1] = a.NG / 2;
