@@ -41,6 +41,9 @@
 #ifndef RSW_PIPE_REUSE_COARSE
 #define RSW_PIPE_REUSE_COARSE 0  // 1: a coarse CTA whose sweeps are done runs an extra fine group (C3: 34.2 -> 34.4 ms, not kept)
 #endif
+#ifndef RSW_PIPE_COARSE_LOW
+#define RSW_PIPE_COARSE_LOW 0  // 1: coarse sub-CTA on the low warps, fine groups on the high ones
+#endif
 #ifndef RSW_PIPE_CLAIM
 #define RSW_PIPE_CLAIM 1  // fine-task claim order: 0 lowest iteration first, 1 oldest ready task first
 #endif
@@ -280,11 +283,14 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
       smem + LY::F_TW, smem + LY::F_CP, reinterpret_cast<double*>(smem + LY::F_D), a.ft, threadIdx.x, TC + NPG * TG);
   __syncthreads();
 
-  constexpr int FT = NPG * TG;  // fine groups take the low warps, the coarse sub-CTA the high ones
-  if ((int)threadIdx.x >= FT) {
+  // fine groups take the low warps and the coarse sub-CTA the high ones (RSW_PIPE_COARSE_LOW = 0), or
+  // the other way round: CB = the coarse sub-CTA's first thread, FB = the first fine group's
+  constexpr int FT = NPG * TG;
+  constexpr int CB = RSW_PIPE_COARSE_LOW ? 0 : FT, FB = RSW_PIPE_COARSE_LOW ? TC : 0;
+  if ((int)threadIdx.x >= CB && (int)threadIdx.x < CB + TC) {
     // ===================================== coarse sub-CTA =====================================
-    const NamedGroup cg{FT, 15, TC};
-    const int ct = (int)threadIdx.x - FT;
+    const NamedGroup cg{CB, 15, TC};
+    const int ct = (int)threadIdx.x - CB;
     // XG more fine groups on the coarse threads (in the coarse region of smem): in a CTA without a coarse
     // role, and in a coarse CTA once its group's sweeps are done (the later iterations' fine tasks are
     // then the bottleneck: each finished group adds GC fine groups)
@@ -292,7 +298,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
       constexpr int XG = TC / TG;
       const int xi = ct / TG;
       if (xi < XG && (NPG + XG) * LY::CPG <= 512)
-        fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{FT + xi * TG, 1 + NPG + xi, TG},
+        fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{CB + xi * TG, 1 + NPG + xi, TG},
                                             smem + LY::C0 + (size_t)xi * 6 * N, ft,
                                             tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi]);
     };
@@ -459,8 +465,8 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
     if (s_role[0] < 0 || RSW_PIPE_REUSE_COARSE) extra_fine();
   } else {
     // ======================================= fine worker group 0 =======================================
-    const int gi = threadIdx.x / TG;
-    fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{gi * TG, 1 + gi, TG, 0, (RSW_PIPE_FINE_WSWAP && TG >= 128) ? 1 : 0}, smem + LY::F_G + (size_t)gi * 6 * N,
+    const int gi = ((int)threadIdx.x - FB) / TG;
+    fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{FB + gi * TG, 1 + gi, TG, 0, (RSW_PIPE_FINE_WSWAP && !RSW_PIPE_COARSE_LOW && TG >= 128) ? 1 : 0}, smem + LY::F_G + (size_t)gi * 6 * N,
                                         ft, tslot + (uint32_t)(gi * LY::CPG), s_task[gi]);
   }
   tmem_fence_before();
