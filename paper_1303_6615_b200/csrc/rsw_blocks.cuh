@@ -13,15 +13,19 @@ namespace rsw {
 // threads rounded up to whole warps.  Plans (passes): 1024 = 4.16.16 at R = 16 (8: 2.8.8.8),
 // 512 = 8.8.8, 256 = 4.8.8, 128 = 2.8.8.  Fine kernel at n = 1024: two 192-thread pair-groups per
 // CTA sharing the tables (fine_groups).  Coarse sweep (latency bound, one sample pair per CTA):
-// radix 8 with 192 threads (the extra threads speed up the mode loops).
+// radix 8 — at n <= 256 with 192 threads (the extra threads speed up the mode loops), at n = 1024 with
+// 384 (four radix-8 passes on twice the warps beat three radix-16 passes: C5 stage 17.1 -> 16.6 us).
 template <int N>
 __host__ __device__ constexpr int fine_radix() { return N <= 32 ? 4 : (N <= 512 ? 8 : 16); }
 template <int N>
 __host__ __device__ constexpr int fine_groups() { return N >= 1024 ? 2 : 1; }
 template <int N, int R>
 __host__ __device__ constexpr int core_threads() { return (3 * (N / R) + 31) / 32 * 32; }
+#ifndef RSW_COARSE_R1024
+#define RSW_COARSE_R1024 8  // radix of the coarse sweep's N-evals at n >= 512: 8 (384 threads at n = 1024) beats 16 (192): C5 stage 17.1 -> 16.6 us
+#endif
 template <int N>
-__host__ __device__ constexpr int coarse_radix() { return N <= 32 ? 4 : N <= 256 ? 8 : 16; }
+__host__ __device__ constexpr int coarse_radix() { return N <= 32 ? 4 : N <= 256 ? 8 : RSW_COARSE_R1024; }
 template <int N>
 __host__ __device__ constexpr int coarse_threads() { return core_threads<N, coarse_radix<N>()>() > 192 ? core_threads<N, coarse_radix<N>()>() : 192; }
 
