@@ -273,13 +273,18 @@ def main():
     measured_peak = rsw.fp64_peak_tflops()
     local_slices = w.n_slices // world
     fine_flops_iter = local_slices * w.m_fine * f_step
-    coarse_flops_sweep = w.n_slices * 4 * (w.M - 1) * f_sample  # averaged RK4: 4 N-bar per coarse step
+    # averaged RK4: 4 N-bar per coarse step, each M-1 samples — or, in triad form, one
+    # contraction with the triad coefficients
+    triad = bool(stats[-1].get("coarse_triad"))
+    f_nbar = rsw.flops_per_unit(w.n, "triad") if triad else (w.M - 1) * f_sample
+    coarse_flops_sweep = w.n_slices * 4 * f_nbar
     if pipelined:
         step_flops = iters * fine_flops_iter + (iters + 1) * coarse_flops_sweep
         kern_ms = ms_max
         roof = {"bound": "alu", "kernel": "k_parareal_pipe (pipelined sweeps + fine solves, 1 launch/step)",
                 "achieved": step_flops / (kern_ms * 1e-3) / 1e12, "flops_per_launch": step_flops,
                 "flops_fine": iters * fine_flops_iter, "flops_coarse": (iters + 1) * coarse_flops_sweep,
+                "coarse_form": "triad (DESIGN §6d)" if triad else "M-sample quadrature",
                 "share_of_step": 1.0}
     else:
         fine_ms = statistics.median(s["fine_ms"] for s in stats) / max(iters, 1)   # per launch

@@ -102,6 +102,21 @@ rsw_status rsw_fine_propagate(const rsw_params* p, int32_t scheme, uint32_t flag
 rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n_states,
                             const double* u_in, double* rhs_out, void* stream);
 
+/* Triad coefficients of N̄ (HOST output).  The paper writes the averaged nonlinear term as
+   a sum over wavenumber triads with interaction coefficients; with Alg.1's quadrature
+   (the same w_m, τ_m as rsw_averaged_rhs) the eigen coordinates (c-, c0, c+) of N̄ are
+     N̄^γ_κ = Σ_{κ1=κ-K}^{K} Σ_{α=±1} Σ_{β=-1,0,1} W^{γαβ}_{κκ1} c^α_{κ1} c^β_{κ-κ1},   κ = 0..K = n/3,
+     W^{γαβ}_{κκ1} = [Σ_{m=1}^{M-1} w_m e^{i(γω_κ - αω_{κ1} - βω_{κ2})τ_m}] C^{γαβ}_{κκ1κ2},
+   in the eigenbasis r^∓ = (∓iω, 1, ia)/(√2ω), r^0 = (0, ia, 1)/ω, a = κ/√F, ω = √(1+a²).
+   The coarse sweeps (rsw_coarse_propagate, parareal_iterate) evaluate N̄ in this form for n <= 256
+   (environment RSW_COARSE_TRIAD=0: the M-sample quadrature instead); rsw_averaged_rhs always uses
+   the quadrature.  Layout of `out` (double[count][2], complex): block κ = 0..K starts at entry
+   18 (κ(2K+1) - κ(κ-1)/2); inside it entry e = (γ+1) 6 + (α > 0) 3 + (β+1) of row i (κ1 = κ - K + i,
+   i = 0..2K-κ) is at e (2K+1-κ) + i.  *count receives the number of complex entries; out may be
+   NULL (size query).  Pure host computation (no GPU needed); RSW_ERR_CONFIG on bad parameters or
+   n > 256. */
+rsw_status rsw_triad_coefficients(const rsw_params* p, double T0, int32_t M, double* out, int64_t* count);
+
 /* Coarse propagator φ̄_ΔT (Alg.2, φ̄ P:415-417) for n_states independent states:
      v = e^{ΔT D̂/2} u;  one RK4 (R6; or midpoint, RSW_COARSE_MIDPOINT) step of size dT on v' = N̄(v);
      v = e^{ΔT D̂/2} v;  G(u) = e^{-(ΔT/ε) L̂} v   (back-transform sign R3).
@@ -145,6 +160,8 @@ typedef struct {
      CTAs sit on one die of the GPU with the group's exchange arrays homed in that die's L2 (probed
      once per workspace) */
   int32_t coarse_groups, group_ctas, die_aware;
+  /* 1: the coarse sweeps evaluated N̄ in triad form (rsw_triad_coefficients), 0: M-sample quadrature */
+  int32_t coarse_triad;
 } rsw_parareal_stats;
 
 /* The asymptotic parareal iteration (Eq. HMM parareal iteration P:428-430; Alg.4):
@@ -216,7 +233,8 @@ rsw_status rsw_comm_destroy(rsw_comm* comm);
 rsw_status rsw_fp64_peak(double* tflops, void* stream);
 
 /* Analytic flop counts per unit of work, for throughput reporting:
-   which = 0: F_N (one N(u)), 1: ETDRK4 step, 2: Strang step, 3: one N̄ sample. */
+   which = 0: F_N (one N(u)), 1: ETDRK4 step, 2: Strang step, 3: one N̄ sample,
+   4: one whole N̄ in triad form (180 flops per (κ, κ1) row: 6 complex products, 18 complex FMAs). */
 double rsw_flops_per_unit(int32_t n, int32_t which);
 
 const char* rsw_last_error(void); /* thread-local; never NULL */

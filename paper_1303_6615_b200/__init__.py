@@ -30,6 +30,7 @@ EXPORTS = [
     "parareal_iterate", "parareal_iterate_ex", "rsw_shard_range", "rsw_nccl_unique_id",
     "rsw_comm_init", "rsw_comm_destroy", "rsw_fp64_peak", "rsw_flops_per_unit", "rsw_last_error",
     "rsw_shutdown", "rsw_check_states", "parareal_resume", "rsw_device_topology",
+    "rsw_triad_coefficients",
 ]
 
 
@@ -57,7 +58,7 @@ class _Stats(ctypes.Structure):
                 ("fine_slice_steps", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
                 ("pipelined", ctypes.c_int32), ("sweep0_ms", ctypes.c_double), ("lag_ms", ctypes.c_double),
                 ("fine_task_ms", ctypes.c_double), ("coarse_groups", ctypes.c_int32),
-                ("group_ctas", ctypes.c_int32), ("die_aware", ctypes.c_int32)]
+                ("group_ctas", ctypes.c_int32), ("die_aware", ctypes.c_int32), ("coarse_triad", ctypes.c_int32)]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -89,6 +90,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.rsw_fine_propagate.argtypes = [P, i32, u32, dbl, dbl, i32, dp, dp, vp]
     L.rsw_averaged_rhs.argtypes = [P, dbl, i32, i32, dp, dp, vp]
     L.rsw_coarse_propagate.argtypes = [P, i32, dbl, dbl, i32, i32, dp, dp, vp]
+    L.rsw_triad_coefficients.argtypes = [P, dbl, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
     L.parareal_iterate.argtypes = [P, ctypes.POINTER(_PararealConfig), dp, dp,
                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32), vp, vp]
     L.parareal_iterate_ex.argtypes = L.parareal_iterate.argtypes + [dp, dp, ctypes.POINTER(_Stats)]
@@ -185,6 +187,18 @@ def averaged_rhs(p: Params, u, T0: float, M: int, validate: bool = True):
     return out
 
 
+def triad_coefficients(p: Params, T0: float, M: int):
+    """Triad coefficients W of N̄ (host computation; rsw.h rsw_triad_coefficients) as a
+    complex numpy array in the library's block layout."""
+    import numpy as np
+    cnt = ctypes.c_int64(0)
+    _check(load().rsw_triad_coefficients(ctypes.byref(p._c()), T0, M, None, ctypes.byref(cnt)))
+    out = np.empty(2 * cnt.value, dtype=np.float64)
+    _check(load().rsw_triad_coefficients(ctypes.byref(p._c()), T0, M,
+                                         out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(cnt)))
+    return out[0::2] + 1j * out[1::2]
+
+
 def coarse_propagate(p: Params, u, dT: float, T0: float, M: int, scheme: int = COARSE_RK4, validate: bool = True):
     """G for a batch of states (Alg.2; R3, R6)."""
     import torch
@@ -271,7 +285,8 @@ def parareal_iterate(p: Params, u0, *, dT, dt, T0, M, n_slices, max_iters, tol=0
                           total_ms=st.total_ms, fine_slice_steps=st.fine_slice_steps,
                           kernel_launches=st.kernel_launches, pipelined=bool(st.pipelined),
                           sweep0_ms=st.sweep0_ms, lag_ms=st.lag_ms, fine_task_ms=st.fine_task_ms,
-                          coarse_groups=st.coarse_groups, group_ctas=st.group_ctas, die_aware=bool(st.die_aware)))
+                          coarse_groups=st.coarse_groups, group_ctas=st.group_ctas, die_aware=bool(st.die_aware),
+                          coarse_triad=bool(st.coarse_triad)))
     if want_FG:
         out["F"], out["G"] = F, G
     return out
@@ -317,4 +332,4 @@ def fp64_peak_tflops() -> float:
 
 
 def flops_per_unit(n: int, which: str) -> float:
-    return load().rsw_flops_per_unit(n, dict(nonlinear=0, etdrk4=1, strang=2, sample=3)[which])
+    return load().rsw_flops_per_unit(n, dict(nonlinear=0, etdrk4=1, strang=2, sample=3, triad=4)[which])

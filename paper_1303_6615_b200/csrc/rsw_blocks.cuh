@@ -588,23 +588,165 @@ __device__ __forceinline__ void coarse_samples_phase(const AX& ax, size_t yoff, 
 #undef STAMP
 }
 
+// ---------------------------------------------------------------------------------------------
+// Triad form of the averaged nonlinearity (round 2).  The paper writes the averaged nonlinear term as
+// a sum over wavenumber triads (Eq. "nonlinear term for average, RSW"):
+//   [e^{sL} N(e^{-sL} u)]_κ^γ = Σ_{κ1+κ2=κ} Σ_{α,β} e^{i(ω^γ_κ - ω^α_κ1 - ω^β_κ2)s} C^{γαβ}_{κκ1κ2} u^α_κ1 u^β_κ2,
+// so the M-sample average of Alg.1 is the same bilinear form with the coefficient
+//   W^{γαβ}_{κκ1} = Φ(γω_κ - αω_κ1 - βω_κ2) C^{γαβ}_{κκ1κ2},   Φ(λ) = Σ_{m=1}^{M-1} w_m e^{iλτ_m}
+// — exactly the quadrature sum (no resonance truncation: every triad is kept with its quadrature
+// weight).  The dealiased pseudo-spectral product is an exact convolution (|κ1|, |κ2| <= K = n/3), and
+// the first factor of every product of N (u u_x = (u²/2)_x, u v_x, (h u)_x) is u, whose eigen expansion
+// has no α = 0 part, so α ranges over {-1, +1}: 18 coefficients per (κ, κ1).  The host builds W once
+// per configuration (rsw_capi.cu build_triad); table layout, double2 units: block κ = 0..K at
+// TRIAD_E * triad_rows_before(κ), inside it entry e = (γ+1)*6 + (α>0)*3 + (β+1) of row i at e*nk + i,
+// row i <-> κ1 = κ - K + i, κ2 = K - i, nk = 2K + 1 - κ rows.  One N̄ evaluation costs 96 DP
+// instructions per (κ, κ1) — for C3 ~1.1 M per stage instead of 64 pair N-evals — and needs no
+// cross-CTA reduction: the CTA that owns κ computes N̄_κ whole.
+// ---------------------------------------------------------------------------------------------
+// TRIAD_E, triad_nk, triad_rows_before, triad_local_entries: rsw_internal.h
+template <int N, int NOWN>
+__device__ __forceinline__ void triad_stage_table(const double2* __restrict__ Wg, double2* Wl, int rank, int P, int tid,
+                                                  int nthr) {
+  constexpr int K = N / 3;
+  size_t lo = 0;
+  for (int o = 0; o < NOWN; ++o) {
+    const int kap = rank + o * P;
+    if (kap > K) break;
+    const size_t cnt = (size_t)TRIAD_E * triad_nk(kap, K);
+    const double2* src = Wg + (size_t)TRIAD_E * triad_rows_before(kap, K);
+    for (size_t i = tid; i < cnt; i += nthr) Wl[lo + i] = __ldg(src + i);
+    lo += cnt;
+  }
+}
+
+// Stage-input ring of the triad sweeps: no barrier separates a stage's reads of its input from the
+// owners' next writes, so the ring is deeper (TRIAD_NB buffers) and publication u resets the buffer of
+// stage u - NB/2: every reader of it is done (publishing u needs all of input u-1, i.e. every owner
+// published u-1, which it did after reading input u-2), and the next writer of it (stage u + NB/2)
+// acted on input u + NB/2 - 1, published after a fence that follows this reset (the resetting
+// threads fence after every odd publication).  TRIAD_NB: rsw_internal.h.
+
+// One RK stage's N̄ in triad form: poll the stage input y (ring buffer at yoff) into C, then for each
+// owned |κ| = rank + o P the 3 eigen entries γ of N̄_κ (coefficients from the shared-memory copy Wl, or
+// — Wl null, the copy does not fit next to the kernel's other buffers — from the global table Wg); the -κ entries by the real-field symmetry
+// N̄^γ_{-κ} = conj N̄^{-γ}_κ (the eigenbasis of -κ is the conjugate of +κ's with α reversed).  Fixed
+// summation order, independent of T, P and the warp that runs an item: for half h in {0, 1} lane l
+// sums rows i ≡ 32h + l (mod 64) in ascending i, a fixed xor tree sums the 32 lanes, then
+// N̄ = half 0 + half 1 — so the bulk and pipelined sweeps agree bitwise.  stopk (pipelined schedule):
+// the poll gives up once the run stopped before iteration kself, or the watchdog fired; returns true
+// then (the whole group takes the same decision on its own, every wait of a discarded sweep aborts).
+template <int N, int T, int NOWN, class GRP = CtaGroup, class AX = FlatX>
+__device__ __forceinline__ bool triad_stage_phase(const AX& ax, size_t yoff, const double2* Wl, const double2* Wg,
+                                                  double2* C, double2* hp,
+                                                  double2* kk, int rank, int P, const GRP& grp,
+                                                  const int* stopk = nullptr, int kself = 0, unsigned* wd = nullptr,
+                                                  const unsigned* hb = nullptr) {
+  constexpr int K = N / 3, Kc = 2 * K + 1;
+  const int tid_ = grp.tid();
+  bool ab = false;
+  for (int i = tid_; i < 3 * Kc; i += T) {
+    const double2* yi = ax.y(yoff + i);
+    double2 v = ld_relaxed_v2(yi);
+    if (stopk && (is_sentinel(v.x) || is_sentinel(v.y))) {
+      Watch w = watch_start(hb);
+      for (unsigned it = 0; is_sentinel(v.x) || is_sentinel(v.y); ++it) {
+        if ((it & 255) == 255 && (*(volatile const int*)stopk < kself || watchdog_expired(w, wd, hb))) {
+          ab = true;
+          break;
+        }
+        v = ld_relaxed_v2(yi);
+      }
+      if (ab) break;
+    } else {
+      while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(yi);
+    }
+    C[i] = v;
+  }
+  if (stopk) {
+    if (grp.sync_or(ab)) return true;
+  } else {
+    grp.sync();
+  }
+  const int lane = tid_ & 31;
+  for (int it = tid_ >> 5; it < 2 * NOWN; it += T / 32) {
+    const int o = it >> 1, hh = it & 1, kap = rank + o * P;
+    if (kap > K) continue;  // (warp-uniform)
+    const int nk = triad_nk(kap, K);
+    // coefficient block: the CTA's shared-memory copy (Wl), or the global table when it did not fit
+    const double2* Wb;
+    if (Wl) {
+      size_t lo = 0;
+      for (int q = 0; q < o; ++q) lo += (size_t)TRIAD_E * triad_nk(rank + q * P, K);
+      Wb = Wl + lo;
+    } else {
+      Wb = Wg + (size_t)TRIAD_E * triad_rows_before(kap, K);
+    }
+    double2 acc[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    for (int i = 32 * hh + lane; i < nk; i += 64) {
+      const int k1 = kap - K + i, k2 = K - i;
+      const int j1 = k1 >= 0 ? k1 : k1 + Kc, j2 = k2 >= 0 ? k2 : k2 + Kc;
+      const double2 am = C[j1], ap = C[2 * Kc + j1];
+      double2 pr[6];
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const double2 yb = C[b * Kc + j2];
+        pr[b] = make_double2(fma(am.x, yb.x, -am.y * yb.y), fma(am.x, yb.y, am.y * yb.x));
+        pr[3 + b] = make_double2(fma(ap.x, yb.x, -ap.y * yb.y), fma(ap.x, yb.y, ap.y * yb.x));
+      }
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {
+#pragma unroll
+        for (int ab2 = 0; ab2 < 6; ++ab2) {
+          const double2 wv = Wb[(size_t)(g * 6 + ab2) * nk + i];
+          acc[g].x = fma(wv.x, pr[ab2].x, fma(-wv.y, pr[ab2].y, acc[g].x));
+          acc[g].y = fma(wv.x, pr[ab2].y, fma(wv.y, pr[ab2].x, acc[g].y));
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 3; ++g)
+      for (int w = 16; w > 0; w >>= 1) {
+        acc[g].x += __shfl_xor_sync(0xffffffffu, acc[g].x, w);
+        acc[g].y += __shfl_xor_sync(0xffffffffu, acc[g].y, w);
+      }
+    if (lane == 0)
+#pragma unroll
+      for (int g = 0; g < 3; ++g) hp[(o * 2 + hh) * 3 + g] = acc[g];
+  }
+  grp.sync();
+  if (tid_ < NOWN * 3) {
+    const int o = tid_ / 3, g = tid_ % 3, kap = rank + o * P;
+    if (kap <= K) {
+      const double2 v = cadd(hp[(o * 2) * 3 + g], hp[(o * 2 + 1) * 3 + g]);
+      kk[o * 6 + g] = v;
+      kk[o * 6 + 3 + (2 - g)] = cconj(v);
+    }
+  }
+  return false;
+}
+
 // phase 2 of one RK stage, thread-parallel over the CTA's owned modes |κ| = b + o P (o < NOWN):
 // items i = o*6 + e, entries e = (α, +κ) for e < 3, (α, -κ) for e >= 3.  The stage base v and the RK
 // accumulator ks of owned modes live in this CTA's shared memory for the whole sweep; the stage
 // input y is published to global memory for the samples phase of every CTA.
-template <int N, int NOWN, int T, class GRP = CtaGroup, class AX = FlatX>
+// NB = 3: the quadrature sweeps' triple buffer (reset of the previous stage's buffer, ordered by the
+// stage's barrier); NB = TRIAD_NB: the triad sweeps' ring (reset NB/2 stages back, fenced; see above)
+template <int N, int NOWN, int T, class GRP = CtaGroup, class AX = FlatX, int NB = 3>
 __device__ __forceinline__ void push_stage_input(const AX& ax, const double2* yv, const int* yidx, unsigned u,
                                                  const GRP& grp = GRP()) {
   const int tid_ = grp.tid();
   constexpr int Kc3 = 3 * (2 * (N / 3) + 1);
+  constexpr unsigned RB = NB == 3 ? 2u : (unsigned)(NB / 2);  // buffer reset: (u + RB) % NB
   grp.sync();
   if (tid_ < NOWN * 6 && yidx[tid_] >= 0) {
-    st_relaxed_v2(ax.y((size_t)(u % 3) * Kc3 + yidx[tid_]), yv[tid_]);
-    st_relaxed_v2(ax.y((size_t)((u + 2) % 3) * Kc3 + yidx[tid_]), yin_sentinel());
+    st_relaxed_v2(ax.y((size_t)(u % NB) * Kc3 + yidx[tid_]), yv[tid_]);
+    st_relaxed_v2(ax.y((size_t)((u + RB) % NB) * Kc3 + yidx[tid_]), yin_sentinel());
+    if (NB != 3 && (u & 1u)) __threadfence();
   }
 }
 
-template <int N, int T, int NOWN, class GRP = CtaGroup, class AX = FlatX>
+template <int N, int T, int NOWN, class GRP = CtaGroup, class AX = FlatX, bool TRIAD = false>
 __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const AX& ax, int stage, int n, double2* Vs,
                                                     double2* KSs, double2* kk, double2* un_s, double* nd_s,
                                                     double2* red_buf, double2* yv, int* yidx, unsigned ucount,
@@ -642,6 +784,7 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
   }
   USTAMP(1)
   if (stage > 0) {
+    if constexpr (!TRIAD) {
     // deterministic reduction of the per-pair partials in a fixed order that depends only on the number
     // of partials (not on the CTA size or the owned-mode count, so every schedule agrees bitwise): RQ
     // lanes per item, lane q sums partials q, q+RQ, ... ascending, then a fixed xor tree over the RQ
@@ -701,6 +844,7 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
     }
     USTAMP(9)
 #endif
+    }  // !TRIAD (the triad stage phase wrote kk whole)
     grp.sync();
     USTAMP(3)
     if (tid_ < NOWN * 6) {
@@ -737,7 +881,7 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
     }
     USTAMP(4)
     if (!last) {
-      push_stage_input<N, NOWN, T>(ax, yv, yidx, ucount, grp);
+      push_stage_input<N, NOWN, T, GRP, AX, TRIAD ? TRIAD_NB : 3>(ax, yv, yidx, ucount, grp);
       USTAMP(5)
       return;
     }
@@ -816,7 +960,7 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
     }
   }
   USTAMP(7)
-  push_stage_input<N, NOWN, T>(ax, yv, yidx, ucount, grp);
+  push_stage_input<N, NOWN, T, GRP, AX, TRIAD ? TRIAD_NB : 3>(ax, yv, yidx, ucount, grp);
   grp.sync();
   USTAMP(8)
 #undef USTAMP

@@ -117,11 +117,16 @@ struct CoarseTables {
   DevBuf dhalf, back;
 };
 
+struct TriadTables {
+  DevBuf W;
+};
+
 std::mutex g_mu;
 std::map<std::tuple<int, int, double>, std::unique_ptr<GeomTables>> g_geom;  // (dev, n, F)
 std::map<std::tuple<int, int, double, double, double, double>, std::unique_ptr<FineTables>> g_fine;
 std::map<std::tuple<int, int, double, double, double, int>, std::unique_ptr<AvgTables>> g_avg;
 std::map<std::tuple<int, int, double, double, double, double>, std::unique_ptr<CoarseTables>> g_coarse;
+std::map<std::tuple<int, int, double, double, double, int>, std::unique_ptr<TriadTables>> g_triad;
 
 int cur_dev() {
   int d = 0;
@@ -235,6 +240,101 @@ cudaError_t get_avg(const rsw_params* p, double T0, int M, AvgTables** out) {
   if ((e = upload(t->w, w)) || (e = upload(t->phase, ph))) return e;
   *out = t.get();
   g_avg[key] = std::move(t);
+  return cudaSuccess;
+}
+
+// Triad coefficients of N̄ (rsw_blocks.cuh; P:1113-1118 with Alg.1's quadrature):
+//   W^{γαβ}_{κκ1} = Φ(γω_κ - αω_κ1 - βω_κ2) Σ_f B_γf(κ) h_f A_0α(κ1) A_fβ(κ2),   κ2 = κ - κ1,
+//   Φ(λ) = Σ_{m=1}^{M-1} w_m e^{iλτ_m}  (w_m, τ_m = T0 m/(M ε) as get_avg; e^{iλτ} from the phase values),
+// with the maps of the pseudo-spectral N (rsw_device.cuh put_input_eigen / eigen_from_raw): FFT inputs
+// X0 = u = i s (c+ - c-), X1 = iκ v = iκ p (c+ + c-) - κ a q c0, X2 = h = q c0 + i a p (c+ + c-);
+// grid products h_f X0 X_f with h = (1/2, 1, 1) (u u_x = (u²/2)_x); outputs
+// N̄^∓ = ±sκ Z0 - p Z1 - p a κ Z2, N̄^0 = i q a Z1 - i q κ Z2  (a = κ/√F signed, p = 1/(√2ω), q = 1/ω).
+// Layout: block κ = 0..K at 18 triad_rows_before(κ), entry e = (γ+1)6 + (α>0)3 + (β+1) of row i at
+// e nk + i, row i <-> κ1 = κ - K + i.
+void build_triad(const rsw_params* p, double T0, int M, std::vector<double2>& Wout) {
+  const int n = p->n, K = n / 3;
+  const double s = std::sqrt(0.5), sF = std::sqrt(p->F);
+  std::vector<double> w(M, 0.0);
+  double tot = 0.0;
+  for (int m = 1; m <= M - 1; ++m) {
+    const double sm = double(m) / M;
+    w[m] = std::exp(-1.0 / (sm * (1.0 - sm)));
+    tot += w[m];
+  }
+  for (int m = 1; m <= M - 1; ++m) w[m] /= tot;
+  // e^{iω_k τ_m}, k = 0..K, m = 1..M-1
+  std::vector<cd> ph((size_t)M * (K + 1));
+  for (int m = 1; m <= M - 1; ++m) {
+    const double tau = (T0 * double(m) / double(M)) / p->eps;
+    for (int k = 0; k <= K; ++k) {
+      const double a = double(k) / sF, om = std::sqrt(1.0 + a * a);
+      ph[(size_t)m * (K + 1) + k] = cd(std::cos(om * tau), std::sin(om * tau));
+    }
+  }
+  const size_t rows = (size_t)rsw::triad_rows_before(K + 1, K);
+  Wout.assign(rows * rsw::TRIAD_E, make_double2(0.0, 0.0));
+  const cd I(0.0, 1.0);
+  std::vector<cd> e1(M), e2(M), e3(M);
+  for (int kap = 0; kap <= K; ++kap) {
+    const int nk = rsw::triad_nk(kap, K);
+    double2* blk = Wout.data() + (size_t)rsw::TRIAD_E * rsw::triad_rows_before(kap, K);
+    const double a = kap / sF, om = std::sqrt(1.0 + a * a), pp = 1.0 / (std::sqrt(2.0) * om), q = 1.0 / om;
+    const cd B[3][3] = {{s * kap, -pp, -pp * a * kap}, {0.0, I * q * a, -I * q * double(kap)}, {-s * kap, -pp, -pp * a * kap}};
+    for (int i = 0; i < nk; ++i) {
+      const int k1 = kap - K + i, k2 = K - i, ak1 = std::abs(k1), ak2 = std::abs(k2);
+      const double a2 = k2 / sF, om2 = std::sqrt(1.0 + a2 * a2), p2 = 1.0 / (std::sqrt(2.0) * om2), q2 = 1.0 / om2;
+      const cd A0[2] = {-I * s, I * s};                                        // α = -1, +1
+      const cd A[3][3] = {{-I * s, 0.0, I * s},                                // X0: β = -1, 0, +1
+                          {I * double(k2) * p2, -double(k2) * a2 * q2, I * double(k2) * p2},  // X1
+                          {I * a2 * p2, q2, I * a2 * p2}};                     // X2
+      const double h[3] = {0.5, 1.0, 1.0};
+      for (int g = 0; g < 3; ++g)
+        for (int ai = 0; ai < 2; ++ai)
+          for (int b = 0; b < 3; ++b) {
+            cd T = 0.0;
+            for (int f = 0; f < 3; ++f) T += B[g][f] * h[f] * A0[ai] * A[f][b];
+            // Φ: e^{i(γω_κ - αω_κ1 - βω_κ2)τ_m} = P(κ)^γ P(κ1)^{-α} P(κ2)^{-β}
+            cd Phi = 0.0;
+            const int gam = g - 1, al = ai ? 1 : -1, be = b - 1;
+            for (int m = 1; m <= M - 1; ++m) {
+              const cd* P = ph.data() + (size_t)m * (K + 1);
+              cd e = 1.0;
+              if (gam) e *= gam > 0 ? P[kap] : std::conj(P[kap]);
+              e *= al > 0 ? std::conj(P[ak1]) : P[ak1];
+              if (be) e *= be > 0 ? std::conj(P[ak2]) : P[ak2];
+              Phi += w[m] * e;
+            }
+            const cd v = Phi * T;
+            blk[(size_t)(g * 6 + ai * 3 + b) * nk + i] = make_double2(v.real(), v.imag());
+          }
+    }
+  }
+}
+
+// the triad form runs where its coefficient blocks fit a CTA's shared memory (n <= 256) unless
+// RSW_COARSE_TRIAD=0 selects the M-sample quadrature
+bool triad_enabled(int n) {
+  const char* e = getenv("RSW_COARSE_TRIAD");
+  return n <= 256 && !(e && e[0] == '0');
+}
+
+cudaError_t get_triad(const rsw_params* p, double T0, int M, const double2** out) {
+  *out = nullptr;
+  if (!triad_enabled(p->n)) return cudaSuccess;
+  auto key = std::make_tuple(cur_dev(), p->n, p->eps, p->F, T0, M);
+  auto it = g_triad.find(key);
+  if (it != g_triad.end()) {
+    *out = (const double2*)it->second->W.p;
+    return cudaSuccess;
+  }
+  std::vector<double2> W;
+  build_triad(p, T0, M, W);
+  auto t = std::make_unique<TriadTables>();
+  cudaError_t e;
+  if ((e = upload(t->W, W))) return e;
+  *out = (const double2*)t->W.p;
+  g_triad[key] = std::move(t);
   return cudaSuccess;
 }
 
@@ -377,6 +477,7 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   ch.M = M;
   ch.dT = dT;
   ch.at = rsw::AvgTab{geom_of(g), (const double*)at->w.p, (const double2*)at->phase.p, (const double2*)g->tw.p};
+  CUDA_TRY(get_triad(p, T0, M, &ch.at.triad));
   rsw::CoarseArgs& ca = ch.ca;
   ca.g = geom_of(g);
   ca.part = nullptr;  // (the sweep's partials and stage inputs live in the die-homed arena)
@@ -508,7 +609,7 @@ rsw_status run_chain(const Chain& ch, Workspace* ws, double* r_out, cudaStream_t
   pl.arena[1] = rsw::HomedArena{ws->arena_base, ~ws->kmask0, 0};
   pl.bpage = 0;
   pl.ypage = 1;
-  pl.ppage = 1 + (3u * 3u * (2u * (unsigned)(ch.p->n / 3) + 1u) + 255u) / 256u;
+  pl.ppage = 1 + rsw::yin_pages(ch.p->n);
   pl.die_ok = ws->die_ok ? 1 : 0;
   pl.die_n[0] = ws->die_n[0];
   pl.die_n[1] = ws->die_n[1];
@@ -692,6 +793,7 @@ double rsw_flops_per_unit(int32_t n, int32_t which) {
     case 1: return 4.0 * FN + 180.0 * Kr;
     case 2: return 2.0 * FN + 52.0 * Kr;
     case 3: return FN + 40.0 * Kr;
+    case 4: return 180.0 * (double)rsw::triad_rows_before(n / 3 + 1, n / 3);
     default: return 0.0;
   }
 }
@@ -792,6 +894,22 @@ rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n
   return RSW_OK;
 }
 
+rsw_status rsw_triad_coefficients(const rsw_params* p, double T0, int32_t M, double* out, int64_t* count) {
+  rsw_status s = check_params(p);
+  if (s != RSW_OK) return s;
+  if (p->n > 256) return fail(RSW_ERR_CONFIG, "triad coefficients: n must be <= 256");
+  if (!finite_pos(T0)) return fail(RSW_ERR_CONFIG, "T0 must be finite and > 0");
+  if (M < 2) return fail(RSW_ERR_CONFIG, "M must be >= 2");
+  if (!count) return fail(RSW_ERR_CONFIG, "NULL count");
+  const int K = p->n / 3;
+  *count = (int64_t)rsw::TRIAD_E * rsw::triad_rows_before(K + 1, K);
+  if (!out) return RSW_OK;
+  std::vector<double2> W;
+  build_triad(p, T0, M, W);
+  std::memcpy(out, W.data(), sizeof(double2) * W.size());
+  return RSW_OK;
+}
+
 rsw_status rsw_coarse_propagate(const rsw_params* p, int32_t coarse_scheme, double dT, double T0, int32_t M,
                                 int32_t n_states, const double* u_in, double* u_out, void* stream) {
   Nvtx nvtx_("rsw_coarse_propagate");
@@ -857,6 +975,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   rsw::PipeArgs a{};
   a.ft = rsw::FineTab{geom_of(g), (const double2*)ft->cp.p, (const double*)ft->c0.p, (const double2*)g->tw.p};
   a.at = rsw::AvgTab{geom_of(g), (const double*)at->w.p, (const double2*)at->phase.p, (const double2*)g->tw.p};
+  CUDA_TRY(get_triad(p, cfg->T0, M, &a.at.triad));
   a.base.g = geom_of(g);
   a.base.scheme = cfg->coarse_scheme;
   a.base.dT = cfg->dT;
@@ -928,13 +1047,25 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
       a.GC = best_gc;
     }
   }
+  const char* en = getenv("RSW_PIPE_NG");
+  if (a.at.triad && !eg) {
+    // triad sweeps: a stage costs one hand-off plus the owned N̄ (~ owned modes x rows), no
+    // sample rounds; NG concurrent sweeps (default 3: sweep g + 3 starts after sweep g ends, which is
+    // before the fine lags would let it start anyway) of the largest GC that fits them on the dies
+    const int ngw = std::max(1, std::min(en ? atoi(en) : 3, K + 1));
+    int gc = std::max(1, grid / ngw);
+    if (ws->die_ok && grid == ws->die_n[0] + ws->die_n[1] && !getenv("RSW_NO_DIE_AWARE"))
+      while (gc > 1 && std::min(ws->die_n[0] / gc, rsw::kMaxDieGroups) + std::min(ws->die_n[1] / gc, rsw::kMaxDieGroups) < ngw) --gc;
+    a.GC = std::max(gc, (Km + 1 + 7) / 8);  // <= 8 owned modes per CTA
+  }
+  const int ng_triad = (a.at.triad && !eg && !en) ? std::max(1, std::min(3, K + 1)) : 0;
   if (a.GC > grid) {
     *unsupported = true;
     return fail(RSW_ERR_CONFIG, "pipelined schedule: not enough co-resident CTAs");
   }
   int ng = grid / a.GC;
-  const char* en = getenv("RSW_PIPE_NG");
   if (en) ng = atoi(en);
+  if (ng_triad) ng = ng_triad;
   a.NG = std::max(1, std::min(std::min(ng, K + 1), grid / a.GC));
   // buffers
   const size_t nU = (size_t)(K + 1) * (S + 1) * L, nG = (size_t)(K + 1) * S * L, nF = (size_t)std::max(K, 1) * S * L;
@@ -948,7 +1079,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   // the coarse groups' exchange arrays in die-homed pages: per group a barrier page, the
   // stage-input pages and the partial pages; arena sized for every group on one die (worst case)
   {
-    const unsigned Kc3 = 3u * Kc, YP = (3 * Kc3 + 255) / 256, PP = ((unsigned)std::max(M / 2, 1) * Kc3 + 255) / 256;
+    const unsigned Kc3 = 3u * Kc, YP = rsw::yin_pages(n), PP = ((unsigned)std::max(M / 2, 1) * Kc3 + 255) / 256;
     const size_t GP = 1 + YP + PP;
     const int nch = (int)((GP * a.NG + 255) / 256);
     if (nch > 64) {
@@ -964,7 +1095,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     // die-aware placement needs one CTA on every SM (then each die holds exactly die_n[d] CTAs) and
     // room for every group on the two dies
     bool aware = ws->die_ok && grid == smc && !getenv("RSW_NO_DIE_AWARE");
-    if (aware && !eg) {
+    if (aware && !eg && !a.at.triad) {
       // shrink the groups (same sample rounds per stage) until NG of them fit on the two dies, e.g. C3 on a
       // 70 / 78 SM split: 24 -> 23 CTAs per group
       const int pairs = std::max(M / 2, 1);
@@ -988,6 +1119,12 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
       }
     }
     a.die_aware = aware ? 1 : 0;
+    if (a.at.triad) {  // shared memory of the largest owned-block copy of the triad coefficients
+      const int nown = (Km + 1 + a.GC - 1) / a.GC;
+      size_t mx = 0;
+      for (int c = 0; c < a.GC; ++c) mx = std::max(mx, rsw::triad_local_entries(Km, c, a.GC, nown));
+      a.wsm = sizeof(double2) * mx;
+    }
     // the final layout's kernel (its template depends on the pairs / modes per CTA) must still fit
     size_t cap2 = 0;
     const cudaError_t qe2 = rsw::launch_parareal_pipe(n, a, cfg->fine_scheme, 0, &cap2, st);
@@ -1204,6 +1341,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     stats->coarse_groups = a.NG;
     stats->group_ctas = a.GC;
     stats->die_aware = a.die_aware;
+    stats->coarse_triad = a.at.triad ? 1 : 0;
   }
   if (kout >= 1 && (!std::isfinite(res[kout]) || res[kout] > 1e6))
     return fail(RSW_ERR_DIVERGED, "parareal residual non-finite or > 1e6");
@@ -1451,6 +1589,7 @@ static rsw_status parareal_impl(const rsw_params* p, const parareal_config* cfg,
     stats->coarse_groups = 1;
     stats->group_ctas = 0;
     stats->die_aware = ws->sweep_die >= 0 ? 1 : 0;
+    stats->coarse_triad = (cfg->coarse_scheme != RSW_COARSE_STRANG && triad_enabled(p->n)) ? 1 : 0;
   }
   if (status == RSW_NOT_CONVERGED) g_err = "parareal: tolerance not reached within max_iters";
   return status;

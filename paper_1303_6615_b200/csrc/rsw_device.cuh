@@ -244,6 +244,7 @@ struct CtaGroup {
   __device__ __forceinline__ int base() const { return 0; }
   __device__ __forceinline__ int tid() const { return threadIdx.x; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ bool sync_or(bool p) const { return __syncthreads_or(p) != 0; }
   __device__ __forceinline__ int fbar() const { return 1; }  // ids 1..3 (kernels whose whole CTA is one group)
   __device__ __forceinline__ int ftid() const { return threadIdx.x; }
 };
@@ -262,6 +263,16 @@ struct NamedGroup {
     return (wsw && (t >> 6) == 1) ? (t ^ 32) : t;
   }
   __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory"); }
+  // barrier that also ORs a predicate over the group's threads
+  __device__ __forceinline__ bool sync_or(bool p) const {
+    unsigned r;
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n bar.red.or.pred q, %2, %3, q;\n selp.u32 %0, 1, 0, q;\n}"
+        : "=r"(r)
+        : "r"((unsigned)p), "r"(id), "r"(nthr)
+        : "memory");
+    return r != 0;
+  }
   __device__ __forceinline__ int fbar() const { return fb; }
 };
 

@@ -25,6 +25,7 @@ struct AvgTab {
   const double* w;
   const double2* phase;
   const double2* tw;
+  const double2* triad = nullptr;  // triad coefficients W (rsw_blocks.cuh), or null: the M-sample quadrature
 };
 
 // Arguments of the coarse combine kernel (one state chain)
@@ -59,6 +60,27 @@ struct CoarseArgs {
 };
 
 constexpr int kMaxPeers = 8;  // ranks of one NVSwitch node
+// stage-input ring depth of the triad coarse sweeps (rsw_blocks.cuh); the exchange arrays always hold
+// this many stage-input buffers (the quadrature sweeps use the first three)
+constexpr int TRIAD_NB = 8;
+__host__ __device__ constexpr unsigned yin_pages(int n) { return (TRIAD_NB * 3u * (2u * (unsigned)(n / 3) + 1u) + 255u) / 256u; }
+
+// triad coefficient table of N̄ (rsw_blocks.cuh triad_stage_phase, rsw_capi.cu build_triad)
+constexpr int TRIAD_E = 18;
+__host__ __device__ constexpr int triad_nk(int kap, int K) { return 2 * K + 1 - kap; }
+__host__ __device__ constexpr long long triad_rows_before(int kap, int K) {
+  return (long long)kap * (2 * K + 1) - (long long)kap * (kap - 1) / 2;
+}
+// double2 entries of the owned blocks of rank (κ = rank + o P, o < nown) — the CTA's shared-memory copy
+__host__ __device__ inline size_t triad_local_entries(int K, int rank, int P, int nown) {
+  size_t s = 0;
+  for (int o = 0; o < nown; ++o) {
+    const int kap = rank + o * P;
+    if (kap > K) break;
+    s += (size_t)TRIAD_E * triad_nk(kap, K);
+  }
+  return s;
+}
 
 // L2 die homing.  A B200 is two dies, each with its own L2; every 4 KB page of device
 // memory is homed on one of them, and a flag / data hand-off between two SMs is about twice as fast
@@ -130,6 +152,7 @@ struct PipeArgs {
   int ndg[2];
   signed char dg[2][kMaxDieGroups];  // group id of slot i on die d
   unsigned* dticket;                 // [2]
+  size_t wsm;                        // triad sweeps (at.triad != null): shared-memory bytes of the largest owned-block copy
 };
 bool pipeline_supported(int n);
 cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);

@@ -30,9 +30,13 @@ static cudaError_t set_smem(KernelT k, size_t bytes) {
 struct SweepRun {
   SweepPlace pl;
   int die, P;
+  size_t wsm;  // triad sweeps: shared-memory bytes of the owned-block copy (0: read the global table)
 };
 
-template <int N, int R, int T, int NOWN>
+// TRIAD: N̄ in triad form (rsw_blocks.cuh triad_stage_phase): each CTA keeps the coefficient blocks of its
+// owned modes in shared memory (after the layout's LY::bytes), a stage is poll -> owned N̄ -> update with
+// no grid barrier (stage-input ring of TRIAD_NB buffers)
+template <int N, int R, int T, int NOWN, bool TRIAD = false>
 __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const AvgTab tab, int M, const SweepRun sr,
                                                     double* r_out) {
   using LY = CoarseLayout<N, R, T, NOWN>;
@@ -75,8 +79,12 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   double* GQ = sd + LY::GQ;
   double* SW = sd + LY::SW;       // [2]
   // per-CTA constants for the whole sweep: geometry, twiddles, and the phases / weights of this
-  // CTA's sample pair
-  fill_packed_twiddles<N, R, T>(TW, tab.tw);
+  // CTA's sample pair (TRIAD: the coefficient blocks of the owned modes)
+  double2* Wl = sr.wsm ? smem + (LY::bytes + 15) / 16 : nullptr;  // (null: read the global table)
+  if constexpr (TRIAD) {
+    if (Wl) triad_stage_table<N, NOWN>(tab.triad, Wl, rank, sr.P, threadIdx.x, T);
+  }
+  else fill_packed_twiddles<N, R, T>(TW, tab.tw);
   for (int k = threadIdx.x; k <= K; k += T) {
     GA[k] = __ldg(tab.g.a + k);
     GP[k] = __ldg(tab.g.p + k);
@@ -84,7 +92,7 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   }
   const unsigned P = (unsigned)sr.P;
   const bool one_pair = (int)P >= M / 2;
-  if (one_pair && rank < M / 2) {
+  if (!TRIAD && one_pair && rank < M / 2) {
     const int mA = 2 * rank + 1, mB = 2 * rank + 2;
     for (int k = threadIdx.x; k <= K; k += T) {
       PH[k] = __ldg(tab.phase + (size_t)mA * KP + k);
@@ -105,10 +113,25 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   const bool prof = ca.prof && rank == 0;
   int ps = 0;
   // the three stage-input buffers start empty (sentinel) before anyone writes
-  for (int i = rank * T + threadIdx.x; i < 3 * Kc3; i += P * T) st_relaxed_v2(ax.y(i), yin_sentinel());
+  constexpr int NB = TRIAD ? TRIAD_NB : 3;
+  for (int i = rank * T + threadIdx.x; i < NB * Kc3; i += P * T) st_relaxed_v2(ax.y(i), yin_sentinel());
   grid_barrier(bar, P, epoch);
-  coarse_update_phase<N, T, NOWN>(ca, ax, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, rank, (int)P);  // slice 0: v = e^{ΔT D̂/2} U_0
+  coarse_update_phase<N, T, NOWN, CtaGroup, HomedX, TRIAD>(ca, ax, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount,
+                                                           rank, (int)P);  // slice 0: v = e^{ΔT D̂/2} U_0
   for (int n = 0; n < ca.n_end; ++n) {
+    if constexpr (TRIAD) {
+      for (int st = 1; st <= nst; ++st) {
+        if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 0] = gtimer();
+        triad_stage_phase<N, T, NOWN, CtaGroup, HomedX>(ax, (size_t)(ucount % NB) * Kc3, Wl, tab.triad, C, A, kk, rank, (int)P,
+                                                        CtaGroup());
+        if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 1] = ca.prof[ps * 4 + 2] = gtimer();
+        ++ucount;
+        coarse_update_phase<N, T, NOWN, CtaGroup, HomedX, TRIAD>(ca, ax, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx,
+                                                                 ucount, rank, (int)P);
+        if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 3] = gtimer();
+        ++ps;
+      }
+    } else {
     for (int st = 1; st <= nst; ++st) {
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 0] = gtimer();
       coarse_samples_phase<N, R, T>(ax, (size_t)(ucount % 3) * Kc3, M, tab, X, Y, TW, C, A, PHc, SW, GA, GP, GQ,
@@ -117,11 +140,12 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
       grid_barrier(bar, P, epoch);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 2] = gtimer();
       ++ucount;
-      coarse_update_phase<N, T, NOWN>(ca, ax, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, rank, (int)P, CtaGroup(),
+      coarse_update_phase<N, T, NOWN, CtaGroup, HomedX>(ca, ax, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount, rank, (int)P, CtaGroup(),
                                       (prof && (ps == 9 || ps == 11)) ? ca.prof + (ps == 9 ? 300 : 320) : nullptr);
       if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 3] = gtimer();
       ++ps;
     }
+    }  // !TRIAD
   }
   grid_barrier(bar, P, epoch);  // every slice's U, G and residual partials are written
   if (r_out && rank == 0) {  // r_k = max_n sqrt(Σ num / Σ den) over slices (fixed order)
@@ -258,16 +282,27 @@ __global__ void __launch_bounds__(T) k_strang_sweep(const FineTab tab, double h,
   if (r_out && threadIdx.x == 0) *r_out = rmax;
 }
 
-template <int N, int NOWN, int R = coarse_radix<N>(), int T = coarse_threads<N>()>
+template <int N, int NOWN, bool TRIAD = false, int R = coarse_radix<N>(), int T = coarse_threads<N>()>
 static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& tab, int M, const SweepPlace& pl,
                                             double* r_out, int grid, bool on_die, int* die_used, cudaStream_t st) {
-  auto kfn = k_coarse_sweep<N, R, T, NOWN>;
+  auto kfn = k_coarse_sweep<N, R, T, NOWN, TRIAD>;
   int dev, sms, per_sm;
   cudaError_t e;
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  SweepRun sr{pl, -1, grid};
+  SweepRun sr{pl, -1, grid, 0};
   size_t sm = CoarseLayout<N, R, T, NOWN>::bytes;
+  if (TRIAD) {  // + the largest owned-block copy of the coefficient table, when it fits
+    size_t mx = 0;
+    for (int r = 0; r < grid; ++r) mx = std::max(mx, triad_local_entries(N / 3, r, grid, NOWN));
+    int optin = 0;
+    if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+    const size_t sw = (sm + 15) / 16 * 16 + sizeof(double2) * mx;
+    if (sw <= (size_t)optin) {
+      sm = sw;
+      sr.wsm = sizeof(double2) * mx;
+    }
+  }
   int launch = grid;
   if (on_die) {  // on the die with more SMs; one CTA per SM on every SM (the others exit at once)
     sr.die = pl.die_n[1] > pl.die_n[0] ? 1 : 0;
@@ -299,8 +334,10 @@ static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
   constexpr int K = N / 3;
   // one sample pair per CTA, but enough CTAs that each owns <= 16 modes in the update phase;
-  // at most one CTA per SM (co-residency of the cooperative launch)
-  int grid = M / 2;
+  // at most one CTA per SM (co-residency of the cooperative launch).  Triad form: two owned modes per
+  // CTA (one warp per half of a mode's rows)
+  const bool triad = N <= 256 && tab.triad != nullptr;
+  int grid = triad ? (K + 2) / 2 : M / 2;
   if (grid < (K + 1 + 15) / 16) grid = (K + 1 + 15) / 16;
   if (grid > sms) grid = sms;
   if (grid < 1) grid = 1;
@@ -309,6 +346,13 @@ static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab
   if (die_used) *die_used = -1;
   const int nown = (K + 1 + grid - 1) / grid;  // owned modes per CTA in the update phase
   if (grid_used) *grid_used = grid;
+  if constexpr (N <= 256) {
+    if (triad) {
+      if (nown <= 1) return launch_coarse_sweep_nown<N, 1, true>(ca, tab, M, pl, r_out, grid, on_die, die_used, st);
+      if (nown <= 2) return launch_coarse_sweep_nown<N, 2, true>(ca, tab, M, pl, r_out, grid, on_die, die_used, st);
+      return cudaErrorInvalidConfiguration;
+    }
+  }
 #define L_(NO) launch_coarse_sweep_nown<N, NO>(ca, tab, M, pl, r_out, grid, on_die, die_used, st)
   if (nown <= 1) return L_(1);
   if (nown <= 2) return L_(2);
@@ -321,7 +365,7 @@ static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab
 
 unsigned sweep_pages(int n, int M) {
   const unsigned Kc3 = 3u * (2u * (unsigned)(n / 3) + 1u), pairs = (unsigned)std::max(M / 2, 1);
-  return 1u + (3u * Kc3 + 255u) / 256u + (pairs * Kc3 + 255u) / 256u;
+  return 1u + yin_pages(n) + (pairs * Kc3 + 255u) / 256u;
 }
 
 template <int N>

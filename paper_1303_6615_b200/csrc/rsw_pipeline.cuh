@@ -50,6 +50,14 @@
 #ifndef RSW_PIPE_FINE_GROUPS
 #define RSW_PIPE_FINE_GROUPS 1  // fine worker groups per CTA (two slowed the sweeps on C3)
 #endif
+// triad sweeps: the coarse sub-CTA needs 2 warps per owned mode, and the fine throughput
+// sets the pace once the chain is short — so fewer coarse threads and more fine groups per CTA
+#ifndef RSW_PIPE_TRIAD_TC
+#define RSW_PIPE_TRIAD_TC 288  // 128 (2 fine groups beside it): C3 29.6-34.4 ms; 128 (1 group): 27.6-27.9; 288: 25.6-26.5
+#endif
+#ifndef RSW_PIPE_TRIAD_NPG
+#define RSW_PIPE_TRIAD_NPG 1
+#endif
 
 namespace rsw {
 
@@ -110,15 +118,29 @@ __host__ __device__ constexpr int pipe_split() {  // sample pairs a coarse sub-C
        : (NPC >= 2 && (TC / 2) % 32 == 0 && 3 * (N / RC0) <= TC / 2) ? 2 : 1;
 }
 
-template <int N, int RC0, int TC, int NOWN, int NPC, int RF, int TG, int NPG>
+// coarse sub-CTA region of the triad sweeps (no FFT buffers, twiddles or sample phases): the stage input
+// C, the half-sums HP, the owned entries' state, and the double / int slots; the coefficient blocks
+// follow the whole layout (runtime size, PipeArgs::wsm)
+template <int N, int T, int NOWN>
+struct TriadCoarseLayout {
+  static constexpr int K = N / 3, Kc = 2 * K + 1, NR = (T > NOWN * 6 ? T : NOWN * 6);
+  static constexpr int C = 0, HP = C + 3 * Kc, VS = HP + NOWN * 6, KS = VS + NOWN * 6, KK = KS + NOWN * 6,
+                       UN = KK + NOWN * 6, YV = UN + NOWN * 3, D = YV + NOWN * 6;
+  static constexpr int RED = 0, YI = RED + NR, ND = YI + NOWN * 6;
+  static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
+};
+
+template <int N, int RC0, int TC, int NOWN, int NPC, int RF, int TG, int NPG, bool TRIAD = false>
 struct PipeLayout {
   static constexpr int SPLIT = pipe_split<N, TC, NPC, RC0>();
   static constexpr int RC = RC0;
   using CL = CoarseLayout<N, RC, TC, NOWN, NPC, SPLIT>;
+  using TL = TriadCoarseLayout<N, TC, NOWN>;
   static constexpr int K = N / 3, KP = K + 1;
   // coarse region: the coarse sub-CTA's layout, or (CTAs without a coarse role) TC/TG extra fine groups' X/Y
   static constexpr int XG = TC / TG;
-  static constexpr size_t CREG = CL::bytes > sizeof(double2) * XG * 6 * N ? CL::bytes : sizeof(double2) * XG * 6 * N;
+  static constexpr size_t CB_ = TRIAD ? TL::bytes : CL::bytes;
+  static constexpr size_t CREG = CB_ > sizeof(double2) * XG * 6 * N ? CB_ : sizeof(double2) * XG * 6 * N;
   static constexpr int C0 = 0, F0 = (int)((CREG + 15) / 16);  // double2 offsets of the coarse / fine regions
   static constexpr int F_TW = F0, F_CP = F_TW + fft_tw_size<N, RF>(), F_D = F_CP + 6 * KP, F_ND = 9 * KP,
                        F_G = F_D + (F_ND + 1) / 2;  // first fine group's X
@@ -234,9 +256,148 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
   }
 }
 
-template <int N, int RC, int TC, int NOWN, int NPC, int RF, int TG, int NPG, int FSCHEME>
+// r_k = max_n sqrt(Σ num / Σ den) over the slices of the sweep (fixed order, as the bulk sweep); the
+// first r_k < tol or a divergence lowers stopk.  Called by the group's rank-0 coarse sub-CTA.
+template <int N, int TC>
+__device__ __forceinline__ void sweep_residual(const PipeArgs& a, const double* rparts, int k, double* red,
+                                               const NamedGroup& cg, int ct) {
+  constexpr int KP = N / 3 + 1;
+  double mx = 0.0;
+  bool bad = false;
+  for (int s = ct; s < a.S; s += TC) {
+    double num = 0.0, den = 0.0;
+    for (int q = 0; q < KP; ++q) {
+      num += __ldcg(rparts + ((size_t)s * KP + q) * 2);
+      den += __ldcg(rparts + ((size_t)s * KP + q) * 2 + 1);
+    }
+    const double r = sqrt(num / den);
+    if (!(r == r) || isinf(r)) bad = true;
+    mx = fmax(mx, r);
+  }
+  red[ct] = bad ? __longlong_as_double(0x7ff8000000000000LL) : mx;
+  cg.sync();
+  if (ct == 0) {
+    double m = 0.0;
+    bool nan = false;
+    for (int t = 0; t < TC; ++t) {
+      if (red[t] != red[t]) nan = true;
+      m = fmax(m, red[t]);
+    }
+    const double r = nan ? __longlong_as_double(0x7ff8000000000000LL) : m;
+    a.resid[k] = r;
+    if (!(r == r) || r > 1e6 || (a.tol > 0 && r < a.tol)) atomicMin(a.stopk, k);
+  }
+}
+
+// Coarse sub-CTA of a triad group: sweeps k = g, g + NG, ... with N̄ in triad form — a stage
+// is poll -> owned N̄ (coefficient blocks in shared memory) -> RK update and publication, with no group
+// barrier (stage-input ring of TRIAD_NB buffers); a discarded sweep aborts in its stage-input poll.
+template <int N, int TC, int NOWN, class LY>
+__device__ __forceinline__ void coarse_role_triad(const PipeArgs& a, const NamedGroup& cg, int ct, int g, int c, int gd,
+                                                  int gslot, double2* smem, unsigned* s_flag) {
+  using TL = typename LY::TL;
+  constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NH = N / 2 + 1, Kc3 = 3 * Kc, NB = TRIAD_NB;
+  constexpr size_t L = (size_t)3 * NH * 2;
+  const int S = a.S, Kit = a.K, P = a.GC, M = a.M;
+  double2* cs = smem + LY::C0;
+  double2* C = cs + TL::C;
+  double2* HP = cs + TL::HP;
+  double2* Vs = cs + TL::VS;
+  double2* KSs = cs + TL::KS;
+  double2* kk = cs + TL::KK;
+  double2* un_s = cs + TL::UN;
+  double2* yv = cs + TL::YV;
+  double* sd = reinterpret_cast<double*>(cs + TL::D);
+  double* red = sd + TL::RED;
+  int* yidx = reinterpret_cast<int*>(sd + TL::YI);
+  double2* Wl = a.wsm ? smem + (LY::bytes + 15) / 16 : nullptr;  // (null: read the global table)
+  if (Wl) triad_stage_table<N, NOWN>(a.at.triad, Wl, c, P, ct, TC);
+  cg.sync();
+  constexpr unsigned YP = yin_pages(N);
+  const unsigned PPG = ((unsigned)(M / 2 > 0 ? M / 2 : 1) * Kc3 + 255) / 256, GPG = 1 + YP + PPG;
+  unsigned* bar = reinterpret_cast<unsigned*>(homed_page(a.arena[gd], gslot * GPG));
+  const HomedX ax{a.arena[gd], gslot * GPG + 1, gslot * GPG + 1 + YP};
+  const int nst = a.base.scheme == 0 ? 4 : 2;
+  unsigned epoch = 0;
+  for (int k = g; k <= Kit; k += a.NG) {
+    for (int i = c * TC + ct; i < NB * Kc3; i += P * TC) st_relaxed_v2(ax.y(i), yin_sentinel());
+    const bool stop_now = (c == 0) && (*(volatile int*)a.stopk < k || *(volatile unsigned*)a.wd != 0);
+    if (group_barrier(bar, P, epoch, stop_now, a.wd, a.hb, s_flag, cg)) break;
+    if (c == 0 && ct == 0) {
+      const unsigned long long t = gtimer();
+      a.stamps[2 * k] = t;
+      if (a.trace) a.trace[2 * k] = t;
+    }
+    CoarseArgs ca = a.base;
+    ca.U = a.Uall + (size_t)k * (S + 1) * L;
+    ca.G = a.Gall + (size_t)k * S * L;
+    ca.Uprev = k ? a.Uall + (size_t)(k - 1) * (S + 1) * L : ca.U;
+    ca.Gprev = k ? a.Gall + (size_t)(k - 1) * S * L : ca.G;
+    ca.F = k ? a.Fall + (size_t)(k - 1) * S * L : nullptr;
+    ca.rparts = k ? a.rparts + (size_t)k * S * KP * 2 : nullptr;
+    ca.part = nullptr;
+    ca.nparts = 1;
+    ca.yin = nullptr;
+    ca.n_end = S;
+    ca.wprog = k ? a.prog + (k - 1) : nullptr;
+    ca.wunit = (unsigned)P;
+    ca.wF = k ? a.doneF + (size_t)(k - 1) * a.npairs : nullptr;
+    ca.wd = a.wd;
+    ca.hb = a.hb;
+    ca.wsys = a.npeers > 0 || a.pair_hi - a.pair_lo < a.npairs;
+    ca.stopk = a.stopk;
+    ca.kself = k;
+    ca.prof = nullptr;
+    unsigned ucount = 0;
+    coarse_update_phase<N, TC, NOWN, NamedGroup, HomedX, true>(ca, ax, 0, 0, Vs, KSs, kk, un_s, red, nullptr, yv, yidx,
+                                                               ucount, c, P, cg);
+    bool aborted = false;
+    for (int n = 0; n < S && !aborted; ++n) {
+      for (int st = 1; st <= nst; ++st) {
+        unsigned long long* stp = (a.trace && g == 0 && c == 0 && ct == 0 && n >= 8 && n < 24 && k == g)
+                                      ? a.trace + 2 * (Kit + 1) + (size_t)(Kit + 1) * S + 2 * (size_t)(Kit > 0 ? Kit : 1) * a.npairs +
+                                            ((n - 8) * nst + st - 1) * 4
+                                      : nullptr;
+        if (stp) stp[0] = gtimer();
+        if (triad_stage_phase<N, TC, NOWN, NamedGroup, HomedX>(ax, (size_t)(ucount % NB) * Kc3, Wl, a.at.triad, C, HP, kk, c, P, cg,
+                                                               a.stopk, k, a.wd, a.hb)) {
+          aborted = true;
+          break;
+        }
+        if (stp) stp[1] = stp[2] = gtimer();
+        ++ucount;
+        coarse_update_phase<N, TC, NOWN, NamedGroup, HomedX, true>(ca, ax, st, n, Vs, KSs, kk, un_s, red, nullptr, yv,
+                                                                   yidx, ucount, c, P, cg);
+        if (stp) stp[3] = gtimer();
+      }
+      if (!aborted) {
+        cg.sync();  // this CTA's part of U^k_{n+1}, G^k_n is written
+        if (ct == 0) {
+          red_release_add(a.prog + k, 1u);
+          if (c == 0) atomicAdd(a.hb, 1u);
+        }
+        if (a.trace && c == 0 && ct == 0) a.trace[2 * (Kit + 1) + (size_t)k * S + n] = gtimer();
+      }
+    }
+    // end of the sweep: every slice's residual partials are written.  A CTA that aborted in a poll raises
+    // the abort bit here: the group's other CTAs either abort in their own polls (no more stage inputs
+    // come from this CTA) or, having finished the sweep, meet the raised bit at this barrier — so the
+    // whole group leaves together (without it a CTA that aborted at the last stage's poll would leave
+    // the others waiting here)
+    if (group_barrier(bar, P, epoch, aborted, a.wd, a.hb, s_flag, cg) || aborted) break;
+    if (c == 0 && ct == 0) {
+      const unsigned long long t = gtimer();
+      a.stamps[2 * k + 1] = t;
+      if (a.trace) a.trace[2 * k + 1] = t;
+    }
+    if (c == 0 && k > 0) sweep_residual<N, TC>(a, ca.rparts, k, red, cg, ct);
+  }
+  cg.sync();
+}
+
+template <int N, int RC, int TC, int NOWN, int NPC, int RF, int TG, int NPG, int FSCHEME, bool TRIAD = false>
 __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeArgs a) {
-  using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG>;
+  using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG, TRIAD>;
   using CL = typename LY::CL;
   static_assert(NPG * LY::CPG <= 512, "fine groups must fit in TMEM");
   static_assert(NPG <= 7, "named barrier ids (fine 1..7, split parts 8..11, staging 14, coarse 15)");
@@ -303,6 +464,10 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
                                             tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi]);
     };
     if (s_role[0] >= 0) {
+      if constexpr (TRIAD) {
+      coarse_role_triad<N, TC, NOWN, LY>(a, cg, ct, s_role[0], s_role[1], s_role[2] & 1, s_role[2] >> 1, smem,
+                                         &s_flag);
+      } else {
       const int g = s_role[0], c = s_role[1], P = a.GC, gd = s_role[2] & 1, gslot = s_role[2] >> 1;
       double2* cs = smem + LY::C0;
       double2* X = cs + CL::X;
@@ -347,7 +512,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
       }
       cg.sync();
       // the group's exchange arrays in pages homed on die gd: barrier counter, stage inputs, partials
-      constexpr unsigned YP = (3 * Kc3 + 255) / 256;
+      constexpr unsigned YP = yin_pages(N);
       const unsigned PPG = ((unsigned)(M / 2 > 0 ? M / 2 : 1) * Kc3 + 255) / 256, GPG = 1 + YP + PPG;
       unsigned* bar = reinterpret_cast<unsigned*>(homed_page(a.arena[gd], gslot * GPG));
       const HomedX ax{a.arena[gd], gslot * GPG + 1, gslot * GPG + 1 + YP};
@@ -461,6 +626,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
         }
       }
       cg.sync();  // every coarse thread is past the sweeps: the coarse region of smem is free
+      }  // !TRIAD
     }
     if (s_role[0] < 0 || RSW_PIPE_REUSE_COARSE) extra_fine();
   } else {
@@ -480,17 +646,27 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
 // ---------------------------------------------------------------------------------------------
 // launcher: picks the configuration for n, checks co-residency (2 CTAs per SM), launches
 // ---------------------------------------------------------------------------------------------
-template <int N, int NOWN, int NPC, int FSCHEME>
+template <int N, int NOWN, int NPC, int FSCHEME, bool TRIAD = false>
 static inline cudaError_t launch_pipe_nf(const PipeArgs& a, int grid, size_t* out, cudaStream_t st) {
   constexpr int RC = coarse_radix<N>();
-  constexpr int TC = RSW_PIPE_COARSE_THREADS > coarse_threads<N>() ? RSW_PIPE_COARSE_THREADS : coarse_threads<N>();
+  constexpr int TC = TRIAD ? RSW_PIPE_TRIAD_TC
+                           : (RSW_PIPE_COARSE_THREADS > coarse_threads<N>() ? RSW_PIPE_COARSE_THREADS : coarse_threads<N>());
   constexpr int RF = fine_radix<N>(), TG = RSW_PIPE_FINE_TMUL * core_threads<N, RF>();
   constexpr int CPG = (FineTmem<N, TG>::COLS + 31) / 32 * 32;
-  constexpr int NPG = RSW_PIPE_FINE_GROUPS * CPG <= 512 ? RSW_PIPE_FINE_GROUPS : 512 / CPG;
-  using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG>;
-  auto kfn = k_parareal_pipe<N, RC, TC, NOWN, NPC, RF, TG, NPG, FSCHEME>;
-  const size_t sm = LY::bytes;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  constexpr int NPG0 = TRIAD ? RSW_PIPE_TRIAD_NPG : RSW_PIPE_FINE_GROUPS;
+  constexpr int NPG = NPG0 * CPG <= 512 ? NPG0 : 512 / CPG;
+  using LY = PipeLayout<N, RC, TC, NOWN, NPC, RF, TG, NPG, TRIAD>;
+  auto kfn = k_parareal_pipe<N, RC, TC, NOWN, NPC, RF, TG, NPG, FSCHEME, TRIAD>;
+  PipeArgs a2 = a;
+  cudaError_t e;
+  if (TRIAD) {  // the owned-block copy of the triad coefficients when it fits, else the global table
+    int dev = 0, optin = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+    if ((LY::bytes + 15) / 16 * 16 + a.wsm > (size_t)optin) a2.wsm = 0;
+  }
+  const size_t sm = TRIAD ? (LY::bytes + 15) / 16 * 16 + a2.wsm : LY::bytes;
+  e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   if (grid <= 0) {  // query: co-resident CTAs (tensor-memory kernels: one per SM)
     int per_sm = 0, dev = 0, sms = 0;
@@ -503,7 +679,9 @@ static inline cudaError_t launch_pipe_nf(const PipeArgs& a, int grid, size_t* ou
               LY::T, TC, NPG, TG, sm, per_sm);
     return cudaSuccess;
   }
-  void* args[] = {(void*)&a};
+  if (getenv("RSW_PIPE_TRACE") && TRIAD)
+    fprintf(stderr, "[rsw pipe] triad coefficients: %s (%zu B per CTA)\n", a2.wsm ? "shared memory" : "global table", a.wsm);
+  void* args[] = {(void*)&a2};
   return cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(LY::T), args, sm, st);
 }
 
@@ -512,6 +690,17 @@ static inline cudaError_t launch_pipe_n(const PipeArgs& a, int fine_scheme, int 
   constexpr int K = N / 3;
   const int nown = (K + 1 + a.GC - 1) / a.GC;
   const int npc = (a.M / 2 + a.GC - 1) / a.GC;  // sample pairs per coarse CTA
+  if (a.at.triad) {  // triad sweeps: owned modes only (no sample pairs)
+#define PIPE_TCFG(NW)                                                                                    \
+  if (nown <= NW) return fine_scheme == 0 ? launch_pipe_nf<N, NW, 1, 0, true>(a, grid, out, st)          \
+                         : fine_scheme == 1 ? launch_pipe_nf<N, NW, 1, 1, true>(a, grid, out, st)        \
+                                            : launch_pipe_nf<N, NW, 1, 2, true>(a, grid, out, st);
+    PIPE_TCFG(2)
+    PIPE_TCFG(4)
+    PIPE_TCFG(8)
+#undef PIPE_TCFG
+    return cudaErrorInvalidConfiguration;
+  }
 #define PIPE_CFG(NW, NP)                                                                            \
   if (nown <= NW && npc <= NP) return fine_scheme == 0 ? launch_pipe_nf<N, NW, NP, 0>(a, grid, out, st) \
                                     : fine_scheme == 1 ? launch_pipe_nf<N, NW, NP, 1>(a, grid, out, st) \

@@ -493,11 +493,14 @@ def test_check_states_layout(rsw_gpu):
     assert g["status"] == rsw_gpu.RSW_OK
 
 
-def test_auto_schedule_falls_back_to_bulk(rsw_gpu):
+def test_auto_schedule_falls_back_to_bulk(rsw_gpu, monkeypatch):
     """AUTO must run the bulk schedule when the pipelined kernel cannot hold the
     configuration (M/2 = 1250 sample pairs > 8 per coarse CTA x 148 co-resident CTAs); an explicit
     PIPELINED request fails with RSW_ERR_CONFIG.  With M/2 = 500 pairs the coarse groups are re-sized
-    (8 pairs per CTA) and the pipelined schedule runs, bitwise equal to bulk."""
+    (8 pairs per CTA) and the pipelined schedule runs, bitwise equal to bulk.  (The sample-pair limits
+    belong to the M-sample quadrature sweeps; the triad sweeps have none, see
+    test_triad_any_M_runs_pipelined.)"""
+    monkeypatch.setenv("RSW_COARSE_TRIAD", "0")
     w = inputs.C1
     p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
     u0 = dev(inputs.initial_state(w))
@@ -710,3 +713,60 @@ def test_parareal_c1_ifrk4_fine(rsw_gpu, orc):
                      max_iters=3, fine_scheme=2)
     assert rel_l2(to_np(g["U"]), r["U"], w.n)[1:].max() < TOL
     assert np.allclose(g["resid"], r["resid"], rtol=1e-8, atol=0)
+
+
+# ------------------------------------------------------ triad form of N̄ in the coarse sweeps
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_triad_sweeps_match_oracle_and_quadrature(rsw_gpu, orc, name, monkeypatch):
+    """The triad coarse sweeps (default for n <= 256) and the M-sample quadrature sweeps
+    (RSW_COARSE_TRIAD=0) both match the oracle's parareal iterates; the iteration count of the
+    tolerance-driven C2 run is the oracle's; bulk and pipelined triad runs agree bitwise."""
+    w = getattr(inputs, name)
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = inputs.initial_state(w)
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=w.n_slices, max_iters=w.max_iters, tol=w.tol)
+    ref = orc.parareal(u0, w.eps, w.F, w.mu, w.n, **kw) if name == "C1" else _fixture("oracle_C2.npz")
+    runs = {}
+    for triad in ("1", "0"):
+        monkeypatch.setenv("RSW_COARSE_TRIAD", triad)
+        for sched in (rsw_gpu.SCHEDULE_BULK, rsw_gpu.SCHEDULE_PIPELINED):
+            g = rsw_gpu.parareal_iterate(p, dev(u0), schedule=sched, **kw)
+            assert g["stats"]["coarse_triad"] == (triad == "1")
+            assert g["iters"] == int(ref["iters"])
+            assert rel_l2(to_np(g["U"]), ref["U"], w.n)[1:].max() < TOL
+            runs[(triad, sched)] = g
+    for triad in ("1", "0"):
+        a, b = runs[(triad, rsw_gpu.SCHEDULE_BULK)], runs[(triad, rsw_gpu.SCHEDULE_PIPELINED)]
+        assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
+
+
+def test_triad_any_M_runs_pipelined(rsw_gpu, orc):
+    """The triad sweeps carry no sample pairs, so M = 2500 (beyond the quadrature layout's limit) runs
+    pipelined, bitwise equal to bulk and within tolerance of the oracle's coarse propagator."""
+    w = inputs.C1
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=2500, n_slices=w.n_slices, max_iters=2)
+    a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_AUTO, **kw)
+    b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    assert a["stats"]["pipelined"] and a["stats"]["coarse_triad"]
+    assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
+    u = inputs.random_states(w.n, 2, seed=11)
+    g = to_np(rsw_gpu.coarse_propagate(p, dev(u), w.dT, w.T0, 2500))
+    assert rel_l2(g, orc.coarse_propagate(u, w.eps, w.F, w.mu, w.n, w.dT, w.T0, 2500), w.n).max() < TOL
+
+
+def test_triad_global_table_layout_bitwise(rsw_gpu, monkeypatch):
+    """A coarse layout whose owned coefficient blocks do not fit shared memory (C3 with 11 CTAs per
+    group: 8 owned modes, ~290 KB of coefficients for rank 0) reads the global table instead: the same
+    values, bitwise equal to the bulk sweep (which holds its blocks in shared memory)."""
+    w = inputs.C3
+    p = P(rsw_gpu, w.eps, w.F, w.mu, w.n)
+    u0 = dev(inputs.initial_state(w))
+    kw = dict(dT=w.dT, dt=w.dt, T0=w.T0, M=w.M, n_slices=64, max_iters=2)
+    b = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_BULK, **kw)
+    monkeypatch.setenv("RSW_PIPE_GC", "11")
+    monkeypatch.setenv("RSW_PIPE_NG", "2")
+    a = rsw_gpu.parareal_iterate(p, u0, schedule=rsw_gpu.SCHEDULE_PIPELINED, **kw)
+    assert a["stats"]["group_ctas"] == 11
+    assert a["resid"] == b["resid"] and torch.equal(a["U"], b["U"])
