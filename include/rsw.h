@@ -105,16 +105,19 @@ rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n
 /* Triad coefficients of N̄ (HOST output).  The paper writes the averaged nonlinear term as
    a sum over wavenumber triads with interaction coefficients; with Alg.1's quadrature
    (the same w_m, τ_m as rsw_averaged_rhs) the eigen coordinates (c-, c0, c+) of N̄ are
-     N̄^γ_κ = Σ_{κ1=κ-K}^{K} Σ_{α=±1} Σ_{β=-1,0,1} W^{γαβ}_{κκ1} c^α_{κ1} c^β_{κ-κ1},   κ = 0..K = n/3,
-     W^{γαβ}_{κκ1} = [Σ_{m=1}^{M-1} w_m e^{i(γω_κ - αω_{κ1} - βω_{κ2})τ_m}] C^{γαβ}_{κκ1κ2},
+     N̄^γ_κ = Σ_{κ1=κ-K}^{K} Σ_{α=±1} Σ_{β=-1,0,1} Φ(γω_κ - αω_{κ1} - βω_{κ2}) C^{γαβ}_{κκ1κ2} c^α_{κ1} c^β_{κ2},
+     Φ(λ) = Σ_{m=1}^{M-1} w_m e^{iλτ_m},   κ2 = κ - κ1,   κ = 0..K = n/3,
    in the eigenbasis r^∓ = (∓iω, 1, ia)/(√2ω), r^0 = (0, ia, 1)/ω, a = κ/√F, ω = √(1+a²).
+   The window is symmetric, so Φ(λ) = e^{iλτ_c} R(λ) with τ_c = T0/(2ε) and R real; each C^{γαβ} is
+   purely real when (γ = 0) == (β = 0) and purely imaginary otherwise.  `out` receives ONE double per
+   coefficient, W' = R(λ) C (its real part, or its imaginary part for the imaginary ones), for the
+   contraction in the rotated frame: c'^α_k = c^α_k e^{-iαω_k τ_c},  N̄^γ_κ = e^{iγω_κ τ_c} Σ W' c' c'
+   (× i for the imaginary ones).  Layout: block κ = 0..K starts at 18 (κ(2K+1) - κ(κ-1)/2); inside it
+   entry e = (γ+1) 6 + (α > 0) 3 + (β+1) of row i (κ1 = κ - K + i, i = 0..2K-κ) is at e (2K+1-κ) + i.
    The coarse sweeps (rsw_coarse_propagate, parareal_iterate) evaluate N̄ in this form for n <= 256
    (environment RSW_COARSE_TRIAD=0: the M-sample quadrature instead); rsw_averaged_rhs always uses
-   the quadrature.  Layout of `out` (double[count][2], complex): block κ = 0..K starts at entry
-   18 (κ(2K+1) - κ(κ-1)/2); inside it entry e = (γ+1) 6 + (α > 0) 3 + (β+1) of row i (κ1 = κ - K + i,
-   i = 0..2K-κ) is at e (2K+1-κ) + i.  *count receives the number of complex entries; out may be
-   NULL (size query).  Pure host computation (no GPU needed); RSW_ERR_CONFIG on bad parameters or
-   n > 256. */
+   the quadrature.  *count receives the number of doubles; out may be NULL (size query).  Pure host
+   computation (no GPU needed); RSW_ERR_CONFIG on bad parameters or n > 256. */
 rsw_status rsw_triad_coefficients(const rsw_params* p, double T0, int32_t M, double* out, int64_t* count);
 
 /* Coarse propagator φ̄_ΔT (Alg.2, φ̄ P:415-417) for n_states independent states:

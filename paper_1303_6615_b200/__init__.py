@@ -188,15 +188,15 @@ def averaged_rhs(p: Params, u, T0: float, M: int, validate: bool = True):
 
 
 def triad_coefficients(p: Params, T0: float, M: int):
-    """Triad coefficients W of N̄ (host computation; rsw.h rsw_triad_coefficients) as a
-    complex numpy array in the library's block layout."""
+    """Triad coefficients W' of N̄ (host computation; rsw.h rsw_triad_coefficients): one
+    float64 per coefficient in the library's block layout, for the contraction in the rotated frame."""
     import numpy as np
     cnt = ctypes.c_int64(0)
     _check(load().rsw_triad_coefficients(ctypes.byref(p._c()), T0, M, None, ctypes.byref(cnt)))
-    out = np.empty(2 * cnt.value, dtype=np.float64)
+    out = np.empty(cnt.value, dtype=np.float64)
     _check(load().rsw_triad_coefficients(ctypes.byref(p._c()), T0, M,
                                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(cnt)))
-    return out[0::2] + 1j * out[1::2]
+    return out
 
 
 def coarse_propagate(p: Params, u, dT: float, T0: float, M: int, scheme: int = COARSE_RK4, validate: bool = True):

@@ -597,16 +597,21 @@ __device__ __forceinline__ void coarse_samples_phase(const AX& ax, size_t yoff, 
 // — exactly the quadrature sum (no resonance truncation: every triad is kept with its quadrature
 // weight).  The dealiased pseudo-spectral product is an exact convolution (|κ1|, |κ2| <= K = n/3), and
 // the first factor of every product of N (u u_x = (u²/2)_x, u v_x, (h u)_x) is u, whose eigen expansion
-// has no α = 0 part, so α ranges over {-1, +1}: 18 coefficients per (κ, κ1).  The host builds W once
-// per configuration (rsw_capi.cu build_triad); table layout, double2 units: block κ = 0..K at
-// TRIAD_E * triad_rows_before(κ), inside it entry e = (γ+1)*6 + (α>0)*3 + (β+1) of row i at e*nk + i,
-// row i <-> κ1 = κ - K + i, κ2 = K - i, nk = 2K + 1 - κ rows.  One N̄ evaluation costs 96 DP
-// instructions per (κ, κ1) — for C3 ~1.1 M per stage instead of 64 pair N-evals — and needs no
-// cross-CTA reduction: the CTA that owns κ computes N̄_κ whole.
+// has no α = 0 part, so α ranges over {-1, +1}: 18 coefficients per (κ, κ1).  Two exact reductions make
+// every coefficient ONE real number: the window is symmetric (w_m = w_{M-m}), so with the centre
+// τ_c = T0/(2ε) Φ(λ) = e^{iλτ_c} R(λ), R(λ) = Σ_m w_m cos(λ(τ_m - τ_c)) real, and e^{iλτ_c} factors into
+// per-mode phases — the contraction runs in the frame rotated by e^{-τ_c L} (stage input y'_α = y_α
+// e^{-iαωτ_c}, output × e^{iγωτ_c}); and each C^{γαβ} is purely real ((γ = 0) == (β = 0)) or purely
+// imaginary (the eigenvectors' components are real or imaginary).  The host builds W' = R C (real or
+// imaginary part) once per configuration (rsw_capi.cu build_triad); table layout, double units: block
+// κ = 0..K at TRIAD_E * triad_rows_before(κ), inside it entry e = (γ+1)*6 + (α>0)*3 + (β+1) of row i at
+// e*nk + i, row i <-> κ1 = κ - K + i, κ2 = K - i, nk = 2K + 1 - κ rows.  One N̄ evaluation costs 60 DP
+// instructions per (κ, κ1) (6 complex products, 18 two-FMA accumulations) — for C3 ~0.66 M per stage
+// instead of 64 pair N-evals — and needs no cross-CTA reduction: the CTA that owns κ computes N̄_κ whole.
 // ---------------------------------------------------------------------------------------------
 // TRIAD_E, triad_nk, triad_rows_before, triad_local_entries: rsw_internal.h
 template <int N, int NOWN>
-__device__ __forceinline__ void triad_stage_table(const double2* __restrict__ Wg, double2* Wl, int rank, int P, int tid,
+__device__ __forceinline__ void triad_stage_table(const double* __restrict__ Wg, double* Wl, int rank, int P, int tid,
                                                   int nthr) {
   constexpr int K = N / 3;
   size_t lo = 0;
@@ -614,7 +619,7 @@ __device__ __forceinline__ void triad_stage_table(const double2* __restrict__ Wg
     const int kap = rank + o * P;
     if (kap > K) break;
     const size_t cnt = (size_t)TRIAD_E * triad_nk(kap, K);
-    const double2* src = Wg + (size_t)TRIAD_E * triad_rows_before(kap, K);
+    const double* src = Wg + (size_t)TRIAD_E * triad_rows_before(kap, K);
     for (size_t i = tid; i < cnt; i += nthr) Wl[lo + i] = __ldg(src + i);
     lo += cnt;
   }
@@ -625,7 +630,7 @@ __device__ __forceinline__ void triad_stage_table(const double2* __restrict__ Wg
 // stage u - NB/2: every reader of it is done (publishing u needs all of input u-1, i.e. every owner
 // published u-1, which it did after reading input u-2), and the next writer of it (stage u + NB/2)
 // acted on input u + NB/2 - 1, published after a fence that follows this reset (the resetting
-// threads fence after every odd publication).  TRIAD_NB: rsw_internal.h.
+// threads fence after every (NB/4)-th publication, NB/4 <= NB/2 - 1).  TRIAD_NB: rsw_internal.h.
 
 // One RK stage's N̄ in triad form: poll the stage input y (ring buffer at yoff) into C, then for each
 // owned |κ| = rank + o P the 3 eigen entries γ of N̄_κ (coefficients from the shared-memory copy Wl, or
@@ -636,15 +641,78 @@ __device__ __forceinline__ void triad_stage_table(const double2* __restrict__ Wg
 // N̄ = half 0 + half 1 — so the bulk and pipelined sweeps agree bitwise.  stopk (pipelined schedule):
 // the poll gives up once the run stopped before iteration kself, or the watchdog fired; returns true
 // then (the whole group takes the same decision on its own, every wait of a discarded sweep aborts).
+// per-sweep constants of the triad coarse CTAs in shared memory (the L1 left beside ~200 KB of shared
+// memory does not keep them): gsm[o*8 + {0..5}] = a, p, q, e^{-μκ⁴ΔT/2}, e^{-iωΔT/ε} of owned mode o, and
+// the frame rotation e^{iω_k τ_c}, k = 0..K
+template <int N, int NOWN>
+__device__ __forceinline__ void owned_consts(const CoarseArgs& ca, const double2* __restrict__ rph_g, double* gsm,
+                                             double2* rph, int rank, int P, int tid, int nthr) {
+  constexpr int K = N / 3;
+  for (int i = tid; i < NOWN * 8; i += nthr) {
+    const int o = i / 8, c = i % 8, ak = rank + o * P;
+    double v = 0.0;
+    if (ak <= K) {
+      if (c == 0) v = __ldg(ca.g.a + ak);
+      else if (c == 1) v = __ldg(ca.g.p + ak);
+      else if (c == 2) v = __ldg(ca.g.q + ak);
+      else if (c == 3) v = __ldg(ca.dhalf + ak);
+      else if (c == 4) v = __ldg(ca.back + ak).x;
+      else if (c == 5) v = __ldg(ca.back + ak).y;
+    }
+    gsm[i] = v;
+  }
+  for (int k = tid; k <= K; k += nthr) rph[k] = __ldg(rph_g + k);
+}
+
+// one lane's share of N̄_κ: rows i = i0, i0 + 64, ... (ascending), all 18 coefficients of a row loaded
+// before its products are used (so the loads overlap), accumulated into acc[γ] in a fixed order
+template <int N, class LDW>
+__device__ __forceinline__ void triad_rows(double2* acc, const double2* C, int kap, int nk, int i0, LDW ldw) {
+  constexpr int K = N / 3, Kc = 2 * K + 1;
+  for (int i = i0; i < nk; i += 64) {
+    double wv[18];
+#pragma unroll
+    for (int e = 0; e < 18; ++e) wv[e] = ldw(e, i);
+    const int k1 = kap - K + i, k2 = K - i;
+    const int j1 = k1 >= 0 ? k1 : k1 + Kc, j2 = k2 >= 0 ? k2 : k2 + Kc;
+    const double2 am = C[j1], ap = C[2 * Kc + j1];
+    double2 pr[6];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const double2 yb = C[b * Kc + j2];
+      pr[b] = make_double2(fma(am.x, yb.x, -am.y * yb.y), fma(am.x, yb.y, am.y * yb.x));
+      pr[3 + b] = make_double2(fma(ap.x, yb.x, -ap.y * yb.y), fma(ap.x, yb.y, ap.y * yb.x));
+    }
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {
+#pragma unroll
+      for (int ab2 = 0; ab2 < 6; ++ab2) {
+        const double w = wv[g * 6 + ab2];
+        if ((g == 1) == (ab2 % 3 == 1)) {  // real coefficient
+          acc[g].x = fma(w, pr[ab2].x, acc[g].x);
+          acc[g].y = fma(w, pr[ab2].y, acc[g].y);
+        } else {  // imaginary coefficient i w
+          acc[g].x = fma(-w, pr[ab2].y, acc[g].x);
+          acc[g].y = fma(w, pr[ab2].x, acc[g].y);
+        }
+      }
+    }
+  }
+}
+
 template <int N, int T, int NOWN, class GRP = CtaGroup, class AX = FlatX>
-__device__ __forceinline__ bool triad_stage_phase(const AX& ax, size_t yoff, const double2* Wl, const double2* Wg,
-                                                  double2* C, double2* hp,
+__device__ __forceinline__ bool triad_stage_phase(const AX& ax, size_t yoff, const double* Wl, const double* Wg,
+                                                  const double2* RPH, double2* C, double2* hp,
                                                   double2* kk, int rank, int P, const GRP& grp,
                                                   const int* stopk = nullptr, int kself = 0, unsigned* wd = nullptr,
-                                                  const unsigned* hb = nullptr) {
+                                                  const unsigned* hb = nullptr, unsigned long long* stamp = nullptr,
+                                                  unsigned long long* cyc = nullptr) {
   constexpr int K = N / 3, Kc = 2 * K + 1;
   const int tid_ = grp.tid();
   bool ab = false;
+#define TSTAMP(i) \
+  if (cyc && tid_ == 0) cyc[i] = clock64();
+  TSTAMP(0)
   for (int i = tid_; i < 3 * Kc; i += T) {
     const double2* yi = ax.y(yoff + i);
     double2 v = ld_relaxed_v2(yi);
@@ -661,48 +729,42 @@ __device__ __forceinline__ bool triad_stage_phase(const AX& ax, size_t yoff, con
     } else {
       while (is_sentinel(v.x) || is_sentinel(v.y)) v = ld_relaxed_v2(yi);
     }
+    // into the rotated frame: y'_α = y_α e^{-iαωτ_c} (α = -1: × e^{iωτ_c}, α = +1: × its conjugate)
+    const int al = i / Kc, j = i - al * Kc, kap = kappa_of(j, K);
+    if (al != 1) {
+      const double2 r = RPH[kap < 0 ? -kap : kap];  // (shared memory, owned_consts)
+      v = al == 0 ? cmul(v, r) : cmulc(v, r);
+    }
     C[i] = v;
   }
+  TSTAMP(1)
   if (stopk) {
     if (grp.sync_or(ab)) return true;
   } else {
     grp.sync();
   }
+  TSTAMP(2)
+  if (stamp && tid_ == 0) stamp[0] = gtimer();  // trace: the whole stage input has arrived
   const int lane = tid_ & 31;
   for (int it = tid_ >> 5; it < 2 * NOWN; it += T / 32) {
     const int o = it >> 1, hh = it & 1, kap = rank + o * P;
     if (kap > K) continue;  // (warp-uniform)
     const int nk = triad_nk(kap, K);
-    // coefficient block: the CTA's shared-memory copy (Wl), or the global table when it did not fit
-    const double2* Wb;
+    double2 acc[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    // coefficient block: the CTA's shared-memory copy (Wl; explicit ld.shared — a pointer that may be
+    // either space compiles to generic loads), or the global table when it did not fit
     if (Wl) {
       size_t lo = 0;
       for (int q = 0; q < o; ++q) lo += (size_t)TRIAD_E * triad_nk(rank + q * P, K);
-      Wb = Wl + lo;
+      const unsigned wsh = (unsigned)__cvta_generic_to_shared(Wl + lo);
+      triad_rows<N>(acc, C, kap, nk, 32 * hh + lane, [&](int e, int i) {
+        double v;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(wsh + 8u * (unsigned)(e * nk + i)));
+        return v;
+      });
     } else {
-      Wb = Wg + (size_t)TRIAD_E * triad_rows_before(kap, K);
-    }
-    double2 acc[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-    for (int i = 32 * hh + lane; i < nk; i += 64) {
-      const int k1 = kap - K + i, k2 = K - i;
-      const int j1 = k1 >= 0 ? k1 : k1 + Kc, j2 = k2 >= 0 ? k2 : k2 + Kc;
-      const double2 am = C[j1], ap = C[2 * Kc + j1];
-      double2 pr[6];
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        const double2 yb = C[b * Kc + j2];
-        pr[b] = make_double2(fma(am.x, yb.x, -am.y * yb.y), fma(am.x, yb.y, am.y * yb.x));
-        pr[3 + b] = make_double2(fma(ap.x, yb.x, -ap.y * yb.y), fma(ap.x, yb.y, ap.y * yb.x));
-      }
-#pragma unroll
-      for (int g = 0; g < 3; ++g) {
-#pragma unroll
-        for (int ab2 = 0; ab2 < 6; ++ab2) {
-          const double2 wv = Wb[(size_t)(g * 6 + ab2) * nk + i];
-          acc[g].x = fma(wv.x, pr[ab2].x, fma(-wv.y, pr[ab2].y, acc[g].x));
-          acc[g].y = fma(wv.x, pr[ab2].y, fma(wv.y, pr[ab2].x, acc[g].y));
-        }
-      }
+      const double* Wb = Wg + (size_t)TRIAD_E * triad_rows_before(kap, K);
+      triad_rows<N>(acc, C, kap, nk, 32 * hh + lane, [&](int e, int i) { return __ldg(Wb + (size_t)e * nk + i); });
     }
 #pragma unroll
     for (int g = 0; g < 3; ++g)
@@ -714,15 +776,24 @@ __device__ __forceinline__ bool triad_stage_phase(const AX& ax, size_t yoff, con
 #pragma unroll
       for (int g = 0; g < 3; ++g) hp[(o * 2 + hh) * 3 + g] = acc[g];
   }
+  TSTAMP(3)
   grp.sync();
+  TSTAMP(4)
   if (tid_ < NOWN * 3) {
     const int o = tid_ / 3, g = tid_ % 3, kap = rank + o * P;
     if (kap <= K) {
-      const double2 v = cadd(hp[(o * 2) * 3 + g], hp[(o * 2 + 1) * 3 + g]);
+      double2 v = cadd(hp[(o * 2) * 3 + g], hp[(o * 2 + 1) * 3 + g]);
+      if (g != 1) {  // back from the rotated frame: × e^{iγωτ_c}
+        const double2 r = RPH[kap];
+        v = g == 0 ? cmulc(v, r) : cmul(v, r);
+      }
       kk[o * 6 + g] = v;
       kk[o * 6 + 3 + (2 - g)] = cconj(v);
     }
   }
+  TSTAMP(5)
+#undef TSTAMP
+  if (stamp && tid_ == 0) stamp[1] = gtimer();  // trace: this CTA's N̄ entries are done
   return false;
 }
 
@@ -742,7 +813,7 @@ __device__ __forceinline__ void push_stage_input(const AX& ax, const double2* yv
   if (tid_ < NOWN * 6 && yidx[tid_] >= 0) {
     st_relaxed_v2(ax.y((size_t)(u % NB) * Kc3 + yidx[tid_]), yv[tid_]);
     st_relaxed_v2(ax.y((size_t)((u + RB) % NB) * Kc3 + yidx[tid_]), yin_sentinel());
-    if (NB != 3 && (u & 1u)) __threadfence();
+    if (NB != 3 && (u % (unsigned)(NB / 4)) == (unsigned)(NB / 4 - 1)) __threadfence();
   }
 }
 
@@ -751,7 +822,7 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
                                                     double2* KSs, double2* kk, double2* un_s, double* nd_s,
                                                     double2* red_buf, double2* yv, int* yidx, unsigned ucount,
                                                     int rank = -1, int P = -1, const GRP& grp = GRP(),
-                                                    unsigned long long* cyc = nullptr) {
+                                                    unsigned long long* cyc = nullptr, const double* gsm = nullptr) {
   const int tid_ = grp.tid();
 #define USTAMP(i) \
   if (cyc && tid_ == 0) cyc[i] = clock64();
@@ -777,9 +848,10 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
       // pipelined parareal: F(U^{k-1}_n) and the previous sweep's slice n must be complete
       if (ca.wF) spin_until_geq(ca.wF + n / 2, 1u, ca.wd, ca.hb, ca.stopk, ca.kself, ca.wsys != 0);
       if (ca.wprog) spin_until_geq(ca.wprog, ca.wunit * (unsigned)(n + 1), ca.wd, ca.hb, ca.stopk, ca.kself);
+      // (G_n only enters the correction, U_{n+1} only the residual: the k = 0 sweep needs neither)
       if (ca.F) pf_F = __ldcg(reinterpret_cast<const double2*>(ca.F) + (size_t)n * Ls + f * NH + ak);
-      pf_G = __ldcg(reinterpret_cast<const double2*>(ca.Gprev) + (size_t)n * Ls + f * NH + ak);
-      pf_U = __ldcg(reinterpret_cast<const double2*>(ca.Uprev) + (size_t)(n + 1) * Ls + f * NH + ak);
+      if (ca.F) pf_G = __ldcg(reinterpret_cast<const double2*>(ca.Gprev) + (size_t)n * Ls + f * NH + ak);
+      if (ca.rparts) pf_U = __ldcg(reinterpret_cast<const double2*>(ca.Uprev) + (size_t)(n + 1) * Ls + f * NH + ak);
     }
   }
   USTAMP(1)
@@ -891,9 +963,12 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
     if (tid_ < NOWN * 3) {
       const int o = tid_ / 3, f = tid_ % 3, ak = rank + o * P;
       if (ak <= K) {
-        const double a = __ldg(ca.g.a + ak), p = __ldg(ca.g.p + ak), q = __ldg(ca.g.q + ak);
-        const double dh = __ldg(ca.dhalf + ak);
-        const double2 bt = __ldg(ca.back + ak);  // e^{-iωΔT/ε}: α=+1 entry of e^{-(ΔT/ε)L̂} (R3)
+        // (gsm: the owned modes' constants staged in shared memory by the caller, owned_consts)
+        const double a = gsm ? gsm[o * 8] : __ldg(ca.g.a + ak), p = gsm ? gsm[o * 8 + 1] : __ldg(ca.g.p + ak),
+                     q = gsm ? gsm[o * 8 + 2] : __ldg(ca.g.q + ak);
+        const double dh = gsm ? gsm[o * 8 + 3] : __ldg(ca.dhalf + ak);
+        // e^{-iωΔT/ε}: α=+1 entry of e^{-(ΔT/ε)L̂} (R3)
+        const double2 bt = gsm ? make_double2(gsm[o * 8 + 4], gsm[o * 8 + 5]) : __ldg(ca.back + ak);
         double2 cg[3], G[3];
 #pragma unroll
         for (int al = 0; al < 3; ++al) {
@@ -946,12 +1021,13 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
     const int it = tid_, o = it / 6, e = it % 6;
     entry(o, e, ak, al, j);
     if (ak <= K && !(ak == 0 && e >= 3)) {
-      const double a = __ldg(ca.g.a + ak), p = __ldg(ca.g.p + ak), q = __ldg(ca.g.q + ak);
+      const double a = gsm ? gsm[o * 8] : __ldg(ca.g.a + ak), p = gsm ? gsm[o * 8 + 1] : __ldg(ca.g.p + ak),
+                   q = gsm ? gsm[o * 8 + 2] : __ldg(ca.g.q + ak);
       double2 u[3], c[3];
 #pragma unroll
       for (int f = 0; f < 3; ++f) u[f] = (e < 3) ? un_s[o * 3 + f] : cconj(un_s[o * 3 + f]);
       to_eigen(e < 3 ? a : -a, p, q, u, c);
-      const double2 v = cscale(c[al], __ldg(ca.dhalf + ak));
+      const double2 v = cscale(c[al], gsm ? gsm[o * 8 + 3] : __ldg(ca.dhalf + ak));
       Vs[it] = v;
       yv[it] = v;
       yidx[it] = al * Kc + j;

@@ -118,7 +118,7 @@ struct CoarseTables {
 };
 
 struct TriadTables {
-  DevBuf W;
+  DevBuf W, ph;
 };
 
 std::mutex g_mu;
@@ -244,46 +244,47 @@ cudaError_t get_avg(const rsw_params* p, double T0, int M, AvgTables** out) {
 }
 
 // Triad coefficients of N̄ (rsw_blocks.cuh; P:1113-1118 with Alg.1's quadrature):
-//   W^{γαβ}_{κκ1} = Φ(γω_κ - αω_κ1 - βω_κ2) Σ_f B_γf(κ) h_f A_0α(κ1) A_fβ(κ2),   κ2 = κ - κ1,
-//   Φ(λ) = Σ_{m=1}^{M-1} w_m e^{iλτ_m}  (w_m, τ_m = T0 m/(M ε) as get_avg; e^{iλτ} from the phase values),
+//   W^{γαβ}_{κκ1} = Φ(λ) C^{γαβ}_{κκ1κ2},  λ = γω_κ - αω_κ1 - βω_κ2,  κ2 = κ - κ1,
+//   C^{γαβ} = Σ_f B_γf(κ) h_f A_0α(κ1) A_fβ(κ2),   Φ(λ) = Σ_{m=1}^{M-1} w_m e^{iλτ_m}  (w_m, τ_m as get_avg),
 // with the maps of the pseudo-spectral N (rsw_device.cuh put_input_eigen / eigen_from_raw): FFT inputs
 // X0 = u = i s (c+ - c-), X1 = iκ v = iκ p (c+ + c-) - κ a q c0, X2 = h = q c0 + i a p (c+ + c-);
 // grid products h_f X0 X_f with h = (1/2, 1, 1) (u u_x = (u²/2)_x); outputs
 // N̄^∓ = ±sκ Z0 - p Z1 - p a κ Z2, N̄^0 = i q a Z1 - i q κ Z2  (a = κ/√F signed, p = 1/(√2ω), q = 1/ω).
-// Layout: block κ = 0..K at 18 triad_rows_before(κ), entry e = (γ+1)6 + (α>0)3 + (β+1) of row i at
-// e nk + i, row i <-> κ1 = κ - K + i.
-void build_triad(const rsw_params* p, double T0, int M, std::vector<double2>& Wout) {
+// Stored: W' = R(λ) C with R(λ) = Σ_m w_m cos(λ(τ_m - τ_c)), τ_c = T0/(2ε) (symmetric window: Φ = e^{iλτ_c} R,
+// the phase goes into the rotated frame), as ONE double — Re C when (γ = 0) == (β = 0), else Im C (C is
+// purely real / imaginary there; checked).  Layout: block κ = 0..K at 18 triad_rows_before(κ) doubles,
+// entry e = (γ+1)6 + (α>0)3 + (β+1) of row i at e nk + i, row i <-> κ1 = κ - K + i.  ph: e^{iω_k τ_c}.
+bool build_triad(const rsw_params* p, double T0, int M, std::vector<double>& Wout, std::vector<double2>& ph) {
   const int n = p->n, K = n / 3;
   const double s = std::sqrt(0.5), sF = std::sqrt(p->F);
-  std::vector<double> w(M, 0.0);
+  std::vector<double> w(M, 0.0), dtau(M, 0.0);
   double tot = 0.0;
   for (int m = 1; m <= M - 1; ++m) {
     const double sm = double(m) / M;
     w[m] = std::exp(-1.0 / (sm * (1.0 - sm)));
     tot += w[m];
   }
-  for (int m = 1; m <= M - 1; ++m) w[m] /= tot;
-  // e^{iω_k τ_m}, k = 0..K, m = 1..M-1
-  std::vector<cd> ph((size_t)M * (K + 1));
+  const double tc = 0.5 * T0 / p->eps;
   for (int m = 1; m <= M - 1; ++m) {
-    const double tau = (T0 * double(m) / double(M)) / p->eps;
-    for (int k = 0; k <= K; ++k) {
-      const double a = double(k) / sF, om = std::sqrt(1.0 + a * a);
-      ph[(size_t)m * (K + 1) + k] = cd(std::cos(om * tau), std::sin(om * tau));
-    }
+    w[m] /= tot;
+    dtau[m] = (T0 * double(m) / double(M)) / p->eps - tc;
   }
+  auto omega = [&](int k) { const double a = k / sF; return std::sqrt(1.0 + a * a); };
+  ph.resize(K + 1);
+  for (int k = 0; k <= K; ++k) ph[k] = make_double2(std::cos(omega(k) * tc), std::sin(omega(k) * tc));
   const size_t rows = (size_t)rsw::triad_rows_before(K + 1, K);
-  Wout.assign(rows * rsw::TRIAD_E, make_double2(0.0, 0.0));
+  Wout.assign(rows * rsw::TRIAD_E, 0.0);
   const cd I(0.0, 1.0);
-  std::vector<cd> e1(M), e2(M), e3(M);
+  bool pure = true;
   for (int kap = 0; kap <= K; ++kap) {
     const int nk = rsw::triad_nk(kap, K);
-    double2* blk = Wout.data() + (size_t)rsw::TRIAD_E * rsw::triad_rows_before(kap, K);
-    const double a = kap / sF, om = std::sqrt(1.0 + a * a), pp = 1.0 / (std::sqrt(2.0) * om), q = 1.0 / om;
+    double* blk = Wout.data() + (size_t)rsw::TRIAD_E * rsw::triad_rows_before(kap, K);
+    const double a = kap / sF, om = omega(kap), pp = 1.0 / (std::sqrt(2.0) * om), q = 1.0 / om;
     const cd B[3][3] = {{s * kap, -pp, -pp * a * kap}, {0.0, I * q * a, -I * q * double(kap)}, {-s * kap, -pp, -pp * a * kap}};
     for (int i = 0; i < nk; ++i) {
-      const int k1 = kap - K + i, k2 = K - i, ak1 = std::abs(k1), ak2 = std::abs(k2);
-      const double a2 = k2 / sF, om2 = std::sqrt(1.0 + a2 * a2), p2 = 1.0 / (std::sqrt(2.0) * om2), q2 = 1.0 / om2;
+      const int k1 = kap - K + i, k2 = K - i;
+      const double om1 = omega(std::abs(k1)), om2 = omega(std::abs(k2));
+      const double a2 = k2 / sF, p2 = 1.0 / (std::sqrt(2.0) * om2), q2 = 1.0 / om2;
       const cd A0[2] = {-I * s, I * s};                                        // α = -1, +1
       const cd A[3][3] = {{-I * s, 0.0, I * s},                                // X0: β = -1, 0, +1
                           {I * double(k2) * p2, -double(k2) * a2 * q2, I * double(k2) * p2},  // X1
@@ -294,22 +295,16 @@ void build_triad(const rsw_params* p, double T0, int M, std::vector<double2>& Wo
           for (int b = 0; b < 3; ++b) {
             cd T = 0.0;
             for (int f = 0; f < 3; ++f) T += B[g][f] * h[f] * A0[ai] * A[f][b];
-            // Φ: e^{i(γω_κ - αω_κ1 - βω_κ2)τ_m} = P(κ)^γ P(κ1)^{-α} P(κ2)^{-β}
-            cd Phi = 0.0;
-            const int gam = g - 1, al = ai ? 1 : -1, be = b - 1;
-            for (int m = 1; m <= M - 1; ++m) {
-              const cd* P = ph.data() + (size_t)m * (K + 1);
-              cd e = 1.0;
-              if (gam) e *= gam > 0 ? P[kap] : std::conj(P[kap]);
-              e *= al > 0 ? std::conj(P[ak1]) : P[ak1];
-              if (be) e *= be > 0 ? std::conj(P[ak2]) : P[ak2];
-              Phi += w[m] * e;
-            }
-            const cd v = Phi * T;
-            blk[(size_t)(g * 6 + ai * 3 + b) * nk + i] = make_double2(v.real(), v.imag());
+            const double lam = (g - 1) * om - (ai ? 1.0 : -1.0) * om1 - (b - 1) * om2;
+            double R = 0.0;
+            for (int m = 1; m <= M - 1; ++m) R += w[m] * std::cos(lam * dtau[m]);
+            const bool re = (g == 1) == (b == 1);
+            if ((re ? T.imag() : T.real()) != 0.0) pure = false;
+            blk[(size_t)(g * 6 + ai * 3 + b) * nk + i] = R * (re ? T.real() : T.imag());
           }
     }
   }
+  return pure;
 }
 
 // the triad form runs where its coefficient blocks fit a CTA's shared memory (n <= 256) unless
@@ -319,22 +314,23 @@ bool triad_enabled(int n) {
   return n <= 256 && !(e && e[0] == '0');
 }
 
-cudaError_t get_triad(const rsw_params* p, double T0, int M, const double2** out) {
-  *out = nullptr;
+cudaError_t get_triad(const rsw_params* p, double T0, int M, rsw::AvgTab* at) {
+  at->triad = nullptr;
+  at->triad_ph = nullptr;
   if (!triad_enabled(p->n)) return cudaSuccess;
   auto key = std::make_tuple(cur_dev(), p->n, p->eps, p->F, T0, M);
   auto it = g_triad.find(key);
-  if (it != g_triad.end()) {
-    *out = (const double2*)it->second->W.p;
-    return cudaSuccess;
+  if (it == g_triad.end()) {
+    std::vector<double> W;
+    std::vector<double2> ph;
+    if (!build_triad(p, T0, M, W, ph)) return cudaErrorInvalidValue;  // (a coefficient not purely real / imaginary)
+    auto t = std::make_unique<TriadTables>();
+    cudaError_t e;
+    if ((e = upload(t->W, W)) || (e = upload(t->ph, ph))) return e;
+    it = g_triad.emplace(key, std::move(t)).first;
   }
-  std::vector<double2> W;
-  build_triad(p, T0, M, W);
-  auto t = std::make_unique<TriadTables>();
-  cudaError_t e;
-  if ((e = upload(t->W, W))) return e;
-  *out = (const double2*)t->W.p;
-  g_triad[key] = std::move(t);
+  at->triad = (const double*)it->second->W.p;
+  at->triad_ph = (const double2*)it->second->ph.p;
   return cudaSuccess;
 }
 
@@ -477,7 +473,7 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   ch.M = M;
   ch.dT = dT;
   ch.at = rsw::AvgTab{geom_of(g), (const double*)at->w.p, (const double2*)at->phase.p, (const double2*)g->tw.p};
-  CUDA_TRY(get_triad(p, T0, M, &ch.at.triad));
+  CUDA_TRY(get_triad(p, T0, M, &ch.at));
   rsw::CoarseArgs& ca = ch.ca;
   ca.g = geom_of(g);
   ca.part = nullptr;  // (the sweep's partials and stage inputs live in the die-homed arena)
@@ -639,7 +635,10 @@ rsw_status run_chain(const Chain& ch, Workspace* ws, double* r_out, cudaStream_t
       d += h[(i + 1) * 4] - h[i * 4 + 3];
       ++cnt;
     }
-    if (h[256])
+    if (h[256] && ch.at.triad)
+      fprintf(stderr, "[rsw coarse n=%d] triad phase cycles: poll %llu, sync %llu, contraction %llu, sync %llu, combine %llu\n",
+              ch.p->n, h[257] - h[256], h[258] - h[257], h[259] - h[258], h[260] - h[259], h[261] - h[260]);
+    else if (h[256])
       fprintf(stderr, "[rsw coarse n=%d] samples phase cycles: load y %llu, prologue %llu, N-eval %llu, epilogue %llu, store %llu\n",
               ch.p->n, h[261] - h[256], h[257] - h[261], h[258] - h[257], h[259] - h[258],
               h[260] - h[259]);
@@ -793,7 +792,7 @@ double rsw_flops_per_unit(int32_t n, int32_t which) {
     case 1: return 4.0 * FN + 180.0 * Kr;
     case 2: return 2.0 * FN + 52.0 * Kr;
     case 3: return FN + 40.0 * Kr;
-    case 4: return 180.0 * (double)rsw::triad_rows_before(n / 3 + 1, n / 3);
+    case 4: return 108.0 * (double)rsw::triad_rows_before(n / 3 + 1, n / 3);
     default: return 0.0;
   }
 }
@@ -904,9 +903,10 @@ rsw_status rsw_triad_coefficients(const rsw_params* p, double T0, int32_t M, dou
   const int K = p->n / 3;
   *count = (int64_t)rsw::TRIAD_E * rsw::triad_rows_before(K + 1, K);
   if (!out) return RSW_OK;
-  std::vector<double2> W;
-  build_triad(p, T0, M, W);
-  std::memcpy(out, W.data(), sizeof(double2) * W.size());
+  std::vector<double> W;
+  std::vector<double2> ph;
+  if (!build_triad(p, T0, M, W, ph)) return fail(RSW_ERR_CONFIG, "triad coefficients: a coefficient is not purely real / imaginary");
+  std::memcpy(out, W.data(), sizeof(double) * W.size());
   return RSW_OK;
 }
 
@@ -975,7 +975,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   rsw::PipeArgs a{};
   a.ft = rsw::FineTab{geom_of(g), (const double2*)ft->cp.p, (const double*)ft->c0.p, (const double2*)g->tw.p};
   a.at = rsw::AvgTab{geom_of(g), (const double*)at->w.p, (const double2*)at->phase.p, (const double2*)g->tw.p};
-  CUDA_TRY(get_triad(p, cfg->T0, M, &a.at.triad));
+  CUDA_TRY(get_triad(p, cfg->T0, M, &a.at));
   a.base.g = geom_of(g);
   a.base.scheme = cfg->coarse_scheme;
   a.base.dT = cfg->dT;
@@ -1052,8 +1052,12 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     // triad sweeps: a stage costs one hand-off plus the owned N̄ (~ owned modes x rows), no
     // sample rounds; NG concurrent sweeps (default 3: sweep g + 3 starts after sweep g ends, which is
     // before the fine lags would let it start anyway) of the largest GC that fits them on the dies
+    // (measured on C3: 4 owned modes per CTA, GC = 22-24, beat 3 (GC = 37) — the CTAs left without a coarse
+    // role run a second fine group; 5 owned modes no longer fit the coefficient blocks in shared memory)
     const int ngw = std::max(1, std::min(en ? atoi(en) : 3, K + 1));
-    int gc = std::max(1, grid / ngw);
+    const char* eo = getenv("RSW_PIPE_TRIAD_NOWN");
+    const int nown_t = std::max(1, std::min(8, eo ? atoi(eo) : 4));
+    int gc = std::min(std::max(1, grid / ngw), (Km + 1 + nown_t - 1) / nown_t);
     if (ws->die_ok && grid == ws->die_n[0] + ws->die_n[1] && !getenv("RSW_NO_DIE_AWARE"))
       while (gc > 1 && std::min(ws->die_n[0] / gc, rsw::kMaxDieGroups) + std::min(ws->die_n[1] / gc, rsw::kMaxDieGroups) < ngw) --gc;
     a.GC = std::max(gc, (Km + 1 + 7) / 8);  // <= 8 owned modes per CTA
@@ -1123,7 +1127,7 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
       const int nown = (Km + 1 + a.GC - 1) / a.GC;
       size_t mx = 0;
       for (int c = 0; c < a.GC; ++c) mx = std::max(mx, rsw::triad_local_entries(Km, c, a.GC, nown));
-      a.wsm = sizeof(double2) * mx;
+      a.wsm = sizeof(double) * mx;
     }
     // the final layout's kernel (its template depends on the pairs / modes per CTA) must still fit
     size_t cap2 = 0;
@@ -1281,8 +1285,24 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
       cyc += (sp[(i + 1) * 4] - sp[i * 4]) * 1e-3;
       ++cs;
     }
+    {  // per RK stage of the slice (the last one also finalizes the slice and starts the next)
+      const int nst = cfg->coarse_scheme == 0 ? 4 : 2;
+      for (int q = 0; q < nst; ++q) {
+        double t[3] = {0, 0, 0};
+        int c = 0;
+        for (int i = q; i + 1 < 64; i += nst) {
+          if (!sp[i * 4] || !sp[(i + 1) * 4]) continue;
+          t[0] += (sp[i * 4 + 1] - sp[i * 4]) * 1e-3;
+          t[1] += (sp[i * 4 + 2] - sp[i * 4 + 1]) * 1e-3;
+          t[2] += (sp[i * 4 + 3] - sp[i * 4 + 2]) * 1e-3;
+          ++c;
+        }
+        if (c) fprintf(stderr, "[rsw pipe]   stage %d of %d (us): %.2f  %.2f  %.2f\n", q + 1, nst, t[0] / c, t[1] / c, t[2] / c);
+      }
+    }
     if (cs)
-      fprintf(stderr, "[rsw pipe] sweep 0 stage (us): samples+poll %.2f  barrier %.2f  update %.2f  total %.2f\n",
+      fprintf(stderr, a.at.triad ? "[rsw pipe] sweep 0 stage (us): poll %.2f  triad N-bar %.2f  update %.2f  total %.2f\n"
+                                 : "[rsw pipe] sweep 0 stage (us): samples+poll %.2f  barrier %.2f  update %.2f  total %.2f\n",
               ph[0] / cs, ph[1] / cs, ph[2] / cs, cyc / cs);
     // stage-input hand-off: the last owner's publication vs CTA 0's own, and the arrival at CTA 0
     const unsigned long long* hd = sp + 256;

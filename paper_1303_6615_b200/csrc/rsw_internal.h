@@ -25,7 +25,8 @@ struct AvgTab {
   const double* w;
   const double2* phase;
   const double2* tw;
-  const double2* triad = nullptr;  // triad coefficients W (rsw_blocks.cuh), or null: the M-sample quadrature
+  const double* triad = nullptr;      // triad coefficients W (rsw_blocks.cuh), or null: the M-sample quadrature
+  const double2* triad_ph = nullptr;  // e^{iω_k τ_c}, k = 0..K: the triad form's frame rotation
 };
 
 // Arguments of the coarse combine kernel (one state chain)
@@ -62,7 +63,10 @@ struct CoarseArgs {
 constexpr int kMaxPeers = 8;  // ranks of one NVSwitch node
 // stage-input ring depth of the triad coarse sweeps (rsw_blocks.cuh); the exchange arrays always hold
 // this many stage-input buffers (the quadrature sweeps use the first three)
-constexpr int TRIAD_NB = 8;
+#ifndef RSW_TRIAD_NB
+#define RSW_TRIAD_NB 16
+#endif
+constexpr int TRIAD_NB = RSW_TRIAD_NB;  // power of two >= 8 (ring reset distance NB/2, fence every NB/4 publications)
 __host__ __device__ constexpr unsigned yin_pages(int n) { return (TRIAD_NB * 3u * (2u * (unsigned)(n / 3) + 1u) + 255u) / 256u; }
 
 // triad coefficient table of N̄ (rsw_blocks.cuh triad_stage_phase, rsw_capi.cu build_triad)

@@ -80,9 +80,13 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   double* SW = sd + LY::SW;       // [2]
   // per-CTA constants for the whole sweep: geometry, twiddles, and the phases / weights of this
   // CTA's sample pair (TRIAD: the coefficient blocks of the owned modes)
-  double2* Wl = sr.wsm ? smem + (LY::bytes + 15) / 16 : nullptr;  // (null: read the global table)
+  // (after the layout and the triad's owned constants; null: read the global table)
+  double* Wl = sr.wsm ? reinterpret_cast<double*>(smem + (LY::bytes + sizeof(double) * NOWN * 8 + 15) / 16) : nullptr;
+  // TRIAD: owned-mode constants after the double slots, frame rotation in the (unused) phase slots
+  double* gsm = TRIAD ? reinterpret_cast<double*>(smem + LY::D) + LY::ND : nullptr;
   if constexpr (TRIAD) {
     if (Wl) triad_stage_table<N, NOWN>(tab.triad, Wl, rank, sr.P, threadIdx.x, T);
+    owned_consts<N, NOWN>(ca, tab.triad_ph, gsm, smem + LY::PH, rank, sr.P, threadIdx.x, T);
   }
   else fill_packed_twiddles<N, R, T>(TW, tab.tw);
   for (int k = threadIdx.x; k <= K; k += T) {
@@ -117,17 +121,18 @@ __global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const A
   for (int i = rank * T + threadIdx.x; i < NB * Kc3; i += P * T) st_relaxed_v2(ax.y(i), yin_sentinel());
   grid_barrier(bar, P, epoch);
   coarse_update_phase<N, T, NOWN, CtaGroup, HomedX, TRIAD>(ca, ax, 0, 0, Vs, KSs, kk, un_s, red, rdb, yv, yidx, ucount,
-                                                           rank, (int)P);  // slice 0: v = e^{ΔT D̂/2} U_0
+                                                           rank, (int)P, CtaGroup(), nullptr, gsm);  // slice 0: v = e^{ΔT D̂/2} U_0
   for (int n = 0; n < ca.n_end; ++n) {
     if constexpr (TRIAD) {
       for (int st = 1; st <= nst; ++st) {
         if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 0] = gtimer();
-        triad_stage_phase<N, T, NOWN, CtaGroup, HomedX>(ax, (size_t)(ucount % NB) * Kc3, Wl, tab.triad, C, A, kk, rank, (int)P,
-                                                        CtaGroup());
+        triad_stage_phase<N, T, NOWN, CtaGroup, HomedX>(ax, (size_t)(ucount % NB) * Kc3, Wl, tab.triad, smem + LY::PH, C, A, kk, rank, (int)P,
+                                                        CtaGroup(), nullptr, 0, nullptr, nullptr, nullptr,
+                                                        (prof && ps == 8) ? ca.prof + 256 : nullptr);
         if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 1] = ca.prof[ps * 4 + 2] = gtimer();
         ++ucount;
         coarse_update_phase<N, T, NOWN, CtaGroup, HomedX, TRIAD>(ca, ax, st, n, Vs, KSs, kk, un_s, red, rdb, yv, yidx,
-                                                                 ucount, rank, (int)P);
+                                                                 ucount, rank, (int)P, CtaGroup(), nullptr, gsm);
         if (prof && threadIdx.x == 0 && ps < 64) ca.prof[ps * 4 + 3] = gtimer();
         ++ps;
       }
@@ -291,16 +296,16 @@ static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& 
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
   SweepRun sr{pl, -1, grid, 0};
-  size_t sm = CoarseLayout<N, R, T, NOWN>::bytes;
+  size_t sm = CoarseLayout<N, R, T, NOWN>::bytes + (TRIAD ? sizeof(double) * NOWN * 8 : 0);  // (+ owned constants)
   if (TRIAD) {  // + the largest owned-block copy of the coefficient table, when it fits
     size_t mx = 0;
     for (int r = 0; r < grid; ++r) mx = std::max(mx, triad_local_entries(N / 3, r, grid, NOWN));
     int optin = 0;
     if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
-    const size_t sw = (sm + 15) / 16 * 16 + sizeof(double2) * mx;
+    const size_t sw = (sm + 15) / 16 * 16 + sizeof(double) * mx;
     if (sw <= (size_t)optin) {
       sm = sw;
-      sr.wsm = sizeof(double2) * mx;
+      sr.wsm = sizeof(double) * mx;
     }
   }
   int launch = grid;

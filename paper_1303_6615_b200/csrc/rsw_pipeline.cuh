@@ -125,8 +125,8 @@ template <int N, int T, int NOWN>
 struct TriadCoarseLayout {
   static constexpr int K = N / 3, Kc = 2 * K + 1, NR = (T > NOWN * 6 ? T : NOWN * 6);
   static constexpr int C = 0, HP = C + 3 * Kc, VS = HP + NOWN * 6, KS = VS + NOWN * 6, KK = KS + NOWN * 6,
-                       UN = KK + NOWN * 6, YV = UN + NOWN * 3, D = YV + NOWN * 6;
-  static constexpr int RED = 0, YI = RED + NR, ND = YI + NOWN * 6;
+                       UN = KK + NOWN * 6, YV = UN + NOWN * 3, RPH = YV + NOWN * 6, D = RPH + K + 1;
+  static constexpr int RED = 0, YI = RED + NR, GS = YI + NOWN * 6, ND = GS + NOWN * 8;
   static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
 };
 
@@ -310,8 +310,11 @@ __device__ __forceinline__ void coarse_role_triad(const PipeArgs& a, const Named
   double* sd = reinterpret_cast<double*>(cs + TL::D);
   double* red = sd + TL::RED;
   int* yidx = reinterpret_cast<int*>(sd + TL::YI);
-  double2* Wl = a.wsm ? smem + (LY::bytes + 15) / 16 : nullptr;  // (null: read the global table)
+  double* gsm = sd + TL::GS;
+  double2* rph = cs + TL::RPH;
+  double* Wl = a.wsm ? reinterpret_cast<double*>(smem + (LY::bytes + 15) / 16) : nullptr;  // (null: read the global table)
   if (Wl) triad_stage_table<N, NOWN>(a.at.triad, Wl, c, P, ct, TC);
+  owned_consts<N, NOWN>(a.base, a.at.triad_ph, gsm, rph, c, P, ct, TC);
   cg.sync();
   constexpr unsigned YP = yin_pages(N);
   const unsigned PPG = ((unsigned)(M / 2 > 0 ? M / 2 : 1) * Kc3 + 255) / 256, GPG = 1 + YP + PPG;
@@ -350,7 +353,7 @@ __device__ __forceinline__ void coarse_role_triad(const PipeArgs& a, const Named
     ca.prof = nullptr;
     unsigned ucount = 0;
     coarse_update_phase<N, TC, NOWN, NamedGroup, HomedX, true>(ca, ax, 0, 0, Vs, KSs, kk, un_s, red, nullptr, yv, yidx,
-                                                               ucount, c, P, cg);
+                                                               ucount, c, P, cg, nullptr, gsm);
     bool aborted = false;
     for (int n = 0; n < S && !aborted; ++n) {
       for (int st = 1; st <= nst; ++st) {
@@ -359,15 +362,14 @@ __device__ __forceinline__ void coarse_role_triad(const PipeArgs& a, const Named
                                             ((n - 8) * nst + st - 1) * 4
                                       : nullptr;
         if (stp) stp[0] = gtimer();
-        if (triad_stage_phase<N, TC, NOWN, NamedGroup, HomedX>(ax, (size_t)(ucount % NB) * Kc3, Wl, a.at.triad, C, HP, kk, c, P, cg,
-                                                               a.stopk, k, a.wd, a.hb)) {
+        if (triad_stage_phase<N, TC, NOWN, NamedGroup, HomedX>(ax, (size_t)(ucount % NB) * Kc3, Wl, a.at.triad, rph, C, HP, kk, c, P, cg,
+                                                               a.stopk, k, a.wd, a.hb, stp ? stp + 1 : nullptr)) {
           aborted = true;
           break;
         }
-        if (stp) stp[1] = stp[2] = gtimer();
         ++ucount;
         coarse_update_phase<N, TC, NOWN, NamedGroup, HomedX, true>(ca, ax, st, n, Vs, KSs, kk, un_s, red, nullptr, yv,
-                                                                   yidx, ucount, c, P, cg);
+                                                                   yidx, ucount, c, P, cg, nullptr, gsm);
         if (stp) stp[3] = gtimer();
       }
       if (!aborted) {

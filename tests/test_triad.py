@@ -12,8 +12,8 @@ import paper_1303_6615_b200 as rsw
 from paper_1303_6615_b200 import inputs
 
 
-def triad_nbar(W, u, n, F):
-    """N̄ (primitive half spectrum) from the triad table in the layout rsw.h documents."""
+def triad_nbar(W, u, n, F, eps, T0):
+    """N̄ (primitive half spectrum) from the triad table in the layout and rotated frame rsw.h documents."""
     K = n // 3
     s = np.sqrt(0.5)
     uc = u[..., 0] + 1j * u[..., 1]
@@ -26,16 +26,21 @@ def triad_nbar(W, u, n, F):
     t = p * (uh[1] - 1j * a * uh[2])
     isu0 = 1j * s * uh[0]
     y = np.array([t + isu0, q * (uh[2] - 1j * a * uh[1]), t - isu0])  # (c-, c0, c+) = R^H û
+    tc = 0.5 * T0 / eps
+    y = y * np.array([np.exp(1j * om * tc), np.ones_like(om), np.exp(-1j * om * tc)])  # c'^α = c^α e^{-iαωτ_c}
+    # the coefficient of entry (γ, α, β) is real when (γ = 0) == (β = 0), else i times the stored value
+    unit = np.array([[1, 1j, 1], [1j, 1, 1j], [1, 1j, 1]])[:, None, :]  # [γ][1][β]
     out = np.zeros((3, n // 2 + 1), complex)
     off = 0
     for kap in range(K + 1):
         nk = 2 * K + 1 - kap
-        blk = W[off:off + 18 * nk].reshape(3, 2, 3, nk)
+        blk = W[off:off + 18 * nk].reshape(3, 2, 3, nk) * unit[..., None]
         off += 18 * nk
         i = np.arange(nk)
         k1, k2 = kap - K + i, K - i
         c = np.einsum("gabi,ai,bi->g", blk, y[[0, 2]][:, k1 + K], y[:, k2 + K])
         om_k = np.sqrt(1 + kap * kap / F)
+        c = c * np.exp(1j * np.array([-1, 0, 1]) * om_k * tc)  # back: × e^{iγωτ_c}
         ak, pk, qk = kap / np.sqrt(F), 1 / (np.sqrt(2) * om_k), 1 / om_k
         d, e = c[2] - c[0], c[2] + c[0]
         out[:, kap] = [1j * s * d, pk * e + 1j * ak * qk * c[1], qk * c[1] + 1j * ak * pk * e]
@@ -54,7 +59,7 @@ def test_triad_table_reproduces_quadrature(n, M, cfg):
     ref = oracle.averaged_rhs(u, w.eps, w.F, w.mu, n, w.T0, M)
     for b in range(2):
         refc = ref[b, ..., 0] + 1j * ref[b, ..., 1]
-        out = triad_nbar(W, u[b], n, w.F)
+        out = triad_nbar(W, u[b], n, w.F, w.eps, w.T0)
         assert np.abs(out - refc).max() <= 1e-13 * np.abs(refc).max()
 
 
