@@ -402,28 +402,45 @@ def main():
     p4 = rsw.Params(w4.eps, w4.F, w4.mu, w4.n)
     s4 = 4096 // world
     u4 = torch.from_numpy(inputs.random_states(w4.n, s4, seed=100 + rank)).cuda()
-    a4 = []
-    for r in range(4):
-        flush.fill_(1.0)
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rsw.averaged_rhs(p4, u4, w4.T0, w4.M, validate=(r == 0))
-        e1.record(stream)
-        e1.synchronize()
-        if r:
-            a4.append(e0.elapsed_time(e1))
-    t = torch.tensor([statistics.median(a4)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    c4_ms = float(t.item())
-    c4_tf = 4096 * (w4.M - 1) * rsw.flops_per_unit(w4.n, "sample") / (c4_ms * 1e-3) / 1e12
+    def time_c4():
+        a4 = []
+        for r in range(4):
+            flush.fill_(1.0)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rsw.averaged_rhs(p4, u4, w4.T0, w4.M, validate=(r == 0))
+            e1.record(stream)
+            e1.synchronize()
+            if r:
+                a4.append(e0.elapsed_time(e1))
+        t = torch.tensor([statistics.median(a4)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # default: N-bar in triad form (the same quadrature sum, 108 flops per (kappa, kappa1) row);
+    # beside it the per-sample pseudo-spectral kernel (RSW_COARSE_TRIAD=0), canonical flops per sample
+    c4_ms = time_c4()
+    c4_tf = 4096 * rsw.flops_per_unit(w4.n, "triad") / (c4_ms * 1e-3) / 1e12
+    os.environ["RSW_COARSE_TRIAD"] = "0"
+    try:
+        c4q_ms = time_c4()
+    finally:
+        del os.environ["RSW_COARSE_TRIAD"]
+    c4q_tf = 4096 * (w4.M - 1) * rsw.flops_per_unit(w4.n, "sample") / (c4q_ms * 1e-3) / 1e12
     avg_c4 = {"workload": "C4 averaged-nonlinearity batch (4096 states, n=512, M=256)", "states_total": 4096,
-              "states_per_rank": s4, "ms_max_over_ranks": c4_ms,
-              "sample_evals_per_s": 4096 * (w4.M - 1) / (c4_ms * 1e-3), "achieved_tflops": c4_tf,
+              "states_per_rank": s4, "ms_max_over_ranks": c4_ms, "form": "triad (DESIGN §6d)",
+              "states_per_s": 4096 / (c4_ms * 1e-3), "sample_evals_per_s": 4096 * (w4.M - 1) / (c4_ms * 1e-3),
+              "achieved_tflops": c4_tf, "flops_per_state": rsw.flops_per_unit(w4.n, "triad"),
               "frac": c4_tf / (nominal_peak * world), "frac_of_measured": c4_tf / (measured_peak * world),
-              "kernel": "k_avg_states<512,8,192> (state, accumulator and twiddles in TMEM)",
-              **measured_flops("k_avg_states C4 per sample-eval", c4_tf / world, nominal_peak)}
+              "kernel": "k_avg_triad<512,4,256> (coefficients streamed from L2, 4 states per CTA)",
+              "speedup_vs_quadrature": c4q_ms / c4_ms,
+              "quadrature": {"ms_max_over_ranks": c4q_ms, "achieved_tflops": c4q_tf,
+                             "flops_per_state": (w4.M - 1) * rsw.flops_per_unit(w4.n, "sample"),
+                             "frac": c4q_tf / (nominal_peak * world), "frac_of_measured": c4q_tf / (measured_peak * world),
+                             "kernel": "k_avg_states<512,8,192> (state, accumulator and twiddles in TMEM)",
+                             **measured_flops("k_avg_states C4 per sample-eval", c4q_tf / world, nominal_peak)}}
     del u4
 
     # ---- C5 (BASELINE configs[4]) time per parareal iteration at this rank count (bulk schedule: the

@@ -98,7 +98,9 @@ rsw_status rsw_fine_propagate(const rsw_params* p, int32_t scheme, uint32_t flag
    Alg.1; kernel ρ P:383-390), for n_states independent states:
      N̄(v) = Σ_{m=1}^{M-1} w_m e^{τ_m L̂} N(e^{-τ_m L̂} v),  τ_m = s_m/ε, s_m = T0 m/M  (R4),
      w_m = ρ(m/M) / Σ_j ρ(j/M),  ρ(s) = exp(-1/(s(1-s)))  (R5).
-   The sum over samples is evaluated in ascending m (deterministic).  rhs_out must not alias. */
+   The sum over samples is evaluated in ascending m (deterministic).  For n <= 512 the sum is taken in
+   triad form (rsw_triad_coefficients: the same quadrature sum, reordered exactly; RSW_COARSE_TRIAD=0
+   selects the per-sample pseudo-spectral evaluation).  rhs_out must not alias. */
 rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n_states,
                             const double* u_in, double* rhs_out, void* stream);
 
@@ -114,10 +116,10 @@ rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n
    contraction in the rotated frame: c'^α_k = c^α_k e^{-iαω_k τ_c},  N̄^γ_κ = e^{iγω_κ τ_c} Σ W' c' c'
    (× i for the imaginary ones).  Layout: block κ = 0..K starts at 18 (κ(2K+1) - κ(κ-1)/2); inside it
    entry e = (γ+1) 6 + (α > 0) 3 + (β+1) of row i (κ1 = κ - K + i, i = 0..2K-κ) is at e (2K+1-κ) + i.
-   The coarse sweeps (rsw_coarse_propagate, parareal_iterate) evaluate N̄ in this form for n <= 256
-   (environment RSW_COARSE_TRIAD=0: the M-sample quadrature instead); rsw_averaged_rhs always uses
-   the quadrature.  *count receives the number of doubles; out may be NULL (size query).  Pure host
-   computation (no GPU needed); RSW_ERR_CONFIG on bad parameters or n > 256. */
+   The coarse sweeps (rsw_coarse_propagate, parareal_iterate) evaluate N̄ in this form for n <= 256,
+   rsw_averaged_rhs for n <= 512 (environment RSW_COARSE_TRIAD=0: the M-sample quadrature instead).
+   *count receives the number of doubles; out may be NULL (size query).  Pure host computation (no GPU
+   needed); RSW_ERR_CONFIG on bad parameters or n > 512. */
 rsw_status rsw_triad_coefficients(const rsw_params* p, double T0, int32_t M, double* out, int64_t* count);
 
 /* Coarse propagator φ̄_ΔT (Alg.2, φ̄ P:415-417) for n_states independent states:

@@ -32,7 +32,7 @@ def compile_cmd(src: str, obj: str) -> list[str]:
 
 def link_cmd(objs: list[str], out: str) -> list[str]:
     return [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-ccbin", _host_cxx(),
-            *objs, "-o", out, "-ldl"]
+            *objs, "-o", out, "-ldl", "-lpthread"]
 
 
 def stale() -> bool:

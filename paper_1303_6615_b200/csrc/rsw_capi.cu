@@ -6,7 +6,9 @@
 #include <nvtx3/nvToolsExt.h>  // header-only; inert unless a profiler (nsys, ncu) injects its library
 
 #include <cmath>
+#include <atomic>
 #include <complex>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -275,8 +277,21 @@ bool build_triad(const rsw_params* p, double T0, int M, std::vector<double>& Wou
   const size_t rows = (size_t)rsw::triad_rows_before(K + 1, K);
   Wout.assign(rows * rsw::TRIAD_E, 0.0);
   const cd I(0.0, 1.0);
-  bool pure = true;
-  for (int kap = 0; kap <= K; ++kap) {
+  const double dl = T0 / (double(M) * p->eps);  // τ_{m+1} - τ_m
+  std::atomic<bool> pure{true};
+  // R(λ) = Σ_m w_m cos(λ dτ_m) with e^{iλ dτ_m} by rotation (one complex product per sample; error ~M ulp)
+  auto Rof = [&](double lam) {
+    const cd step(std::cos(lam * dl), std::sin(lam * dl));
+    cd z(std::cos(lam * dtau[1]), std::sin(lam * dtau[1]));
+    double R = 0.0;
+    for (int m = 1; m <= M - 1; ++m) {
+      R += w[m] * z.real();
+      z *= step;
+    }
+    return R;
+  };
+  // κ blocks split over host threads (C4-size tables: 0.8 M coefficients x M samples)
+  auto block = [&](int kap) {
     const int nk = rsw::triad_nk(kap, K);
     double* blk = Wout.data() + (size_t)rsw::TRIAD_E * rsw::triad_rows_before(kap, K);
     const double a = kap / sF, om = omega(kap), pp = 1.0 / (std::sqrt(2.0) * om), q = 1.0 / om;
@@ -296,28 +311,36 @@ bool build_triad(const rsw_params* p, double T0, int M, std::vector<double>& Wou
             cd T = 0.0;
             for (int f = 0; f < 3; ++f) T += B[g][f] * h[f] * A0[ai] * A[f][b];
             const double lam = (g - 1) * om - (ai ? 1.0 : -1.0) * om1 - (b - 1) * om2;
-            double R = 0.0;
-            for (int m = 1; m <= M - 1; ++m) R += w[m] * std::cos(lam * dtau[m]);
+            const double R = Rof(lam);
             const bool re = (g == 1) == (b == 1);
             if ((re ? T.imag() : T.real()) != 0.0) pure = false;
             blk[(size_t)(g * 6 + ai * 3 + b) * nk + i] = R * (re ? T.real() : T.imag());
           }
     }
-  }
+  };
+  const int nth = std::max(1, std::min(16, (int)std::thread::hardware_concurrency()));
+  std::atomic<int> next{0};
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nth; ++t)
+    pool.emplace_back([&] {
+      for (int kap; (kap = next.fetch_add(1)) <= K;) block(kap);
+    });
+  for (auto& th : pool) th.join();
   return pure;
 }
 
 // the triad form runs where its coefficient blocks fit a CTA's shared memory (n <= 256) unless
 // RSW_COARSE_TRIAD=0 selects the M-sample quadrature
-bool triad_enabled(int n) {
+bool triad_enabled(int n, int max_n = 256) {
   const char* e = getenv("RSW_COARSE_TRIAD");
-  return n <= 256 && !(e && e[0] == '0');
+  return n <= max_n && !(e && e[0] == '0');
 }
 
-cudaError_t get_triad(const rsw_params* p, double T0, int M, rsw::AvgTab* at) {
+// max_n: 256 for the coarse sweeps (the owned blocks in shared memory), 512 for the batched N̄
+cudaError_t get_triad(const rsw_params* p, double T0, int M, rsw::AvgTab* at, int max_n = 256) {
   at->triad = nullptr;
   at->triad_ph = nullptr;
-  if (!triad_enabled(p->n)) return cudaSuccess;
+  if (!triad_enabled(p->n, max_n)) return cudaSuccess;
   auto key = std::make_tuple(cur_dev(), p->n, p->eps, p->F, T0, M);
   auto it = g_triad.find(key);
   if (it == g_triad.end()) {
@@ -889,6 +912,7 @@ rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n
   CUDA_TRY(get_geom(p, &g));
   CUDA_TRY(get_avg(p, T0, M, &at));
   rsw::AvgTab tab{geom_of(g), (const double*)at->w.p, (const double2*)at->phase.p, (const double2*)g->tw.p};
+  CUDA_TRY(get_triad(p, T0, M, &tab, 512));  // triad form for n <= 512 (RSW_COARSE_TRIAD=0: quadrature)
   CUDA_TRY(rsw::launch_avg_states(p->n, u_in, rhs_out, n_states, M, tab, (cudaStream_t)stream));
   return RSW_OK;
 }
@@ -896,7 +920,7 @@ rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n
 rsw_status rsw_triad_coefficients(const rsw_params* p, double T0, int32_t M, double* out, int64_t* count) {
   rsw_status s = check_params(p);
   if (s != RSW_OK) return s;
-  if (p->n > 256) return fail(RSW_ERR_CONFIG, "triad coefficients: n must be <= 256");
+  if (p->n > 512) return fail(RSW_ERR_CONFIG, "triad coefficients: n must be <= 512");
   if (!finite_pos(T0)) return fail(RSW_ERR_CONFIG, "T0 must be finite and > 0");
   if (M < 2) return fail(RSW_ERR_CONFIG, "M must be >= 2");
   if (!count) return fail(RSW_ERR_CONFIG, "NULL count");

@@ -279,6 +279,127 @@ static cudaError_t launch_avg_n(const double* in, double* out, int S, int M, con
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Batched N̄ in triad form (P:1113-1118 with Alg.1's quadrature in the coefficients): a CTA
+// takes B states, stages their eigen coordinates in the rotated frame (c'^α = c^α e^{-iαωτ_c}) in shared
+// memory, and computes N̄_κ, κ = 0..K, for all of them.  A warp works on one κ at a time: lane
+// (s, r) = (lane / RG, lane % RG) accumulates state s over the rows i ≡ r (mod RG) in ascending order
+// (each coefficient load serves the warp's B states — RG distinct addresses per load, consecutive rows),
+// a fixed xor tree over the RG lanes of a state sums them.  The coefficients (6.3 MB at n = 512) stream
+// from L2; the per-state work is 60 DP instructions per (κ, κ1) row instead of M - 1 pseudo-spectral
+// N-evals (C4: 4.7 vs 21.9 Mflop per state).
+// ---------------------------------------------------------------------------------------------
+template <int N, int B>
+struct AvgTriadLayout {  // Y[B][3][Kc] rotated eigen states, the frame rotation e^{iω_k τ_c}
+  static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
+  static constexpr int Y = 0, RPH = Y + B * 3 * Kc, D = RPH + KP;
+  static constexpr size_t bytes = sizeof(double2) * D;
+};
+
+template <int N, int B, int T>
+__global__ void __launch_bounds__(T) k_avg_triad(const double* __restrict__ u_in, double* __restrict__ out,
+                                                 int n_states, const AvgTab tab) {
+  using LY = AvgTriadLayout<N, B>;
+  constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NH = N / 2 + 1, RG = 32 / B;
+  static_assert(B * RG == 32, "k_avg_triad: B states x RG row groups per warp");
+  extern __shared__ double2 smem[];
+  double2* Y = smem + LY::Y;
+  double2* RPH = smem + LY::RPH;
+  const int s0 = blockIdx.x * B;
+  for (int k = threadIdx.x; k <= K; k += T) RPH[k] = __ldg(tab.triad_ph + k);
+  __syncthreads();
+  // stage: primitive half spectra -> eigen coordinates of both signs of κ -> rotated frame
+  for (int t = threadIdx.x; t < B * Kc; t += T) {
+    const int s = t / Kc, j = t - s * Kc, kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
+    double2 c[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    if (s0 + s < n_states) {
+      const double2* U = reinterpret_cast<const double2*>(u_in) + (size_t)(s0 + s) * 3 * NH;
+      double2 z[3];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) z[f] = kap < 0 ? cconj(__ldg(U + f * NH + ak)) : __ldg(U + f * NH + ak);
+      const double as = kap < 0 ? -__ldg(tab.g.a + ak) : __ldg(tab.g.a + ak);
+      to_eigen(as, __ldg(tab.g.p + ak), __ldg(tab.g.q + ak), z, c);
+      const double2 r = RPH[ak];
+      c[0] = cmul(c[0], r);
+      c[2] = cmulc(c[2], r);
+    }
+#pragma unroll
+    for (int al = 0; al < 3; ++al) Y[(s * 3 + al) * Kc + j] = c[al];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, sl = lane / RG, r = lane % RG;
+  const double2* Ys = Y + sl * 3 * Kc;
+  for (int kap = threadIdx.x >> 5; kap <= K; kap += T / 32) {
+    const int nk = triad_nk(kap, K);
+    const double* Wb = tab.triad + (size_t)TRIAD_E * triad_rows_before(kap, K);
+    double2 acc[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    for (int i = r; i < nk; i += RG) {
+      double wv[18];
+#pragma unroll
+      for (int e = 0; e < 18; ++e) wv[e] = __ldg(Wb + (size_t)e * nk + i);
+      const int k1 = kap - K + i, k2 = K - i;
+      const int j1 = k1 >= 0 ? k1 : k1 + Kc, j2 = k2 >= 0 ? k2 : k2 + Kc;
+      const double2 am = Ys[j1], ap = Ys[2 * Kc + j1];
+      double2 pr[6];
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const double2 yb = Ys[b * Kc + j2];
+        pr[b] = make_double2(fma(am.x, yb.x, -am.y * yb.y), fma(am.x, yb.y, am.y * yb.x));
+        pr[3 + b] = make_double2(fma(ap.x, yb.x, -ap.y * yb.y), fma(ap.x, yb.y, ap.y * yb.x));
+      }
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {
+#pragma unroll
+        for (int ab2 = 0; ab2 < 6; ++ab2) {
+          const double w = wv[g * 6 + ab2];
+          if ((g == 1) == (ab2 % 3 == 1)) {
+            acc[g].x = fma(w, pr[ab2].x, acc[g].x);
+            acc[g].y = fma(w, pr[ab2].y, acc[g].y);
+          } else {
+            acc[g].x = fma(-w, pr[ab2].y, acc[g].x);
+            acc[g].y = fma(w, pr[ab2].x, acc[g].y);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 3; ++g)
+      for (int m = RG / 2; m > 0; m >>= 1) {
+        acc[g].x += __shfl_xor_sync(0xffffffffu, acc[g].x, m);
+        acc[g].y += __shfl_xor_sync(0xffffffffu, acc[g].y, m);
+      }
+    if (r == 0 && s0 + sl < n_states) {  // back from the rotated frame (× e^{iγωτ_c}), to the primitive spectrum
+      const double2 ph = RPH[kap];
+      const double2 c[3] = {cmulc(acc[0], ph), acc[1], cmul(acc[2], ph)};
+      double2 u[3];
+      to_prim(__ldg(tab.g.a + kap), __ldg(tab.g.p + kap), __ldg(tab.g.q + kap), c, u);
+      if (kap == 0) u[0].y = u[1].y = u[2].y = 0.0;
+      double2* O = reinterpret_cast<double2*>(out) + (size_t)(s0 + sl) * 3 * NH;
+#pragma unroll
+      for (int f = 0; f < 3; ++f) O[f * NH + kap] = u[f];
+    }
+  }
+  // modes K < k <= N/2 are zero
+  for (int t = threadIdx.x; t < B * 3 * (NH - KP); t += T) {
+    const int s = t / (3 * (NH - KP)), q = t - s * 3 * (NH - KP), f = q / (NH - KP), k = KP + q % (NH - KP);
+    if (s0 + s < n_states) reinterpret_cast<double2*>(out)[(size_t)(s0 + s) * 3 * NH + f * NH + k] = make_double2(0.0, 0.0);
+  }
+}
+
+#ifndef RSW_AVG_TRIAD_B
+#define RSW_AVG_TRIAD_B 4  // states per CTA of the batched triad N̄ (x 32/B row groups per warp); C4: 4 -> 3.44 ms, 8 -> 7.90 ms (1 CTA per SM)
+#endif
+template <int N>
+static cudaError_t launch_avg_triad_n(const double* in, double* out, int S, const AvgTab& tab, cudaStream_t st) {
+  constexpr int B = RSW_AVG_TRIAD_B, T = 256;
+  auto kfn = k_avg_triad<N, B, T>;
+  constexpr size_t sm = AvgTriadLayout<N, B>::bytes;
+  cudaError_t e = set_smem(kfn, sm);
+  if (e != cudaSuccess) return e;
+  kfn<<<(S + B - 1) / B, T, sm, st>>>(in, out, S, tab);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_nonlinear(int n, const double* in, double* out, int S, const FineTab& tab, cudaStream_t st) {
 #define C(NN) launch_nl_n<NN>(in, out, S, tab, st)
   RSW_DISPATCH(n, C)
@@ -287,6 +408,17 @@ cudaError_t launch_nonlinear(int n, const double* in, double* out, int S, const 
 
 cudaError_t launch_avg_states(int n, const double* in, double* out, int S, int M, const AvgTab& tab,
                               cudaStream_t st) {
+  if (tab.triad) {  // triad form (n <= 512)
+    switch (n) {
+      case 16: return launch_avg_triad_n<16>(in, out, S, tab, st);
+      case 32: return launch_avg_triad_n<32>(in, out, S, tab, st);
+      case 64: return launch_avg_triad_n<64>(in, out, S, tab, st);
+      case 128: return launch_avg_triad_n<128>(in, out, S, tab, st);
+      case 256: return launch_avg_triad_n<256>(in, out, S, tab, st);
+      case 512: return launch_avg_triad_n<512>(in, out, S, tab, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
 #define C(NN) launch_avg_n<NN>(in, out, S, M, tab, st)
   RSW_DISPATCH(n, C)
 #undef C

@@ -48,7 +48,7 @@ def triad_nbar(W, u, n, F, eps, T0):
     return out
 
 
-@pytest.mark.parametrize("n,M,cfg", [(16, 8, "C1"), (64, 32, "C1"), (128, 64, "C2"), (256, 128, "C3")])
+@pytest.mark.parametrize("n,M,cfg", [(16, 8, "C1"), (64, 32, "C1"), (128, 64, "C2"), (256, 128, "C3"), (512, 32, "C4")])
 def test_triad_table_reproduces_quadrature(n, M, cfg):
     w = getattr(inputs, cfg)
     p = rsw.Params(w.eps, w.F, w.mu, n)
@@ -64,8 +64,8 @@ def test_triad_table_reproduces_quadrature(n, M, cfg):
 
 
 def test_triad_table_errors():
-    p = rsw.Params(0.01, 1.0, 1e-4, 512)
+    p = rsw.Params(0.01, 1.0, 1e-4, 1024)
     with pytest.raises(rsw.RSWError):
-        rsw.triad_coefficients(p, 0.05, 32)  # n > 256
+        rsw.triad_coefficients(p, 0.05, 32)  # n > 512
     with pytest.raises(rsw.RSWError):
         rsw.triad_coefficients(rsw.Params(0.01, 1.0, 1e-4, 64), 0.05, 1)  # M < 2
