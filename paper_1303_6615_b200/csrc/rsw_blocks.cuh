@@ -636,9 +636,9 @@ __device__ __forceinline__ void triad_stage_table(const double* __restrict__ Wg,
 // owned |κ| = rank + o P the 3 eigen entries γ of N̄_κ (coefficients from the shared-memory copy Wl, or
 // — Wl null, the copy does not fit next to the kernel's other buffers — from the global table Wg); the -κ entries by the real-field symmetry
 // N̄^γ_{-κ} = conj N̄^{-γ}_κ (the eigenbasis of -κ is the conjugate of +κ's with α reversed).  Fixed
-// summation order, independent of T, P and the warp that runs an item: for half h in {0, 1} lane l
-// sums rows i ≡ 32h + l (mod 64) in ascending i, a fixed xor tree sums the 32 lanes, then
-// N̄ = half 0 + half 1 — so the bulk and pipelined sweeps agree bitwise.  stopk (pipelined schedule):
+// summation order, independent of T, P and the warp that runs an item: for part h < NPART (triad_parts)
+// lane l sums rows i ≡ 32h + l (mod 32 NPART) in ascending i, a fixed xor tree sums the 32 lanes, then
+// N̄ = ((part 0 + part 1) + part 2) + ... — so the bulk and pipelined sweeps agree bitwise.  stopk (pipelined schedule):
 // the poll gives up once the run stopped before iteration kself, or the watchdog fired; returns true
 // then (the whole group takes the same decision on its own, every wait of a discarded sweep aborts).
 // per-sweep constants of the triad coarse CTAs in shared memory (the L1 left beside ~200 KB of shared
@@ -664,15 +664,32 @@ __device__ __forceinline__ void owned_consts(const CoarseArgs& ca, const double2
   for (int k = tid; k <= K; k += nthr) rph[k] = __ldg(rph_g + k);
 }
 
-// one lane's share of N̄_κ: rows i = i0, i0 + 64, ... (ascending), all 18 coefficients of a row loaded
+// warps per owned mode of the triad sweeps: 2 at n <= 256 (<= 171 rows), 4 above (683 rows at n = 1024)
+template <int N>
+__host__ __device__ constexpr int triad_parts() { return N <= 256 ? 2 : 4; }
+
+// one lane's share of N̄_κ: rows i = i0, i0 + 32 NPART, ... (ascending), all 18 coefficients of a row loaded
 // before its products are used (so the loads overlap), accumulated into acc[γ] in a fixed order
-template <int N, class LDW>
+// PREF: the next row's coefficients are loaded while this row is computed (coefficients from L2)
+template <int N, int NPART, bool PREF = false, class LDW>
 __device__ __forceinline__ void triad_rows(double2* acc, const double2* C, int kap, int nk, int i0, LDW ldw) {
   constexpr int K = N / 3, Kc = 2 * K + 1;
-  for (int i = i0; i < nk; i += 64) {
-    double wv[18];
+  double wn[18];
+  if (PREF && i0 < nk)
 #pragma unroll
-    for (int e = 0; e < 18; ++e) wv[e] = ldw(e, i);
+    for (int e = 0; e < 18; ++e) wn[e] = ldw(e, i0);
+  for (int i = i0; i < nk; i += 32 * NPART) {
+    double wv[18];
+    if (PREF) {
+#pragma unroll
+      for (int e = 0; e < 18; ++e) wv[e] = wn[e];
+      if (i + 32 * NPART < nk)
+#pragma unroll
+        for (int e = 0; e < 18; ++e) wn[e] = ldw(e, i + 32 * NPART);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 18; ++e) wv[e] = ldw(e, i);
+    }
     const int k1 = kap - K + i, k2 = K - i;
     const int j1 = k1 >= 0 ? k1 : k1 + Kc, j2 = k2 >= 0 ? k2 : k2 + Kc;
     const double2 am = C[j1], ap = C[2 * Kc + j1];
@@ -746,8 +763,9 @@ __device__ __forceinline__ bool triad_stage_phase(const AX& ax, size_t yoff, con
   TSTAMP(2)
   if (stamp && tid_ == 0) stamp[0] = gtimer();  // trace: the whole stage input has arrived
   const int lane = tid_ & 31;
-  for (int it = tid_ >> 5; it < 2 * NOWN; it += T / 32) {
-    const int o = it >> 1, hh = it & 1, kap = rank + o * P;
+  constexpr int NPART = triad_parts<N>();  // warps per owned mode (rows i ≡ 32h + l mod 32 NPART)
+  for (int it = tid_ >> 5; it < NPART * NOWN; it += T / 32) {
+    const int o = it / NPART, hh = it % NPART, kap = rank + o * P;
     if (kap > K) continue;  // (warp-uniform)
     const int nk = triad_nk(kap, K);
     double2 acc[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
@@ -757,14 +775,14 @@ __device__ __forceinline__ bool triad_stage_phase(const AX& ax, size_t yoff, con
       size_t lo = 0;
       for (int q = 0; q < o; ++q) lo += (size_t)TRIAD_E * triad_nk(rank + q * P, K);
       const unsigned wsh = (unsigned)__cvta_generic_to_shared(Wl + lo);
-      triad_rows<N>(acc, C, kap, nk, 32 * hh + lane, [&](int e, int i) {
+      triad_rows<N, NPART>(acc, C, kap, nk, 32 * hh + lane, [&](int e, int i) {
         double v;
         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(wsh + 8u * (unsigned)(e * nk + i)));
         return v;
       });
     } else {
       const double* Wb = Wg + (size_t)TRIAD_E * triad_rows_before(kap, K);
-      triad_rows<N>(acc, C, kap, nk, 32 * hh + lane, [&](int e, int i) { return __ldg(Wb + (size_t)e * nk + i); });
+      triad_rows<N, NPART, true>(acc, C, kap, nk, 32 * hh + lane, [&](int e, int i) { return __ldg(Wb + (size_t)e * nk + i); });
     }
 #pragma unroll
     for (int g = 0; g < 3; ++g)
@@ -774,7 +792,7 @@ __device__ __forceinline__ bool triad_stage_phase(const AX& ax, size_t yoff, con
       }
     if (lane == 0)
 #pragma unroll
-      for (int g = 0; g < 3; ++g) hp[(o * 2 + hh) * 3 + g] = acc[g];
+      for (int g = 0; g < 3; ++g) hp[(o * NPART + hh) * 3 + g] = acc[g];
   }
   TSTAMP(3)
   grp.sync();
@@ -782,7 +800,9 @@ __device__ __forceinline__ bool triad_stage_phase(const AX& ax, size_t yoff, con
   if (tid_ < NOWN * 3) {
     const int o = tid_ / 3, g = tid_ % 3, kap = rank + o * P;
     if (kap <= K) {
-      double2 v = cadd(hp[(o * 2) * 3 + g], hp[(o * 2 + 1) * 3 + g]);
+      double2 v = hp[(o * NPART) * 3 + g];
+#pragma unroll
+      for (int h = 1; h < NPART; ++h) v = cadd(v, hp[(o * NPART + h) * 3 + g]);
       if (g != 1) {  // back from the rotated frame: × e^{iγωτ_c}
         const double2 r = RPH[kap];
         v = g == 0 ? cmulc(v, r) : cmul(v, r);

@@ -496,7 +496,7 @@ rsw_status setup_chain(Chain& ch, const rsw_params* p, int scheme, double dT, do
   ch.M = M;
   ch.dT = dT;
   ch.at = rsw::AvgTab{geom_of(g), (const double*)at->w.p, (const double2*)at->phase.p, (const double2*)g->tw.p};
-  CUDA_TRY(get_triad(p, T0, M, &ch.at));
+  CUDA_TRY(get_triad(p, T0, M, &ch.at, 1024));  // bulk sweeps: any n (coefficients in shared memory or L2)
   rsw::CoarseArgs& ca = ch.ca;
   ca.g = geom_of(g);
   ca.part = nullptr;  // (the sweep's partials and stage inputs live in the die-homed arena)
@@ -920,7 +920,7 @@ rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n
 rsw_status rsw_triad_coefficients(const rsw_params* p, double T0, int32_t M, double* out, int64_t* count) {
   rsw_status s = check_params(p);
   if (s != RSW_OK) return s;
-  if (p->n > 512) return fail(RSW_ERR_CONFIG, "triad coefficients: n must be <= 512");
+  if (p->n > 1024) return fail(RSW_ERR_CONFIG, "triad coefficients: n must be <= 1024");
   if (!finite_pos(T0)) return fail(RSW_ERR_CONFIG, "T0 must be finite and > 0");
   if (M < 2) return fail(RSW_ERR_CONFIG, "M must be >= 2");
   if (!count) return fail(RSW_ERR_CONFIG, "NULL count");
@@ -1633,7 +1633,7 @@ static rsw_status parareal_impl(const rsw_params* p, const parareal_config* cfg,
     stats->coarse_groups = 1;
     stats->group_ctas = 0;
     stats->die_aware = ws->sweep_die >= 0 ? 1 : 0;
-    stats->coarse_triad = (cfg->coarse_scheme != RSW_COARSE_STRANG && triad_enabled(p->n)) ? 1 : 0;
+    stats->coarse_triad = (cfg->coarse_scheme != RSW_COARSE_STRANG && triad_enabled(p->n, 1024)) ? 1 : 0;
   }
   if (status == RSW_NOT_CONVERGED) g_err = "parareal: tolerance not reached within max_iters";
   return status;

@@ -341,7 +341,7 @@ static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab
   // one sample pair per CTA, but enough CTAs that each owns <= 16 modes in the update phase;
   // at most one CTA per SM (co-residency of the cooperative launch).  Triad form: two owned modes per
   // CTA (one warp per half of a mode's rows)
-  const bool triad = N <= 256 && tab.triad != nullptr;
+  const bool triad = tab.triad != nullptr;
   int grid = triad ? (K + 2) / 2 : M / 2;
   if (grid < (K + 1 + 15) / 16) grid = (K + 1 + 15) / 16;
   if (grid > sms) grid = sms;
@@ -351,12 +351,11 @@ static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab
   if (die_used) *die_used = -1;
   const int nown = (K + 1 + grid - 1) / grid;  // owned modes per CTA in the update phase
   if (grid_used) *grid_used = grid;
-  if constexpr (N <= 256) {
-    if (triad) {
-      if (nown <= 1) return launch_coarse_sweep_nown<N, 1, true>(ca, tab, M, pl, r_out, grid, on_die, die_used, st);
-      if (nown <= 2) return launch_coarse_sweep_nown<N, 2, true>(ca, tab, M, pl, r_out, grid, on_die, die_used, st);
-      return cudaErrorInvalidConfiguration;
-    }
+  if (triad) {
+    if (nown <= 1) return launch_coarse_sweep_nown<N, 1, true>(ca, tab, M, pl, r_out, grid, on_die, die_used, st);
+    if (nown <= 2) return launch_coarse_sweep_nown<N, 2, true>(ca, tab, M, pl, r_out, grid, on_die, die_used, st);
+    if (nown <= 4) return launch_coarse_sweep_nown<N, 4, true>(ca, tab, M, pl, r_out, grid, on_die, die_used, st);
+    return cudaErrorInvalidConfiguration;
   }
 #define L_(NO) launch_coarse_sweep_nown<N, NO>(ca, tab, M, pl, r_out, grid, on_die, die_used, st)
   if (nown <= 1) return L_(1);

@@ -333,10 +333,18 @@ __global__ void __launch_bounds__(T) k_avg_triad(const double* __restrict__ u_in
     const int nk = triad_nk(kap, K);
     const double* Wb = tab.triad + (size_t)TRIAD_E * triad_rows_before(kap, K);
     double2 acc[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    // the next row's coefficients (L2) are in flight while this row is computed
+    double wn[18];
+    if (r < nk)
+#pragma unroll
+      for (int e = 0; e < 18; ++e) wn[e] = __ldg(Wb + (size_t)e * nk + r);
     for (int i = r; i < nk; i += RG) {
       double wv[18];
 #pragma unroll
-      for (int e = 0; e < 18; ++e) wv[e] = __ldg(Wb + (size_t)e * nk + i);
+      for (int e = 0; e < 18; ++e) wv[e] = wn[e];
+      if (i + RG < nk)
+#pragma unroll
+        for (int e = 0; e < 18; ++e) wn[e] = __ldg(Wb + (size_t)e * nk + i + RG);
       const int k1 = kap - K + i, k2 = K - i;
       const int j1 = k1 >= 0 ? k1 : k1 + Kc, j2 = k2 >= 0 ? k2 : k2 + Kc;
       const double2 am = Ys[j1], ap = Ys[2 * Kc + j1];
