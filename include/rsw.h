@@ -116,10 +116,10 @@ rsw_status rsw_averaged_rhs(const rsw_params* p, double T0, int32_t M, int32_t n
    contraction in the rotated frame: c'^α_k = c^α_k e^{-iαω_k τ_c},  N̄^γ_κ = e^{iγω_κ τ_c} Σ W' c' c'
    (× i for the imaginary ones).  Layout: block κ = 0..K starts at 18 (κ(2K+1) - κ(κ-1)/2); inside it
    entry e = (γ+1) 6 + (α > 0) 3 + (β+1) of row i (κ1 = κ - K + i, i = 0..2K-κ) is at e (2K+1-κ) + i.
-   The coarse sweeps (rsw_coarse_propagate, parareal_iterate) evaluate N̄ in this form for n <= 256,
-   rsw_averaged_rhs for n <= 512 (environment RSW_COARSE_TRIAD=0: the M-sample quadrature instead).
-   *count receives the number of doubles; out may be NULL (size query).  Pure host computation (no GPU
-   needed); RSW_ERR_CONFIG on bad parameters or n > 512. */
+   The coarse sweeps (rsw_coarse_propagate, parareal_iterate) evaluate N̄ in this form (pipelined
+   schedule n <= 256, bulk any n), rsw_averaged_rhs for n <= 512 (environment RSW_COARSE_TRIAD=0: the
+   M-sample quadrature everywhere).  *count receives the number of doubles; out may be NULL (size
+   query).  Pure host computation (no GPU needed); RSW_ERR_CONFIG on bad parameters. */
 rsw_status rsw_triad_coefficients(const rsw_params* p, double T0, int32_t M, double* out, int64_t* count);
 
 /* Coarse propagator φ̄_ΔT (Alg.2, φ̄ P:415-417) for n_states independent states:

@@ -64,8 +64,8 @@ def test_triad_table_reproduces_quadrature(n, M, cfg):
 
 
 def test_triad_table_errors():
-    p = rsw.Params(0.01, 1.0, 1e-4, 1024)
+    p = rsw.Params(0.01, 1.0, 1e-4, 2048)
     with pytest.raises(rsw.RSWError):
-        rsw.triad_coefficients(p, 0.05, 32)  # n > 512
+        rsw.triad_coefficients(p, 0.05, 32)  # n > 1024
     with pytest.raises(rsw.RSWError):
         rsw.triad_coefficients(rsw.Params(0.01, 1.0, 1e-4, 64), 0.05, 1)  # M < 2
