@@ -671,9 +671,17 @@ __host__ __device__ constexpr int triad_parts() { return N <= 256 ? 2 : 4; }
 // one lane's share of N̄_κ: rows i = i0, i0 + 32 NPART, ... (ascending), all 18 coefficients of a row loaded
 // before its products are used (so the loads overlap), accumulated into acc[γ] in a fixed order
 // PREF: the next row's coefficients are loaded while this row is computed (coefficients from L2)
+#ifndef RSW_TRIAD_SPLIT
+#define RSW_TRIAD_SPLIT 0  // 1: separate accumulators for the α = -1 and α = +1 terms (12 FMA chains per lane, not 6): measured neutral-to-worse (C3 22.9 vs 22.6 ms)
+#endif
 template <int N, int NPART, bool PREF = false, class LDW>
-__device__ __forceinline__ void triad_rows(double2* acc, const double2* C, int kap, int nk, int i0, LDW ldw) {
-  constexpr int K = N / 3, Kc = 2 * K + 1;
+__device__ __forceinline__ void triad_rows(double2* acc_out, const double2* C, int kap, int nk, int i0, LDW ldw) {
+  constexpr int K = N / 3, Kc = 2 * K + 1, NA = RSW_TRIAD_SPLIT ? 2 : 1;
+  double2 acc[NA][3];
+#pragma unroll
+  for (int a = 0; a < NA; ++a)
+#pragma unroll
+    for (int g = 0; g < 3; ++g) acc[a][g] = make_double2(0.0, 0.0);
   double wn[18];
   if (PREF && i0 < nk)
 #pragma unroll
@@ -705,16 +713,19 @@ __device__ __forceinline__ void triad_rows(double2* acc, const double2* C, int k
 #pragma unroll
       for (int ab2 = 0; ab2 < 6; ++ab2) {
         const double w = wv[g * 6 + ab2];
+        double2& A = acc[NA == 2 ? ab2 / 3 : 0][g];
         if ((g == 1) == (ab2 % 3 == 1)) {  // real coefficient
-          acc[g].x = fma(w, pr[ab2].x, acc[g].x);
-          acc[g].y = fma(w, pr[ab2].y, acc[g].y);
+          A.x = fma(w, pr[ab2].x, A.x);
+          A.y = fma(w, pr[ab2].y, A.y);
         } else {  // imaginary coefficient i w
-          acc[g].x = fma(-w, pr[ab2].y, acc[g].x);
-          acc[g].y = fma(w, pr[ab2].x, acc[g].y);
+          A.x = fma(-w, pr[ab2].y, A.x);
+          A.y = fma(w, pr[ab2].x, A.y);
         }
       }
     }
   }
+#pragma unroll
+  for (int g = 0; g < 3; ++g) acc_out[g] = NA == 2 ? cadd(acc[0][g], acc[1][g]) : acc[0][g];
 }
 
 template <int N, int T, int NOWN, class GRP = CtaGroup, class AX = FlatX>
@@ -782,7 +793,10 @@ __device__ __forceinline__ bool triad_stage_phase(const AX& ax, size_t yoff, con
       });
     } else {
       const double* Wb = Wg + (size_t)TRIAD_E * triad_rows_before(kap, K);
-      triad_rows<N, NPART, true>(acc, C, kap, nk, 32 * hh + lane, [&](int e, int i) { return __ldg(Wb + (size_t)e * nk + i); });
+      // (next-row prefetch where the global table is the rule, n >= 512; at n <= 256 it is a rare fallback
+      // whose extra registers cost the pipelined kernel's shared-memory path: C3 22.4 -> 25.5 ms)
+      triad_rows<N, NPART, (N >= 512)>(acc, C, kap, nk, 32 * hh + lane,
+                                       [&](int e, int i) { return __ldg(Wb + (size_t)e * nk + i); });
     }
 #pragma unroll
     for (int g = 0; g < 3; ++g)
