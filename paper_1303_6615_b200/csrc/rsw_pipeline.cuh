@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
       cg.sync();  // every coarse thread is past the sweeps: the coarse region of smem is free
       }  // !TRIAD
     }
-    if (s_role[0] < 0 || RSW_PIPE_REUSE_COARSE) extra_fine();
+    if ((s_role[0] < 0 && a.extra_fine) || RSW_PIPE_REUSE_COARSE) extra_fine();
   } else {
     // ======================================= fine worker group 0 =======================================
     const int gi = ((int)threadIdx.x - FB) / TG;
