@@ -102,7 +102,12 @@ def test_fine_in_place(rsw_gpu, orc):
 @pytest.mark.parametrize("n,eps,T0,M", [(16, 1e-2, 0.05, 8), (32, 1e-2, 0.05, 16), (64, 1e-2, 0.05, 32),
                                         (128, 1e-2, 0.05, 64), (256, 1e-3, 0.01, 128), (512, 1e-3, 0.01, 256),
                                         (1024, 1e-4, 0.002, 16)])
-def test_averaged_rhs(rsw_gpu, orc, n, eps, T0, M):
+@pytest.mark.parametrize("form", ["triad", "quadrature"])
+def test_averaged_rhs(rsw_gpu, orc, n, eps, T0, M, form, monkeypatch):
+    """Both evaluations of N̄ (triad form for n <= 512, else / RSW_COARSE_TRIAD=0 the
+    per-sample pseudo-spectral kernel) against the oracle's Alg.1 quadrature."""
+    if form == "quadrature":
+        monkeypatch.setenv("RSW_COARSE_TRIAD", "0")
     nb = 3 if n < 512 else 2
     u = inputs.random_states(n, nb, seed=11)
     got = to_np(rsw_gpu.averaged_rhs(P(rsw_gpu, eps, 1.0, 1e-5, n), dev(u), T0, M))
@@ -220,9 +225,13 @@ def test_parareal_c5_prefix(rsw_gpu, k):
     assert rel_l2(to_np(g["U"])[1:9], ref[1:9], w.n).max() < TOL
 
 
-def test_averaged_rhs_c4_full_size_sampled(rsw_gpu, orc):
-    """C4 at full size (4096 states, n = 512, M = 256) in the bench's launch configuration; the oracle
-    evaluates sampled states one by one (first and last pair, a pair in the middle)."""
+@pytest.mark.parametrize("form", ["triad", "quadrature"])
+def test_averaged_rhs_c4_full_size_sampled(rsw_gpu, orc, form, monkeypatch):
+    """C4 at full size (4096 states, n = 512, M = 256) in the bench's launch configurations (triad form,
+    and the per-sample kernel beside it); the oracle evaluates sampled states one by one (first and
+    last pair, a pair in the middle)."""
+    if form == "quadrature":
+        monkeypatch.setenv("RSW_COARSE_TRIAD", "0")
     w = inputs.C4
     u = inputs.initial_state(w)
     assert u.shape[0] == 4096
