@@ -1076,10 +1076,13 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
 #undef USTAMP
 }
 
-template <int N, int R, int T, int NOWN, int NPC = 1, int SPLIT = 1>
+// LEAN (triad sweeps): no FFT buffers or twiddles (X, Y, TW empty); A holds the triad half-sums, PH the
+// frame rotation
+template <int N, int R, int T, int NOWN, int NPC = 1, int SPLIT = 1, bool LEAN = false>
 struct CoarseLayout {  // dynamic shared memory of a coarse-sweep CTA (double2 units, then doubles); NPC cached pairs
   static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NR = (T > NOWN * 6 ? T : NOWN * 6);
-  static constexpr int X = 0, Y = X + 3 * N, TW = X + SPLIT * 6 * N, C = TW + fft_tw_size<N, R>(), A = C + 3 * Kc,
+  static constexpr int X = 0, Y = LEAN ? 0 : X + 3 * N, TW = LEAN ? 0 : X + SPLIT * 6 * N,
+                       C = TW + (LEAN ? 0 : fft_tw_size<N, R>()), A = C + 3 * Kc,
                        VS = A + 3 * Kc, KS = VS + NOWN * 6, KK = KS + NOWN * 6, UN = KK + NOWN * 6,
                        RDB = UN + NOWN * 3, PH = RDB + T, YV = PH + NPC * 2 * KP, D = YV + NOWN * 6;
   static constexpr int RED = 0, GA = RED + NR, GP = GA + KP, GQ = GP + KP, SW = GQ + KP, YI = SW + 2 * NPC,

@@ -36,10 +36,11 @@ struct SweepRun {
 // TRIAD: N̄ in triad form (rsw_blocks.cuh triad_stage_phase): each CTA keeps the coefficient blocks of its
 // owned modes in shared memory (after the layout's LY::bytes), a stage is poll -> owned N̄ -> update with
 // no grid barrier (stage-input ring of TRIAD_NB buffers)
+// (triad sweeps at n >= 512: two 256-thread CTAs per SM, so registers are capped at 128)
 template <int N, int R, int T, int NOWN, bool TRIAD = false>
-__global__ void __launch_bounds__(T) k_coarse_sweep(const CoarseArgs ca, const AvgTab tab, int M, const SweepRun sr,
+__global__ void __launch_bounds__(T, (TRIAD && N >= 512) ? 2 : 1) k_coarse_sweep(const CoarseArgs ca, const AvgTab tab, int M, const SweepRun sr,
                                                     double* r_out) {
-  using LY = CoarseLayout<N, R, T, NOWN>;
+  using LY = CoarseLayout<N, R, T, NOWN, 1, 1, TRIAD>;
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
   extern __shared__ double2 smem[];
   __shared__ int s_rank;
@@ -296,7 +297,7 @@ static cudaError_t launch_coarse_sweep_nown(const CoarseArgs& ca, const AvgTab& 
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
   SweepRun sr{pl, -1, grid, 0};
-  size_t sm = CoarseLayout<N, R, T, NOWN>::bytes + (TRIAD ? sizeof(double) * NOWN * 8 : 0);  // (+ owned constants)
+  size_t sm = CoarseLayout<N, R, T, NOWN, 1, 1, TRIAD>::bytes + (TRIAD ? sizeof(double) * NOWN * 8 : 0);  // (+ owned constants)
   if (TRIAD) {  // + the largest owned-block copy of the coefficient table, when it fits
     size_t mx = 0;
     for (int r = 0; r < grid; ++r) mx = std::max(mx, triad_local_entries(N / 3, r, grid, NOWN));
@@ -351,6 +352,15 @@ static cudaError_t launch_coarse_sweep_n(const CoarseArgs& ca, const AvgTab& tab
   if (die_used) *die_used = -1;
   const int nown = (K + 1 + grid - 1) / grid;  // owned modes per CTA in the update phase
   if (grid_used) *grid_used = grid;
+  if constexpr (N >= 512) {
+    // n >= 512: the coefficients come from L2 and a mode has up to 683 rows: two owned modes per 256-thread
+    // CTA (four warps each), (K+2)/2 CTAs, two per SM (C5: 171 CTAs instead of 148 with 3 modes each)
+    if (triad && !getenv("RSW_TRIAD_WIDE_OFF")) {
+      const int g2 = (K + 2) / 2;
+      if (grid_used) *grid_used = g2;
+      return launch_coarse_sweep_nown<N, 2, true, coarse_radix<N>(), 256>(ca, tab, M, pl, r_out, g2, false, die_used, st);
+    }
+  }
   if (triad) {
     if (nown <= 1) return launch_coarse_sweep_nown<N, 1, true>(ca, tab, M, pl, r_out, grid, on_die, die_used, st);
     if (nown <= 2) return launch_coarse_sweep_nown<N, 2, true>(ca, tab, M, pl, r_out, grid, on_die, die_used, st);
