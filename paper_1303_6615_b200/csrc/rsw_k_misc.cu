@@ -296,8 +296,11 @@ struct AvgTriadLayout {  // Y[B][3][Kc] rotated eigen states, the frame rotation
   static constexpr size_t bytes = sizeof(double2) * D;
 };
 
+#ifndef RSW_AVG_TRIAD_MINB
+#define RSW_AVG_TRIAD_MINB 1
+#endif
 template <int N, int B, int T>
-__global__ void __launch_bounds__(T) k_avg_triad(const double* __restrict__ u_in, double* __restrict__ out,
+__global__ void __launch_bounds__(T, RSW_AVG_TRIAD_MINB) k_avg_triad(const double* __restrict__ u_in, double* __restrict__ out,
                                                  int n_states, const AvgTab tab) {
   using LY = AvgTriadLayout<N, B>;
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NH = N / 2 + 1, RG = 32 / B;

@@ -681,7 +681,7 @@ static inline cudaError_t launch_pipe_nf(const PipeArgs& a, int grid, size_t* ou
               LY::T, TC, NPG, TG, sm, per_sm);
     return cudaSuccess;
   }
-  if (getenv("RSW_PIPE_TRACE") && TRIAD)
+  if (TRIAD && getenv("RSW_PIPE_TRACE"))
     fprintf(stderr, "[rsw pipe] triad coefficients: %s (%zu B per CTA)\n", a2.wsm ? "shared memory" : "global table", a.wsm);
   void* args[] = {(void*)&a2};
   return cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(LY::T), args, sm, st);
