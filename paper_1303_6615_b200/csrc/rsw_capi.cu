@@ -1091,6 +1091,10 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   // 256 pairs per iteration); with few tasks (C2: 32) a second group on an SM only stretches the tasks
   // placed there (C2 23.6 vs 21.3 ms)
   a.extra_fine = (a.npairs / world >= grid || getenv("RSW_PIPE_EXTRA_FINE")) ? 1 : 0;
+  {
+    const char* ey = getenv("RSW_PIPE_EXTRA_YOUNG");
+    a.extra_young = (ey && ey[0] == '1') ? 1 : 0;
+  }
   if (a.GC > grid) {
     *unsupported = true;
     return fail(RSW_ERR_CONFIG, "pipelined schedule: not enough co-resident CTAs");

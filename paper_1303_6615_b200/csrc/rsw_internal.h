@@ -158,6 +158,7 @@ struct PipeArgs {
   unsigned* dticket;                 // [2]
   size_t wsm;                        // triad sweeps (at.triad != null): shared-memory bytes of the largest owned-block copy
   int extra_fine;                    // CTAs without a coarse role run a second fine group on their coarse threads
+  int extra_young;                   // ... which claims the most recently ready task (not the oldest)
 };
 bool pipeline_supported(int n);
 cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);

@@ -154,9 +154,11 @@ struct PipeLayout {
 
 // fine worker group: claim the lowest-iteration ready pair task (k, p) — slices 2p, 2p+1 of U^k, ready
 // when prog[k] covers them — run the fine pair integrator, write F^k, set doneF[k][p] (release)
+// young: claim the most recently ready task instead of the oldest (the second fine group of a CTA
+// without a coarse role: its tasks run slower beside the first, so it takes those with the most slack)
 template <int N, int RF, int TG, int FSCHEME, int TWT>
 __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedGroup grp, double2* W,
-                                                 const FineSmemTab& ft, uint32_t tcol, int* task) {
+                                                 const FineSmemTab& ft, uint32_t tcol, int* task, bool young = false) {
   constexpr size_t L = (size_t)3 * (N / 2 + 1) * 2;
   const int S = a.S, Kit = a.K, npairs = a.npairs;
   double2* Yb = W + 3 * N;
@@ -186,7 +188,7 @@ __device__ __forceinline__ void fine_worker_loop(const PipeArgs& a, const NamedG
           const int pp = a.pair_lo + (int)t;
           const int need = (2 * pp + 1 < S) ? 2 * pp + 1 : 2 * pp;
           const int age = (int)(ld_acquire_gpu(a.prog + k) / (unsigned)a.GC) - need;  // slices finalized past it
-          if (age >= 0 && age > bage) {
+          if (age >= 0 && (bage < 0 || (young ? age < bage : age > bage))) {
             bage = age;
             bk = k;
             bt = (int)t;
@@ -463,7 +465,8 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
       if (xi < XG && (NPG + XG) * LY::CPG <= 512)
         fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{CB + xi * TG, 1 + NPG + xi, TG},
                                             smem + LY::C0 + (size_t)xi * 6 * N, ft,
-                                            tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi]);
+                                            tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi],
+                                            a.extra_young != 0);
     };
     if (s_role[0] >= 0) {
       if constexpr (TRIAD) {
