@@ -58,6 +58,12 @@
 #ifndef RSW_PIPE_TRIAD_NPG
 #define RSW_PIPE_TRIAD_NPG 1
 #endif
+#ifndef RSW_PIPE_TRIAD_TMUL
+#define RSW_PIPE_TRIAD_TMUL 2  // threads of the fine group beside a triad coarse sub-CTA = TMUL x 3N/R
+#endif
+#ifndef RSW_PIPE_TRIAD_XMUL
+#define RSW_PIPE_TRIAD_XMUL 2  // ... and of the second fine group of a CTA without a coarse role (on the coarse threads)
+#endif
 
 namespace rsw {
 
@@ -138,7 +144,9 @@ struct PipeLayout {
   using TL = TriadCoarseLayout<N, TC, NOWN>;
   static constexpr int K = N / 3, KP = K + 1;
   // coarse region: the coarse sub-CTA's layout, or (CTAs without a coarse role) TC/TG extra fine groups' X/Y
-  static constexpr int XG = TC / TG;
+  // second fine groups on the coarse threads of CTAs without a coarse role: TGX threads each
+  static constexpr int TGX = TRIAD ? RSW_PIPE_TRIAD_XMUL * core_threads<N, RF>() : TG;
+  static constexpr int XG = TC / TGX;
   static constexpr size_t CB_ = TRIAD ? TL::bytes : CL::bytes;
   static constexpr size_t CREG = CB_ > sizeof(double2) * XG * 6 * N ? CB_ : sizeof(double2) * XG * 6 * N;
   static constexpr int C0 = 0, F0 = (int)((CREG + 15) / 16);  // double2 offsets of the coarse / fine regions
@@ -148,7 +156,8 @@ struct PipeLayout {
   // fine groups read their radix-R twiddles from TMEM whenever the transform keeps full tables (as k_fine
   // does: the two schedules must round alike)
   static constexpr int TWT = fft_tw_tcols<N, RF>() > 0 ? 2 : 0;
-  static constexpr int CPG = (FineTmem<N, TG>::COLS + (TWT == 2 ? fft_tw_tcols<N, RF>() : 0) + 31) / 32 * 32;  // TMEM columns per fine group
+  static constexpr int CPG0 = FineTmem<N, TG>::COLS > FineTmem<N, TGX>::COLS ? FineTmem<N, TG>::COLS : FineTmem<N, TGX>::COLS;
+  static constexpr int CPG = (CPG0 + (TWT == 2 ? fft_tw_tcols<N, RF>() : 0) + 31) / 32 * 32;  // TMEM columns per fine group
   static constexpr int T = TC + NPG * TG;
 };
 
@@ -411,7 +420,7 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
   __shared__ uint32_t tslot;
   __shared__ unsigned s_flag;
   __shared__ int s_role[3];  // coarse group (-1: none), rank in the group, die of the group's arrays
-  __shared__ int s_task[NPG + TC / TG][2];
+  __shared__ int s_task[NPG + LY::XG][2];
   const int warp = threadIdx.x >> 5;
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (threadIdx.x == 0) {  // role: coarse group g, rank c (or none); die-aware: from this SM's die ticket
@@ -460,10 +469,10 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
     // role, and in a coarse CTA once its group's sweeps are done (the later iterations' fine tasks are
     // then the bottleneck: each finished group adds GC fine groups)
     auto extra_fine = [&]() {
-      constexpr int XG = TC / TG;
-      const int xi = ct / TG;
+      constexpr int XG = LY::XG, TGX = LY::TGX;
+      const int xi = ct / TGX;
       if (xi < XG && (NPG + XG) * LY::CPG <= 512)
-        fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{CB + xi * TG, 1 + NPG + xi, TG},
+        fine_worker_loop<N, RF, TGX, FSCHEME, LY::TWT>(a, NamedGroup{CB + xi * TGX, 1 + NPG + xi, TGX},
                                             smem + LY::C0 + (size_t)xi * 6 * N, ft,
                                             tslot + (uint32_t)((NPG + xi) * LY::CPG), s_task[NPG + xi],
                                             a.extra_young != 0);
@@ -656,7 +665,7 @@ static inline cudaError_t launch_pipe_nf(const PipeArgs& a, int grid, size_t* ou
   constexpr int RC = coarse_radix<N>();
   constexpr int TC = TRIAD ? RSW_PIPE_TRIAD_TC
                            : (RSW_PIPE_COARSE_THREADS > coarse_threads<N>() ? RSW_PIPE_COARSE_THREADS : coarse_threads<N>());
-  constexpr int RF = fine_radix<N>(), TG = RSW_PIPE_FINE_TMUL * core_threads<N, RF>();
+  constexpr int RF = fine_radix<N>(), TG = (TRIAD ? RSW_PIPE_TRIAD_TMUL : RSW_PIPE_FINE_TMUL) * core_threads<N, RF>();
   constexpr int CPG = (FineTmem<N, TG>::COLS + 31) / 32 * 32;
   constexpr int NPG0 = TRIAD ? RSW_PIPE_TRIAD_NPG : RSW_PIPE_FINE_GROUPS;
   constexpr int NPG = NPG0 * CPG <= 512 ? NPG0 : 512 / CPG;
