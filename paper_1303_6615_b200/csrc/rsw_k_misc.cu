@@ -297,7 +297,7 @@ struct AvgTriadLayout {  // Y[B][3][Kc] rotated eigen states, the frame rotation
 };
 
 #ifndef RSW_AVG_TRIAD_MINB
-#define RSW_AVG_TRIAD_MINB 1
+#define RSW_AVG_TRIAD_MINB 2  // two CTAs per SM (registers 162 -> 108): C4 1.83 -> 1.56 ms; 3 (80 registers) 4.2 ms
 #endif
 template <int N, int B, int T>
 __global__ void __launch_bounds__(T, RSW_AVG_TRIAD_MINB) k_avg_triad(const double* __restrict__ u_in, double* __restrict__ out,
