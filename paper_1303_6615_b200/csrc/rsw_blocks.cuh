@@ -843,7 +843,9 @@ __device__ __forceinline__ void push_stage_input(const AX& ax, const double2* yv
   const int tid_ = grp.tid();
   constexpr int Kc3 = 3 * (2 * (N / 3) + 1);
   constexpr unsigned RB = NB == 3 ? 2u : (unsigned)(NB / 2);  // buffer reset: (u + RB) % NB
-  grp.sync();
+  // (each entry is published by the thread that computed it — yv[t], yidx[t] — so the triad sweeps need
+  // no barrier here; the quadrature sweeps keep theirs)
+  if (NB == 3) grp.sync();
   if (tid_ < NOWN * 6 && yidx[tid_] >= 0) {
     st_relaxed_v2(ax.y((size_t)(u % NB) * Kc3 + yidx[tid_]), yv[tid_]);
     st_relaxed_v2(ax.y((size_t)((u + RB) % NB) * Kc3 + yidx[tid_]), yin_sentinel());
@@ -874,6 +876,14 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
     j = (e < 3) ? ak : ((ak == 0) ? 0 : Kc - ak);
   };
   const bool last = (ca.scheme == 0) ? (stage == 4) : (stage == 2);
+  double2 *zU = nullptr, *zG = nullptr;  // finalize: the tail modes of U_{n+1} and G_n, zeroed off the critical path
+  auto zero_tail = [&]() {
+    if (zU)
+      for (int k = K + 1; k < NH; ++k) {
+        zU[k - K] = make_double2(0.0, 0.0);
+        zG[k - K] = make_double2(0.0, 0.0);
+      }
+  };
   // prefetch the finalize operands (F_n, old G_n, old U_{n+1}) before the reduction's L2 round trip
   double2 pf_F = make_double2(0.0, 0.0), pf_G = make_double2(0.0, 0.0), pf_U = make_double2(0.0, 0.0);
   if (stage > 0 && last && tid_ < NOWN * 3) {
@@ -1023,11 +1033,10 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
         *Gst = g;
         *Uo = un;
         un_s[tid_] = un;
-        if (ak == K)  // modes K < k <= N/2 stay zero
-          for (int k = K + 1; k < NH; ++k) {
-            Uo[k - K] = make_double2(0.0, 0.0);
-            Gst[k - K] = make_double2(0.0, 0.0);
-          }
+        if (ak == K) {  // modes K < k <= N/2 stay zero: written after the next stage input is out (zero_tail)
+          zU = Uo;
+          zG = Gst;
+        }
       }
     }
     grp.sync();
@@ -1040,7 +1049,10 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
       }
     }
     USTAMP(6)
-    if (n + 1 >= ca.n_end) return;  // no next slice
+    if (n + 1 >= ca.n_end) {  // no next slice
+      zero_tail();
+      return;
+    }
   } else {
     // stage 0: load U_0 of owned modes
     if (tid_ < NOWN * 3) {
@@ -1071,6 +1083,7 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
   }
   USTAMP(7)
   push_stage_input<N, NOWN, T, GRP, AX, TRIAD ? TRIAD_NB : 3>(ax, yv, yidx, ucount, grp);
+  zero_tail();
   grp.sync();
   USTAMP(8)
 #undef USTAMP
