@@ -1094,6 +1094,8 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   {
     const char* ey = getenv("RSW_PIPE_EXTRA_YOUNG");
     a.extra_young = (ey && ey[0] == '1') ? 1 : 0;
+    const char* es = getenv("RSW_PIPE_COARSE_SOLO");
+    a.coarse_solo = (es && es[0] == '1') ? 1 : 0;
   }
   if (a.GC > grid) {
     *unsupported = true;

@@ -159,6 +159,7 @@ struct PipeArgs {
   size_t wsm;                        // triad sweeps (at.triad != null): shared-memory bytes of the largest owned-block copy
   int extra_fine;                    // CTAs without a coarse role run a second fine group on their coarse threads
   int extra_young;                   // ... which claims the most recently ready task (not the oldest)
+  int coarse_solo;                   // CTAs with a coarse role run no fine group (RSW_PIPE_COARSE_SOLO=1)
 };
 bool pipeline_supported(int n);
 cudaError_t launch_parareal_pipe(int n, const PipeArgs& a, int fine_scheme, int grid, size_t* out, cudaStream_t st);

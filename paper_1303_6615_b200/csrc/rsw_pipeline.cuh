@@ -645,9 +645,14 @@ __global__ void __launch_bounds__(TC + NPG * TG, 1) k_parareal_pipe(const PipeAr
     if ((s_role[0] < 0 && a.extra_fine) || RSW_PIPE_REUSE_COARSE) extra_fine();
   } else {
     // ======================================= fine worker group 0 =======================================
+    // (coarse_solo: the CTAs of a coarse group leave their SM to the sweep, no fine work beside it)
+    if (a.coarse_solo && s_role[0] >= 0) goto fine_done;
+    {
     const int gi = ((int)threadIdx.x - FB) / TG;
     fine_worker_loop<N, RF, TG, FSCHEME, LY::TWT>(a, NamedGroup{FB + gi * TG, 1 + gi, TG, 0, (RSW_PIPE_FINE_WSWAP && !RSW_PIPE_COARSE_LOW && TG >= 128) ? 1 : 0}, smem + LY::F_G + (size_t)gi * 6 * N,
                                         ft, tslot + (uint32_t)(gi * LY::CPG), s_task[gi]);
+    }
+  fine_done:;
   }
   tmem_fence_before();
   __syncthreads();
