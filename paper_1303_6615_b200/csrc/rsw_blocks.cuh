@@ -853,12 +853,42 @@ __device__ __forceinline__ void push_stage_input(const AX& ax, const double2* yv
   }
 }
 
+// Early prefetch of the finalize operands (F_n, G_n of the previous sweep, U_{n+1} of the previous
+// iterate) at the start of a slice's last stage, when the fine task and the previous sweep's slice are
+// ALREADY complete (non-blocking acquire checks): their L2 round trip then overlaps the stage's N̄
+// instead of following it.  pre_ok[t] = 0 leaves the wait and the loads to coarse_update_phase.
+template <int N, int NOWN>
+__device__ __forceinline__ void finalize_early(const CoarseArgs& ca, int n, int rank, int P, int tid_, double2* pre,
+                                               int* pre_ok) {
+  constexpr int K = N / 3, NH = N / 2 + 1;
+  if (tid_ >= NOWN * 3) return;
+  const size_t Ls = (size_t)3 * NH;
+  const int o = tid_ / 3, f = tid_ % 3, ak = rank + o * P;
+  int ok = 0;
+  if (ak <= K) {
+    const bool fr = !ca.wF || (ca.wsys ? ld_acquire_sys(ca.wF + n / 2) : ld_acquire_gpu(ca.wF + n / 2)) >= 1u;
+    const bool pr = !ca.wprog || ld_acquire_gpu(ca.wprog) >= ca.wunit * (unsigned)(n + 1);
+    if (fr && pr) {
+      double2 F = make_double2(0.0, 0.0), G = make_double2(0.0, 0.0), U = make_double2(0.0, 0.0);
+      if (ca.F) F = __ldcg(reinterpret_cast<const double2*>(ca.F) + (size_t)n * Ls + f * NH + ak);
+      if (ca.F) G = __ldcg(reinterpret_cast<const double2*>(ca.Gprev) + (size_t)n * Ls + f * NH + ak);
+      if (ca.rparts) U = __ldcg(reinterpret_cast<const double2*>(ca.Uprev) + (size_t)(n + 1) * Ls + f * NH + ak);
+      pre[tid_ * 3] = F;
+      pre[tid_ * 3 + 1] = G;
+      pre[tid_ * 3 + 2] = U;
+      ok = 1;
+    }
+  }
+  pre_ok[tid_] = ok;
+}
+
 template <int N, int T, int NOWN, class GRP = CtaGroup, class AX = FlatX, bool TRIAD = false>
 __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const AX& ax, int stage, int n, double2* Vs,
                                                     double2* KSs, double2* kk, double2* un_s, double* nd_s,
                                                     double2* red_buf, double2* yv, int* yidx, unsigned ucount,
                                                     int rank = -1, int P = -1, const GRP& grp = GRP(),
-                                                    unsigned long long* cyc = nullptr, const double* gsm = nullptr) {
+                                                    unsigned long long* cyc = nullptr, const double* gsm = nullptr,
+                                                    const double2* pre = nullptr, const int* pre_ok = nullptr) {
   const int tid_ = grp.tid();
 #define USTAMP(i) \
   if (cyc && tid_ == 0) cyc[i] = clock64();
@@ -886,7 +916,11 @@ __device__ __forceinline__ void coarse_update_phase(const CoarseArgs& ca, const 
   };
   // prefetch the finalize operands (F_n, old G_n, old U_{n+1}) before the reduction's L2 round trip
   double2 pf_F = make_double2(0.0, 0.0), pf_G = make_double2(0.0, 0.0), pf_U = make_double2(0.0, 0.0);
-  if (stage > 0 && last && tid_ < NOWN * 3) {
+  if (stage > 0 && last && tid_ < NOWN * 3 && pre && pre_ok[tid_]) {  // early prefetch (finalize_early) succeeded
+    pf_F = pre[tid_ * 3];
+    pf_G = pre[tid_ * 3 + 1];
+    pf_U = pre[tid_ * 3 + 2];
+  } else if (stage > 0 && last && tid_ < NOWN * 3) {
     const int o = tid_ / 3, f = tid_ % 3, ak = rank + o * P;
     if (ak <= K) {
       // pipelined parareal: F(U^{k-1}_n) and the previous sweep's slice n must be complete

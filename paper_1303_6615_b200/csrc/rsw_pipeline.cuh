@@ -131,8 +131,9 @@ template <int N, int T, int NOWN>
 struct TriadCoarseLayout {
   static constexpr int K = N / 3, Kc = 2 * K + 1, NR = (T > NOWN * 6 ? T : NOWN * 6);
   static constexpr int C = 0, HP = C + 3 * Kc, VS = HP + NOWN * 6, KS = VS + NOWN * 6, KK = KS + NOWN * 6,
-                       UN = KK + NOWN * 6, YV = UN + NOWN * 3, RPH = YV + NOWN * 6, D = RPH + K + 1;
-  static constexpr int RED = 0, YI = RED + NR, GS = YI + NOWN * 6, ND = GS + NOWN * 8;
+                       UN = KK + NOWN * 6, YV = UN + NOWN * 3, RPH = YV + NOWN * 6, PRE = RPH + K + 1,
+                       D = PRE + NOWN * 9;
+  static constexpr int RED = 0, YI = RED + NR, GS = YI + NOWN * 6, POK = GS + NOWN * 8, ND = POK + NOWN * 3;
   static constexpr size_t bytes = sizeof(double2) * D + sizeof(double) * ND;
 };
 
@@ -323,6 +324,8 @@ __device__ __forceinline__ void coarse_role_triad(const PipeArgs& a, const Named
   int* yidx = reinterpret_cast<int*>(sd + TL::YI);
   double* gsm = sd + TL::GS;
   double2* rph = cs + TL::RPH;
+  double2* pre = cs + TL::PRE;
+  int* pre_ok = reinterpret_cast<int*>(sd + TL::POK);
   double* Wl = a.wsm ? reinterpret_cast<double*>(smem + (LY::bytes + 15) / 16) : nullptr;  // (null: read the global table)
   if (Wl) triad_stage_table<N, NOWN>(a.at.triad, Wl, c, P, ct, TC);
   owned_consts<N, NOWN>(a.base, a.at.triad_ph, gsm, rph, c, P, ct, TC);
@@ -373,6 +376,7 @@ __device__ __forceinline__ void coarse_role_triad(const PipeArgs& a, const Named
                                             ((n - 8) * nst + st - 1) * 4
                                       : nullptr;
         if (stp) stp[0] = gtimer();
+        if (st == nst && k > 0) finalize_early<N, NOWN>(ca, n, c, P, ct, pre, pre_ok);
         if (triad_stage_phase<N, TC, NOWN, NamedGroup, HomedX>(ax, (size_t)(ucount % NB) * Kc3, Wl, a.at.triad, rph, C, HP, kk, c, P, cg,
                                                                a.stopk, k, a.wd, a.hb, stp ? stp + 1 : nullptr)) {
           aborted = true;
@@ -380,7 +384,8 @@ __device__ __forceinline__ void coarse_role_triad(const PipeArgs& a, const Named
         }
         ++ucount;
         coarse_update_phase<N, TC, NOWN, NamedGroup, HomedX, true>(ca, ax, st, n, Vs, KSs, kk, un_s, red, nullptr, yv,
-                                                                   yidx, ucount, c, P, cg, nullptr, gsm);
+                                                                   yidx, ucount, c, P, cg, nullptr, gsm,
+                                                                   k > 0 ? pre : nullptr, pre_ok);
         if (stp) stp[3] = gtimer();
       }
       if (!aborted) {
