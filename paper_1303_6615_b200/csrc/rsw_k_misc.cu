@@ -289,12 +289,25 @@ static cudaError_t launch_avg_n(const double* in, double* out, int S, int M, con
 // from L2; the per-state work is 60 DP instructions per (κ, κ1) row instead of M - 1 pseudo-spectral
 // N-evals (C4: 4.7 vs 21.9 Mflop per state).
 // ---------------------------------------------------------------------------------------------
-template <int N, int B>
-struct AvgTriadLayout {  // Y[B][3][Kc] rotated eigen states, the frame rotation e^{iω_k τ_c}
-  static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1;
-  static constexpr int Y = 0, RPH = Y + B * 3 * Kc, D = RPH + KP;
+#ifndef RSW_AVG_TRIAD_ASYNC
+#define RSW_AVG_TRIAD_ASYNC 0  // 1: coefficients staged per warp with cp.async, TRIAD_STG chunks in flight (C4 2.11 ms vs 1.56 ms for the register prefetch: one row per lane per chunk costs more in waits and copies than it hides)
+#endif
+constexpr int TRIAD_STG = 4;  // chunk buffers per warp (TRIAD_STG - 1 chunks in flight)
+template <int N, int B, int T = 256>
+struct AvgTriadLayout {  // Y[B][3][Kc] rotated eigen states, the frame rotation e^{iω_k τ_c}, per-warp chunk buffers
+  static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, RG = 32 / B;
+  static constexpr int Y = 0, RPH = Y + B * 3 * Kc, WB = RPH + KP;
+  static constexpr int WCH = 18 * RG / 2;  // double2 per chunk: 18 coefficients x RG rows
+  static constexpr int D = WB + (RSW_AVG_TRIAD_ASYNC ? (T / 32) * TRIAD_STG * WCH : 0);
   static constexpr size_t bytes = sizeof(double2) * D;
 };
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NW>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NW) : "memory"); }
 
 #ifndef RSW_AVG_TRIAD_MINB
 #define RSW_AVG_TRIAD_MINB 2  // two CTAs per SM (registers 162 -> 108): C4 1.83 -> 1.56 ms; 3 (80 registers) 4.2 ms
@@ -302,7 +315,7 @@ struct AvgTriadLayout {  // Y[B][3][Kc] rotated eigen states, the frame rotation
 template <int N, int B, int T>
 __global__ void __launch_bounds__(T, RSW_AVG_TRIAD_MINB) k_avg_triad(const double* __restrict__ u_in, double* __restrict__ out,
                                                  int n_states, const AvgTab tab) {
-  using LY = AvgTriadLayout<N, B>;
+  using LY = AvgTriadLayout<N, B, T>;
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NH = N / 2 + 1, RG = 32 / B;
   static_assert(B * RG == 32, "k_avg_triad: B states x RG row groups per warp");
   extern __shared__ double2 smem[];
@@ -336,6 +349,63 @@ __global__ void __launch_bounds__(T, RSW_AVG_TRIAD_MINB) k_avg_triad(const doubl
     const int nk = triad_nk(kap, K);
     const double* Wb = tab.triad + (size_t)TRIAD_E * triad_rows_before(kap, K);
     double2 acc[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+#if RSW_AVG_TRIAD_ASYNC
+    // chunks of RG rows (row i = RG c + r): the warp copies chunk c + STG - 1 (18 RG doubles, 8-byte
+    // cp.async: the rows of an entry are contiguous in the table but not 16-byte aligned) while it
+    // computes chunk c from shared memory (layout [e][RG]: lane (s, r) reads entry e of its row)
+    double* wbuf = reinterpret_cast<double*>(smem + LY::WB) + (size_t)(threadIdx.x >> 5) * TRIAD_STG * 18 * RG;
+    const int nch = (nk + RG - 1) / RG;
+    auto issue = [&](int c) {
+      if (c < nch) {
+        double* dst = wbuf + (size_t)(c % TRIAD_STG) * 18 * RG;
+        for (int q = lane; q < 18 * RG; q += 32) {
+          const int e = q / RG, rr = q % RG, i = c * RG + rr;
+          if (i < nk) cp_async8(dst + q, Wb + (size_t)e * nk + i);
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int c = 0; c < TRIAD_STG - 1; ++c) issue(c);
+    for (int c = 0; c < nch; ++c) {
+      cp_async_wait<TRIAD_STG - 2>();
+      __syncwarp();
+      const int i = c * RG + r;
+      if (i < nk) {
+        const double* wc = wbuf + (size_t)(c % TRIAD_STG) * 18 * RG;
+        double wv[18];
+#pragma unroll
+        for (int e = 0; e < 18; ++e) wv[e] = wc[e * RG + r];
+        const int k1 = kap - K + i, k2 = K - i;
+        const int j1 = k1 >= 0 ? k1 : k1 + Kc, j2 = k2 >= 0 ? k2 : k2 + Kc;
+        const double2 am = Ys[j1], ap = Ys[2 * Kc + j1];
+        double2 pr[6];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const double2 yb = Ys[b * Kc + j2];
+          pr[b] = make_double2(fma(am.x, yb.x, -am.y * yb.y), fma(am.x, yb.y, am.y * yb.x));
+          pr[3 + b] = make_double2(fma(ap.x, yb.x, -ap.y * yb.y), fma(ap.x, yb.y, ap.y * yb.x));
+        }
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+#pragma unroll
+          for (int ab2 = 0; ab2 < 6; ++ab2) {
+            const double w = wv[g * 6 + ab2];
+            if ((g == 1) == (ab2 % 3 == 1)) {
+              acc[g].x = fma(w, pr[ab2].x, acc[g].x);
+              acc[g].y = fma(w, pr[ab2].y, acc[g].y);
+            } else {
+              acc[g].x = fma(-w, pr[ab2].y, acc[g].x);
+              acc[g].y = fma(w, pr[ab2].x, acc[g].y);
+            }
+          }
+        }
+      }
+      __syncwarp();  // every lane is done with chunk c's buffer before it is refilled
+      issue(c + TRIAD_STG - 1);
+    }
+    cp_async_wait<0>();
+#else
     // the next row's coefficients (L2) are in flight while this row is computed
     double wn[18];
     if (r < nk)
@@ -373,6 +443,7 @@ __global__ void __launch_bounds__(T, RSW_AVG_TRIAD_MINB) k_avg_triad(const doubl
         }
       }
     }
+#endif
 #pragma unroll
     for (int g = 0; g < 3; ++g)
       for (int m = RG / 2; m > 0; m >>= 1) {
@@ -404,7 +475,7 @@ template <int N>
 static cudaError_t launch_avg_triad_n(const double* in, double* out, int S, const AvgTab& tab, cudaStream_t st) {
   constexpr int B = RSW_AVG_TRIAD_B, T = 256;
   auto kfn = k_avg_triad<N, B, T>;
-  constexpr size_t sm = AvgTriadLayout<N, B>::bytes;
+  constexpr size_t sm = AvgTriadLayout<N, B, T>::bytes;
   cudaError_t e = set_smem(kfn, sm);
   if (e != cudaSuccess) return e;
   kfn<<<(S + B - 1) / B, T, sm, st>>>(in, out, S, tab);
