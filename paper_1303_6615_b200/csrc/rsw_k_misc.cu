@@ -293,10 +293,10 @@ static cudaError_t launch_avg_n(const double* in, double* out, int S, int M, con
 #define RSW_AVG_TRIAD_ASYNC 0  // 1: coefficients staged per warp with cp.async, TRIAD_STG chunks in flight (C4 2.11 ms vs 1.56 ms for the register prefetch: one row per lane per chunk costs more in waits and copies than it hides)
 #endif
 constexpr int TRIAD_STG = 4;  // chunk buffers per warp (TRIAD_STG - 1 chunks in flight)
-template <int N, int B, int T = 256>
-struct AvgTriadLayout {  // Y[B][3][Kc] rotated eigen states, the frame rotation e^{iω_k τ_c}, per-warp chunk buffers
+template <int N, int B, int T = 256, int SG = 1>
+struct AvgTriadLayout {  // Y[SG B][3][Kc] rotated eigen states, the frame rotation e^{iω_k τ_c}, per-warp chunk buffers
   static constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, RG = 32 / B;
-  static constexpr int Y = 0, RPH = Y + B * 3 * Kc, WB = RPH + KP;
+  static constexpr int Y = 0, RPH = Y + SG * B * 3 * Kc, WB = RPH + KP;
   static constexpr int WCH = 18 * RG / 2;  // double2 per chunk: 18 coefficients x RG rows
   static constexpr int D = WB + (RSW_AVG_TRIAD_ASYNC ? (T / 32) * TRIAD_STG * WCH : 0);
   static constexpr size_t bytes = sizeof(double2) * D;
@@ -312,20 +312,25 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef RSW_AVG_TRIAD_MINB
 #define RSW_AVG_TRIAD_MINB 2  // two CTAs per SM (registers 162 -> 108): C4 1.83 -> 1.56 ms; 3 (80 registers) 4.2 ms
 #endif
-template <int N, int B, int T>
-__global__ void __launch_bounds__(T, RSW_AVG_TRIAD_MINB) k_avg_triad(const double* __restrict__ u_in, double* __restrict__ out,
-                                                 int n_states, const AvgTab tab) {
-  using LY = AvgTriadLayout<N, B, T>;
+// SG state groups per CTA (RSW_AVG_TRIAD_SG): warp w serves group w / (T / 32 / SG); the groups walk the
+// same κ sequence in step, so a coefficient row fetched from L2 by one group's warp is read by the
+// others' from L1.
+template <int N, int B, int T, int SG>
+__global__ void __launch_bounds__(T, (RSW_AVG_TRIAD_MINB / SG > 0 ? RSW_AVG_TRIAD_MINB / SG : 1))
+    k_avg_triad(const double* __restrict__ u_in, double* __restrict__ out, int n_states, const AvgTab tab) {
+  using LY = AvgTriadLayout<N, B, T, SG>;
+  constexpr int NWG = T / 32 / SG;  // warps per state group
+  static_assert(NWG * SG * 32 == T, "k_avg_triad: T / 32 warps split evenly over SG state groups");
   constexpr int K = N / 3, Kc = 2 * K + 1, KP = K + 1, NH = N / 2 + 1, RG = 32 / B;
   static_assert(B * RG == 32, "k_avg_triad: B states x RG row groups per warp");
   extern __shared__ double2 smem[];
   double2* Y = smem + LY::Y;
   double2* RPH = smem + LY::RPH;
-  const int s0 = blockIdx.x * B;
+  const int s0 = blockIdx.x * B * SG;
   for (int k = threadIdx.x; k <= K; k += T) RPH[k] = __ldg(tab.triad_ph + k);
   __syncthreads();
   // stage: primitive half spectra -> eigen coordinates of both signs of κ -> rotated frame
-  for (int t = threadIdx.x; t < B * Kc; t += T) {
+  for (int t = threadIdx.x; t < SG * B * Kc; t += T) {
     const int s = t / Kc, j = t - s * Kc, kap = kappa_of(j, K), ak = kap < 0 ? -kap : kap;
     double2 c[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     if (s0 + s < n_states) {
@@ -343,9 +348,9 @@ __global__ void __launch_bounds__(T, RSW_AVG_TRIAD_MINB) k_avg_triad(const doubl
     for (int al = 0; al < 3; ++al) Y[(s * 3 + al) * Kc + j] = c[al];
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, sl = lane / RG, r = lane % RG;
+  const int lane = threadIdx.x & 31, sg = (int)(threadIdx.x >> 5) / NWG, sl = sg * B + lane / RG, r = lane % RG;
   const double2* Ys = Y + sl * 3 * Kc;
-  for (int kap = threadIdx.x >> 5; kap <= K; kap += T / 32) {
+  for (int kap = (int)(threadIdx.x >> 5) % NWG; kap <= K; kap += NWG) {
     const int nk = triad_nk(kap, K);
     const double* Wb = tab.triad + (size_t)TRIAD_E * triad_rows_before(kap, K);
     double2 acc[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
@@ -462,23 +467,26 @@ __global__ void __launch_bounds__(T, RSW_AVG_TRIAD_MINB) k_avg_triad(const doubl
     }
   }
   // modes K < k <= N/2 are zero
-  for (int t = threadIdx.x; t < B * 3 * (NH - KP); t += T) {
+  for (int t = threadIdx.x; t < SG * B * 3 * (NH - KP); t += T) {
     const int s = t / (3 * (NH - KP)), q = t - s * 3 * (NH - KP), f = q / (NH - KP), k = KP + q % (NH - KP);
     if (s0 + s < n_states) reinterpret_cast<double2*>(out)[(size_t)(s0 + s) * 3 * NH + f * NH + k] = make_double2(0.0, 0.0);
   }
 }
 
+#ifndef RSW_AVG_TRIAD_SG
+#define RSW_AVG_TRIAD_SG 1  // state groups per CTA (each of 256 threads, B states); 2 (one 512-thread CTA per SM, L1 reuse of the rows): C4 1.74 vs 1.56 ms, off
+#endif
 #ifndef RSW_AVG_TRIAD_B
 #define RSW_AVG_TRIAD_B 4  // states per CTA of the batched triad N̄ (x 32/B row groups per warp); C4: 4 -> 3.44 ms, 8 -> 7.90 ms (1 CTA per SM)
 #endif
 template <int N>
 static cudaError_t launch_avg_triad_n(const double* in, double* out, int S, const AvgTab& tab, cudaStream_t st) {
-  constexpr int B = RSW_AVG_TRIAD_B, T = 256;
-  auto kfn = k_avg_triad<N, B, T>;
-  constexpr size_t sm = AvgTriadLayout<N, B, T>::bytes;
+  constexpr int B = RSW_AVG_TRIAD_B, SG = RSW_AVG_TRIAD_SG, T = 256 * SG;
+  auto kfn = k_avg_triad<N, B, T, SG>;
+  constexpr size_t sm = AvgTriadLayout<N, B, T, SG>::bytes;
   cudaError_t e = set_smem(kfn, sm);
   if (e != cudaSuccess) return e;
-  kfn<<<(S + B - 1) / B, T, sm, st>>>(in, out, S, tab);
+  kfn<<<(S + B * SG - 1) / (B * SG), T, sm, st>>>(in, out, S, tab);
   return cudaGetLastError();
 }
 
