@@ -1074,8 +1074,9 @@ rsw_status run_pipelined(const rsw_params* p, const parareal_config* cfg, const 
   const char* en = getenv("RSW_PIPE_NG");
   if (a.at.triad && !eg) {
     // triad sweeps: a stage costs one hand-off plus the owned N̄ (~ owned modes x rows), no
-    // sample rounds; NG concurrent sweeps (default 3: sweep g + 3 starts after sweep g ends, which is
-    // before the fine lags would let it start anyway) of the largest GC that fits them on the dies
+    // sample rounds; NG concurrent sweeps (default 3: sweep g + 3 starts after sweep g ends — on C3 that
+    // holds sweep 3 back ~0.6 ms past its first input (trace, profiles/r02_c3_trace_ng.txt), but NG 4 /
+    // 5 / 6 cost more through the fine groups they take: 26.2 / 26.7 / 28.1 vs 23.2 ms) of the largest GC that fits them on the dies
     // (measured on C3: 4 owned modes per CTA, GC = 22-24, beat 3 (GC = 37) — the CTAs left without a coarse
     // role run a second fine group; 5 owned modes no longer fit the coefficient blocks in shared memory)
     const int ngw = std::max(1, std::min(en ? atoi(en) : 3, K + 1));
